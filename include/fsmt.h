@@ -1,0 +1,205 @@
+/*
+ * fsmt.h — C ABI of the B200-native FourierSMT hot path (arXiv 2603.22877).
+ *
+ * Citation convention: P:n = /root/reference/PAPER.md line n, S:n = SPEC.md line n,
+ * R<k> = reading k in DESIGN.md §3.  The library is one shared object
+ * (paper_2603_22877_b200/libfsmt.so); every step of the path runs in its own
+ * sm_100a CUDA kernels.  No C++ exception crosses this boundary; every call
+ * returns an fsmt_status, and on failure fsmt_last_error() holds a message
+ * (parse errors carry "line:col: msg").  Outputs are written only on FSMT_OK.
+ *
+ * Call order (enforced, FSMT_ERR_STATE otherwise):
+ *     fsmt_create -> fsmt_load_formula -> fsmt_build_xbdd -> [fsmt_set_params]
+ *       -> fsmt_solve                                   (whole Alg.2, one call)
+ *       -> fsmt_begin -> {fsmt_sweep, fsmt_update, fsmt_stage_end}*   (step API)
+ * A context is bound to one CUDA device, owns all its device memory and is not
+ * thread-safe.  Pointer arguments marked "where" are host pointers when
+ * where == FSMT_HOST and device pointers (on the ctx's device) when
+ * where == FSMT_DEVICE; the library never keeps a caller pointer after return.
+ *
+ * Layouts: per-restart state is restart-minor, row = variable:
+ *     a[n_bool][R] f32, b[n_real][R] f32, grad_a[n_bool][R] f64, grad_b[n_real][R] f64,
+ *     U[n_cons][R] u8, x[n_bool][R] i8, obj[R] f64, unsat[R] u32.
+ * Truth encoding: -1 = True, +1 = False.
+ */
+#ifndef FSMT_H
+#define FSMT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct fsmt_ctx fsmt_ctx;
+
+typedef enum {
+    FSMT_OK = 0,
+    FSMT_ERR_ARG = 1,          /* NULL / out-of-range argument */
+    FSMT_ERR_PARSE = 2,        /* HSMT syntax / validation error */
+    FSMT_ERR_UNSUPPORTED = 3,  /* '=' atoms (R9), non-positive weights */
+    FSMT_ERR_STATE = 4,        /* call out of order */
+    FSMT_ERR_NODE_BUDGET = 5,  /* a constraint's xBDD exceeds the node budget / encoding limits */
+    FSMT_ERR_OOM = 6,          /* device or host allocation failed */
+    FSMT_ERR_CUDA = 7,         /* CUDA runtime error (no device, launch failure, ...) */
+    FSMT_ERR_TIMEOUT = 8       /* time limit hit inside fsmt_solve (verdict is still set) */
+} fsmt_status;
+
+typedef enum { FSMT_UNKNOWN = 0, FSMT_SAT = 10 } fsmt_verdict;   /* S:514 exit codes */
+
+enum { FSMT_HOST = 0, FSMT_DEVICE = 1 };
+enum { FSMT_ROUND_SIGN = 0, FSMT_ROUND_PHILOX = 1 };             /* R17 */
+enum { FSMT_ERWA_VERBATIM = 0, FSMT_ERWA_RESET0 = 1 };           /* R18 */
+
+typedef struct {
+    uint32_t n_bool, n_real, n_atoms, n_cons;
+    uint32_t n_templates;      /* distinct canonical xBDDs (Def.2, R7) */
+    uint32_t max_slots;        /* max distinct variables in one constraint (R5) */
+    uint32_t max_nodes;        /* max decision nodes in one template */
+    uint32_t n_bounded;        /* reals with a finite projection bound (R15) */
+    uint64_t n_nodes;          /* sum over constraints of |V_c| */
+    uint64_t n_slot_refs;      /* sum over constraints of slot count */
+} fsmt_dims;
+
+typedef struct {
+    const float* kappas;       /* annealing schedule as kappa_t = 1/sigma_t >= 0 (Alg.2, R11/R12); NULL -> 0.1..2.0 */
+    uint32_t n_stages;         /* length of kappas (ignored when kappas == NULL) */
+    float eta;                 /* PGD step size (Eq.11, R13); <= 0 -> 0.05 */
+    float eps;                 /* epsilon of Eq.14 (R14); <= 0 -> 1e-2 */
+    uint32_t rounding;         /* FSMT_ROUND_SIGN (Alg.1 line 10) | FSMT_ROUND_PHILOX (Eq.4) */
+    uint32_t erwa_mode;        /* FSMT_ERWA_VERBATIM (Alg.2 h<-1) | FSMT_ERWA_RESET0 */
+    double time_limit_s;       /* <= 0: none (P:696 uses 1000 s) */
+} fsmt_params;
+
+typedef struct {
+    uint32_t stages_run;       /* annealing stages executed */
+    uint32_t steps_run;        /* PGD steps executed (all stages) */
+    uint32_t winner_restart;   /* restart whose model is returned */
+    uint32_t winner_stage;     /* stage at which it was found (1-based) */
+    uint32_t best_unsat;       /* unsat count of the returned model (0 iff SAT) */
+    uint32_t host_verified;    /* 1 iff the returned model passed the host fp64 re-check */
+    double solve_ms;           /* wall time of fsmt_solve after build */
+    double evals;              /* constraint x restart COP+grad evaluations performed */
+} fsmt_stats;
+
+/* ---- lifecycle -------------------------------------------------------------------------- */
+
+/* Create a context on CUDA device `cuda_device`. FSMT_ERR_CUDA if the device is unusable.
+ * cuda_device == -1 creates a HOST-ONLY context: load / build / dims / bounds / dump /
+ * fsmt_verify work (they are host code); every kernel-backed call returns FSMT_ERR_CUDA. */
+fsmt_status fsmt_create(int cuda_device, fsmt_ctx** out);
+void fsmt_destroy(fsmt_ctx* ctx);
+/* Last error message of ctx (never NULL; "" when none). */
+const char* fsmt_last_error(const fsmt_ctx* ctx);
+/* Bind a cudaStream_t (as void*) for all subsequent launches; NULL = the ctx's own stream. */
+fsmt_status fsmt_bind_stream(fsmt_ctx* ctx, void* cuda_stream);
+
+/* ---- a0: formula -> xBDDs (Alg.1 lines 1-2) ---------------------------------- */
+
+/* Parse HSMT text (grammar in DESIGN.md §2).  Atoms are canonicalised to
+ * q.y <= q0 / < q0; '=' is rejected (FSMT_ERR_UNSUPPORTED, R9).  The text is
+ * copied; a prior formula is replaced (and all derived state dropped). */
+fsmt_status fsmt_load_formula(fsmt_ctx* ctx, const char* hsmt, size_t len);
+
+/* Compile every constraint to its reduced ordered xBDD over its slots (Def.2
+ * "atomic constraints as propositional variables"; slot order R6, numbering R7),
+ * dedup into templates, derive the projection bounds (R15), flatten to SoA and upload.
+ * node_budget: max decision nodes per constraint (0 -> 32767, also the encoding limit). */
+fsmt_status fsmt_build_xbdd(fsmt_ctx* ctx, uint64_t node_budget);
+
+fsmt_status fsmt_get_dims(const fsmt_ctx* ctx, fsmt_dims* out);
+/* Projection bounds lo[n_real], hi[n_real] (host, f32; +-inf when unbounded). */
+fsmt_status fsmt_get_bounds(const fsmt_ctx* ctx, float* lo, float* hi);
+/* Canonical structure dump: <dir>/templates.jsonl + <dir>/constraints.bin. */
+fsmt_status fsmt_dump_structure(const fsmt_ctx* ctx, const char* dir);
+
+/* ---- whole solve (Alg.2 around Alg.1) ----------------------------- */
+
+fsmt_status fsmt_set_params(fsmt_ctx* ctx, const fsmt_params* params);   /* NULL -> defaults */
+
+/* Run `restarts` lock-step restarts of Alg.2 with `steps` PGD steps per stage (R21),
+ * seeded Philox init (R20).  verdict = FSMT_SAT only if a restart's rounded model passes
+ * the device exact check (K5) AND the host fp64 re-check; the winner is the
+ * lexicographically smallest (stage, restart).  Otherwise FSMT_UNKNOWN and the
+ * outputs hold the model with the smallest (unsat, stage, restart).
+ * x_out[n_bool] in {-1,+1}, y_out[n_real] (host, caller-allocated); stats may be NULL. */
+fsmt_status fsmt_solve(fsmt_ctx* ctx, uint32_t restarts, uint32_t steps, uint64_t seed,
+                       fsmt_verdict* verdict, int8_t* x_out, float* y_out, fsmt_stats* stats);
+
+/* ---- step API (one stage = S x {sweep, update} + stage_end); the multi-GPU driver and
+ *      the parity tests use it; it runs exactly the kernels fsmt_solve runs ------------- */
+
+/* Allocate per-restart state for R restarts and run K0 (Philox init, R20) with global
+ * restart ids restart_offset..restart_offset+R-1; U <- 0. */
+fsmt_status fsmt_begin(fsmt_ctx* ctx, uint32_t restarts, uint64_t seed, uint32_t restart_offset);
+/* Overwrite / read the relaxed point (a[n_bool][R], b[n_real][R]). set_state does NOT project. */
+fsmt_status fsmt_set_state(fsmt_ctx* ctx, const float* a, const float* b, int where);
+fsmt_status fsmt_get_state(fsmt_ctx* ctx, float* a, float* b, int where);
+/* Overwrite / read the ERWA violation counters U[n_cons][R] (R18). */
+fsmt_status fsmt_set_counters(fsmt_ctx* ctx, const uint8_t* U, int where);
+fsmt_status fsmt_get_counters(fsmt_ctx* ctx, uint8_t* U, int where);
+
+/* K1: objective and gradient at the current point for all restarts (a1-a4 of SURVEY §8(a)):
+ * obj[r] = sum_c w_cr E_c (Eq.10), grad = dC/d(a,b) (Alg.B with the sign of R1, chain rule
+ * P:1326-1327), w_cr = w_c * 2^(U[c][r] + e_t), e_t = max(t-2,0)/2 (VERBATIM) or 0 (RESET0). */
+fsmt_status fsmt_sweep(fsmt_ctx* ctx, float kappa, uint32_t stage_t);
+/* Read the last sweep's outputs: grad_a[n_bool][R], grad_b[n_real][R] (f64), obj[R] (f64).
+ * Any pointer may be NULL. */
+fsmt_status fsmt_get_sweep(fsmt_ctx* ctx, double* grad_a, double* grad_b, double* obj, int where);
+/* Per-constraint E_c for restart r from the last sweep's kernels (debug/parity hook, host E[n_cons]). */
+fsmt_status fsmt_constraint_terms(fsmt_ctx* ctx, float kappa, uint32_t restart, double* E);
+
+/* K3: projected gradient step (Eq.11-14): for every non-frozen restart,
+ * (a',b') = proj((a,b) - eta*grad); gm2[r] = ||((a,b)-(a',b'))/eta||^2; if gm2 <= eps^2 the
+ * restart is frozen for the rest of the stage (no update), else (a,b) <- (a',b').
+ * gm2_out[R] (host, may be NULL) receives the squared gradient-mapping norms. */
+fsmt_status fsmt_update(fsmt_ctx* ctx, float eta, float eps, double* gm2_out);
+
+/* K4+K5 (a6-a9): round x = sgn(a) or R(a) (R17), y = b; exact check of every constraint
+ * (R22); U[c][r] += u_c; unsat[r] = #violated; clears the per-stage frozen flags.
+ * unsat_out[R] (host, may be NULL). */
+fsmt_status fsmt_stage_end(fsmt_ctx* ctx, uint32_t stage_t, uint32_t* unsat_out);
+/* One whole annealing stage for all restarts, as fsmt_solve runs it (Alg.2 loop body,
+ * P:513-528): `steps` x {K1 sweep at kappa, K3 update(eta, eps)} then K4+K5 stage_end.
+ * The frozen flags are cleared first.  unsat_out[R] (host, may be NULL); *min_unsat (may be
+ * NULL) receives min_r unsat[r].  Uses the ctx params (eta, eps, rounding, erwa_mode). */
+fsmt_status fsmt_run_stage(fsmt_ctx* ctx, uint32_t stage_t, float kappa, uint32_t steps, uint32_t* unsat_out,
+                           uint32_t* min_unsat);
+
+/* Rounded model of one restart from the last stage_end: x[n_bool] (-1/+1), y[n_real] (host). */
+fsmt_status fsmt_get_model(fsmt_ctx* ctx, uint32_t restart, int8_t* x_out, float* y_out);
+/* Rounded Booleans of all restarts from the last stage_end: x[n_bool][R] int8 (where). */
+fsmt_status fsmt_get_rounded(fsmt_ctx* ctx, int8_t* x, int where);
+
+/* Host exact fp64 check of one model (Thm.1, R22): n_unsat, per_con[n_cons] (1 = violated,
+ * may be NULL). Runs on the CPU (it is the re-verification step of fsmt_solve). */
+fsmt_status fsmt_verify(fsmt_ctx* ctx, const int8_t* x, const float* y, uint32_t* n_unsat, uint8_t* per_con);
+
+/* Device verification of arbitrary models: x[n_bool][R] i8, y[n_real][R] f32 (where),
+ * unsat_out[R] (host), per_con[n_cons][R] u8 (host, may be NULL). Uses the K5 kernel. */
+fsmt_status fsmt_verify_batch(fsmt_ctx* ctx, uint32_t R, const int8_t* x, const float* y, int where,
+                              uint32_t* unsat_out, uint8_t* per_con);
+
+/* ---- introspection ------------------------------------------------------------------------ */
+/* Number of this library's kernel launches since the ctx was created. */
+uint64_t fsmt_kernel_launches(const fsmt_ctx* ctx);
+/* Current restart count (0 before fsmt_begin). */
+uint32_t fsmt_restarts(const fsmt_ctx* ctx);
+/* Device pointers of the state buffers (for torch.distributed collectives); any may be NULL. */
+fsmt_status fsmt_device_buffers(fsmt_ctx* ctx, void** a, void** b, void** grad_a, void** grad_b,
+                                void** U, void** obj, void** unsat);
+/* Time the sweep kernel alone: runs `iters` K1 launches on the ctx stream and returns the
+ * average per-launch device time in ms measured with CUDA events on that stream. */
+fsmt_status fsmt_time_sweep(fsmt_ctx* ctx, float kappa, uint32_t stage_t, uint32_t iters, double* ms_out);
+/* Per-kernel device timing: when enabled, every K1 / K3 / K5 launch is bracketed by CUDA
+ * events on the launch stream.  fsmt_get_timing synchronises and returns, per kernel class
+ * k in {0: K1 sweep, 1: K3 update (3 launches), 2: K4+K5 stage end}, the summed device ms
+ * and the launch-group count since the last reset.  ms[3], count[3]. */
+fsmt_status fsmt_set_timing(fsmt_ctx* ctx, int enable);
+fsmt_status fsmt_get_timing(fsmt_ctx* ctx, double* ms, uint64_t* count, int reset);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FSMT_H */

@@ -190,7 +190,7 @@ def solve_restart(f, seed, r, params: Params, lo=None, hi=None):
     a, b = init_point(f, seed, r, lo, hi)
     C_n = len(f.constraints)
     h = np.zeros(C_n)
-    w = np.ones(C_n)
+    w = np.array([c.weight for c in f.constraints], dtype=np.float64)   # initial w_c (Alg.2 input)
     best = None
     hist = []
     for t, kappa in enumerate(params.kappas, start=1):

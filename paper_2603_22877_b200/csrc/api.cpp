@@ -1,0 +1,784 @@
+// C-ABI implementation (include/fsmt.h): context, call-order state machine, device buffers,
+// and the Alg.2 / Alg.1 driver loop around the sm_100a kernels.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/fsmt.h"
+#include "fsmt_internal.hpp"
+#include "kernels.hpp"
+
+using namespace fsmt;
+
+struct fsmt_ctx {
+    int device = 0;
+    bool host_only = false;     // cuda_device == -1: parse/build/dump/host-verify only
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    int stage = 0;              // 0 created, 1 loaded, 2 built, 3 begun
+    Formula f;
+    Built b;
+    DevFormula F{};
+    std::vector<void*> fallocs;
+    DevState S{};
+    std::vector<void*> sallocs;
+    double* terms = nullptr;    // [C] debug hook buffer
+    // params
+    std::vector<float> kappas;
+    float eta = 0.05f, eps = 1e-2f;
+    uint32_t rounding = FSMT_ROUND_SIGN, erwa_mode = FSMT_ERWA_VERBATIM;
+    double time_limit = 0.0;
+    // run
+    uint64_t seed = 0;
+    uint32_t restart_offset = 0;
+    bool rounded = false;
+    uint64_t launches = 0;
+    // per-kernel-class device timing (fsmt_set_timing)
+    bool timing = false;
+    std::vector<cudaEvent_t> ev_pool;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_open[3];
+    double t_ms[3] = {0, 0, 0};
+    uint64_t t_cnt[3] = {0, 0, 0};
+};
+
+namespace {
+cudaEvent_t ev_get(fsmt_ctx* ctx) {
+    if (!ctx->ev_pool.empty()) {
+        cudaEvent_t e = ctx->ev_pool.back();
+        ctx->ev_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+// Brackets a launch group of kernel class k with events on the launch stream.
+struct Timed {
+    fsmt_ctx* ctx;
+    int k;
+    cudaEvent_t e0 = nullptr;
+    Timed(fsmt_ctx* c, int kk) : ctx(c), k(kk) {
+        if (ctx->timing) {
+            e0 = ev_get(ctx);
+            cudaEventRecord(e0, ctx->stream);
+        }
+    }
+    ~Timed() {
+        if (ctx->timing) {
+            cudaEvent_t e1 = ev_get(ctx);
+            cudaEventRecord(e1, ctx->stream);
+            ctx->ev_open[k].emplace_back(e0, e1);
+        }
+    }
+};
+void timing_collect(fsmt_ctx* ctx) {
+    for (int k = 0; k < 3; ++k) {
+        for (auto& pr : ctx->ev_open[k]) {
+            cudaEventSynchronize(pr.second);
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, pr.first, pr.second);
+            ctx->t_ms[k] += ms;
+            ctx->t_cnt[k] += 1;
+            ctx->ev_pool.push_back(pr.first);
+            ctx->ev_pool.push_back(pr.second);
+        }
+        ctx->ev_open[k].clear();
+    }
+}
+}  // namespace
+
+namespace {
+
+void default_kappas(std::vector<float>& k) {
+    k.clear();
+    for (int i = 1; i <= 20; ++i) k.push_back((float)(0.1 * i));   // 1/sigma = 0.1..2.0 (R12)
+}
+
+fsmt_status fail(fsmt_ctx* c, fsmt_status s, const std::string& msg) {
+    if (c) c->err = msg;
+    return s;
+}
+
+#define CK(call)                                                                             \
+    do {                                                                                     \
+        cudaError_t e_ = (call);                                                             \
+        if (e_ != cudaSuccess) return fail(ctx, FSMT_ERR_CUDA, std::string(#call ": ") + cudaGetErrorString(e_)); \
+    } while (0)
+
+template <typename T>
+fsmt_status upload(fsmt_ctx* ctx, const std::vector<T>& v, const T*& dst, std::vector<void*>& allocs) {
+    void* p = nullptr;
+    size_t bytes = std::max<size_t>(v.size() * sizeof(T), sizeof(T));
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e != cudaSuccess) return fail(ctx, FSMT_ERR_OOM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    allocs.push_back(p);
+    if (!v.empty()) CK(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+    dst = (const T*)p;
+    return FSMT_OK;
+}
+
+void free_list(std::vector<void*>& v) {
+    for (void* p : v) cudaFree(p);
+    v.clear();
+}
+
+void drop_state(fsmt_ctx* ctx) {
+    free_list(ctx->sallocs);
+    ctx->S = DevState{};
+    ctx->rounded = false;
+    if (ctx->terms) { cudaFree(ctx->terms); ctx->terms = nullptr; }
+}
+
+void drop_formula(fsmt_ctx* ctx) {
+    drop_state(ctx);
+    free_list(ctx->fallocs);
+    ctx->F = DevFormula{};
+}
+
+float wscale_of(uint32_t stage_t, uint32_t mode) {
+    // R18: weight during stage t = w_c * 2^(U + e_t), e_t = max(t-2,0)/2 (Alg.2 verbatim) or 0
+    if (mode == FSMT_ERWA_RESET0 || stage_t <= 2) return 1.0f;
+    return (float)std::pow(2.0, (double)(stage_t - 2) / 2.0);
+}
+
+fsmt_status need(fsmt_ctx* ctx, int stage, const char* what) {
+    if (!ctx) return FSMT_ERR_ARG;
+    if (stage >= 3 && ctx->host_only) return fail(ctx, FSMT_ERR_CUDA, std::string(what) + ": host-only context has no device");
+    if (ctx->stage < stage) return fail(ctx, FSMT_ERR_STATE, std::string(what) + ": called out of order");
+    return FSMT_OK;
+}
+
+template <typename T>
+fsmt_status copy_in(fsmt_ctx* ctx, T* dst, const T* src, size_t n, int where) {
+    if (n == 0) return FSMT_OK;
+    if (!src) return fail(ctx, FSMT_ERR_ARG, "null input pointer");
+    CK(cudaMemcpyAsync(dst, src, n * sizeof(T), where == FSMT_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                       ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return FSMT_OK;
+}
+
+template <typename T>
+fsmt_status copy_out(fsmt_ctx* ctx, T* dst, const T* src, size_t n, int where) {
+    if (n == 0 || !dst) return FSMT_OK;
+    CK(cudaMemcpyAsync(dst, src, n * sizeof(T), where == FSMT_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return FSMT_OK;
+}
+
+fsmt_status check_launch(fsmt_ctx* ctx) {
+    CK(cudaGetLastError());
+    return FSMT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+fsmt_status fsmt_create(int cuda_device, fsmt_ctx** out) {
+    if (!out) return FSMT_ERR_ARG;
+    *out = nullptr;
+    if (cuda_device == -1) {
+        fsmt_ctx* h = new (std::nothrow) fsmt_ctx();
+        if (!h) return FSMT_ERR_OOM;
+        h->host_only = true;
+        default_kappas(h->kappas);
+        *out = h;
+        return FSMT_OK;
+    }
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) return FSMT_ERR_CUDA;
+    if (cuda_device < 0 || cuda_device >= n) return FSMT_ERR_ARG;
+    if (cudaSetDevice(cuda_device) != cudaSuccess) return FSMT_ERR_CUDA;
+    fsmt_ctx* ctx = new (std::nothrow) fsmt_ctx();
+    if (!ctx) return FSMT_ERR_OOM;
+    ctx->device = cuda_device;
+    if (cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking) != cudaSuccess) {
+        delete ctx;
+        return FSMT_ERR_CUDA;
+    }
+    ctx->stream = ctx->own_stream;
+    default_kappas(ctx->kappas);
+    *out = ctx;
+    return FSMT_OK;
+}
+
+void fsmt_destroy(fsmt_ctx* ctx) {
+    if (!ctx) return;
+    if (ctx->host_only) {
+        delete ctx;
+        return;
+    }
+    cudaSetDevice(ctx->device);
+    drop_formula(ctx);
+    timing_collect(ctx);
+    for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+    delete ctx;
+}
+
+const char* fsmt_last_error(const fsmt_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+fsmt_status fsmt_bind_stream(fsmt_ctx* ctx, void* s) {
+    if (!ctx) return FSMT_ERR_ARG;
+    ctx->stream = s ? (cudaStream_t)s : ctx->own_stream;
+    return FSMT_OK;
+}
+
+fsmt_status fsmt_load_formula(fsmt_ctx* ctx, const char* text, size_t len) {
+    if (!ctx || (!text && len)) return FSMT_ERR_ARG;
+    if (!ctx->host_only) {
+        cudaSetDevice(ctx->device);
+        drop_formula(ctx);
+    }
+    ctx->stage = 0;
+    try {
+        ctx->f = parse_hsmt(text, len);
+    } catch (const ParseError& e) {
+        return fail(ctx, e.unsupported ? FSMT_ERR_UNSUPPORTED : FSMT_ERR_PARSE,
+                    std::to_string(e.line) + ":" + std::to_string(e.col) + ": " + e.msg);
+    } catch (const std::bad_alloc&) {
+        return fail(ctx, FSMT_ERR_OOM, "host allocation failed while parsing");
+    }
+    ctx->b = Built{};
+    ctx->stage = 1;
+    ctx->err.clear();
+    return FSMT_OK;
+}
+
+fsmt_status fsmt_build_xbdd(fsmt_ctx* ctx, uint64_t node_budget) {
+    fsmt_status s = need(ctx, 1, "fsmt_build_xbdd");
+    if (s) return s;
+    if (!ctx->host_only) {
+        cudaSetDevice(ctx->device);
+        drop_formula(ctx);
+    }
+    ctx->stage = 1;
+    try {
+        ctx->b = build_xbdds(ctx->f, node_budget);
+    } catch (const BuildError& e) {
+        return fail(ctx, e.budget ? FSMT_ERR_NODE_BUDGET : FSMT_ERR_ARG, e.msg);
+    } catch (const std::bad_alloc&) {
+        return fail(ctx, FSMT_ERR_OOM, "host allocation failed while building xBDDs");
+    }
+    if (ctx->host_only) {
+        ctx->stage = 2;
+        ctx->err.clear();
+        return FSMT_OK;
+    }
+    const Formula& f = ctx->f;
+    const Built& b = ctx->b;
+    // flatten templates
+    std::vector<uint32_t> node_off{0}, kind_off{0};
+    std::vector<DevNode> nodes;
+    std::vector<uint8_t> kinds;
+    std::vector<int32_t> roots;
+    for (const Template& t : b.tmpls) {
+        for (const TNode& n : t.nodes) nodes.push_back(DevNode{n.level, n.hi, n.lo, 0});
+        kinds.insert(kinds.end(), t.kinds.begin(), t.kinds.end());
+        node_off.push_back((uint32_t)nodes.size());
+        kind_off.push_back((uint32_t)kinds.size());
+        roots.push_back(t.root);
+    }
+    std::vector<float> aval(f.atom_val.size()), arhs(f.n_atoms()), ainv(f.n_atoms());
+    for (size_t i = 0; i < f.atom_val.size(); ++i) aval[i] = (float)f.atom_val[i];
+    for (uint32_t i = 0; i < f.n_atoms(); ++i) {
+        arhs[i] = (float)f.atom_rhs[i];
+        double n2 = 0.0;
+        for (uint32_t t = f.atom_rowptr[i]; t < f.atom_rowptr[i + 1]; ++t) n2 += f.atom_val[t] * f.atom_val[t];
+        ainv[i] = (float)(1.0 / std::sqrt(n2));
+    }
+    DevFormula& F = ctx->F;
+    F.n_bool = f.n_bool;
+    F.n_real = f.n_real;
+    F.n_cons = (uint32_t)f.cons.size();
+    F.n_atoms = f.n_atoms();
+    F.max_slots = b.max_slots;
+    F.max_nodes = b.max_nodes;
+#define UP(vec, field) do { s = upload(ctx, vec, F.field, ctx->fallocs); if (s) return s; } while (0)
+    UP(b.cons_tmpl, cons_tmpl);
+    UP(b.cons_slot_off, cons_slot_off);
+    UP(b.slot_ids, slot_ids);
+    UP(b.cons_w, cons_w);
+    UP(node_off, tmpl_node_off);
+    UP(nodes, nodes);
+    UP(kind_off, tmpl_kind_off);
+    UP(kinds, kinds);
+    UP(roots, tmpl_root);
+    UP(f.atom_rowptr, atom_rowptr);
+    UP(f.atom_col, atom_col);
+    UP(aval, atom_val);
+    UP(f.atom_val, atom_val64);
+    UP(arhs, atom_rhs);
+    UP(f.atom_rhs, atom_rhs64);
+    UP(f.atom_strict, atom_strict);
+    UP(ainv, atom_invnorm);
+    UP(b.lo, lo);
+    UP(b.hi, hi);
+#undef UP
+    ctx->stage = 2;
+    ctx->err.clear();
+    return FSMT_OK;
+}
+
+fsmt_status fsmt_get_dims(const fsmt_ctx* ctx, fsmt_dims* out) {
+    if (!ctx || !out) return FSMT_ERR_ARG;
+    if (ctx->stage < 1) return FSMT_ERR_STATE;
+    fsmt_dims d{};
+    d.n_bool = ctx->f.n_bool;
+    d.n_real = ctx->f.n_real;
+    d.n_atoms = ctx->f.n_atoms();
+    d.n_cons = (uint32_t)ctx->f.cons.size();
+    if (ctx->stage >= 2) {
+        d.n_templates = (uint32_t)ctx->b.tmpls.size();
+        d.max_slots = ctx->b.max_slots;
+        d.max_nodes = ctx->b.max_nodes;
+        d.n_bounded = ctx->b.n_bounded;
+        d.n_nodes = ctx->b.n_nodes;
+        d.n_slot_refs = ctx->b.slot_ids.size();
+    }
+    *out = d;
+    return FSMT_OK;
+}
+
+fsmt_status fsmt_get_bounds(const fsmt_ctx* ctx, float* lo, float* hi) {
+    if (!ctx) return FSMT_ERR_ARG;
+    if (ctx->stage < 2) return FSMT_ERR_STATE;
+    if (lo) std::copy(ctx->b.lo.begin(), ctx->b.lo.end(), lo);
+    if (hi) std::copy(ctx->b.hi.begin(), ctx->b.hi.end(), hi);
+    return FSMT_OK;
+}
+
+fsmt_status fsmt_dump_structure(const fsmt_ctx* cctx, const char* dir) {
+    fsmt_ctx* ctx = const_cast<fsmt_ctx*>(cctx);
+    if (!ctx || !dir) return FSMT_ERR_ARG;
+    if (ctx->stage < 2) return fail(ctx, FSMT_ERR_STATE, "fsmt_dump_structure: build first");
+    std::string p1 = std::string(dir) + "/templates.jsonl", p2 = std::string(dir) + "/constraints.bin";
+    FILE* fp = fopen(p1.c_str(), "wb");
+    if (!fp) return fail(ctx, FSMT_ERR_ARG, "cannot write " + p1);
+    std::string t = dump_templates_jsonl(ctx->b);
+    fwrite(t.data(), 1, t.size(), fp);
+    fclose(fp);
+    fp = fopen(p2.c_str(), "wb");
+    if (!fp) return fail(ctx, FSMT_ERR_ARG, "cannot write " + p2);
+    std::vector<uint8_t> c = dump_constraints_bin(ctx->b);
+    fwrite(c.data(), 1, c.size(), fp);
+    fclose(fp);
+    return FSMT_OK;
+}
+
+fsmt_status fsmt_set_params(fsmt_ctx* ctx, const fsmt_params* p) {
+    if (!ctx) return FSMT_ERR_ARG;
+    if (!p) {
+        default_kappas(ctx->kappas);
+        ctx->eta = 0.05f;
+        ctx->eps = 1e-2f;
+        ctx->rounding = FSMT_ROUND_SIGN;
+        ctx->erwa_mode = FSMT_ERWA_VERBATIM;
+        ctx->time_limit = 0;
+        return FSMT_OK;
+    }
+    if (p->kappas) {
+        if (p->n_stages == 0) return fail(ctx, FSMT_ERR_ARG, "empty kappa schedule");
+        for (uint32_t i = 0; i < p->n_stages; ++i)
+            if (!(p->kappas[i] >= 0.f) || !std::isfinite(p->kappas[i])) return fail(ctx, FSMT_ERR_ARG, "kappa must be finite and >= 0");
+        ctx->kappas.assign(p->kappas, p->kappas + p->n_stages);
+    } else {
+        default_kappas(ctx->kappas);
+    }
+    if (p->rounding > 1 || p->erwa_mode > 1) return fail(ctx, FSMT_ERR_ARG, "bad rounding / erwa_mode");
+    ctx->eta = p->eta > 0 ? p->eta : 0.05f;
+    ctx->eps = p->eps > 0 ? p->eps : 1e-2f;
+    ctx->rounding = p->rounding;
+    ctx->erwa_mode = p->erwa_mode;
+    ctx->time_limit = p->time_limit_s;
+    return FSMT_OK;
+}
+
+fsmt_status fsmt_begin(fsmt_ctx* ctx, uint32_t R, uint64_t seed, uint32_t restart_offset) {
+    fsmt_status s = need(ctx, 2, "fsmt_begin");
+    if (s) return s;
+    if (ctx->host_only) return fail(ctx, FSMT_ERR_CUDA, "fsmt_begin: host-only context has no device");
+    if (R == 0) return fail(ctx, FSMT_ERR_ARG, "restarts must be > 0");
+    cudaSetDevice(ctx->device);
+    drop_state(ctx);
+    const DevFormula& F = ctx->F;
+    DevState& S = ctx->S;
+    S.R = R;
+    auto alloc = [&](void** p, size_t bytes) -> fsmt_status {
+        cudaError_t e = cudaMalloc(p, std::max<size_t>(bytes, 16));
+        if (e != cudaSuccess) return fail(ctx, FSMT_ERR_OOM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+        ctx->sallocs.push_back(*p);
+        return FSMT_OK;
+    };
+    const size_t nb = (size_t)F.n_bool * R, nr = (size_t)F.n_real * R, nc = (size_t)F.n_cons * R;
+    const size_t parts = (size_t)update_parts(F);
+    if ((s = alloc((void**)&S.a, nb * 4)) || (s = alloc((void**)&S.b, nr * 4)) || (s = alloc((void**)&S.ga, nb * 8)) ||
+        (s = alloc((void**)&S.gb, nr * 8)) || (s = alloc((void**)&S.U, nc)) || (s = alloc((void**)&S.obj, (size_t)R * 8)) ||
+        (s = alloc((void**)&S.x, nb)) || (s = alloc((void**)&S.unsat, (size_t)R * 4)) ||
+        (s = alloc((void**)&S.frozen, R)) || (s = alloc((void**)&S.gm2, (size_t)R * 8)) ||
+        (s = alloc((void**)&S.gm2_part, std::max<size_t>(parts, 1) * R * 8))) {
+        drop_state(ctx);
+        return s;
+    }
+    CK(cudaMemsetAsync(S.U, 0, nc, ctx->stream));
+    CK(cudaMemsetAsync(S.frozen, 0, R, ctx->stream));
+    CK(cudaMemsetAsync(S.ga, 0, nb * 8, ctx->stream));
+    CK(cudaMemsetAsync(S.gb, 0, nr * 8, ctx->stream));
+    CK(cudaMemsetAsync(S.obj, 0, (size_t)R * 8, ctx->stream));
+    launch_init(F, S, seed, restart_offset, ctx->stream);
+    ctx->launches += 1;
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->seed = seed;
+    ctx->restart_offset = restart_offset;
+    ctx->stage = 3;
+    return FSMT_OK;
+}
+
+fsmt_status fsmt_set_state(fsmt_ctx* ctx, const float* a, const float* b, int where) {
+    fsmt_status s = need(ctx, 3, "fsmt_set_state");
+    if (s) return s;
+    if ((s = copy_in(ctx, ctx->S.a, a, (size_t)ctx->F.n_bool * ctx->S.R, where))) return s;
+    return copy_in(ctx, ctx->S.b, b, (size_t)ctx->F.n_real * ctx->S.R, where);
+}
+
+fsmt_status fsmt_get_state(fsmt_ctx* ctx, float* a, float* b, int where) {
+    fsmt_status s = need(ctx, 3, "fsmt_get_state");
+    if (s) return s;
+    if ((s = copy_out(ctx, a, ctx->S.a, (size_t)ctx->F.n_bool * ctx->S.R, where))) return s;
+    return copy_out(ctx, b, ctx->S.b, (size_t)ctx->F.n_real * ctx->S.R, where);
+}
+
+fsmt_status fsmt_set_counters(fsmt_ctx* ctx, const uint8_t* U, int where) {
+    fsmt_status s = need(ctx, 3, "fsmt_set_counters");
+    if (s) return s;
+    return copy_in(ctx, ctx->S.U, U, (size_t)ctx->F.n_cons * ctx->S.R, where);
+}
+
+fsmt_status fsmt_get_counters(fsmt_ctx* ctx, uint8_t* U, int where) {
+    fsmt_status s = need(ctx, 3, "fsmt_get_counters");
+    if (s) return s;
+    return copy_out(ctx, U, ctx->S.U, (size_t)ctx->F.n_cons * ctx->S.R, where);
+}
+
+static fsmt_status sweep_impl(fsmt_ctx* ctx, float kappa, uint32_t stage_t, double* terms, uint32_t terms_r) {
+    const DevFormula& F = ctx->F;
+    const DevState& S = ctx->S;
+    CK(cudaMemsetAsync(S.ga, 0, (size_t)F.n_bool * S.R * 8, ctx->stream));
+    CK(cudaMemsetAsync(S.gb, 0, (size_t)F.n_real * S.R * 8, ctx->stream));
+    CK(cudaMemsetAsync(S.obj, 0, (size_t)S.R * 8, ctx->stream));
+    {
+        Timed tm(ctx, 0);
+        launch_sweep(F, S, kappa, wscale_of(stage_t, ctx->erwa_mode), terms, terms_r, ctx->stream);
+    }
+    ctx->launches += 1;
+    return check_launch(ctx);
+}
+
+static fsmt_status update_impl(fsmt_ctx* ctx, float eta, float eps) {
+    {
+        Timed tm(ctx, 1);
+        launch_update(ctx->F, ctx->S, eta, eps, ctx->stream);
+    }
+    ctx->launches += 3;
+    return check_launch(ctx);
+}
+
+static fsmt_status stage_end_impl(fsmt_ctx* ctx, uint32_t stage_t) {
+    const DevState& S = ctx->S;
+    CK(cudaMemsetAsync(S.unsat, 0, (size_t)S.R * 4, ctx->stream));
+    {
+        Timed tm(ctx, 2);
+        launch_round(ctx->F, S, ctx->rounding, ctx->seed, ctx->restart_offset, stage_t, ctx->stream);
+        launch_verify(ctx->F, S, S.x, S.b, S.U, nullptr, ctx->stream);
+    }
+    CK(cudaMemsetAsync(S.frozen, 0, S.R, ctx->stream));
+    ctx->launches += 2;
+    fsmt_status s = check_launch(ctx);
+    if (s) return s;
+    ctx->rounded = true;
+    return FSMT_OK;
+}
+
+fsmt_status fsmt_sweep(fsmt_ctx* ctx, float kappa, uint32_t stage_t) {
+    fsmt_status s = need(ctx, 3, "fsmt_sweep");
+    if (s) return s;
+    if (!(kappa >= 0.f) || !std::isfinite(kappa)) return fail(ctx, FSMT_ERR_ARG, "kappa must be finite and >= 0");
+    if (stage_t == 0) stage_t = 1;
+    return sweep_impl(ctx, kappa, stage_t, nullptr, 0);
+}
+
+fsmt_status fsmt_get_sweep(fsmt_ctx* ctx, double* ga, double* gb, double* obj, int where) {
+    fsmt_status s = need(ctx, 3, "fsmt_get_sweep");
+    if (s) return s;
+    if ((s = copy_out(ctx, ga, ctx->S.ga, (size_t)ctx->F.n_bool * ctx->S.R, where))) return s;
+    if ((s = copy_out(ctx, gb, ctx->S.gb, (size_t)ctx->F.n_real * ctx->S.R, where))) return s;
+    return copy_out(ctx, obj, ctx->S.obj, (size_t)ctx->S.R, where);
+}
+
+fsmt_status fsmt_constraint_terms(fsmt_ctx* ctx, float kappa, uint32_t restart, double* E) {
+    fsmt_status s = need(ctx, 3, "fsmt_constraint_terms");
+    if (s) return s;
+    if (restart >= ctx->S.R || !E) return fail(ctx, FSMT_ERR_ARG, "bad restart / output");
+    if (!ctx->terms) CK(cudaMalloc((void**)&ctx->terms, std::max<size_t>((size_t)ctx->F.n_cons * 8, 8)));
+    if ((s = sweep_impl(ctx, kappa, 1, ctx->terms, restart))) return s;
+    return copy_out(ctx, E, ctx->terms, ctx->F.n_cons, FSMT_HOST);
+}
+
+fsmt_status fsmt_update(fsmt_ctx* ctx, float eta, float eps, double* gm2_out) {
+    fsmt_status s = need(ctx, 3, "fsmt_update");
+    if (s) return s;
+    if (!(eta > 0.f) || !(eps >= 0.f)) return fail(ctx, FSMT_ERR_ARG, "eta must be > 0 and eps >= 0");
+    if ((s = update_impl(ctx, eta, eps))) return s;
+    if (gm2_out) return copy_out(ctx, gm2_out, ctx->S.gm2, ctx->S.R, FSMT_HOST);
+    return FSMT_OK;
+}
+
+fsmt_status fsmt_stage_end(fsmt_ctx* ctx, uint32_t stage_t, uint32_t* unsat_out) {
+    fsmt_status s = need(ctx, 3, "fsmt_stage_end");
+    if (s) return s;
+    if (stage_t == 0) stage_t = 1;
+    if ((s = stage_end_impl(ctx, stage_t))) return s;
+    if (unsat_out) return copy_out(ctx, unsat_out, ctx->S.unsat, ctx->S.R, FSMT_HOST);
+    CK(cudaStreamSynchronize(ctx->stream));
+    return FSMT_OK;
+}
+
+fsmt_status fsmt_run_stage(fsmt_ctx* ctx, uint32_t stage_t, float kappa, uint32_t steps, uint32_t* unsat_out,
+                           uint32_t* min_unsat) {
+    fsmt_status s = need(ctx, 3, "fsmt_run_stage");
+    if (s) return s;
+    if (!(kappa >= 0.f) || !std::isfinite(kappa)) return fail(ctx, FSMT_ERR_ARG, "kappa must be finite and >= 0");
+    if (stage_t == 0) stage_t = 1;
+    CK(cudaMemsetAsync(ctx->S.frozen, 0, ctx->S.R, ctx->stream));
+    for (uint32_t k = 0; k < steps; ++k) {
+        if ((s = sweep_impl(ctx, kappa, stage_t, nullptr, 0))) return s;
+        if ((s = update_impl(ctx, ctx->eta, ctx->eps))) return s;
+    }
+    if ((s = stage_end_impl(ctx, stage_t))) return s;
+    if (unsat_out || min_unsat) {
+        std::vector<uint32_t> tmp;
+        uint32_t* u = unsat_out;
+        if (!u) {
+            tmp.resize(ctx->S.R);
+            u = tmp.data();
+        }
+        if ((s = copy_out(ctx, u, ctx->S.unsat, ctx->S.R, FSMT_HOST))) return s;
+        if (min_unsat) *min_unsat = *std::min_element(u, u + ctx->S.R);
+    } else {
+        CK(cudaStreamSynchronize(ctx->stream));
+    }
+    return FSMT_OK;
+}
+
+fsmt_status fsmt_set_timing(fsmt_ctx* ctx, int enable) {
+    if (!ctx) return FSMT_ERR_ARG;
+    if (ctx->host_only) return fail(ctx, FSMT_ERR_CUDA, "host-only context has no device");
+    ctx->timing = enable != 0;
+    return FSMT_OK;
+}
+
+fsmt_status fsmt_get_timing(fsmt_ctx* ctx, double* ms, uint64_t* count, int reset) {
+    if (!ctx) return FSMT_ERR_ARG;
+    if (ctx->host_only) return fail(ctx, FSMT_ERR_CUDA, "host-only context has no device");
+    timing_collect(ctx);
+    for (int k = 0; k < 3; ++k) {
+        if (ms) ms[k] = ctx->t_ms[k];
+        if (count) count[k] = ctx->t_cnt[k];
+        if (reset) {
+            ctx->t_ms[k] = 0;
+            ctx->t_cnt[k] = 0;
+        }
+    }
+    return FSMT_OK;
+}
+
+fsmt_status fsmt_get_model(fsmt_ctx* ctx, uint32_t r, int8_t* x_out, float* y_out) {
+    fsmt_status s = need(ctx, 3, "fsmt_get_model");
+    if (s) return s;
+    if (!ctx->rounded) return fail(ctx, FSMT_ERR_STATE, "fsmt_get_model: no stage_end yet");
+    const DevState& S = ctx->S;
+    if (r >= S.R) return fail(ctx, FSMT_ERR_ARG, "restart out of range");
+    if (x_out && ctx->F.n_bool)
+        CK(cudaMemcpy2DAsync(x_out, 1, S.x + r, S.R, 1, ctx->F.n_bool, cudaMemcpyDeviceToHost, ctx->stream));
+    if (y_out && ctx->F.n_real)
+        CK(cudaMemcpy2DAsync(y_out, 4, S.b + r, (size_t)S.R * 4, 4, ctx->F.n_real, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return FSMT_OK;
+}
+
+fsmt_status fsmt_get_rounded(fsmt_ctx* ctx, int8_t* x, int where) {
+    fsmt_status s = need(ctx, 3, "fsmt_get_rounded");
+    if (s) return s;
+    if (!ctx->rounded) return fail(ctx, FSMT_ERR_STATE, "fsmt_get_rounded: no stage_end yet");
+    return copy_out(ctx, x, ctx->S.x, (size_t)ctx->F.n_bool * ctx->S.R, where);
+}
+
+fsmt_status fsmt_verify(fsmt_ctx* ctx, const int8_t* x, const float* y, uint32_t* n_unsat, uint8_t* per_con) {
+    fsmt_status s = need(ctx, 2, "fsmt_verify");
+    if (s) return s;
+    if ((!x && ctx->f.n_bool) || (!y && ctx->f.n_real) || !n_unsat) return fail(ctx, FSMT_ERR_ARG, "null argument");
+    *n_unsat = verify_host(ctx->f, ctx->b, x, y, per_con);
+    return FSMT_OK;
+}
+
+fsmt_status fsmt_verify_batch(fsmt_ctx* ctx, uint32_t R, const int8_t* x, const float* y, int where,
+                              uint32_t* unsat_out, uint8_t* per_con) {
+    fsmt_status s = need(ctx, 2, "fsmt_verify_batch");
+    if (s) return s;
+    if (ctx->host_only) return fail(ctx, FSMT_ERR_CUDA, "fsmt_verify_batch: host-only context has no device");
+    if (R == 0 || !unsat_out) return fail(ctx, FSMT_ERR_ARG, "bad arguments");
+    cudaSetDevice(ctx->device);
+    const DevFormula& F = ctx->F;
+    DevState T{};
+    T.R = R;
+    int8_t* dx = nullptr;
+    float* dy = nullptr;
+    uint8_t* dpc = nullptr;
+    std::vector<void*> tmp;
+    auto alloc = [&](void** p, size_t bytes) -> bool {
+        if (cudaMalloc(p, std::max<size_t>(bytes, 16)) != cudaSuccess) return false;
+        tmp.push_back(*p);
+        return true;
+    };
+    const size_t nb = (size_t)F.n_bool * R, nr = (size_t)F.n_real * R, nc = (size_t)F.n_cons * R;
+    if (!alloc((void**)&dx, nb) || !alloc((void**)&dy, nr * 4) || !alloc((void**)&T.unsat, (size_t)R * 4) ||
+        (per_con && !alloc((void**)&dpc, nc))) {
+        free_list(tmp);
+        return fail(ctx, FSMT_ERR_OOM, "cudaMalloc failed in fsmt_verify_batch");
+    }
+    cudaMemcpyKind k = where == FSMT_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    cudaError_t e = cudaSuccess;
+    if (nb) e = cudaMemcpyAsync(dx, x, nb, k, ctx->stream);
+    if (e == cudaSuccess && nr) e = cudaMemcpyAsync(dy, y, nr * 4, k, ctx->stream);
+    if (e == cudaSuccess) e = cudaMemsetAsync(T.unsat, 0, (size_t)R * 4, ctx->stream);
+    if (e == cudaSuccess) {
+        launch_verify(F, T, dx, dy, nullptr, dpc, ctx->stream);
+        ctx->launches += 1;
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpyAsync(unsat_out, T.unsat, (size_t)R * 4, cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess && per_con) e = cudaMemcpyAsync(per_con, dpc, nc, cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    free_list(tmp);
+    if (e != cudaSuccess) return fail(ctx, FSMT_ERR_CUDA, std::string("fsmt_verify_batch: ") + cudaGetErrorString(e));
+    return FSMT_OK;
+}
+
+fsmt_status fsmt_solve(fsmt_ctx* ctx, uint32_t restarts, uint32_t steps, uint64_t seed, fsmt_verdict* verdict,
+                       int8_t* x_out, float* y_out, fsmt_stats* stats) {
+    fsmt_status s = need(ctx, 2, "fsmt_solve");
+    if (s) return s;
+    if (ctx->host_only) return fail(ctx, FSMT_ERR_CUDA, "fsmt_solve: host-only context has no device");
+    if (!verdict || restarts == 0) return fail(ctx, FSMT_ERR_ARG, "bad arguments");
+    auto t0 = std::chrono::steady_clock::now();
+    if ((s = fsmt_begin(ctx, restarts, seed, 0))) return s;
+    const uint32_t nbool = ctx->F.n_bool, nreal = ctx->F.n_real;
+    std::vector<uint32_t> unsat(restarts);
+    std::vector<int8_t> bx(nbool), cx(nbool);
+    std::vector<float> by(nreal), cy(nreal);
+    uint32_t best_unsat = UINT32_MAX, best_stage = 0, best_r = 0;
+    uint32_t stages = 0, steps_run = 0;
+    bool sat = false, timeout = false;
+    fsmt_stats st{};
+    for (uint32_t t = 1; t <= ctx->kappas.size(); ++t) {
+        const float kappa = ctx->kappas[t - 1];
+        if ((s = fsmt_run_stage(ctx, t, kappa, steps, unsat.data(), nullptr))) return s;
+        steps_run += steps;
+        ++stages;
+        // lowest restart with unsat == 0 wins (smallest (t, r)); else track min (unsat, t, r)
+        uint32_t r_min = 0;
+        for (uint32_t r = 1; r < restarts; ++r)
+            if (unsat[r] < unsat[r_min]) r_min = r;
+        if (unsat[r_min] < best_unsat) {
+            if ((s = fsmt_get_model(ctx, r_min, cx.data(), cy.data()))) return s;
+            uint32_t host_unsat = verify_host(ctx->f, ctx->b, cx.data(), cy.data(), nullptr);
+            if (unsat[r_min] == 0 && host_unsat != 0)
+                return fail(ctx, FSMT_ERR_CUDA, "device verdict SAT contradicted by host re-verification");
+            best_unsat = unsat[r_min];
+            best_stage = t;
+            best_r = r_min;
+            bx = cx;
+            by = cy;
+            st.host_verified = host_unsat == unsat[r_min];
+        }
+        if (best_unsat == 0) {
+            sat = true;
+            break;
+        }
+        double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if (ctx->time_limit > 0 && el > ctx->time_limit) {
+            timeout = true;
+            break;
+        }
+    }
+    *verdict = sat ? FSMT_SAT : FSMT_UNKNOWN;
+    if (x_out) std::copy(bx.begin(), bx.end(), x_out);
+    if (y_out) std::copy(by.begin(), by.end(), y_out);
+    if (stats) {
+        st.stages_run = stages;
+        st.steps_run = steps_run;
+        st.winner_restart = best_r;
+        st.winner_stage = best_stage;
+        st.best_unsat = best_unsat;
+        st.solve_ms = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() * 1e3;
+        st.evals = (double)steps_run * (double)ctx->F.n_cons * (double)restarts;
+        *stats = st;
+    }
+    return timeout ? FSMT_ERR_TIMEOUT : FSMT_OK;
+}
+
+uint64_t fsmt_kernel_launches(const fsmt_ctx* ctx) { return ctx ? ctx->launches : 0; }
+uint32_t fsmt_restarts(const fsmt_ctx* ctx) { return ctx && ctx->stage >= 3 ? ctx->S.R : 0; }
+
+fsmt_status fsmt_device_buffers(fsmt_ctx* ctx, void** a, void** b, void** ga, void** gb, void** U, void** obj,
+                                void** unsat) {
+    fsmt_status s = need(ctx, 3, "fsmt_device_buffers");
+    if (s) return s;
+    if (a) *a = ctx->S.a;
+    if (b) *b = ctx->S.b;
+    if (ga) *ga = ctx->S.ga;
+    if (gb) *gb = ctx->S.gb;
+    if (U) *U = ctx->S.U;
+    if (obj) *obj = ctx->S.obj;
+    if (unsat) *unsat = ctx->S.unsat;
+    return FSMT_OK;
+}
+
+fsmt_status fsmt_time_sweep(fsmt_ctx* ctx, float kappa, uint32_t stage_t, uint32_t iters, double* ms_out) {
+    fsmt_status s = need(ctx, 3, "fsmt_time_sweep");
+    if (s) return s;
+    if (!ms_out || iters == 0) return fail(ctx, FSMT_ERR_ARG, "bad arguments");
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    float total = 0.f;
+    for (uint32_t i = 0; i < iters; ++i) {
+        CK(cudaMemsetAsync(ctx->S.ga, 0, (size_t)ctx->F.n_bool * ctx->S.R * 8, ctx->stream));
+        CK(cudaMemsetAsync(ctx->S.gb, 0, (size_t)ctx->F.n_real * ctx->S.R * 8, ctx->stream));
+        CK(cudaMemsetAsync(ctx->S.obj, 0, (size_t)ctx->S.R * 8, ctx->stream));
+        CK(cudaEventRecord(e0, ctx->stream));
+        launch_sweep(ctx->F, ctx->S, kappa, wscale_of(stage_t, ctx->erwa_mode), nullptr, 0, ctx->stream);
+        CK(cudaEventRecord(e1, ctx->stream));
+        ctx->launches += 1;
+        CK(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        total += ms;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *ms_out = total / iters;
+    return check_launch(ctx);
+}
+
+}  // extern "C"

@@ -1,0 +1,106 @@
+// Internal data model of the FourierSMT core (host side).  See include/fsmt.h for the ABI.
+// P:n = PAPER.md line n, S:n = SPEC.md line n, R<k> = DESIGN.md §3 reading k.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace fsmt {
+
+// Truth encoding: -1 = True. Terminal ids in the canonical xBDD numbering (R7).
+constexpr int kFalse = -1;
+constexpr int kTrue = -2;
+
+struct ParseError {
+    int line, col;
+    std::string msg;
+    bool unsupported;  // maps to FSMT_ERR_UNSUPPORTED ('=' atoms, bad weights)
+};
+
+// Expression pool node: op in {LIT, AND, OR, XOR, NOT}; LIT: kind 0 = Boolean var, 1 = atom.
+enum ExprOp : uint8_t { OP_LIT = 0, OP_AND = 1, OP_OR = 2, OP_XOR = 3, OP_NOT = 4 };
+struct ExprNode {
+    uint8_t op;
+    uint8_t kind;     // LIT only
+    uint32_t idx;     // LIT only
+    uint32_t first;   // first child index in Formula::kids (AND/OR/XOR/NOT)
+    uint32_t n;       // number of children
+};
+
+enum ConsKind : uint8_t { K_OR = 0, K_CARD = 1, K_NAE = 2, K_XOR = 3, K_EXPR = 4 };
+struct Lit {
+    uint8_t kind;     // 0 Boolean, 1 atom
+    uint8_t neg;
+    uint32_t idx;
+};
+struct Constraint {
+    uint8_t kind;
+    uint32_t k;           // CARD threshold: sat iff #true <= k
+    uint32_t lit_first;   // symmetric: literals in Formula::lits
+    uint32_t lit_n;
+    uint32_t expr_root;   // K_EXPR: root node in Formula::expr
+    double weight;
+};
+
+// Canonical atoms q.y <= q0 / q.y < q0, CSR over reals.
+struct Formula {
+    uint32_t n_bool = 0, n_real = 0;
+    std::vector<uint32_t> atom_rowptr{0};
+    std::vector<uint32_t> atom_col;
+    std::vector<double> atom_val;
+    std::vector<double> atom_rhs;
+    std::vector<uint8_t> atom_strict;
+    std::vector<Constraint> cons;
+    std::vector<Lit> lits;
+    std::vector<ExprNode> expr;
+    std::vector<uint32_t> kids;
+    uint32_t n_atoms() const { return (uint32_t)atom_rhs.size(); }
+};
+
+// Parses HSMT. Throws ParseError.
+Formula parse_hsmt(const char* text, size_t len);
+
+// Decision node of a template: level = slot position; hi = slot literal True.
+struct TNode {
+    uint16_t level;
+    int16_t hi;
+    int16_t lo;
+    uint16_t pad;
+};
+
+struct Template {
+    std::vector<uint8_t> kinds;   // per slot: 0 Boolean, 1 atom
+    std::vector<TNode> nodes;     // canonical numbering (R7)
+    int root;                     // node id, or kFalse / kTrue for constant constraints
+};
+
+struct Built {
+    std::vector<Template> tmpls;
+    std::vector<uint32_t> cons_tmpl;       // [C]
+    std::vector<uint32_t> cons_slot_off;   // [C+1]
+    std::vector<uint32_t> slot_ids;        // global var / atom ids, per constraint slot
+    std::vector<float> cons_w;             // [C] base weights w_c (Alg.2 input)
+    std::vector<float> lo, hi;             // projection bounds (R15), f32
+    uint32_t max_slots = 0, max_nodes = 0, n_bounded = 0;
+    uint64_t n_nodes = 0;
+};
+
+struct BuildError {
+    std::string msg;
+    bool budget;
+};
+
+// Compiles every constraint (a0 of SURVEY §8(a)). Throws BuildError.
+Built build_xbdds(const Formula& f, uint64_t node_budget);
+
+// Exact fp64 check of one atom at y (R22): s = 0; s += q_j*y_j in stored order; s <= q0 (< q0 strict).
+bool eval_atom_exact(const Formula& f, uint32_t atom, const float* y, size_t stride);
+
+// Host exact check of a full model (used as the host re-verification of fsmt_solve).
+uint32_t verify_host(const Formula& f, const Built& b, const int8_t* x, const float* y, uint8_t* per_con);
+
+std::string dump_templates_jsonl(const Built& b);
+std::vector<uint8_t> dump_constraints_bin(const Built& b);
+
+}  // namespace fsmt

@@ -1,0 +1,356 @@
+// sm_100a kernels of the FourierSMT hot path.
+//
+//   K0 k0_init    Philox init of (a, b) + projection            (R20; Def.1)
+//   K1 k1_sweep   slot probabilities + Gaussian smoothing (Eq.4, Eq.7), forward xBDD pass
+//                 (Alg.F), backward pass (Alg.B, sign R1), chain rule
+//                 (P:1326-1327), weighted objective and gradient accumulation (Eq.10)
+//   K3 k3_*       projected gradient step, gradient mapping, eps-freeze (Eq.11-14)
+//   K4 k4_round   x = sgn(a) | R(a) (Alg.1 line 10; Eq.4; R17)
+//   K5 k5_verify  exact check of every constraint (R22) + ERWA violation counters (R18)
+//
+// Layout: restart-minor; a warp's 32 lanes are 32 restarts of the same constraint, so every
+// structure load is warp-uniform (one transaction, broadcast) and every state load/store is
+// a coalesced 128 B row segment.  No tensor cores: nothing here is a dense contraction.
+#include <cmath>
+#include <cstdio>
+
+#include "kernels.hpp"
+
+namespace fsmt {
+namespace {
+
+constexpr int kFalseT = -1;
+constexpr int kTrueT = -2;
+constexpr int kChunk = 16;        // constraints per warp in K1 / K5
+
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
+#pragma unroll
+    for (int i = 0; i < 10; ++i) {
+        const uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+        const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+        c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+        k.x += 0x9E3779B9u;
+        k.y += 0xBB67AE85u;
+    }
+    return c;
+}
+
+__device__ __forceinline__ uint32_t draw24(uint64_t seed, uint32_t r, uint32_t var, uint32_t stage, uint32_t tag) {
+    const uint4 o = philox4x32_10(make_uint4(r, var, stage, tag), make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)));
+    return o.x >> 8;
+}
+
+// ---------------------------------------------------------------------------------------- K0
+
+__global__ void k0_init(DevFormula F, DevState S, uint64_t seed, uint32_t off) {
+    const uint64_t n = (uint64_t)(F.n_bool + F.n_real) * S.R;
+    for (uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t v = (uint32_t)(idx / S.R), r = (uint32_t)(idx % S.R);
+        if (v < F.n_bool) {
+            const uint32_t k = draw24(seed, off + r, v, 0, 0);
+            const float a = (float)((int32_t)(2u * k + 1u) - (1 << 24)) * 0x1p-24f;   // exact (R20)
+            S.a[(size_t)v * S.R + r] = fminf(fmaxf(a, -1.f), 1.f);
+        } else {
+            const uint32_t j = v - F.n_bool;
+            const uint32_t k = draw24(seed, off + r, j, 0, 1);
+            const double u = (double)(2u * k + 1u) * 0x1p-25;
+            const float lo = F.lo[j], hi = F.hi[j];
+            double val;
+            if (isfinite(lo) && isfinite(hi))
+                val = __dadd_rn((double)lo, __dmul_rn(__dsub_rn((double)hi, (double)lo), u));
+            else
+                val = __dsub_rn(__dmul_rn(2.0, u), 1.0);
+            S.b[(size_t)j * S.R + r] = fminf(fmaxf(__double2float_rn(val), lo), hi);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------------------- K1
+
+__global__ void __launch_bounds__(256) k1_sweep(DevFormula F, DevState S, float kappa, float wscale,
+                                                double* __restrict__ terms, uint32_t terms_r, int smax, int nmax) {
+    extern __shared__ float smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t R = S.R;
+    const uint32_t rtiles = (R + 31) / 32;
+    const uint64_t gw = (uint64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+    const uint32_t rt = (uint32_t)(gw % rtiles);
+    const uint64_t c0 = (gw / rtiles) * kChunk;
+    if (c0 >= F.n_cons) return;
+    const uint64_t c1 = min(c0 + (uint64_t)kChunk, (uint64_t)F.n_cons);
+    const uint32_t r = rt * 32 + lane;
+    const bool live = r < R;
+    const size_t rr = live ? r : 0;
+    float* PT = smem + (size_t)warp * (4 * smax + nmax) * 32;   // P[slot True]   (Eq.4 / Eq.7)
+    float* PF = PT + smax * 32;                                   // P[slot False]
+    float* DD = PF + smax * 32;                                   // dd/dz' factor for atom slots
+    float* G = DD + smax * 32;                                    // dE/dv per slot
+    float* M = G + smax * 32;                                     // m_td, then m_bu (in place)
+    const float kq = kappa * 0.70710678118654752f;               // kappa / sqrt(2)
+    const float dcoef = kappa * 0.79788456080286536f;            // kappa * sqrt(2/pi)
+    double objacc = 0.0;
+    for (uint64_t c = c0; c < c1; ++c) {
+        const uint32_t tid = F.cons_tmpl[c];
+        const uint32_t so = F.cons_slot_off[c];
+        const uint32_t ns = F.cons_slot_off[c + 1] - so;
+        const uint32_t ko = F.tmpl_kind_off[tid];
+        const uint32_t no = F.tmpl_node_off[tid];
+        const uint32_t nn = F.tmpl_node_off[tid + 1] - no;
+        const int root = F.tmpl_root[tid];
+        float w = F.cons_w[c] * wscale;                               // w_cr = w_c 2^(U + e_t)  (R18)
+        if (S.U) w = ldexpf(w, (int)S.U[(size_t)c * R + rr]);
+        // a1: slot probabilities (Eq.4 for Booleans, Eq.7 for atoms; erfc form, R28b)
+        for (uint32_t s = 0; s < ns; ++s) {
+            const uint32_t gid = F.slot_ids[so + s];
+            float pt, pf, dd = 0.f;
+            if (F.kinds[ko + s] == 0) {
+                const float v = S.a[(size_t)gid * R + rr];
+                pt = 0.5f * (1.f - v);
+                pf = 0.5f * (1.f + v);
+            } else {
+                const uint32_t k0 = F.atom_rowptr[gid], k1 = F.atom_rowptr[gid + 1];
+                float z = -F.atom_rhs[gid];
+                for (uint32_t k = k0; k < k1; ++k) z = fmaf(F.atom_val[k], S.b[(size_t)F.atom_col[k] * R + rr], z);
+                const float inv = F.atom_invnorm[gid];
+                const float u = kq * z * inv;                           // z / (sqrt2 ||q|| sigma)
+                pt = 0.5f * erfcf(u);                                   // (1 - d)/2, d = erf(u)
+                pf = 0.5f * erfcf(-u);                                  // (1 + d)/2
+                dd = dcoef * inv * expf(-u * u);                        // dd/db_j = dd * q_j
+            }
+            PT[s * 32 + lane] = pt;
+            PF[s * 32 + lane] = pf;
+            DD[s * 32 + lane] = dd;
+            G[s * 32 + lane] = 0.f;
+        }
+        // a2: forward pass, Alg.F: m_td[root] = 1; m_td[v.t] += p m_td[v]; m_td[v.f] += (1-p) m_td[v]
+        for (uint32_t v = 0; v < nn; ++v) M[v * 32 + lane] = 0.f;
+        float pT = (root == kTrueT) ? 1.f : 0.f;
+        if (root >= 0) M[root * 32 + lane] = 1.f;
+        for (uint32_t v = 0; v < nn; ++v) {
+            const DevNode nd = F.nodes[no + v];
+            const float m = M[v * 32 + lane];
+            const float th = PT[nd.level * 32 + lane] * m;
+            const float tl = PF[nd.level * 32 + lane] * m;
+            if (nd.hi >= 0) M[nd.hi * 32 + lane] += th; else if (nd.hi == kTrueT) pT += th;
+            if (nd.lo >= 0) M[nd.lo * 32 + lane] += tl; else if (nd.lo == kTrueT) pT += tl;
+        }
+        const float E = 1.f - 2.f * pT;                               // Alg.F line P:1170
+        // a3: backward pass, Alg.B: m_bu[T]=1, m_bu[F]=0, m_bu[v] = p m_bu[v.t] + (1-p) m_bu[v.f];
+        //     dE/dv_s = sum_{v: slot s} m_td[v] (m_bu[v.t] - m_bu[v.f])     (R1)
+        for (int v = (int)nn - 1; v >= 0; --v) {
+            const DevNode nd = F.nodes[no + v];
+            const float bh = nd.hi >= 0 ? M[nd.hi * 32 + lane] : (nd.hi == kTrueT ? 1.f : 0.f);
+            const float bl = nd.lo >= 0 ? M[nd.lo * 32 + lane] : (nd.lo == kTrueT ? 1.f : 0.f);
+            const float mt = M[v * 32 + lane];
+            G[nd.level * 32 + lane] += mt * (bh - bl);
+            M[v * 32 + lane] = PT[nd.level * 32 + lane] * bh + PF[nd.level * 32 + lane] * bl;
+        }
+        // a4: chain rule + accumulate (fp64, R28)
+        if (live) {
+            for (uint32_t s = 0; s < ns; ++s) {
+                const uint32_t gid = F.slot_ids[so + s];
+                const float g = w * G[s * 32 + lane];
+                if (F.kinds[ko + s] == 0) {
+                    atomicAdd(&S.ga[(size_t)gid * R + r], (double)g);
+                } else {
+                    const float gd = g * DD[s * 32 + lane];
+                    for (uint32_t k = F.atom_rowptr[gid]; k < F.atom_rowptr[gid + 1]; ++k)
+                        atomicAdd(&S.gb[(size_t)F.atom_col[k] * R + r], (double)(gd * F.atom_val[k]));
+                }
+            }
+            objacc += (double)w * (double)E;
+            if (terms != nullptr && r == terms_r) terms[c] = (double)E;
+        }
+    }
+    if (live) atomicAdd(&S.obj[r], objacc);
+}
+
+// ---------------------------------------------------------------------------------------- K3
+
+constexpr int kVarsPerPart = 64;
+
+__device__ __forceinline__ float step_value(float x, double g, float eta, float lo, float hi) {
+    double t = (double)x - (double)eta * g;
+    t = fmin(fmax(t, (double)lo), (double)hi);
+    return __double2float_rn(t);
+}
+
+__global__ void k3_norm(DevFormula F, DevState S, float eta) {
+    const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= S.R) return;
+    const uint32_t part = blockIdx.y;
+    const uint32_t nv = F.n_bool + F.n_real;
+    const uint32_t v0 = part * kVarsPerPart, v1 = min(v0 + kVarsPerPart, nv);
+    double acc = 0.0;
+    for (uint32_t v = v0; v < v1; ++v) {
+        float x, xn;
+        if (v < F.n_bool) {
+            x = S.a[(size_t)v * S.R + r];
+            xn = step_value(x, S.ga[(size_t)v * S.R + r], eta, -1.f, 1.f);
+        } else {
+            const uint32_t j = v - F.n_bool;
+            x = S.b[(size_t)j * S.R + r];
+            xn = step_value(x, S.gb[(size_t)j * S.R + r], eta, F.lo[j], F.hi[j]);
+        }
+        const double d = ((double)x - (double)xn) / (double)eta;
+        acc += d * d;
+    }
+    S.gm2_part[(size_t)part * S.R + r] = acc;
+}
+
+__global__ void k3_final(DevState S, uint32_t n_parts, float eps) {
+    const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= S.R) return;
+    double acc = 0.0;
+    for (uint32_t p = 0; p < n_parts; ++p) acc += S.gm2_part[(size_t)p * S.R + r];
+    S.gm2[r] = acc;
+    if (!S.frozen[r] && acc <= (double)eps * (double)eps) S.frozen[r] = 1;   // Eq.14
+}
+
+__global__ void k3_apply(DevFormula F, DevState S, float eta) {
+    const uint64_t n = (uint64_t)(F.n_bool + F.n_real) * S.R;
+    for (uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t v = (uint32_t)(idx / S.R), r = (uint32_t)(idx % S.R);
+        if (S.frozen[r]) continue;
+        if (v < F.n_bool) {
+            float& x = S.a[(size_t)v * S.R + r];
+            x = step_value(x, S.ga[(size_t)v * S.R + r], eta, -1.f, 1.f);
+        } else {
+            const uint32_t j = v - F.n_bool;
+            float& x = S.b[(size_t)j * S.R + r];
+            x = step_value(x, S.gb[(size_t)j * S.R + r], eta, F.lo[j], F.hi[j]);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------------------- K4
+
+__global__ void k4_round(DevFormula F, DevState S, uint32_t rounding, uint64_t seed, uint32_t off, uint32_t stage) {
+    const uint64_t n = (uint64_t)F.n_bool * S.R;
+    for (uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t i = (uint32_t)(idx / S.R), r = (uint32_t)(idx % S.R);
+        const float a = S.a[idx];
+        bool is_true;
+        if (rounding == 0) {
+            is_true = a < 0.f;                                    // sgn(0) = +1
+        } else {
+            const uint32_t k = draw24(seed, off + r, i, stage, 2);
+            is_true = a < 1.f - (float)k * 0x1p-23f;              // P[x=-1] = (1-a)/2 (Eq.4)
+        }
+        S.x[idx] = is_true ? (int8_t)-1 : (int8_t)1;
+    }
+}
+
+// ---------------------------------------------------------------------------------------- K5
+
+__global__ void __launch_bounds__(256) k5_verify(DevFormula F, DevState S, const int8_t* __restrict__ x,
+                                                 const float* __restrict__ y, uint8_t* __restrict__ Uupd,
+                                                 uint8_t* __restrict__ per_con) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t R = S.R;
+    const uint32_t rtiles = (R + 31) / 32;
+    const uint64_t gw = (uint64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+    const uint32_t rt = (uint32_t)(gw % rtiles);
+    const uint64_t c0 = (gw / rtiles) * kChunk;
+    if (c0 >= F.n_cons) return;
+    const uint64_t c1 = min(c0 + (uint64_t)kChunk, (uint64_t)F.n_cons);
+    const uint32_t r = rt * 32 + lane;
+    if (r >= R) return;
+    uint32_t cnt = 0;
+    for (uint64_t c = c0; c < c1; ++c) {
+        const uint32_t tid = F.cons_tmpl[c];
+        const uint32_t so = F.cons_slot_off[c];
+        const uint32_t ko = F.tmpl_kind_off[tid];
+        const uint32_t no = F.tmpl_node_off[tid];
+        int v = F.tmpl_root[tid];
+        while (v >= 0) {
+            const DevNode nd = F.nodes[no + v];
+            const uint32_t gid = F.slot_ids[so + nd.level];
+            bool truth;
+            if (F.kinds[ko + nd.level] == 0) {
+                truth = x[(size_t)gid * R + r] == -1;
+            } else {                                          // exact fp64, stored order, no FMA (R22)
+                double s = 0.0;
+                for (uint32_t k = F.atom_rowptr[gid]; k < F.atom_rowptr[gid + 1]; ++k)
+                    s = __dadd_rn(s, __dmul_rn(F.atom_val64[k], (double)y[(size_t)F.atom_col[k] * R + r]));
+                truth = F.atom_strict[gid] ? (s < F.atom_rhs64[gid]) : (s <= F.atom_rhs64[gid]);
+            }
+            v = truth ? nd.hi : nd.lo;
+        }
+        const uint32_t u = (v == kFalseT) ? 1u : 0u;            // u_c = f_c/2 + 1/2 (Alg.2 line 7)
+        cnt += u;
+        if (Uupd) {
+            uint8_t& cell = Uupd[(size_t)c * R + r];
+            cell = (uint8_t)min(255u, (uint32_t)cell + u);
+        }
+        if (per_con) per_con[(size_t)c * R + r] = (uint8_t)u;
+    }
+    atomicAdd(&S.unsat[r], cnt);
+}
+
+
+}  // namespace
+
+int sweep_smem_bytes(const DevFormula& F, int warps) {
+    const int smax = (int)F.max_slots > 0 ? (int)F.max_slots : 1;
+    const int nmax = (int)F.max_nodes > 0 ? (int)F.max_nodes : 1;
+    return warps * (4 * smax + nmax) * 32 * (int)sizeof(float);
+}
+
+static int sweep_warps(const DevFormula& F) {
+    for (int w = 8; w >= 1; w >>= 1)
+        if (sweep_smem_bytes(F, w) <= 110 * 1024) return w;
+    return 1;
+}
+
+void launch_init(const DevFormula& F, const DevState& S, uint64_t seed, uint32_t off, cudaStream_t st) {
+    const uint64_t n = (uint64_t)(F.n_bool + F.n_real) * S.R;
+    const int threads = 256;
+    const uint64_t blocks = std::min<uint64_t>((n + threads - 1) / threads, 148ull * 16);
+    if (n) k0_init<<<(unsigned)std::max<uint64_t>(blocks, 1), threads, 0, st>>>(F, S, seed, off);
+}
+
+void launch_sweep(const DevFormula& F, const DevState& S, float kappa, float wscale, double* terms, uint32_t terms_r,
+                  cudaStream_t st) {
+    if (F.n_cons == 0 || S.R == 0) return;
+    const int warps = sweep_warps(F);
+    const int smem = sweep_smem_bytes(F, warps);
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k1_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    const uint64_t chunks = (F.n_cons + kChunk - 1) / kChunk;
+    const uint64_t nw = chunks * ((S.R + 31) / 32);
+    const uint64_t blocks = (nw + warps - 1) / warps;
+    k1_sweep<<<(unsigned)blocks, warps * 32, smem, st>>>(F, S, kappa, wscale, terms, terms_r,
+                                                         std::max<int>(1, F.max_slots), std::max<int>(1, F.max_nodes));
+}
+
+int update_parts(const DevFormula& F) { return (int)((F.n_bool + F.n_real + kVarsPerPart - 1) / kVarsPerPart); }
+
+void launch_update(const DevFormula& F, const DevState& S, float eta, float eps, cudaStream_t st) {
+    const uint32_t parts = (uint32_t)update_parts(F);
+    if (parts == 0 || S.R == 0) return;
+    dim3 g1((S.R + 127) / 128, parts);
+    k3_norm<<<g1, 128, 0, st>>>(F, S, eta);
+    k3_final<<<(S.R + 127) / 128, 128, 0, st>>>(S, parts, eps);
+    const uint64_t n = (uint64_t)(F.n_bool + F.n_real) * S.R;
+    const uint64_t blocks = std::min<uint64_t>((n + 255) / 256, 148ull * 16);
+    k3_apply<<<(unsigned)blocks, 256, 0, st>>>(F, S, eta);
+}
+
+void launch_round(const DevFormula& F, const DevState& S, uint32_t rounding, uint64_t seed, uint32_t off,
+                  uint32_t stage, cudaStream_t st) {
+    const uint64_t n = (uint64_t)F.n_bool * S.R;
+    if (!n) return;
+    const uint64_t blocks = std::min<uint64_t>((n + 255) / 256, 148ull * 16);
+    k4_round<<<(unsigned)blocks, 256, 0, st>>>(F, S, rounding, seed, off, stage);
+}
+
+void launch_verify(const DevFormula& F, const DevState& S, const int8_t* x, const float* y, uint8_t* U_update,
+                   uint8_t* per_con, cudaStream_t st) {
+    if (F.n_cons == 0 || S.R == 0) return;
+    const uint64_t chunks = (F.n_cons + kChunk - 1) / kChunk;
+    const uint64_t nw = chunks * ((S.R + 31) / 32);
+    const uint64_t blocks = (nw + 7) / 8;
+    k5_verify<<<(unsigned)blocks, 256, 0, st>>>(F, S, x, y, U_update, per_con);
+}
+
+}  // namespace fsmt

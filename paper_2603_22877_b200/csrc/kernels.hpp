@@ -1,0 +1,74 @@
+// Device-side data structures and kernel launchers (K0-K5) of the FourierSMT hot path.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace fsmt {
+
+struct DevNode {          // = TNode (8 bytes): level, hi, lo (-1 FALSE, -2 TRUE), pad
+    uint16_t level;
+    int16_t hi;
+    int16_t lo;
+    uint16_t pad;
+};
+
+// Read-only formula structure in HBM (SoA).
+struct DevFormula {
+    uint32_t n_bool, n_real, n_cons, n_atoms;
+    uint32_t max_slots, max_nodes;
+    const uint32_t* cons_tmpl;      // [C]
+    const uint32_t* cons_slot_off;  // [C+1]
+    const uint32_t* slot_ids;       // [sum slots]
+    const float* cons_w;            // [C]
+    const uint32_t* tmpl_node_off;  // [T+1]
+    const DevNode* nodes;           // [sum template nodes]
+    const uint32_t* tmpl_kind_off;  // [T+1]
+    const uint8_t* kinds;           // [sum template slots]
+    const int32_t* tmpl_root;       // [T]
+    const uint32_t* atom_rowptr;    // [K+1]
+    const uint32_t* atom_col;       // [nnz]
+    const float* atom_val;          // [nnz] f32 (smoothing)
+    const double* atom_val64;       // [nnz] f64 (exact check, R22)
+    const float* atom_rhs;          // [K]
+    const double* atom_rhs64;       // [K]
+    const uint8_t* atom_strict;     // [K]
+    const float* atom_invnorm;      // [K] 1/||q_i||
+    const float* lo;                // [n_real]
+    const float* hi;                // [n_real]
+};
+
+// Per-restart state, restart-minor (row = variable / constraint).
+struct DevState {
+    uint32_t R;
+    float* a;          // [n_bool][R]
+    float* b;          // [n_real][R]
+    double* ga;        // [n_bool][R]
+    double* gb;        // [n_real][R]
+    uint8_t* U;        // [C][R]
+    double* obj;       // [R]
+    int8_t* x;         // [n_bool][R]
+    uint32_t* unsat;   // [R]
+    uint8_t* frozen;   // [R]
+    double* gm2;       // [R]
+    double* gm2_part;  // [n_parts][R]
+};
+
+int sweep_smem_bytes(const DevFormula& F, int warps);
+
+// K0: Philox init (R20) + projection.
+void launch_init(const DevFormula& F, const DevState& S, uint64_t seed, uint32_t restart_offset, cudaStream_t st);
+// K1: forward/backward xBDD sweep, objective + gradient (fp64 accumulation).
+void launch_sweep(const DevFormula& F, const DevState& S, float kappa, float wscale, double* terms, uint32_t terms_r,
+                  cudaStream_t st);
+// K3: projected step (three launches: partial norms, finalize, apply).
+int update_parts(const DevFormula& F);
+void launch_update(const DevFormula& F, const DevState& S, float eta, float eps, cudaStream_t st);
+// K4: rounding (R17).
+void launch_round(const DevFormula& F, const DevState& S, uint32_t rounding, uint64_t seed, uint32_t restart_offset,
+                  uint32_t stage, cudaStream_t st);
+// K5: exact verification + ERWA counter update (R18, R22).
+void launch_verify(const DevFormula& F, const DevState& S, const int8_t* x, const float* y, uint8_t* U_update,
+                   uint8_t* per_con, cudaStream_t st);
+
+}  // namespace fsmt

@@ -1,0 +1,218 @@
+"""Thin Python face of the C ABI (include/fsmt.h): same names, argument marshalling only."""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import native as N
+
+
+@dataclass
+class SolveResult:
+    verdict: int            # N.SAT (10) or N.UNKNOWN (0)
+    x: np.ndarray           # int8 [n_bool], -1 = True
+    y: np.ndarray           # float32 [n_real]
+    stats: dict
+
+
+class Solver:
+    """One fsmt_ctx.  device=-1 gives a host-only context (parse / build / dump / host verify)."""
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        s = N.lib.fsmt_create(int(device), C.byref(h))
+        if s != N.OK:
+            raise N.FsmtError(s, f"fsmt_create(device={device}) failed")
+        self._h = h
+        self.device = device
+        self.dims = None
+
+    # ---------------------------------------------------------------- plumbing
+    def _check(self, s):
+        if s != N.OK:
+            raise N.FsmtError(s, N.lib.fsmt_last_error(self._h).decode())
+
+    def close(self):
+        if getattr(self, "_h", None):
+            N.lib.fsmt_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def bind_stream(self, stream_ptr: int | None):
+        self._check(N.lib.fsmt_bind_stream(self._h, stream_ptr))
+
+    # ---------------------------------------------------------------- a0
+    def load_formula(self, text: str | bytes):
+        data = text.encode() if isinstance(text, str) else text
+        self._check(N.lib.fsmt_load_formula(self._h, data, len(data)))
+        self.dims = None
+
+    def build_xbdd(self, node_budget: int = 0):
+        self._check(N.lib.fsmt_build_xbdd(self._h, int(node_budget)))
+        d = N.Dims()
+        self._check(N.lib.fsmt_get_dims(self._h, C.byref(d)))
+        self.dims = d
+
+    def get_dims(self) -> dict:
+        d = N.Dims()
+        self._check(N.lib.fsmt_get_dims(self._h, C.byref(d)))
+        return {k: getattr(d, k) for k, _ in d._fields_}
+
+    def get_bounds(self):
+        lo = np.empty(self.dims.n_real, dtype=np.float32)
+        hi = np.empty(self.dims.n_real, dtype=np.float32)
+        self._check(N.lib.fsmt_get_bounds(self._h, lo.ctypes.data, hi.ctypes.data))
+        return lo, hi
+
+    def dump_structure(self, directory: str):
+        self._check(N.lib.fsmt_dump_structure(self._h, directory.encode()))
+
+    # ---------------------------------------------------------------- solve
+    def set_params(self, kappas=None, eta=0.0, eps=0.0, rounding=N.ROUND_SIGN, erwa_mode=N.ERWA_VERBATIM,
+                   time_limit_s=0.0):
+        p = N.Params()
+        if kappas is not None:
+            self._kappas = np.ascontiguousarray(kappas, dtype=np.float32)
+            p.kappas = self._kappas.ctypes.data_as(C.POINTER(C.c_float))
+            p.n_stages = len(self._kappas)
+        p.eta, p.eps, p.rounding, p.erwa_mode, p.time_limit_s = eta, eps, rounding, erwa_mode, time_limit_s
+        self._check(N.lib.fsmt_set_params(self._h, C.byref(p)))
+
+    def solve(self, restarts: int, steps: int, seed: int) -> SolveResult:
+        v = C.c_int()
+        x = np.empty(self.dims.n_bool, dtype=np.int8)
+        y = np.empty(self.dims.n_real, dtype=np.float32)
+        st = N.Stats()
+        s = N.lib.fsmt_solve(self._h, restarts, steps, seed, C.byref(v), x.ctypes.data, y.ctypes.data, C.byref(st))
+        if s not in (N.OK, N.ERR_TIMEOUT):
+            self._check(s)
+        stats = {k: getattr(st, k) for k, _ in st._fields_}
+        stats["timeout"] = s == N.ERR_TIMEOUT
+        return SolveResult(v.value, x, y, stats)
+
+    # ---------------------------------------------------------------- step API
+    def begin(self, restarts: int, seed: int, restart_offset: int = 0):
+        self._check(N.lib.fsmt_begin(self._h, restarts, seed, restart_offset))
+        self.R = restarts
+
+    def set_state(self, a, b):
+        pa, wa = N._ptr(a, np.float32)
+        pb, wb = N._ptr(b, np.float32)
+        if a is not None and b is not None and wa != wb:
+            raise ValueError("a and b must both be host or both be device arrays")
+        self._check(N.lib.fsmt_set_state(self._h, pa, pb, wa if a is not None else wb))
+
+    def get_state(self):
+        a = np.empty((self.dims.n_bool, self.R), dtype=np.float32)
+        b = np.empty((self.dims.n_real, self.R), dtype=np.float32)
+        self._check(N.lib.fsmt_get_state(self._h, a.ctypes.data, b.ctypes.data, N.HOST))
+        return a, b
+
+    def set_counters(self, U):
+        p, w = N._ptr(U, np.uint8)
+        self._check(N.lib.fsmt_set_counters(self._h, p, w))
+
+    def get_counters(self):
+        U = np.empty((self.dims.n_cons, self.R), dtype=np.uint8)
+        self._check(N.lib.fsmt_get_counters(self._h, U.ctypes.data, N.HOST))
+        return U
+
+    def sweep(self, kappa: float, stage_t: int = 1):
+        self._check(N.lib.fsmt_sweep(self._h, kappa, stage_t))
+
+    def get_sweep(self):
+        ga = np.empty((self.dims.n_bool, self.R), dtype=np.float64)
+        gb = np.empty((self.dims.n_real, self.R), dtype=np.float64)
+        obj = np.empty(self.R, dtype=np.float64)
+        self._check(N.lib.fsmt_get_sweep(self._h, ga.ctypes.data, gb.ctypes.data, obj.ctypes.data, N.HOST))
+        return obj, ga, gb
+
+    def constraint_terms(self, kappa: float, restart: int):
+        E = np.empty(self.dims.n_cons, dtype=np.float64)
+        self._check(N.lib.fsmt_constraint_terms(self._h, kappa, restart, E.ctypes.data))
+        return E
+
+    def update(self, eta: float, eps: float, want_gm2: bool = False):
+        gm2 = np.empty(self.R, dtype=np.float64) if want_gm2 else None
+        self._check(N.lib.fsmt_update(self._h, eta, eps, gm2.ctypes.data if want_gm2 else None))
+        return gm2
+
+    def stage_end(self, stage_t: int):
+        u = np.empty(self.R, dtype=np.uint32)
+        self._check(N.lib.fsmt_stage_end(self._h, stage_t, u.ctypes.data))
+        return u
+
+    def run_stage(self, stage_t: int, kappa: float, steps: int, want_unsat: bool = True):
+        """One annealing stage (steps x {K1, K3} + K4/K5); returns (unsat[R] or None, min_unsat)."""
+        u = np.empty(self.R, dtype=np.uint32) if want_unsat else None
+        m = C.c_uint32()
+        self._check(N.lib.fsmt_run_stage(self._h, stage_t, kappa, steps, u.ctypes.data if want_unsat else None,
+                                         C.byref(m)))
+        return u, m.value
+
+    def set_timing(self, enable: bool):
+        self._check(N.lib.fsmt_set_timing(self._h, int(enable)))
+
+    def get_timing(self, reset: bool = False):
+        """{kernel class: (total device ms, launch groups)} for k1_sweep / k3_update / k45_stage_end."""
+        ms = np.zeros(3, dtype=np.float64)
+        cnt = np.zeros(3, dtype=np.uint64)
+        self._check(N.lib.fsmt_get_timing(self._h, ms.ctypes.data, cnt.ctypes.data, int(reset)))
+        return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(["k1_sweep", "k3_update", "k45_stage_end"])}
+
+    def get_model(self, restart: int):
+        x = np.empty(self.dims.n_bool, dtype=np.int8)
+        y = np.empty(self.dims.n_real, dtype=np.float32)
+        self._check(N.lib.fsmt_get_model(self._h, restart, x.ctypes.data, y.ctypes.data))
+        return x, y
+
+    def get_rounded(self):
+        x = np.empty((self.dims.n_bool, self.R), dtype=np.int8)
+        self._check(N.lib.fsmt_get_rounded(self._h, x.ctypes.data, N.HOST))
+        return x
+
+    def verify(self, x, y, per_con: bool = False):
+        x = np.ascontiguousarray(x, dtype=np.int8)
+        y = np.ascontiguousarray(y, dtype=np.float32)
+        n = C.c_uint32()
+        pc = np.empty(self.dims.n_cons, dtype=np.uint8) if per_con else None
+        self._check(N.lib.fsmt_verify(self._h, x.ctypes.data, y.ctypes.data, C.byref(n),
+                                      pc.ctypes.data if per_con else None))
+        return (n.value, pc) if per_con else n.value
+
+    def verify_batch(self, x, y, per_con: bool = False):
+        """x[n_bool][R] int8, y[n_real][R] float32 (numpy or device tensors)."""
+        px, wx = N._ptr(x, np.int8)
+        py, _ = N._ptr(y, np.float32)
+        R = x.shape[1] if x.ndim == 2 else y.shape[1]
+        u = np.empty(R, dtype=np.uint32)
+        pc = np.empty((self.dims.n_cons, R), dtype=np.uint8) if per_con else None
+        self._check(N.lib.fsmt_verify_batch(self._h, R, px, py, wx, u.ctypes.data, pc.ctypes.data if per_con else None))
+        return (u, pc) if per_con else u
+
+    # ---------------------------------------------------------------- introspection
+    def kernel_launches(self) -> int:
+        return int(N.lib.fsmt_kernel_launches(self._h))
+
+    def device_buffers(self) -> dict:
+        ptrs = [C.c_void_p() for _ in range(7)]
+        self._check(N.lib.fsmt_device_buffers(self._h, *[C.byref(p) for p in ptrs]))
+        return dict(zip(["a", "b", "grad_a", "grad_b", "U", "obj", "unsat"], [p.value for p in ptrs]))
+
+    def time_sweep(self, kappa: float, stage_t: int, iters: int) -> float:
+        ms = C.c_double()
+        self._check(N.lib.fsmt_time_sweep(self._h, kappa, stage_t, iters, C.byref(ms)))
+        return ms.value

@@ -562,3 +562,18 @@ def test_oracle_solve_cfg1_sound():
     g = hsmt.parse("p hsmt 1 0\nc or 1 +b0\nc or 1 -b0")
     verdict, _, _ = solve.solve(g, 2, 1, solve.Params(kappas=[1.0, 2.0], steps=5))
     assert verdict == "UNKNOWN"
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2s", "cfg3s", "cfg4s"])
+def test_grouped_sparse_path_matches_enumeration(name):
+    inst = fsmt_gen.config(name)
+    f = hsmt.parse(inst.text)
+    rng = np.random.default_rng(21)
+    a = rng.uniform(-1, 1, f.n_bool)
+    b = rng.uniform(0, 1, f.n_real)
+    w = rng.integers(1, 5, len(f.constraints)).astype(float)
+    C1, ga1, gb1, t1 = objective.objective_and_gradient(f, a, b, 1.7, w, want_terms=True)
+    C2, ga2, gb2, t2 = objective.objective_and_gradient_grouped(f, a, b, 1.7, w, want_terms=True)
+    assert abs(C1 - C2) < 1e-10 * max(1, abs(C1))
+    assert np.allclose(ga1, ga2, atol=1e-12) and np.allclose(gb1, gb2, atol=1e-12)
+    assert all(abs(t1[i] - t2[i]) < 1e-13 for i in t1)
