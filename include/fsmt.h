@@ -182,6 +182,20 @@ fsmt_status fsmt_verify_batch(fsmt_ctx* ctx, uint32_t R, const int8_t* x, const 
                               uint32_t* unsat_out, uint8_t* per_con);
 
 /* ---- introspection ------------------------------------------------------------------------ */
+/* Work plan of the sweep: number of JIT-specialised kernel classes, tiles, and
+ * constraints the specialised kernel covers (0 when it is not active); msg receives
+ * "active", "host-only", "no JIT classes" or the NVRTC / load error. Setting FSMT_JIT=0 in the
+ * environment before fsmt_build_xbdd disables specialisation (every constraint then runs
+ * through the generic interpreter kernel). */
+fsmt_status fsmt_jit_info(const fsmt_ctx* ctx, uint32_t* n_jit_classes, uint32_t* n_tiles, uint32_t* jit_cons,
+                          char* msg, size_t msg_len);
+/* Copies the generated CUDA source of the specialised sweep into buf (NUL-terminated, truncated
+ * to len); returns the full size including the NUL (0 if not built). Host-only contexts too. */
+size_t fsmt_jit_source(const fsmt_ctx* ctx, char* buf, size_t len);
+/* Compile the specialised sweep with NVRTC only (no device needed; host-only contexts too):
+ * FSMT_OK and the cubin size, or FSMT_ERR_CUDA with the compiler log in fsmt_last_error. The
+ * compiler log (ptxas register / spill report) is copied to log (may be NULL). */
+fsmt_status fsmt_jit_check(fsmt_ctx* ctx, size_t* cubin_bytes, char* log, size_t log_len);
 /* Number of this library's kernel launches since the ctx was created. */
 uint64_t fsmt_kernel_launches(const fsmt_ctx* ctx);
 /* Current restart count (0 before fsmt_begin). */

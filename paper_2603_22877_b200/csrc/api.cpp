@@ -12,6 +12,7 @@
 
 #include "../../include/fsmt.h"
 #include "fsmt_internal.hpp"
+#include "jit.hpp"
 #include "kernels.hpp"
 
 using namespace fsmt;
@@ -30,6 +31,13 @@ struct fsmt_ctx {
     DevState S{};
     std::vector<void*> sallocs;
     double* terms = nullptr;    // [C] debug hook buffer
+    // device work plan (tiles.cpp) + JIT-specialised sweep (jit.cpp)
+    bool jit_enabled = true;
+    Plan plan;
+    std::string jit_src, jit_error;
+    JitKernel jit;
+    DevTiles T{};
+    const uint32_t* d_pos = nullptr;   // original -> internal constraint index (device)
     // params
     std::vector<float> kappas;
     float eta = 0.05f, eps = 1e-2f;
@@ -140,6 +148,19 @@ void drop_formula(fsmt_ctx* ctx) {
     drop_state(ctx);
     free_list(ctx->fallocs);
     ctx->F = DevFormula{};
+    jit_release(ctx->jit);
+    ctx->T = DevTiles{};
+    ctx->d_pos = nullptr;
+}
+
+fsmt_status upload_bytes(fsmt_ctx* ctx, const void* src, size_t bytes, const void*& dst) {
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, std::max<size_t>(bytes, 16));
+    if (e != cudaSuccess) return fail(ctx, FSMT_ERR_OOM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    ctx->fallocs.push_back(p);
+    if (bytes) CK(cudaMemcpy(p, src, bytes, cudaMemcpyHostToDevice));
+    dst = p;
+    return FSMT_OK;
 }
 
 float wscale_of(uint32_t stage_t, uint32_t mode) {
@@ -269,6 +290,12 @@ fsmt_status fsmt_build_xbdd(fsmt_ctx* ctx, uint64_t node_budget) {
     } catch (const std::bad_alloc&) {
         return fail(ctx, FSMT_ERR_OOM, "host allocation failed while building xBDDs");
     }
+    {
+        const char* env = getenv("FSMT_JIT");
+        ctx->jit_enabled = !(env && env[0] == '0');
+        ctx->plan = make_plan(ctx->f, ctx->b, ctx->jit_enabled);
+        ctx->jit_src = ctx->plan.n_jit_kclasses ? jit_source(ctx->f, ctx->b, ctx->plan) : std::string();
+    }
     if (ctx->host_only) {
         ctx->stage = 2;
         ctx->err.clear();
@@ -276,6 +303,20 @@ fsmt_status fsmt_build_xbdd(fsmt_ctx* ctx, uint64_t node_budget) {
     }
     const Formula& f = ctx->f;
     const Built& b = ctx->b;
+    const Plan& P = ctx->plan;
+    // constraint arrays in the internal (tile-sorted) order
+    const size_t C = f.cons.size();
+    std::vector<uint32_t> c_tmpl(C), c_off(C + 1), c_ids;
+    std::vector<float> c_w(C);
+    c_ids.reserve(b.slot_ids.size());
+    c_off[0] = 0;
+    for (size_t i = 0; i < C; ++i) {
+        const uint32_t o = P.order[i];
+        c_tmpl[i] = b.cons_tmpl[o];
+        c_w[i] = b.cons_w[o];
+        c_ids.insert(c_ids.end(), b.slot_ids.begin() + b.cons_slot_off[o], b.slot_ids.begin() + b.cons_slot_off[o + 1]);
+        c_off[i + 1] = (uint32_t)c_ids.size();
+    }
     // flatten templates
     std::vector<uint32_t> node_off{0}, kind_off{0};
     std::vector<DevNode> nodes;
@@ -304,10 +345,11 @@ fsmt_status fsmt_build_xbdd(fsmt_ctx* ctx, uint64_t node_budget) {
     F.max_slots = b.max_slots;
     F.max_nodes = b.max_nodes;
 #define UP(vec, field) do { s = upload(ctx, vec, F.field, ctx->fallocs); if (s) return s; } while (0)
-    UP(b.cons_tmpl, cons_tmpl);
-    UP(b.cons_slot_off, cons_slot_off);
-    UP(b.slot_ids, slot_ids);
-    UP(b.cons_w, cons_w);
+    UP(c_tmpl, cons_tmpl);
+    UP(c_off, cons_slot_off);
+    UP(c_ids, slot_ids);
+    UP(c_w, cons_w);
+    UP(P.order, orig);
     UP(node_off, tmpl_node_off);
     UP(nodes, nodes);
     UP(kind_off, tmpl_kind_off);
@@ -324,6 +366,33 @@ fsmt_status fsmt_build_xbdd(fsmt_ctx* ctx, uint64_t node_budget) {
     UP(b.lo, lo);
     UP(b.hi, hi);
 #undef UP
+    s = upload(ctx, P.pos, ctx->d_pos, ctx->fallocs);
+    if (s) return s;
+    // JIT-specialised sweep for the hot kernel classes (tiles.cpp); on failure everything runs
+    // through the generic kernel and the reason is kept in jit_error.
+    F.generic_begin = 0;
+    ctx->jit_error.clear();
+    if (!P.tiles.empty()) {
+        std::string err;
+        if (jit_compile(ctx->jit_src, ctx->jit, err)) {
+            const void* tp = nullptr;
+            s = upload_bytes(ctx, P.tiles.data(), P.tiles.size() * sizeof(TileDesc), tp);
+            if (s) return s;
+            const uint32_t* rp = nullptr;
+            s = upload(ctx, P.recs, rp, ctx->fallocs);
+            if (s) return s;
+            const uint32_t* vp = nullptr;
+            s = upload(ctx, P.tile_vars, vp, ctx->fallocs);
+            if (s) return s;
+            ctx->T.tiles = tp;
+            ctx->T.n_tiles = (uint32_t)P.tiles.size();
+            ctx->T.recs = rp;
+            ctx->T.tile_vars = vp;
+            F.generic_begin = P.jit_cons_end;
+        } else {
+            ctx->jit_error = err;
+        }
+    }
     ctx->stage = 2;
     ctx->err.clear();
     return FSMT_OK;
@@ -458,16 +527,76 @@ fsmt_status fsmt_get_state(fsmt_ctx* ctx, float* a, float* b, int where) {
     return copy_out(ctx, b, ctx->S.b, (size_t)ctx->F.n_real * ctx->S.R, where);
 }
 
+// U is kept in the internal constraint order; the ABI speaks the original order.
 fsmt_status fsmt_set_counters(fsmt_ctx* ctx, const uint8_t* U, int where) {
     fsmt_status s = need(ctx, 3, "fsmt_set_counters");
     if (s) return s;
-    return copy_in(ctx, ctx->S.U, U, (size_t)ctx->F.n_cons * ctx->S.R, where);
+    const size_t n = (size_t)ctx->F.n_cons * ctx->S.R;
+    if (n == 0) return FSMT_OK;
+    if (!U) return fail(ctx, FSMT_ERR_ARG, "null input pointer");
+    uint8_t* tmp = nullptr;
+    CK(cudaMalloc((void**)&tmp, n));
+    cudaError_t e = cudaMemcpyAsync(tmp, U, n, where == FSMT_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                                    ctx->stream);
+    if (e == cudaSuccess) {
+        launch_gather_rows_u8(ctx->S.U, tmp, ctx->F.orig, ctx->F.n_cons, ctx->S.R, ctx->stream);
+        ctx->launches += 1;
+        e = cudaStreamSynchronize(ctx->stream);
+    }
+    cudaFree(tmp);
+    if (e != cudaSuccess) return fail(ctx, FSMT_ERR_CUDA, std::string("fsmt_set_counters: ") + cudaGetErrorString(e));
+    return check_launch(ctx);
 }
 
 fsmt_status fsmt_get_counters(fsmt_ctx* ctx, uint8_t* U, int where) {
     fsmt_status s = need(ctx, 3, "fsmt_get_counters");
     if (s) return s;
-    return copy_out(ctx, U, ctx->S.U, (size_t)ctx->F.n_cons * ctx->S.R, where);
+    const size_t n = (size_t)ctx->F.n_cons * ctx->S.R;
+    if (n == 0 || !U) return FSMT_OK;
+    uint8_t* tmp = nullptr;
+    CK(cudaMalloc((void**)&tmp, n));
+    launch_gather_rows_u8(tmp, ctx->S.U, ctx->d_pos, ctx->F.n_cons, ctx->S.R, ctx->stream);
+    ctx->launches += 1;
+    cudaError_t e = cudaMemcpyAsync(U, tmp, n, where == FSMT_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                                    ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    cudaFree(tmp);
+    if (e != cudaSuccess) return fail(ctx, FSMT_ERR_CUDA, std::string("fsmt_get_counters: ") + cudaGetErrorString(e));
+    return check_launch(ctx);
+}
+
+fsmt_status fsmt_jit_info(const fsmt_ctx* ctx, uint32_t* n_jit_classes, uint32_t* n_tiles, uint32_t* jit_cons,
+                          char* msg, size_t msg_len) {
+    if (!ctx) return FSMT_ERR_ARG;
+    if (ctx->stage < 2) return FSMT_ERR_STATE;
+    const bool active = !ctx->host_only && ctx->T.n_tiles > 0;
+    if (n_jit_classes) *n_jit_classes = ctx->plan.n_jit_kclasses;
+    if (n_tiles) *n_tiles = (uint32_t)ctx->plan.tiles.size();
+    if (jit_cons) *jit_cons = active ? ctx->plan.jit_cons_end : 0;
+    if (msg && msg_len) {
+        std::string m = ctx->host_only ? "host-only" : (active ? "active" : (ctx->plan.tiles.empty() ? "no JIT classes" : ctx->jit_error));
+        snprintf(msg, msg_len, "%s", m.c_str());
+    }
+    return FSMT_OK;
+}
+
+fsmt_status fsmt_jit_check(fsmt_ctx* ctx, size_t* cubin_bytes, char* log, size_t log_len) {
+    if (!ctx) return FSMT_ERR_ARG;
+    if (ctx->stage < 2) return fail(ctx, FSMT_ERR_STATE, "fsmt_jit_check: build first");
+    if (ctx->jit_src.empty()) return fail(ctx, FSMT_ERR_STATE, "fsmt_jit_check: no JIT classes");
+    std::vector<char> cubin;
+    std::string lg, err;
+    bool ok = jit_cubin(ctx->jit_src, cubin, lg, err);
+    if (log && log_len) snprintf(log, log_len, "%s", lg.c_str());
+    if (!ok) return fail(ctx, FSMT_ERR_CUDA, err);
+    if (cubin_bytes) *cubin_bytes = cubin.size();
+    return FSMT_OK;
+}
+
+size_t fsmt_jit_source(const fsmt_ctx* ctx, char* buf, size_t len) {
+    if (!ctx || ctx->stage < 2) return 0;
+    if (buf && len) snprintf(buf, len, "%s", ctx->jit_src.c_str());
+    return ctx->jit_src.size() + 1;
 }
 
 static fsmt_status sweep_impl(fsmt_ctx* ctx, float kappa, uint32_t stage_t, double* terms, uint32_t terms_r) {
@@ -478,9 +607,16 @@ static fsmt_status sweep_impl(fsmt_ctx* ctx, float kappa, uint32_t stage_t, doub
     CK(cudaMemsetAsync(S.obj, 0, (size_t)S.R * 8, ctx->stream));
     {
         Timed tm(ctx, 0);
-        launch_sweep(F, S, kappa, wscale_of(stage_t, ctx->erwa_mode), terms, terms_r, ctx->stream);
+        const float ws = wscale_of(stage_t, ctx->erwa_mode);
+        if (ctx->T.n_tiles) {
+            launch_sweep_jit(ctx->jit.kernel, F, S, ctx->T, kappa, ws, terms, terms_r, ctx->stream);
+            ctx->launches += 1;
+        }
+        if (F.generic_begin < F.n_cons) {
+            launch_sweep(F, S, kappa, ws, terms, terms_r, ctx->stream);
+            ctx->launches += 1;
+        }
     }
-    ctx->launches += 1;
     return check_launch(ctx);
 }
 

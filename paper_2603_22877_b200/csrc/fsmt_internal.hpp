@@ -86,6 +86,44 @@ struct Built {
     uint64_t n_nodes = 0;
 };
 
+// ---- device work plan (csrc/tiles.cpp) -----------------------------------------------------
+// Constraints are permuted into an internal order grouped into tiles: a tile is a run of
+// constraints of one kernel class (template + nnz of each atom slot) whose variables fit a
+// small local table, so the JIT-specialised sweep accumulates their gradients on chip.
+constexpr uint32_t kTileVmax = 128;       // local variables per tile
+constexpr uint32_t kTileCmax = 64;        // constraints per tile
+constexpr uint32_t kGroupVars = 64;       // variables per footprint group
+
+struct KClass {
+    uint32_t tmpl;
+    std::vector<uint8_t> nnz;    // per atom slot (slot order)
+    uint32_t n_refs;             // Boolean slots + sum nnz
+    uint32_t words;              // record words before padding
+    uint32_t stride4;            // record stride in uint4
+    bool jit;
+    uint64_t n_cons;
+};
+
+struct TileDesc {                // mirrored in the JIT source (32 bytes)
+    uint32_t kclass, cons_begin, n_cons, var_off, n_vars, rec_off, pad0, pad1;
+};
+
+struct Plan {
+    std::vector<uint32_t> order;      // internal -> original constraint id
+    std::vector<uint32_t> pos;        // original -> internal
+    std::vector<KClass> kclasses;
+    std::vector<uint32_t> cons_kclass;  // internal order
+    std::vector<TileDesc> tiles;      // JIT tiles only, in internal order
+    std::vector<uint32_t> tile_vars;  // unified var ids: Boolean i -> i, real j -> n_bool + j
+    std::vector<uint32_t> recs;       // JIT records (uint32 words, stride4*4 per constraint)
+    uint32_t jit_cons_end = 0;        // internal [0, jit_cons_end) are JIT constraints
+    uint32_t n_jit_kclasses = 0;
+};
+
+Plan make_plan(const Formula& f, const Built& b, bool enable_jit);
+// CUDA source of the specialised sweep kernel for the plan's JIT classes.
+std::string jit_source(const Formula& f, const Built& b, const Plan& p);
+
 struct BuildError {
     std::string msg;
     bool budget;

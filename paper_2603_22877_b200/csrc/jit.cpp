@@ -1,0 +1,144 @@
+// Runtime compilation of the specialised sweep (tiles.cpp emits the source) with NVRTC,
+// loaded through the CUDA runtime's library API.  NVRTC is dlopen'ed so the library has no
+// link-time dependency on it (host-only contexts and the CPU tests never touch it).
+#include <dlfcn.h>
+
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "jit.hpp"
+
+namespace fsmt {
+namespace {
+
+typedef int nvrtcResult_t;
+typedef struct _nvrtcProgram* nvrtcProgram_t;
+struct Nvrtc {
+    void* h = nullptr;
+    nvrtcResult_t (*create)(nvrtcProgram_t*, const char*, const char*, int, const char* const*, const char* const*);
+    nvrtcResult_t (*compile)(nvrtcProgram_t, int, const char* const*);
+    nvrtcResult_t (*cubin_size)(nvrtcProgram_t, size_t*);
+    nvrtcResult_t (*cubin)(nvrtcProgram_t, char*);
+    nvrtcResult_t (*log_size)(nvrtcProgram_t, size_t*);
+    nvrtcResult_t (*log)(nvrtcProgram_t, char*);
+    nvrtcResult_t (*destroy)(nvrtcProgram_t*);
+    bool ok = false;
+    std::string err;
+};
+
+Nvrtc& nvrtc() {
+    static Nvrtc n;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        const char* cands[] = {getenv("FSMT_NVRTC"), "/usr/local/cuda/lib64/libnvrtc.so.12", "libnvrtc.so.12",
+                               "libnvrtc.so"};
+        for (const char* c : cands) {
+            if (!c) continue;
+            n.h = dlopen(c, RTLD_NOW | RTLD_LOCAL);
+            if (n.h) break;
+        }
+        if (!n.h) {
+            n.err = "cannot dlopen libnvrtc.so.12";
+            return;
+        }
+#define SYM(field, name)                                                    \
+    *(void**)(&n.field) = dlsym(n.h, name);                                 \
+    if (!n.field) {                                                         \
+        n.err = std::string("missing NVRTC symbol ") + name;                \
+        return;                                                             \
+    }
+        SYM(create, "nvrtcCreateProgram");
+        SYM(compile, "nvrtcCompileProgram");
+        SYM(cubin_size, "nvrtcGetCUBINSize");
+        SYM(cubin, "nvrtcGetCUBIN");
+        SYM(log_size, "nvrtcGetProgramLogSize");
+        SYM(log, "nvrtcGetProgramLog");
+        SYM(destroy, "nvrtcDestroyProgram");
+#undef SYM
+        n.ok = true;
+    });
+    return n;
+}
+
+// process-wide cache: identical sources compile once
+std::mutex g_mu;
+std::unordered_map<std::string, std::vector<char>> g_cubins;
+
+}  // namespace
+
+bool jit_cubin(const std::string& src, std::vector<char>& cubin, std::string& log, std::string& err) {
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        auto it = g_cubins.find(src);
+        if (it != g_cubins.end()) {
+            cubin = it->second;
+            return true;
+        }
+    }
+    Nvrtc& n = nvrtc();
+    if (!n.ok) {
+        err = n.err;
+        return false;
+    }
+    nvrtcProgram_t prog = nullptr;
+    if (n.create(&prog, src.c_str(), "fsmt_k1_jit.cu", 0, nullptr, nullptr) != 0) {
+        err = "nvrtcCreateProgram failed";
+        return false;
+    }
+    const char* opts[] = {"--gpu-architecture=sm_100a", "-lineinfo", "--std=c++17", "-default-device",
+                          "--ptxas-options=-v"};
+    int rc = n.compile(prog, 5, opts);
+    size_t ls = 0;
+    n.log_size(prog, &ls);
+    log.assign(ls, '\0');
+    if (ls) n.log(prog, &log[0]);
+    if (rc != 0) {
+        err = "NVRTC compile failed: " + log.substr(0, 2000);
+        n.destroy(&prog);
+        return false;
+    }
+    size_t cs = 0;
+    n.cubin_size(prog, &cs);
+    cubin.resize(cs);
+    n.cubin(prog, cubin.data());
+    n.destroy(&prog);
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_cubins.emplace(src, cubin);
+    return true;
+}
+
+bool jit_compile(const std::string& src, JitKernel& out, std::string& err) {
+    std::vector<char> cubin;
+    if (!jit_cubin(src, cubin, out.log, err)) return false;
+    cudaLibrary_t lib = nullptr;
+    cudaError_t e = cudaLibraryLoadData(&lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
+    if (e != cudaSuccess) {
+        err = std::string("cudaLibraryLoadData: ") + cudaGetErrorString(e);
+        return false;
+    }
+    cudaKernel_t k = nullptr;
+    e = cudaLibraryGetKernel(&k, lib, "fsmt_k1_jit");
+    if (e != cudaSuccess) {
+        cudaLibraryUnload(lib);
+        err = std::string("cudaLibraryGetKernel: ") + cudaGetErrorString(e);
+        return false;
+    }
+    out.lib = lib;
+    out.kernel = k;
+    out.cubin_bytes = cubin.size();
+    return true;
+}
+
+void jit_release(JitKernel& k) {
+    if (k.lib) cudaLibraryUnload((cudaLibrary_t)k.lib);
+    k.lib = nullptr;
+    k.kernel = nullptr;
+}
+
+}  // namespace fsmt

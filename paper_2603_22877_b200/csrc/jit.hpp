@@ -1,0 +1,22 @@
+#pragma once
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+namespace fsmt {
+
+struct JitKernel {
+    void* lib = nullptr;          // cudaLibrary_t
+    cudaKernel_t kernel = nullptr;
+    size_t cubin_bytes = 0;
+    std::string log;
+};
+
+// Compiles `src` for sm_100a with NVRTC and loads kernel "fsmt_k1_jit". false + err on failure.
+bool jit_compile(const std::string& src, JitKernel& out, std::string& err);
+// NVRTC only (no device needed): cubin + compiler log.
+bool jit_cubin(const std::string& src, std::vector<char>& cubin, std::string& log, std::string& err);
+void jit_release(JitKernel& k);
+
+}  // namespace fsmt

@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(256) k1_sweep(DevFormula F, DevState S, float 
     const uint32_t rtiles = (R + 31) / 32;
     const uint64_t gw = (uint64_t)blockIdx.x * (blockDim.x >> 5) + warp;
     const uint32_t rt = (uint32_t)(gw % rtiles);
-    const uint64_t c0 = (gw / rtiles) * kChunk;
+    const uint64_t c0 = F.generic_begin + (gw / rtiles) * kChunk;
     if (c0 >= F.n_cons) return;
     const uint64_t c1 = min(c0 + (uint64_t)kChunk, (uint64_t)F.n_cons);
     const uint32_t r = rt * 32 + lane;
@@ -159,7 +159,7 @@ __global__ void __launch_bounds__(256) k1_sweep(DevFormula F, DevState S, float 
                 }
             }
             objacc += (double)w * (double)E;
-            if (terms != nullptr && r == terms_r) terms[c] = (double)E;
+            if (terms != nullptr && r == terms_r) terms[F.orig[c]] = (double)E;
         }
     }
     if (live) atomicAdd(&S.obj[r], objacc);
@@ -283,7 +283,7 @@ __global__ void __launch_bounds__(256) k5_verify(DevFormula F, DevState S, const
             uint8_t& cell = Uupd[(size_t)c * R + r];
             cell = (uint8_t)min(255u, (uint32_t)cell + u);
         }
-        if (per_con) per_con[(size_t)c * R + r] = (uint8_t)u;
+        if (per_con) per_con[(size_t)F.orig[c] * R + r] = (uint8_t)u;
     }
     atomicAdd(&S.unsat[r], cnt);
 }
@@ -310,13 +310,50 @@ void launch_init(const DevFormula& F, const DevState& S, uint64_t seed, uint32_t
     if (n) k0_init<<<(unsigned)std::max<uint64_t>(blocks, 1), threads, 0, st>>>(F, S, seed, off);
 }
 
+__global__ void k_gather_rows_u8(uint8_t* __restrict__ dst, const uint8_t* __restrict__ src,
+                                 const uint32_t* __restrict__ idx, uint32_t rows, uint32_t R, int scatter) {
+    const uint64_t n = (uint64_t)rows * R;
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t i = (uint32_t)(t / R), r = (uint32_t)(t % R);
+        if (scatter) dst[(size_t)idx[i] * R + r] = src[t];
+        else dst[t] = src[(size_t)idx[i] * R + r];
+    }
+}
+
+void launch_gather_rows_u8(uint8_t* dst, const uint8_t* src, const uint32_t* idx, uint32_t rows, uint32_t R,
+                           cudaStream_t st) {
+    if (!rows || !R) return;
+    k_gather_rows_u8<<<148 * 8, 256, 0, st>>>(dst, src, idx, rows, R, 0);
+}
+
+void launch_scatter_rows_u8(uint8_t* dst, const uint8_t* src, const uint32_t* idx, uint32_t rows, uint32_t R,
+                            cudaStream_t st) {
+    if (!rows || !R) return;
+    k_gather_rows_u8<<<148 * 8, 256, 0, st>>>(dst, src, idx, rows, R, 1);
+}
+
+void launch_sweep_jit(cudaKernel_t k, const DevFormula& F, const DevState& S, const DevTiles& T, float kappa,
+                      float wscale, double* terms, uint32_t terms_r, cudaStream_t st) {
+    if (T.n_tiles == 0 || S.R == 0) return;
+    constexpr int kJitWarps = 2, kVmax = 128;                       // must match tiles.cpp
+    const uint64_t nw = (uint64_t)T.n_tiles * ((S.R + 31) / 32);
+    const unsigned blocks = (unsigned)((nw + kJitWarps - 1) / kJitWarps);
+    const size_t smem = (size_t)kJitWarps * (kVmax * 32 * 4 + kVmax * 4);
+    uint32_t n_tiles = T.n_tiles, R = S.R, n_bool = F.n_bool;
+    const uint8_t* U = S.U;
+    void* args[] = {(void*)&T.tiles, &n_tiles, (void*)&T.recs, (void*)&T.tile_vars, (void*)&S.a, (void*)&S.b,
+                    (void*)&S.ga, (void*)&S.gb, (void*)&U, (void*)&S.obj, &R, &n_bool, &kappa, &wscale,
+                    &terms, &terms_r, (void*)&F.orig};
+    cudaLaunchKernel((const void*)k, dim3(blocks), dim3(kJitWarps * 32), args, smem, st);
+}
+
 void launch_sweep(const DevFormula& F, const DevState& S, float kappa, float wscale, double* terms, uint32_t terms_r,
                   cudaStream_t st) {
-    if (F.n_cons == 0 || S.R == 0) return;
+    if (F.n_cons <= F.generic_begin || S.R == 0) return;
     const int warps = sweep_warps(F);
     const int smem = sweep_smem_bytes(F, warps);
     if (smem > 48 * 1024) cudaFuncSetAttribute(k1_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    const uint64_t chunks = (F.n_cons + kChunk - 1) / kChunk;
+    const uint64_t chunks = (F.n_cons - F.generic_begin + kChunk - 1) / kChunk;
     const uint64_t nw = chunks * ((S.R + 31) / 32);
     const uint64_t blocks = (nw + warps - 1) / warps;
     k1_sweep<<<(unsigned)blocks, warps * 32, smem, st>>>(F, S, kappa, wscale, terms, terms_r,

@@ -36,6 +36,9 @@ struct DevFormula {
     const float* atom_invnorm;      // [K] 1/||q_i||
     const float* lo;                // [n_real]
     const float* hi;                // [n_real]
+    const uint32_t* orig;           // [C] internal -> original constraint id (constraint arrays and U
+                                    //     are in the internal, tile-sorted order; see tiles.cpp)
+    uint32_t generic_begin;         // internal [generic_begin, n_cons) run through the generic K1
 };
 
 // Per-restart state, restart-minor (row = variable / constraint).
@@ -58,9 +61,24 @@ int sweep_smem_bytes(const DevFormula& F, int warps);
 
 // K0: Philox init (R20) + projection.
 void launch_init(const DevFormula& F, const DevState& S, uint64_t seed, uint32_t restart_offset, cudaStream_t st);
-// K1: forward/backward xBDD sweep, objective + gradient (fp64 accumulation).
+// K1 (generic interpreter): forward/backward xBDD sweep over internal constraints
+// [F.generic_begin, n_cons), objective + gradient (fp64 accumulation).
 void launch_sweep(const DevFormula& F, const DevState& S, float kappa, float wscale, double* terms, uint32_t terms_r,
                   cudaStream_t st);
+// K1 (JIT-specialised, tiles): see tiles.cpp / jit.cpp.
+struct DevTiles {
+    const void* tiles;           // TileDesc[n_tiles]
+    uint32_t n_tiles;
+    const void* recs;            // uint4 records
+    const uint32_t* tile_vars;
+};
+void launch_sweep_jit(cudaKernel_t k, const DevFormula& F, const DevState& S, const DevTiles& T, float kappa,
+                      float wscale, double* terms, uint32_t terms_r, cudaStream_t st);
+// row gather for u8 matrices: dst[i][:] = src[idx[i]][:]  (U between original and internal order)
+void launch_gather_rows_u8(uint8_t* dst, const uint8_t* src, const uint32_t* idx, uint32_t rows, uint32_t R,
+                           cudaStream_t st);
+void launch_scatter_rows_u8(uint8_t* dst, const uint8_t* src, const uint32_t* idx, uint32_t rows, uint32_t R,
+                            cudaStream_t st);
 // K3: projected step (three launches: partial norms, finalize, apply).
 int update_parts(const DevFormula& F);
 void launch_update(const DevFormula& F, const DevState& S, float eta, float eps, cudaStream_t st);

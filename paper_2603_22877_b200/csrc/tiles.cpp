@@ -1,0 +1,431 @@
+// Device work plan and the JIT-specialised sweep source (K1).
+//
+// Plan: every constraint gets a kernel class (template + nnz of each atom slot).  Variables
+// are grouped by first appearance (a constraint's newly seen variables form one batch; a
+// batch never straddles a group), each constraint is keyed by (kernel class, footprint
+// groups) and the stable sort of these keys is the internal constraint order.  Runs of one
+// key become tiles of <= kTileCmax constraints over <= kTileVmax local variables, so the
+// sweep accumulates a tile's gradient contributions on chip and flushes each local
+// variable once per tile.
+//
+// JIT: for each hot kernel class the forward pass (Alg.F) and backward pass
+// (Alg.B, sign R1) are emitted as straight-line code over the class's
+// canonical xBDD, with messages in registers; slot probabilities follow Eq.4 / Eq.7 and the
+// chain rule P:1326-1327.  Constraints of other classes run through the generic kernel.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <sstream>
+#include <unordered_map>
+
+#include "fsmt_internal.hpp"
+
+namespace fsmt {
+
+namespace {
+constexpr uint32_t kJitMaxNodes = 96;
+constexpr uint32_t kJitMaxRefs = 64;
+constexpr uint32_t kJitMaxClasses = 32;
+constexpr uint64_t kJitMinCons = 32;      // specialise only classes with enough constraints
+}  // namespace
+
+Plan make_plan(const Formula& f, const Built& b, bool enable_jit) {
+    Plan p;
+    const uint32_t C = (uint32_t)b.cons_tmpl.size();
+    // 1. kernel classes
+    std::map<std::vector<uint32_t>, uint32_t> kc_of;
+    std::vector<uint32_t> kcl(C);
+    for (uint32_t c = 0; c < C; ++c) {
+        const Template& t = b.tmpls[b.cons_tmpl[c]];
+        std::vector<uint32_t> key{b.cons_tmpl[c]};
+        const uint32_t* ids = b.slot_ids.data() + b.cons_slot_off[c];
+        uint32_t refs = 0;
+        for (size_t s = 0; s < t.kinds.size(); ++s) {
+            if (t.kinds[s] == 0) {
+                ++refs;
+            } else {
+                uint32_t nnz = f.atom_rowptr[ids[s] + 1] - f.atom_rowptr[ids[s]];
+                key.push_back(nnz);
+                refs += nnz;
+            }
+        }
+        auto it = kc_of.find(key);
+        uint32_t k;
+        if (it == kc_of.end()) {
+            k = (uint32_t)p.kclasses.size();
+            kc_of.emplace(key, k);
+            KClass kc;
+            kc.tmpl = b.cons_tmpl[c];
+            for (size_t i = 1; i < key.size(); ++i) kc.nnz.push_back((uint8_t)std::min<uint32_t>(key[i], 255));
+            kc.n_refs = refs;
+            uint32_t atom_words = 0;
+            bool small_nnz = true;
+            for (size_t i = 1; i < key.size(); ++i) {
+                atom_words += 2 + key[i];
+                small_nnz &= key[i] <= 8;
+            }
+            kc.words = 1 + (refs + 1) / 2 + atom_words;
+            kc.stride4 = (kc.words + 3) / 4;
+            kc.jit = enable_jit && small_nnz && t.nodes.size() <= kJitMaxNodes && refs <= kJitMaxRefs && t.root >= 0;
+            kc.n_cons = 0;
+            p.kclasses.push_back(kc);
+        } else {
+            k = it->second;
+        }
+        kcl[c] = k;
+        p.kclasses[k].n_cons++;
+    }
+    // keep the kJitMaxClasses heaviest JIT-able classes; renumber so JIT classes come first
+    std::vector<uint32_t> idx(p.kclasses.size());
+    for (size_t i = 0; i < idx.size(); ++i) idx[i] = (uint32_t)i;
+    auto work = [&](uint32_t k) {
+        return p.kclasses[k].n_cons * (uint64_t)(b.tmpls[p.kclasses[k].tmpl].nodes.size() + p.kclasses[k].n_refs);
+    };
+    std::stable_sort(idx.begin(), idx.end(), [&](uint32_t x, uint32_t y) {
+        if (p.kclasses[x].jit != p.kclasses[y].jit) return p.kclasses[x].jit;
+        return work(x) > work(y);
+    });
+    uint32_t njit = 0;
+    for (uint32_t k : idx)
+        if (p.kclasses[k].jit && p.kclasses[k].n_cons < kJitMinCons) p.kclasses[k].jit = false;
+    for (uint32_t k : idx)
+        if (p.kclasses[k].jit) {
+            if (njit < kJitMaxClasses) ++njit;
+            else p.kclasses[k].jit = false;
+        }
+    std::stable_sort(idx.begin(), idx.end(), [&](uint32_t x, uint32_t y) {
+        if (p.kclasses[x].jit != p.kclasses[y].jit) return p.kclasses[x].jit;
+        return work(x) > work(y);
+    });
+    std::vector<uint32_t> ren(p.kclasses.size());
+    std::vector<KClass> sorted;
+    for (size_t i = 0; i < idx.size(); ++i) {
+        ren[idx[i]] = (uint32_t)i;
+        sorted.push_back(p.kclasses[idx[i]]);
+    }
+    p.kclasses.swap(sorted);
+    for (uint32_t& k : kcl) k = ren[k];
+    p.n_jit_kclasses = njit;
+
+    // 2. footprint groups by first-appearance batches
+    const uint32_t NV = f.n_bool + f.n_real;
+    std::vector<uint32_t> group(NV, UINT32_MAX);
+    uint32_t cur_group = 0, cur_size = 0;
+    std::vector<uint32_t> batch;
+    auto cons_vars = [&](uint32_t c, std::vector<uint32_t>& out) {
+        out.clear();
+        const Template& t = b.tmpls[b.cons_tmpl[c]];
+        const uint32_t* ids = b.slot_ids.data() + b.cons_slot_off[c];
+        for (size_t s = 0; s < t.kinds.size(); ++s) {
+            if (t.kinds[s] == 0) out.push_back(ids[s]);
+            else
+                for (uint32_t k = f.atom_rowptr[ids[s]]; k < f.atom_rowptr[ids[s] + 1]; ++k)
+                    out.push_back(f.n_bool + f.atom_col[k]);
+        }
+    };
+    std::vector<uint32_t> vars;
+    for (uint32_t c = 0; c < C; ++c) {
+        cons_vars(c, vars);
+        batch.clear();
+        for (uint32_t u : vars)
+            if (group[u] == UINT32_MAX && std::find(batch.begin(), batch.end(), u) == batch.end()) batch.push_back(u);
+        if (batch.empty()) continue;
+        if (cur_size > 0 && cur_size + batch.size() > kGroupVars) {
+            ++cur_group;
+            cur_size = 0;
+        }
+        for (uint32_t u : batch) group[u] = cur_group;
+        cur_size += (uint32_t)batch.size();
+    }
+    // 3. sort keys
+    struct Key {
+        uint32_t kc;
+        uint32_t g[4];
+    };
+    std::vector<Key> keys(C);
+    std::vector<uint32_t> gs;
+    for (uint32_t c = 0; c < C; ++c) {
+        cons_vars(c, vars);
+        gs.clear();
+        for (uint32_t u : vars) gs.push_back(group[u]);
+        std::sort(gs.begin(), gs.end());
+        gs.erase(std::unique(gs.begin(), gs.end()), gs.end());
+        Key k{kcl[c], {UINT32_MAX, UINT32_MAX, UINT32_MAX, UINT32_MAX}};
+        if (gs.size() <= 4) {
+            for (size_t i = 0; i < gs.size(); ++i) k.g[i] = gs[i];
+        } else {
+            k.g[0] = UINT32_MAX - 1;          // wide footprint: keep original order
+        }
+        keys[c] = k;
+    }
+    p.order.resize(C);
+    for (uint32_t c = 0; c < C; ++c) p.order[c] = c;
+    std::stable_sort(p.order.begin(), p.order.end(), [&](uint32_t x, uint32_t y) {
+        const Key &a = keys[x], &bb = keys[y];
+        if (a.kc != bb.kc) return a.kc < bb.kc;
+        return std::lexicographical_compare(a.g, a.g + 4, bb.g, bb.g + 4);
+    });
+    p.pos.resize(C);
+    p.cons_kclass.resize(C);
+    for (uint32_t i = 0; i < C; ++i) {
+        p.pos[p.order[i]] = i;
+        p.cons_kclass[i] = kcl[p.order[i]];
+    }
+    // 4. tiles + records over the JIT prefix
+    uint32_t i = 0;
+    std::vector<uint32_t> local;
+    while (i < C && p.kclasses[p.cons_kclass[i]].jit) {
+        const uint32_t kc = p.cons_kclass[i];
+        const KClass& K = p.kclasses[kc];
+        TileDesc T{kc, i, 0, (uint32_t)p.tile_vars.size(), 0, (uint32_t)(p.recs.size() / 4), 0, 0};
+        local.clear();
+        const Key& k0 = keys[p.order[i]];
+        while (i < C && p.cons_kclass[i] == kc && T.n_cons < kTileCmax) {
+            const Key& ki = keys[p.order[i]];
+            if (T.n_cons > 0 && (memcmp(ki.g, k0.g, sizeof(k0.g)) != 0)) break;
+            cons_vars(p.order[i], vars);
+            size_t add = 0;
+            for (uint32_t u : vars)
+                if (std::find(local.begin(), local.end(), u) == local.end()) ++add;
+            if (T.n_cons > 0 && local.size() + add > kTileVmax) break;
+            if (local.size() + add > kTileVmax) break;   // a single constraint over > VMAX vars: generic path
+            for (uint32_t u : vars)
+                if (std::find(local.begin(), local.end(), u) == local.end()) local.push_back(u);
+            // record
+            const uint32_t c = p.order[i];
+            const Template& t = b.tmpls[K.tmpl];
+            const uint32_t* ids = b.slot_ids.data() + b.cons_slot_off[c];
+            std::vector<uint32_t> rec(K.stride4 * 4, 0);
+            float w = b.cons_w[c];
+            memcpy(&rec[0], &w, 4);
+            uint32_t ref = 0;
+            auto put_ref = [&](uint32_t u) {
+                uint32_t l = (uint32_t)(std::find(local.begin(), local.end(), u) - local.begin());
+                rec[1 + ref / 2] |= (l & 0xFFFFu) << (16 * (ref % 2));
+                ++ref;
+            };
+            uint32_t aw = 1 + (K.n_refs + 1) / 2;
+            for (size_t s = 0; s < t.kinds.size(); ++s) {
+                if (t.kinds[s] == 0) {
+                    put_ref(ids[s]);
+                } else {
+                    uint32_t atom = ids[s];
+                    float rhs = (float)f.atom_rhs[atom];
+                    double n2 = 0.0;
+                    for (uint32_t kk = f.atom_rowptr[atom]; kk < f.atom_rowptr[atom + 1]; ++kk)
+                        n2 += f.atom_val[kk] * f.atom_val[kk];
+                    float inv = (float)(1.0 / std::sqrt(n2));
+                    memcpy(&rec[aw], &rhs, 4);
+                    memcpy(&rec[aw + 1], &inv, 4);
+                    aw += 2;
+                    for (uint32_t kk = f.atom_rowptr[atom]; kk < f.atom_rowptr[atom + 1]; ++kk) {
+                        put_ref(f.n_bool + f.atom_col[kk]);
+                        float q = (float)f.atom_val[kk];
+                        memcpy(&rec[aw++], &q, 4);
+                    }
+                }
+            }
+            p.recs.insert(p.recs.end(), rec.begin(), rec.end());
+            ++T.n_cons;
+            ++i;
+        }
+        if (T.n_cons == 0) break;   // cannot tile (too many variables): rest is generic
+        T.n_vars = (uint32_t)local.size();
+        p.tile_vars.insert(p.tile_vars.end(), local.begin(), local.end());
+        p.tiles.push_back(T);
+    }
+    p.jit_cons_end = i;
+    // any JIT-class constraints after the cut run through the generic kernel
+    return p;
+}
+
+// ------------------------------------------------------------------------------ codegen
+
+namespace {
+
+std::string fnum(float v) {
+    char buf[64];
+    snprintf(buf, sizeof(buf), "%.9gf", v);
+    return buf;
+}
+
+const char* comp(uint32_t w) {
+    static const char* c[] = {"x", "y", "z", "w"};
+    return c[w % 4];
+}
+
+std::string word(uint32_t w) { return "q" + std::to_string(w / 4) + "." + comp(w); }
+
+void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Template& t) {
+    const size_t ns = t.kinds.size();
+    o << "__device__ __forceinline__ void kc" << kid
+      << "(const TileDesc& T, const uint4* __restrict__ rp, const u32* __restrict__ vs, float* __restrict__ accs,\n"
+         "    const float* __restrict__ a, const float* __restrict__ b, const unsigned char* __restrict__ U,\n"
+         "    u32 R, u64 rr, u32 r, bool live, u32 n_bool, float kq, float dcoef, float wscale, double& objacc,\n"
+         "    double* __restrict__ terms, u32 terms_r, const u32* __restrict__ orig) {\n";
+    // refs
+    std::vector<int> ref_kind;      // 0 Boolean, 1 real
+    std::vector<int> slot_ref0(ns);
+    for (size_t s = 0, ai = 0; s < ns; ++s) {
+        slot_ref0[s] = (int)ref_kind.size();
+        if (t.kinds[s] == 0) {
+            ref_kind.push_back(0);
+        } else {
+            const uint32_t nz = K.nnz[ai++];
+            for (uint32_t k = 0; k < nz; ++k) ref_kind.push_back(1);
+        }
+    }
+    const size_t nr = ref_kind.size();
+    for (size_t i = 0; i < nr; ++i) o << "  u32 cur" << i << " = 0xffffffffu; float val" << i << " = 0.f, acc" << i << " = 0.f;\n";
+    o << "  for (u32 c = 0; c < T.n_cons; ++c, rp += " << K.stride4 << ") {\n";
+    for (uint32_t q = 0; q < K.stride4; ++q) o << "    const uint4 q" << q << " = __ldg(rp + " << q << ");\n";
+    o << "    float w = __uint_as_float(q0.x) * wscale;\n"
+         "    if (U) w = ldexpf(w, (int)U[(u64)(T.cons_begin + c) * R + rr]);\n";
+    for (size_t i = 0; i < nr; ++i) {
+        uint32_t wd = 1 + (uint32_t)i / 2;
+        o << "    { const u32 l = (" << word(wd) << " >> " << (16 * (i % 2)) << ") & 0xffffu; if (l != cur" << i
+          << ") { if (cur" << i << " != 0xffffffffu) accs[cur" << i << " * 32] += acc" << i << "; cur" << i
+          << " = l; acc" << i << " = 0.f; val" << i << " = "
+          << (ref_kind[i] == 0 ? "a[(u64)vs[l] * R + rr]" : "b[(u64)(vs[l] - n_bool) * R + rr]") << "; } }\n";
+    }
+    // slot probabilities
+    uint32_t aw = 1 + ((uint32_t)nr + 1) / 2;
+    std::vector<uint32_t> coef_word(nr, 0);
+    for (size_t s = 0, ai = 0; s < ns; ++s) {
+        if (t.kinds[s] == 0) {
+            o << "    const float pt" << s << " = 0.5f * (1.f - val" << slot_ref0[s] << "), pf" << s << " = 0.5f * (1.f + val"
+              << slot_ref0[s] << ");\n";
+        } else {
+            const uint32_t nnz = K.nnz[ai++];
+            o << "    float z" << s << " = -__uint_as_float(" << word(aw) << ");\n";
+            o << "    const float inv" << s << " = __uint_as_float(" << word(aw + 1) << ");\n";
+            for (uint32_t k = 0; k < nnz; ++k) {
+                coef_word[slot_ref0[s] + k] = aw + 2 + k;
+                o << "    z" << s << " = fmaf(__uint_as_float(" << word(aw + 2 + k) << "), val" << slot_ref0[s] + k << ", z" << s << ");\n";
+            }
+            aw += 2 + nnz;
+            o << "    const float u" << s << " = kq * z" << s << " * inv" << s << ";\n"
+              << "    const float e" << s << " = 0.5f * erfcf(fabsf(u" << s << "));\n"
+              << "    const float pt" << s << " = u" << s << " >= 0.f ? e" << s << " : 1.f - e" << s << ";\n"
+              << "    const float pf" << s << " = u" << s << " >= 0.f ? 1.f - e" << s << " : e" << s << ";\n"
+              << "    const float dd" << s << " = dcoef * inv" << s << " * expf(-u" << s << " * u" << s << ");\n";
+        }
+    }
+    // forward pass (Alg.F): m_td in registers
+    const size_t nn = t.nodes.size();
+    for (size_t v = 0; v < nn; ++v) o << "    float m" << v << " = " << ((int)v == t.root ? "1.f" : "0.f") << ";\n";
+    o << "    float pT = 0.f;\n";
+    for (size_t v = 0; v < nn; ++v) {
+        const TNode& nd = t.nodes[v];
+        auto push = [&](int child, const char* pn) {
+            if (child >= 0) o << "    m" << child << " = fmaf(" << pn << nd.level << ", m" << v << ", m" << child << ");\n";
+            else if (child == kTrue) o << "    pT = fmaf(" << pn << nd.level << ", m" << v << ", pT);\n";
+        };
+        push(nd.hi, "pt");
+        push(nd.lo, "pf");
+    }
+    // backward pass (Alg.B, sign R1): m_bu in registers, dE/dv per slot
+    for (size_t s = 0; s < ns; ++s) o << "    float G" << s << " = 0.f;\n";
+    auto bu = [&](int child) -> std::string {
+        if (child >= 0) return "bu" + std::to_string(child);
+        return child == kTrue ? "1.f" : "0.f";
+    };
+    for (size_t vv = nn; vv-- > 0;) {
+        const TNode& nd = t.nodes[vv];
+        std::string bh = bu(nd.hi), bl = bu(nd.lo);
+        std::string lv = std::to_string(nd.level);
+        // m_bu[v] = p m_bu[hi] + (1-p) m_bu[lo]
+        std::string val;
+        if (bh == "1.f" && bl == "0.f") val = "pt" + lv;
+        else if (bh == "0.f" && bl == "1.f") val = "pf" + lv;
+        else if (bh == "1.f") val = "fmaf(pf" + lv + ", " + bl + ", pt" + lv + ")";
+        else if (bl == "1.f") val = "fmaf(pt" + lv + ", " + bh + ", pf" + lv + ")";
+        else if (bh == "0.f") val = "pf" + lv + " * " + bl;
+        else if (bl == "0.f") val = "pt" + lv + " * " + bh;
+        else val = "fmaf(pt" + lv + ", " + bh + ", pf" + lv + " * " + bl + ")";
+        o << "    const float bu" << vv << " = " << val << ";\n";
+        std::string diff;
+        if (bh == "1.f" && bl == "0.f") diff = "";
+        else if (bh == "0.f" && bl == "1.f") diff = "-";
+        else diff = "(" + bh + " - " + bl + ")";
+        if (diff.empty()) o << "    G" << lv << " += m" << vv << ";\n";
+        else if (diff == "-") o << "    G" << lv << " -= m" << vv << ";\n";
+        else o << "    G" << lv << " = fmaf(m" << vv << ", " << diff << ", G" << lv << ");\n";
+    }
+    o << "    const float E = 1.f - 2.f * pT;\n"
+         "    objacc += (double)w * (double)E;\n"
+         "    if (terms != nullptr && live && r == terms_r) terms[orig[T.cons_begin + c]] = (double)E;\n";
+    for (size_t s = 0; s < ns; ++s) {
+        if (t.kinds[s] == 0) {
+            o << "    acc" << slot_ref0[s] << " = fmaf(w, G" << s << ", acc" << slot_ref0[s] << ");\n";
+        } else {
+            o << "    { const float gd = w * G" << s << " * dd" << s << ";\n";
+            size_t ai = 0;
+            for (size_t s2 = 0; s2 < s; ++s2) ai += t.kinds[s2] == 1;
+            for (uint32_t k = 0; k < K.nnz[ai]; ++k) {
+                int ri = slot_ref0[s] + (int)k;
+                o << "      acc" << ri << " = fmaf(gd, __uint_as_float(" << word(coef_word[ri]) << "), acc" << ri << ");\n";
+            }
+            o << "    }\n";
+        }
+    }
+    o << "  }\n";
+    for (size_t i = 0; i < nr; ++i) o << "  if (cur" << i << " != 0xffffffffu) accs[cur" << i << " * 32] += acc" << i << ";\n";
+    o << "}\n\n";
+}
+
+}  // namespace
+
+std::string jit_source(const Formula& f, const Built& b, const Plan& p) {
+    std::ostringstream o;
+    o << "// generated by fsmt tiles.cpp: specialised K1 sweep for " << p.n_jit_kclasses << " kernel classes\n"
+         "typedef unsigned int u32;\ntypedef unsigned long long u64;\n"
+         "struct TileDesc { u32 kclass, cons_begin, n_cons, var_off, n_vars, rec_off, pad0, pad1; };\n"
+      << "#define VMAX " << kTileVmax << "\n#define WARPS 2\n\n";
+    for (uint32_t k = 0; k < p.n_jit_kclasses; ++k) emit_class(o, k, p.kclasses[k], b.tmpls[p.kclasses[k].tmpl]);
+    o << "extern \"C\" __global__ void __launch_bounds__(WARPS * 32) fsmt_k1_jit(\n"
+         "    const TileDesc* __restrict__ tiles, u32 n_tiles, const uint4* __restrict__ recs,\n"
+         "    const u32* __restrict__ tile_vars, const float* __restrict__ a, const float* __restrict__ b,\n"
+         "    double* __restrict__ ga, double* __restrict__ gb, const unsigned char* __restrict__ U,\n"
+         "    double* __restrict__ obj, u32 R, u32 n_bool, float kappa, float wscale,\n"
+         "    double* __restrict__ terms, u32 terms_r, const u32* __restrict__ orig) {\n"
+         "  extern __shared__ float smem[];\n"
+         "  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;\n"
+         "  float* acc = smem + warp * (VMAX * 32);\n"
+         "  u32* vs = (u32*)(smem + WARPS * VMAX * 32) + warp * VMAX;\n"
+         "  const u32 rtiles = (R + 31) / 32;\n"
+         "  const u64 gw = (u64)blockIdx.x * WARPS + warp;\n"
+         "  const u32 rt = (u32)(gw % rtiles);\n"
+         "  const u64 ti = gw / rtiles;\n"
+         "  if (ti >= n_tiles) return;\n"
+         "  const TileDesc T = tiles[ti];\n"
+         "  const u32 r = rt * 32 + lane;\n"
+         "  const bool live = r < R;\n"
+         "  const u64 rr = live ? r : 0;\n"
+         "  for (u32 l = lane; l < T.n_vars; l += 32) vs[l] = tile_vars[T.var_off + l];\n"
+         "  for (u32 l = 0; l < T.n_vars; ++l) acc[l * 32 + lane] = 0.f;\n"
+         "  __syncwarp();\n"
+         "  const float kq = kappa * 0.70710678118654752f;\n"
+         "  const float dcoef = kappa * 0.79788456080286536f;\n"
+         "  double objacc = 0.0;\n"
+         "  const uint4* rp = recs + T.rec_off;\n"
+         "  switch (T.kclass) {\n";
+    for (uint32_t k = 0; k < p.n_jit_kclasses; ++k)
+        o << "    case " << k << ": kc" << k
+          << "(T, rp, vs, acc + lane, a, b, U, R, rr, r, live, n_bool, kq, dcoef, wscale, objacc, terms, terms_r, orig); break;\n";
+    o << "    default: break;\n  }\n"
+         "  __syncwarp();\n"
+         "  if (!live) return;\n"
+         "  for (u32 l = 0; l < T.n_vars; ++l) {\n"
+         "    const u32 g = vs[l];\n"
+         "    const double v = (double)acc[l * 32 + lane];\n"
+         "    if (g < n_bool) atomicAdd(ga + (u64)g * R + r, v); else atomicAdd(gb + (u64)(g - n_bool) * R + r, v);\n"
+         "  }\n"
+         "  atomicAdd(obj + r, objacc);\n"
+         "}\n";
+    (void)f;
+    return o.str();
+}
+
+}  // namespace fsmt

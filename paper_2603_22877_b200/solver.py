@@ -212,6 +212,27 @@ class Solver:
         self._check(N.lib.fsmt_device_buffers(self._h, *[C.byref(p) for p in ptrs]))
         return dict(zip(["a", "b", "grad_a", "grad_b", "U", "obj", "unsat"], [p.value for p in ptrs]))
 
+    def jit_info(self) -> dict:
+        n1, n2, n3 = C.c_uint32(), C.c_uint32(), C.c_uint32()
+        buf = C.create_string_buffer(4096)
+        self._check(N.lib.fsmt_jit_info(self._h, C.byref(n1), C.byref(n2), C.byref(n3), buf, 4096))
+        return {"jit_classes": n1.value, "tiles": n2.value, "jit_cons": n3.value, "status": buf.value.decode()}
+
+    def jit_check(self):
+        """NVRTC-compile the specialised sweep (no device needed): (cubin bytes, compiler log)."""
+        n = C.c_size_t()
+        buf = C.create_string_buffer(1 << 16)
+        self._check(N.lib.fsmt_jit_check(self._h, C.byref(n), buf, 1 << 16))
+        return n.value, buf.value.decode(errors="replace")
+
+    def jit_source(self) -> str:
+        n = N.lib.fsmt_jit_source(self._h, None, 0)
+        if n == 0:
+            return ""
+        buf = C.create_string_buffer(n)
+        N.lib.fsmt_jit_source(self._h, buf, n)
+        return buf.value.decode()
+
     def time_sweep(self, kappa: float, stage_t: int, iters: int) -> float:
         ms = C.c_double()
         self._check(N.lib.fsmt_time_sweep(self._h, kappa, stage_t, iters, C.byref(ms)))

@@ -151,3 +151,21 @@ def test_dims_cfg3_cfg4_shapes():
     assert d["n_bool"] + d["n_real"] == 2240 and d["n_cons"] == inst.n_cons
     # 1 non-overlap template (14 nodes, 10 slots) + feasibility (5 nodes) + unit atom
     assert d["max_nodes"] == 14 and d["max_slots"] == 10
+
+
+@pytest.mark.parametrize("name", ["cfg3s", "cfg4s"])
+def test_jit_source_compiles_for_sm100a(tmp_path, name):
+    """The specialised sweep emitted by the plan (tiles.cpp) is valid sm_100a CUDA without spills."""
+    import subprocess
+    s = _host(fsmt_gen.config(name).text)
+    info = s.jit_info()
+    assert info["jit_classes"] >= 1 and info["tiles"] >= 1 and info["status"] == "host-only"
+    src = s.jit_source()
+    assert "fsmt_k1_jit" in src
+    cu = tmp_path / "k1.cu"
+    cu.write_text(src)
+    out = subprocess.run(["/usr/local/cuda/bin/nvcc", "-cubin", "-gencode", "arch=compute_100a,code=sm_100a", "-O3",
+                          "-Xptxas", "-v", str(cu), "-o", str(tmp_path / "k1.cubin")],
+                         capture_output=True, text=True)
+    assert out.returncode == 0, out.stderr[-3000:]
+    assert "0 bytes spill stores" in out.stderr, out.stderr[-2000:]

@@ -335,3 +335,34 @@ def test_restart_offset_independence(gpu_mod):
     af, bf = full.get_state()
     ah, bh = half.get_state()
     assert np.allclose(af[:, 32:], ah, atol=1e-6) and np.allclose(bf[:, 32:], bh, atol=1e-6)
+
+
+# ------------------------------------------------------------------------------------- JIT path
+
+@pytest.mark.parametrize("name", ["cfg3s", "cfg4s"])
+def test_jit_active_and_matches_generic(gpu_mod, name, monkeypatch):
+    """The JIT-specialised sweep is the one that runs, and it agrees with the generic kernel."""
+    inst, f = parsed(name)
+    jit = make(gpu_mod, inst.text)
+    info = jit.jit_info()
+    assert info["status"] == "active" and info["jit_cons"] > 0, info
+    monkeypatch.setenv("FSMT_JIT", "0")
+    gen = make(gpu_mod, inst.text)
+    assert gen.jit_info()["jit_cons"] == 0
+    R = 96
+    a, b = random_points(f.n_bool, f.n_real, R, seed=31, b_lo=0.0, b_hi=1.0)
+    U = random_counters(len(f.constraints), R, seed=32, max_u=3)
+    outs = []
+    for s in (jit, gen):
+        s.begin(R, 5)
+        s.set_state(a, b)
+        s.set_counters(U)
+        assert np.array_equal(s.get_counters(), U)
+        s.sweep(1.3, 4)
+        outs.append(s.get_sweep())
+        E = s.constraint_terms(1.3, 7)
+        outs.append((E,))
+    (oj, gaj, gbj), (Ej,), (og, gag, gbg), (Eg,) = outs
+    assert np.allclose(oj, og, rtol=1e-6, atol=1e-6)
+    assert np.allclose(gaj, gag, rtol=1e-5, atol=1e-6) and np.allclose(gbj, gbg, rtol=1e-5, atol=1e-6)
+    assert np.max(np.abs(Ej - Eg)) <= 1e-6
