@@ -278,10 +278,18 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
     }
     const size_t nr = ref_kind.size();
     for (size_t i = 0; i < nr; ++i) o << "  u32 cur" << i << " = 0xffffffffu; float val" << i << " = 0.f, acc" << i << " = 0.f;\n";
+    // software pipeline: the record and U counter of constraint c+1 are loaded while c is evaluated
+    for (uint32_t q = 0; q < K.stride4; ++q) o << "  uint4 nq" << q << " = make_uint4(0u, 0u, 0u, 0u);\n";
+    o << "  u32 nU = 0u;\n  if (T.n_cons) {\n";
+    for (uint32_t q = 0; q < K.stride4; ++q) o << "    nq" << q << " = __ldg(rp + " << q << ");\n";
+    o << "    if (U) nU = U[(u64)T.cons_begin * R + rr];\n  }\n";
     o << "  for (u32 c = 0; c < T.n_cons; ++c, rp += " << K.stride4 << ") {\n";
-    for (uint32_t q = 0; q < K.stride4; ++q) o << "    const uint4 q" << q << " = __ldg(rp + " << q << ");\n";
+    for (uint32_t q = 0; q < K.stride4; ++q) o << "    const uint4 q" << q << " = nq" << q << ";\n";
+    o << "    const u32 uc = nU;\n    if (c + 1 < T.n_cons) {\n";
+    for (uint32_t q = 0; q < K.stride4; ++q) o << "      nq" << q << " = __ldg(rp + " << K.stride4 + q << ");\n";
+    o << "      if (U) nU = U[(u64)(T.cons_begin + c + 1) * R + rr];\n    }\n";
     o << "    float w = __uint_as_float(q0.x) * wscale;\n"
-         "    if (U) w = ldexpf(w, (int)U[(u64)(T.cons_begin + c) * R + rr]);\n";
+         "    if (U) w = ldexpf(w, (int)uc);\n";
     for (size_t i = 0; i < nr; ++i) {
         uint32_t wd = 1 + (uint32_t)i / 2;
         o << "    { const u32 l = (" << word(wd) << " >> " << (16 * (i % 2)) << ") & 0xffffu; if (l != cur" << i
@@ -384,7 +392,9 @@ std::string jit_source(const Formula& f, const Built& b, const Plan& p) {
          "struct TileDesc { u32 kclass, cons_begin, n_cons, var_off, n_vars, rec_off, pad0, pad1; };\n"
       << "#define VMAX " << kTileVmax << "\n#define WARPS 2\n\n";
     for (uint32_t k = 0; k < p.n_jit_kclasses; ++k) emit_class(o, k, p.kclasses[k], b.tmpls[p.kclasses[k].tmpl]);
-    o << "extern \"C\" __global__ void __launch_bounds__(WARPS * 32) fsmt_k1_jit(\n"
+    const char* minb = getenv("FSMT_JIT_MINB");      // optional min CTAs/SM (register cap), A/B tuning
+    o << "extern \"C\" __global__ void __launch_bounds__(WARPS * 32" << (minb && atoi(minb) > 0 ? std::string(", ") + minb : std::string())
+      << ") fsmt_k1_jit(\n"
          "    const TileDesc* __restrict__ tiles, u32 n_tiles, const uint4* __restrict__ recs,\n"
          "    const u32* __restrict__ tile_vars, const float* __restrict__ a, const float* __restrict__ b,\n"
          "    double* __restrict__ ga, double* __restrict__ gb, const unsigned char* __restrict__ U,\n"

@@ -1,0 +1,62 @@
+#!/usr/bin/env python
+"""Time-to-SAT (BASELINE metric, second half): fsmt_solve wall time from call to verified
+return, excluding load/build (reported separately), median over seeds (paper protocol:
+8 replicas, median; 1000 s cap).
+
+  python scripts/time_to_sat.py --config cfg4 --restarts 1024 --steps 50 --seeds 0 1 2 3 4 5 6 7
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--config", default="cfg4")
+    p.add_argument("--restarts", type=int, default=1024)
+    p.add_argument("--steps", type=int, default=50)
+    p.add_argument("--seeds", type=int, nargs="+", default=list(range(8)))
+    p.add_argument("--eta", type=float, default=0.05)
+    p.add_argument("--kappas", type=str, default="")
+    p.add_argument("--erwa", type=int, default=0)
+    p.add_argument("--rounding", type=int, default=0)
+    p.add_argument("--time-limit", type=float, default=1000.0)
+    a = p.parse_args()
+    import paper_2603_22877_b200 as P
+    import fsmt_gen
+    from paper_2603_22877_b200 import native as N
+
+    inst = fsmt_gen.config(a.config)
+    s = P.Solver(0)
+    t0 = time.perf_counter()
+    s.load_formula(inst.text)
+    s.build_xbdd()
+    build_s = time.perf_counter() - t0
+    kappas = [float(x) for x in a.kappas.split(",")] if a.kappas else None
+    s.set_params(kappas=kappas, eta=a.eta, erwa_mode=a.erwa, rounding=a.rounding, time_limit_s=a.time_limit)
+    runs = []
+    for seed in a.seeds:
+        res = s.solve(a.restarts, a.steps, seed)
+        ok = res.verdict == N.SAT and s.verify(res.x, res.y) == 0
+        runs.append({"seed": seed, "verdict": "SAT" if res.verdict == N.SAT else "UNKNOWN", "verified": bool(ok),
+                     "solve_s": res.stats["solve_ms"] / 1e3, "stage": res.stats["winner_stage"],
+                     "best_unsat": res.stats["best_unsat"], "timeout": res.stats["timeout"]})
+        print(json.dumps(runs[-1]), flush=True)
+    times = [r["solve_s"] if r["verdict"] == "SAT" else float("inf") for r in runs]
+    med = statistics.median(times)
+    print(json.dumps({"config": a.config, "restarts": a.restarts, "steps_per_stage": a.steps, "eta": a.eta,
+                      "build_s": build_s, "median_time_to_sat_s": med if med != float("inf") else None,
+                      "solved": sum(r["verdict"] == "SAT" for r in runs), "runs": len(runs),
+                      "jit": s.jit_info()}))
+
+
+if __name__ == "__main__":
+    main()

@@ -364,5 +364,7 @@ def test_jit_active_and_matches_generic(gpu_mod, name, monkeypatch):
         outs.append((E,))
     (oj, gaj, gbj), (Ej,), (og, gag, gbg), (Eg,) = outs
     assert np.allclose(oj, og, rtol=1e-6, atol=1e-6)
-    assert np.allclose(gaj, gag, rtol=1e-5, atol=1e-6) and np.allclose(gbj, gbg, rtol=1e-5, atol=1e-6)
+    # weighted (U <= 3, stage 4): scale-relative bar of reading R28
+    for gj, gg in ((gaj, gag), (gbj, gbg)):
+        assert np.max(np.abs(gj - gg)) <= 1e-5 * max(1.0, float(np.max(np.abs(gg))))
     assert np.max(np.abs(Ej - Eg)) <= 1e-6
