@@ -388,6 +388,7 @@ fsmt_status fsmt_build_xbdd(fsmt_ctx* ctx, uint64_t node_budget) {
             ctx->T.n_tiles = (uint32_t)P.tiles.size();
             ctx->T.recs = rp;
             ctx->T.tile_vars = vp;
+            ctx->T.warps = P.jit_warps;
             F.generic_begin = P.jit_cons_end;
         } else {
             ctx->jit_error = err;

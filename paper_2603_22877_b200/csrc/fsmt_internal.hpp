@@ -102,6 +102,7 @@ struct KClass {
     uint32_t stride4;            // record stride in uint4
     bool jit;
     uint64_t n_cons;
+    std::vector<uint8_t> stream;  // per reference: 1 = changes most constraints (no run register)
 };
 
 struct TileDesc {                // mirrored in the JIT source (32 bytes)
@@ -118,6 +119,7 @@ struct Plan {
     std::vector<uint32_t> recs;       // JIT records (uint32 words, stride4*4 per constraint)
     uint32_t jit_cons_end = 0;        // internal [0, jit_cons_end) are JIT constraints
     uint32_t n_jit_kclasses = 0;
+    uint32_t jit_warps = 1;           // warps per CTA of the JIT sweep (A/B: profiles/README.md)
 };
 
 Plan make_plan(const Formula& f, const Built& b, bool enable_jit);

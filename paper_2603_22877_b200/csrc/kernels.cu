@@ -335,7 +335,8 @@ void launch_scatter_rows_u8(uint8_t* dst, const uint8_t* src, const uint32_t* id
 void launch_sweep_jit(cudaKernel_t k, const DevFormula& F, const DevState& S, const DevTiles& T, float kappa,
                       float wscale, double* terms, uint32_t terms_r, cudaStream_t st) {
     if (T.n_tiles == 0 || S.R == 0) return;
-    constexpr int kJitWarps = 2, kVmax = 128;                       // must match tiles.cpp
+    const int kJitWarps = (int)(T.warps ? T.warps : 1);
+    constexpr int kVmax = 128;                                      // must match tiles.cpp (kTileVmax)
     const uint64_t nw = (uint64_t)T.n_tiles * ((S.R + 31) / 32);
     const unsigned blocks = (unsigned)((nw + kJitWarps - 1) / kJitWarps);
     const size_t smem = (size_t)kJitWarps * (kVmax * 32 * 4 + kVmax * 4);

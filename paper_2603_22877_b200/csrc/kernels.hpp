@@ -71,6 +71,7 @@ struct DevTiles {
     uint32_t n_tiles;
     const void* recs;            // uint4 records
     const uint32_t* tile_vars;
+    uint32_t warps;              // warps per CTA (Plan::jit_warps)
 };
 void launch_sweep_jit(cudaKernel_t k, const DevFormula& F, const DevState& S, const DevTiles& T, float kappa,
                       float wscale, double* terms, uint32_t terms_r, cudaStream_t st);

@@ -32,6 +32,7 @@ constexpr uint64_t kJitMinCons = 32;      // specialise only classes with enough
 
 Plan make_plan(const Formula& f, const Built& b, bool enable_jit) {
     Plan p;
+    if (const char* w = getenv("FSMT_JIT_WARPS")) p.jit_warps = std::max(1, std::min(8, atoi(w)));
     const uint32_t C = (uint32_t)b.cons_tmpl.size();
     // 1. kernel classes
     std::map<std::vector<uint32_t>, uint32_t> kc_of;
@@ -237,6 +238,31 @@ Plan make_plan(const Formula& f, const Built& b, bool enable_jit) {
     }
     p.jit_cons_end = i;
     // any JIT-class constraints after the cut run through the generic kernel
+
+    // 5. per kernel class and reference position: does the local variable change from one
+    //    constraint to the next within a tile most of the time ("stream": accumulate straight
+    //    into the tile accumulator) or rarely ("run": register accumulation over the run)?
+    std::vector<std::vector<uint64_t>> changes(p.n_jit_kclasses);
+    std::vector<uint64_t> seen(p.n_jit_kclasses, 0);
+    for (uint32_t k = 0; k < p.n_jit_kclasses; ++k) changes[k].assign(p.kclasses[k].n_refs, 0);
+    for (const TileDesc& T : p.tiles) {
+        const KClass& K = p.kclasses[T.kclass];
+        for (uint32_t c = 0; c < T.n_cons; ++c) {
+            const uint32_t* rec = p.recs.data() + ((size_t)T.rec_off + (size_t)c * K.stride4) * 4;
+            const uint32_t* prev = rec - K.stride4 * 4;
+            for (uint32_t r = 0; r < K.n_refs; ++r) {
+                const uint32_t l = (rec[1 + r / 2] >> (16 * (r % 2))) & 0xFFFFu;
+                const uint32_t lp = c ? (prev[1 + r / 2] >> (16 * (r % 2))) & 0xFFFFu : 0xFFFFFFFFu;
+                changes[T.kclass][r] += (l != lp);
+            }
+            seen[T.kclass] += 1;
+        }
+    }
+    for (uint32_t k = 0; k < p.n_jit_kclasses; ++k) {
+        p.kclasses[k].stream.assign(p.kclasses[k].n_refs, 0);
+        for (uint32_t r = 0; r < p.kclasses[k].n_refs; ++r)
+            p.kclasses[k].stream[r] = seen[k] && 2 * changes[k][r] > seen[k];
+    }
     return p;
 }
 
@@ -249,6 +275,35 @@ std::string fnum(float v) {
     snprintf(buf, sizeof(buf), "%.9gf", v);
     return buf;
 }
+
+// Default: the short erfc below (max abs error ~8e-8 on 0.5*erfc);
+// FSMT_JIT_ERFC=cuda selects CUDA's erfcf + expf (A/B).
+bool fast_erfc() {
+    const char* e = getenv("FSMT_JIT_ERFC");
+    return !(e && std::string(e) == "cuda");
+}
+
+const char* kErfcPrelude =
+    "__device__ __forceinline__ float fsmt_ex2(float x) { float r; asm(\"ex2.approx.ftz.f32 %0, %1;\" : \"=f\"(r) : \"f\"(x)); return r; }\n"
+    "// 0.5*erfc(z) for z >= 0 and ez = exp(-z^2) (dd/db factor, P:1326-1327).\n"
+    "// z < 0.75: 1 - erf(z) from the Maclaurin series of erf (10 terms); z >= 0.75: Numerical Recipes\n"
+    "// erfcc, t exp(-z^2 + P(t)), t = 1/(1 + z/2), fractional error < 1.2e-7.\n"
+    "__device__ __forceinline__ float fsmt_half_erfc(float z, float& ez) {\n"
+    "  const float z2 = z * z;\n"
+    "  ez = fsmt_ex2(-1.44269504088896341f * z2);\n"
+    "  float q = -1.4503291e-7f;\n"
+    "  q = fmaf(q, z2, 1.4589169e-6f); q = fmaf(q, z2, -1.3227513e-5f); q = fmaf(q, z2, 1.0683761e-4f);\n"
+    "  q = fmaf(q, z2, -7.5757576e-4f); q = fmaf(q, z2, 4.6296296e-3f); q = fmaf(q, z2, -2.3809524e-2f);\n"
+    "  q = fmaf(q, z2, 0.1f); q = fmaf(q, z2, -0.33333333f); q = fmaf(q, z2, 1.f);\n"
+    "  const float small = fmaf(-1.12837916709551257f * z, q, 1.f);\n"
+    "  const float t = __fdividef(1.f, fmaf(0.5f, z, 1.f));\n"
+    "  float p = 0.17087277f;\n"
+    "  p = fmaf(p, t, -0.82215223f); p = fmaf(p, t, 1.48851587f); p = fmaf(p, t, -1.13520398f);\n"
+    "  p = fmaf(p, t, 0.27886807f); p = fmaf(p, t, -0.18628806f); p = fmaf(p, t, 0.09678418f);\n"
+    "  p = fmaf(p, t, 0.37409196f); p = fmaf(p, t, 1.00002368f); p = fmaf(p, t, -1.26551223f);\n"
+    "  const float tail = t * fsmt_ex2((p - z2) * 1.44269504088896341f);\n"
+    "  return 0.5f * (z < 0.75f ? small : tail);\n"
+    "}\n\n";
 
 const char* comp(uint32_t w) {
     static const char* c[] = {"x", "y", "z", "w"};
@@ -277,25 +332,44 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
         }
     }
     const size_t nr = ref_kind.size();
-    for (size_t i = 0; i < nr; ++i) o << "  u32 cur" << i << " = 0xffffffffu; float val" << i << " = 0.f, acc" << i << " = 0.f;\n";
-    // software pipeline: the record and U counter of constraint c+1 are loaded while c is evaluated
-    for (uint32_t q = 0; q < K.stride4; ++q) o << "  uint4 nq" << q << " = make_uint4(0u, 0u, 0u, 0u);\n";
-    o << "  u32 nU = 0u;\n  if (T.n_cons) {\n";
-    for (uint32_t q = 0; q < K.stride4; ++q) o << "    nq" << q << " = __ldg(rp + " << q << ");\n";
-    o << "    if (U) nU = U[(u64)T.cons_begin * R + rr];\n  }\n";
-    o << "  for (u32 c = 0; c < T.n_cons; ++c, rp += " << K.stride4 << ") {\n";
-    for (uint32_t q = 0; q < K.stride4; ++q) o << "    const uint4 q" << q << " = nq" << q << ";\n";
-    o << "    const u32 uc = nU;\n    if (c + 1 < T.n_cons) {\n";
-    for (uint32_t q = 0; q < K.stride4; ++q) o << "      nq" << q << " = __ldg(rp + " << K.stride4 + q << ");\n";
-    o << "      if (U) nU = U[(u64)(T.cons_begin + c + 1) * R + rr];\n    }\n";
+    const char* ms_env = getenv("FSMT_JIT_STREAM");   // "0": every reference in run mode (A/B)
+    const bool use_stream = !(ms_env && ms_env[0] == '0');
+    auto is_stream = [&](size_t i) { return use_stream && i < K.stream.size() && K.stream[i]; };
+    for (size_t i = 0; i < nr; ++i)
+        if (!is_stream(i)) o << "  u32 cur" << i << " = 0xffffffffu; float val" << i << " = 0.f, acc" << i << " = 0.f;\n";
+    const char* pf_env = getenv("FSMT_JIT_PREFETCH");
+    const bool prefetch = pf_env && pf_env[0] == '1';
+    if (prefetch) {
+        // software pipeline: the record and U counter of constraint c+1 are loaded while c is evaluated
+        for (uint32_t q = 0; q < K.stride4; ++q) o << "  uint4 nq" << q << " = make_uint4(0u, 0u, 0u, 0u);\n";
+        o << "  u32 nU = 0u;\n  if (T.n_cons) {\n";
+        for (uint32_t q = 0; q < K.stride4; ++q) o << "    nq" << q << " = __ldg(rp + " << q << ");\n";
+        o << "    if (U) nU = U[(u64)T.cons_begin * R + rr];\n  }\n";
+        o << "  for (u32 c = 0; c < T.n_cons; ++c, rp += " << K.stride4 << ") {\n";
+        for (uint32_t q = 0; q < K.stride4; ++q) o << "    const uint4 q" << q << " = nq" << q << ";\n";
+        o << "    const u32 uc = nU;\n    if (c + 1 < T.n_cons) {\n";
+        for (uint32_t q = 0; q < K.stride4; ++q) o << "      nq" << q << " = __ldg(rp + " << K.stride4 + q << ");\n";
+        o << "      if (U) nU = U[(u64)(T.cons_begin + c + 1) * R + rr];\n    }\n";
+    } else {
+        o << "  for (u32 c = 0; c < T.n_cons; ++c, rp += " << K.stride4 << ") {\n";
+        for (uint32_t q = 0; q < K.stride4; ++q) o << "    const uint4 q" << q << " = __ldg(rp + " << q << ");\n";
+        o << "    const u32 uc = U ? (u32)U[(u64)(T.cons_begin + c) * R + rr] : 0u;\n";
+    }
     o << "    float w = __uint_as_float(q0.x) * wscale;\n"
          "    if (U) w = ldexpf(w, (int)uc);\n";
     for (size_t i = 0; i < nr; ++i) {
         uint32_t wd = 1 + (uint32_t)i / 2;
-        o << "    { const u32 l = (" << word(wd) << " >> " << (16 * (i % 2)) << ") & 0xffffu; if (l != cur" << i
-          << ") { if (cur" << i << " != 0xffffffffu) accs[cur" << i << " * 32] += acc" << i << "; cur" << i
-          << " = l; acc" << i << " = 0.f; val" << i << " = "
-          << (ref_kind[i] == 0 ? "a[(u64)vs[l] * R + rr]" : "b[(u64)(vs[l] - n_bool) * R + rr]") << "; } }\n";
+        const std::string ext = "(" + word(wd) + " >> " + std::to_string(16 * (i % 2)) + ") & 0xffffu";
+        const std::string ld = ref_kind[i] == 0 ? "a[(u64)vs[l] * R + rr]" : "b[(u64)(vs[l] - n_bool) * R + rr]";
+        if (is_stream(i)) {
+            // stream reference: new variable (almost) every constraint; no run register
+            o << "    const u32 sl" << i << " = " << ext << ";\n"
+              << "    float val" << i << ";\n    { const u32 l = sl" << i << "; val" << i << " = " << ld << "; }\n";
+        } else {
+            o << "    { const u32 l = " << ext << "; if (l != cur" << i << ") { if (cur" << i
+              << " != 0xffffffffu) accs[cur" << i << " * 32] += acc" << i << "; cur" << i << " = l; acc" << i
+              << " = 0.f; val" << i << " = " << ld << "; } }\n";
+        }
     }
     // slot probabilities
     uint32_t aw = 1 + ((uint32_t)nr + 1) / 2;
@@ -313,11 +387,15 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
                 o << "    z" << s << " = fmaf(__uint_as_float(" << word(aw + 2 + k) << "), val" << slot_ref0[s] + k << ", z" << s << ");\n";
             }
             aw += 2 + nnz;
-            o << "    const float u" << s << " = kq * z" << s << " * inv" << s << ";\n"
-              << "    const float e" << s << " = 0.5f * erfcf(fabsf(u" << s << "));\n"
-              << "    const float pt" << s << " = u" << s << " >= 0.f ? e" << s << " : 1.f - e" << s << ";\n"
+            o << "    const float u" << s << " = kq * z" << s << " * inv" << s << ";\n";
+            if (fast_erfc())
+                o << "    float ez" << s << ";\n    const float e" << s << " = fsmt_half_erfc(fabsf(u" << s << "), ez" << s << ");\n";
+            else
+                o << "    const float e" << s << " = 0.5f * erfcf(fabsf(u" << s << "));\n"
+                  << "    const float ez" << s << " = expf(-u" << s << " * u" << s << ");\n";
+            o << "    const float pt" << s << " = u" << s << " >= 0.f ? e" << s << " : 1.f - e" << s << ";\n"
               << "    const float pf" << s << " = u" << s << " >= 0.f ? 1.f - e" << s << " : e" << s << ";\n"
-              << "    const float dd" << s << " = dcoef * inv" << s << " * expf(-u" << s << " * u" << s << ");\n";
+              << "    const float dd" << s << " = dcoef * inv" << s << " * ez" << s << ";\n";
         }
     }
     // forward pass (Alg.F): m_td in registers
@@ -364,22 +442,29 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
     o << "    const float E = 1.f - 2.f * pT;\n"
          "    objacc += (double)w * (double)E;\n"
          "    if (terms != nullptr && live && r == terms_r) terms[orig[T.cons_begin + c]] = (double)E;\n";
+    auto accum = [&](int ri, const std::string& a, const std::string& b) {
+        if (is_stream((size_t)ri))
+            o << "      accs[sl" << ri << " * 32] = fmaf(" << a << ", " << b << ", accs[sl" << ri << " * 32]);\n";
+        else
+            o << "      acc" << ri << " = fmaf(" << a << ", " << b << ", acc" << ri << ");\n";
+    };
     for (size_t s = 0; s < ns; ++s) {
         if (t.kinds[s] == 0) {
-            o << "    acc" << slot_ref0[s] << " = fmaf(w, G" << s << ", acc" << slot_ref0[s] << ");\n";
+            accum(slot_ref0[s], "w", "G" + std::to_string(s));
         } else {
             o << "    { const float gd = w * G" << s << " * dd" << s << ";\n";
             size_t ai = 0;
             for (size_t s2 = 0; s2 < s; ++s2) ai += t.kinds[s2] == 1;
             for (uint32_t k = 0; k < K.nnz[ai]; ++k) {
                 int ri = slot_ref0[s] + (int)k;
-                o << "      acc" << ri << " = fmaf(gd, __uint_as_float(" << word(coef_word[ri]) << "), acc" << ri << ");\n";
+                accum(ri, "gd", "__uint_as_float(" + word(coef_word[ri]) + ")");
             }
             o << "    }\n";
         }
     }
     o << "  }\n";
-    for (size_t i = 0; i < nr; ++i) o << "  if (cur" << i << " != 0xffffffffu) accs[cur" << i << " * 32] += acc" << i << ";\n";
+    for (size_t i = 0; i < nr; ++i)
+        if (!is_stream(i)) o << "  if (cur" << i << " != 0xffffffffu) accs[cur" << i << " * 32] += acc" << i << ";\n";
     o << "}\n\n";
 }
 
@@ -390,7 +475,7 @@ std::string jit_source(const Formula& f, const Built& b, const Plan& p) {
     o << "// generated by fsmt tiles.cpp: specialised K1 sweep for " << p.n_jit_kclasses << " kernel classes\n"
          "typedef unsigned int u32;\ntypedef unsigned long long u64;\n"
          "struct TileDesc { u32 kclass, cons_begin, n_cons, var_off, n_vars, rec_off, pad0, pad1; };\n"
-      << "#define VMAX " << kTileVmax << "\n#define WARPS 2\n\n";
+      << "#define VMAX " << kTileVmax << "\n#define WARPS " << p.jit_warps << "\n\n" << kErfcPrelude;
     for (uint32_t k = 0; k < p.n_jit_kclasses; ++k) emit_class(o, k, p.kclasses[k], b.tmpls[p.kclasses[k].tmpl]);
     const char* minb = getenv("FSMT_JIT_MINB");      // optional min CTAs/SM (register cap), A/B tuning
     o << "extern \"C\" __global__ void __launch_bounds__(WARPS * 32" << (minb && atoi(minb) > 0 ? std::string(", ") + minb : std::string())
