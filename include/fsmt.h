@@ -167,6 +167,19 @@ fsmt_status fsmt_stage_end(fsmt_ctx* ctx, uint32_t stage_t, uint32_t* unsat_out)
 fsmt_status fsmt_run_stage(fsmt_ctx* ctx, uint32_t stage_t, float kappa, uint32_t steps, uint32_t* unsat_out,
                            uint32_t* min_unsat);
 
+/* Multi-GPU sharding. mode 0 = restart-sharded: this context evaluates every
+ * constraint (ranks differ only by fsmt_begin's restart_offset). mode 1 = constraint-sharded:
+ * this context sweeps (K1) and checks (K5) only its contiguous share of the constraints
+ * (tile range balanced by constraint count), so grad_a/grad_b/obj and unsat are PARTIAL sums
+ * the caller must all-reduce (SUM) across ranks before fsmt_update / before reading unsat;
+ * every rank then holds and updates all R restarts identically. Call after fsmt_build_xbdd. */
+fsmt_status fsmt_shard(fsmt_ctx* ctx, uint32_t rank, uint32_t world, uint32_t mode);
+/* Replace the ctx's grad_a[n_bool][R] f64, grad_b[n_real][R] f64, obj[R] f64 and unsat[R] u32
+ * device buffers with caller-owned device memory of the same shapes (NULL keeps the ctx's own),
+ * e.g. torch tensors that torch.distributed all-reduces. Valid until the next fsmt_begin; the
+ * caller keeps ownership and must keep them alive. */
+fsmt_status fsmt_bind_buffers(fsmt_ctx* ctx, void* grad_a, void* grad_b, void* obj, void* unsat);
+
 /* Rounded model of one restart from the last stage_end: x[n_bool] (-1/+1), y[n_real] (host). */
 fsmt_status fsmt_get_model(fsmt_ctx* ctx, uint32_t restart, int8_t* x_out, float* y_out);
 /* Rounded Booleans of all restarts from the last stage_end: x[n_bool][R] int8 (where). */

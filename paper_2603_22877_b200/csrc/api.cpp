@@ -38,6 +38,10 @@ struct fsmt_ctx {
     JitKernel jit;
     DevTiles T{};
     const uint32_t* d_pos = nullptr;   // original -> internal constraint index (device)
+    // constraint sharding (fsmt_shard): this context's part of the sweep and of the check
+    DevTiles T_all{};                  // every JIT tile
+    uint32_t vrange[2][2] = {{0, 0}, {0, 0}};   // internal constraint ranges verified by K5
+    uint32_t shard_mode = 0, shard_rank = 0, shard_world = 1;
     // params
     std::vector<float> kappas;
     float eta = 0.05f, eps = 1e-2f;
@@ -150,6 +154,7 @@ void drop_formula(fsmt_ctx* ctx) {
     ctx->F = DevFormula{};
     jit_release(ctx->jit);
     ctx->T = DevTiles{};
+    ctx->T_all = DevTiles{};
     ctx->d_pos = nullptr;
 }
 
@@ -389,11 +394,18 @@ fsmt_status fsmt_build_xbdd(fsmt_ctx* ctx, uint64_t node_budget) {
             ctx->T.recs = rp;
             ctx->T.tile_vars = vp;
             ctx->T.warps = P.jit_warps;
+            ctx->T.vmax = P.vmax;
             F.generic_begin = P.jit_cons_end;
         } else {
             ctx->jit_error = err;
         }
     }
+    F.generic_end = F.n_cons;
+    ctx->T_all = ctx->T;
+    ctx->vrange[0][0] = 0;
+    ctx->vrange[0][1] = F.n_cons;
+    ctx->vrange[1][0] = ctx->vrange[1][1] = 0;
+    ctx->shard_mode = 0;
     ctx->stage = 2;
     ctx->err.clear();
     return FSMT_OK;
@@ -613,7 +625,7 @@ static fsmt_status sweep_impl(fsmt_ctx* ctx, float kappa, uint32_t stage_t, doub
             launch_sweep_jit(ctx->jit.kernel, F, S, ctx->T, kappa, ws, terms, terms_r, ctx->stream);
             ctx->launches += 1;
         }
-        if (F.generic_begin < F.n_cons) {
+        if (F.generic_begin < F.generic_end) {
             launch_sweep(F, S, kappa, ws, terms, terms_r, ctx->stream);
             ctx->launches += 1;
         }
@@ -636,10 +648,14 @@ static fsmt_status stage_end_impl(fsmt_ctx* ctx, uint32_t stage_t) {
     {
         Timed tm(ctx, 2);
         launch_round(ctx->F, S, ctx->rounding, ctx->seed, ctx->restart_offset, stage_t, ctx->stream);
-        launch_verify(ctx->F, S, S.x, S.b, S.U, nullptr, ctx->stream);
+        ctx->launches += 1;
+        for (int k = 0; k < 2; ++k)                 // the constraint ranges this context owns
+            if (ctx->vrange[k][1] > ctx->vrange[k][0]) {
+                launch_verify(ctx->F, S, S.x, S.b, S.U, nullptr, ctx->stream, ctx->vrange[k][0], ctx->vrange[k][1]);
+                ctx->launches += 1;
+            }
     }
     CK(cudaMemsetAsync(S.frozen, 0, S.R, ctx->stream));
-    ctx->launches += 2;
     fsmt_status s = check_launch(ctx);
     if (s) return s;
     ctx->rounded = true;
@@ -687,6 +703,73 @@ fsmt_status fsmt_stage_end(fsmt_ctx* ctx, uint32_t stage_t, uint32_t* unsat_out)
     if ((s = stage_end_impl(ctx, stage_t))) return s;
     if (unsat_out) return copy_out(ctx, unsat_out, ctx->S.unsat, ctx->S.R, FSMT_HOST);
     CK(cudaStreamSynchronize(ctx->stream));
+    return FSMT_OK;
+}
+
+fsmt_status fsmt_shard(fsmt_ctx* ctx, uint32_t rank, uint32_t world, uint32_t mode) {
+    fsmt_status s = need(ctx, 2, "fsmt_shard");
+    if (s) return s;
+    if (ctx->host_only) return fail(ctx, FSMT_ERR_CUDA, "fsmt_shard: host-only context has no device");
+    if (world == 0 || rank >= world || mode > 1) return fail(ctx, FSMT_ERR_ARG, "bad rank / world / mode");
+    const Plan& P = ctx->plan;
+    DevFormula& F = ctx->F;
+    const uint32_t C = F.n_cons;
+    const uint32_t jit_end = ctx->T_all.n_tiles ? P.jit_cons_end : 0;
+    ctx->shard_mode = mode;
+    ctx->shard_rank = rank;
+    ctx->shard_world = world;
+    if (mode == 0 || world == 1) {         // restart sharding: every constraint here
+        ctx->T = ctx->T_all;
+        F.generic_begin = jit_end;
+        F.generic_end = C;
+        ctx->vrange[0][0] = 0;
+        ctx->vrange[0][1] = C;
+        ctx->vrange[1][0] = ctx->vrange[1][1] = 0;
+        return FSMT_OK;
+    }
+    // constraint sharding: contiguous tile range balanced by constraint count,
+    // plus an even split of the generic tail
+    const uint32_t nt = ctx->T_all.n_tiles;
+    uint32_t t0 = 0, t1 = 0;
+    if (nt) {
+        const uint64_t lo_target = (uint64_t)jit_end * rank / world, hi_target = (uint64_t)jit_end * (rank + 1) / world;
+        uint64_t acc = 0;
+        t0 = nt;
+        t1 = nt;
+        for (uint32_t t = 0; t < nt; ++t) {
+            if (acc >= lo_target && t0 == nt) t0 = t;
+            if (acc >= hi_target) {
+                t1 = t;
+                break;
+            }
+            acc += P.tiles[t].n_cons;
+        }
+        if (t0 > t1) t0 = t1;
+    }
+    ctx->T = ctx->T_all;
+    ctx->T.tiles = (const char*)ctx->T_all.tiles + (size_t)t0 * sizeof(TileDesc);
+    ctx->T.n_tiles = t1 - t0;
+    const uint32_t gn = C - jit_end;
+    F.generic_begin = jit_end + (uint32_t)((uint64_t)gn * rank / world);
+    F.generic_end = jit_end + (uint32_t)((uint64_t)gn * (rank + 1) / world);
+    if (t1 > t0) {
+        ctx->vrange[0][0] = P.tiles[t0].cons_begin;
+        ctx->vrange[0][1] = P.tiles[t1 - 1].cons_begin + P.tiles[t1 - 1].n_cons;
+    } else {
+        ctx->vrange[0][0] = ctx->vrange[0][1] = 0;
+    }
+    ctx->vrange[1][0] = F.generic_begin;
+    ctx->vrange[1][1] = F.generic_end;
+    return FSMT_OK;
+}
+
+fsmt_status fsmt_bind_buffers(fsmt_ctx* ctx, void* grad_a, void* grad_b, void* obj, void* unsat) {
+    fsmt_status s = need(ctx, 3, "fsmt_bind_buffers");
+    if (s) return s;
+    if (grad_a) ctx->S.ga = (double*)grad_a;
+    if (grad_b) ctx->S.gb = (double*)grad_b;
+    if (obj) ctx->S.obj = (double*)obj;
+    if (unsat) ctx->S.unsat = (uint32_t*)unsat;
     return FSMT_OK;
 }
 
@@ -895,27 +978,18 @@ fsmt_status fsmt_time_sweep(fsmt_ctx* ctx, float kappa, uint32_t stage_t, uint32
     fsmt_status s = need(ctx, 3, "fsmt_time_sweep");
     if (s) return s;
     if (!ms_out || iters == 0) return fail(ctx, FSMT_ERR_ARG, "bad arguments");
-    cudaEvent_t e0, e1;
-    CK(cudaEventCreate(&e0));
-    CK(cudaEventCreate(&e1));
-    float total = 0.f;
-    for (uint32_t i = 0; i < iters; ++i) {
-        CK(cudaMemsetAsync(ctx->S.ga, 0, (size_t)ctx->F.n_bool * ctx->S.R * 8, ctx->stream));
-        CK(cudaMemsetAsync(ctx->S.gb, 0, (size_t)ctx->F.n_real * ctx->S.R * 8, ctx->stream));
-        CK(cudaMemsetAsync(ctx->S.obj, 0, (size_t)ctx->S.R * 8, ctx->stream));
-        CK(cudaEventRecord(e0, ctx->stream));
-        launch_sweep(ctx->F, ctx->S, kappa, wscale_of(stage_t, ctx->erwa_mode), nullptr, 0, ctx->stream);
-        CK(cudaEventRecord(e1, ctx->stream));
-        ctx->launches += 1;
-        CK(cudaEventSynchronize(e1));
-        float ms = 0.f;
-        CK(cudaEventElapsedTime(&ms, e0, e1));
-        total += ms;
-    }
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    *ms_out = total / iters;
-    return check_launch(ctx);
+    const bool was = ctx->timing;
+    timing_collect(ctx);
+    const double ms0 = ctx->t_ms[0];
+    const uint64_t n0 = ctx->t_cnt[0];
+    ctx->timing = true;
+    for (uint32_t i = 0; i < iters; ++i)
+        if ((s = sweep_impl(ctx, kappa, stage_t ? stage_t : 1, nullptr, 0))) break;
+    timing_collect(ctx);
+    ctx->timing = was;
+    if (s) return s;
+    *ms_out = (ctx->t_ms[0] - ms0) / (double)std::max<uint64_t>(ctx->t_cnt[0] - n0, 1);
+    return FSMT_OK;
 }
 
 }  // extern "C"

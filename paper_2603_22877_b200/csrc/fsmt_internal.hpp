@@ -90,9 +90,9 @@ struct Built {
 // Constraints are permuted into an internal order grouped into tiles: a tile is a run of
 // constraints of one kernel class (template + nnz of each atom slot) whose variables fit a
 // small local table, so the JIT-specialised sweep accumulates their gradients on chip.
-constexpr uint32_t kTileVmax = 128;       // local variables per tile
+constexpr uint32_t kTileVmaxDefault = 128;   // local variables per tile (FSMT_TILE_VMAX)
 constexpr uint32_t kTileCmax = 64;        // constraints per tile
-constexpr uint32_t kGroupVars = 64;       // variables per footprint group
+constexpr uint32_t kGroupVarsDefault = 64;   // variables per footprint group (VMAX/2)
 
 struct KClass {
     uint32_t tmpl;
@@ -120,6 +120,7 @@ struct Plan {
     uint32_t jit_cons_end = 0;        // internal [0, jit_cons_end) are JIT constraints
     uint32_t n_jit_kclasses = 0;
     uint32_t jit_warps = 1;           // warps per CTA of the JIT sweep (A/B: profiles/README.md)
+    uint32_t vmax = kTileVmaxDefault; // local variables per tile (on-chip accumulator rows)
 };
 
 Plan make_plan(const Formula& f, const Built& b, bool enable_jit);

@@ -76,8 +76,8 @@ __global__ void __launch_bounds__(256) k1_sweep(DevFormula F, DevState S, float 
     const uint64_t gw = (uint64_t)blockIdx.x * (blockDim.x >> 5) + warp;
     const uint32_t rt = (uint32_t)(gw % rtiles);
     const uint64_t c0 = F.generic_begin + (gw / rtiles) * kChunk;
-    if (c0 >= F.n_cons) return;
-    const uint64_t c1 = min(c0 + (uint64_t)kChunk, (uint64_t)F.n_cons);
+    if (c0 >= F.generic_end) return;
+    const uint64_t c1 = min(c0 + (uint64_t)kChunk, (uint64_t)F.generic_end);
     const uint32_t r = rt * 32 + lane;
     const bool live = r < R;
     const size_t rr = live ? r : 0;
@@ -245,15 +245,15 @@ __global__ void k4_round(DevFormula F, DevState S, uint32_t rounding, uint64_t s
 
 __global__ void __launch_bounds__(256) k5_verify(DevFormula F, DevState S, const int8_t* __restrict__ x,
                                                  const float* __restrict__ y, uint8_t* __restrict__ Uupd,
-                                                 uint8_t* __restrict__ per_con) {
+                                                 uint8_t* __restrict__ per_con, uint32_t cb, uint32_t ce) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t R = S.R;
     const uint32_t rtiles = (R + 31) / 32;
     const uint64_t gw = (uint64_t)blockIdx.x * (blockDim.x >> 5) + warp;
     const uint32_t rt = (uint32_t)(gw % rtiles);
-    const uint64_t c0 = (gw / rtiles) * kChunk;
-    if (c0 >= F.n_cons) return;
-    const uint64_t c1 = min(c0 + (uint64_t)kChunk, (uint64_t)F.n_cons);
+    const uint64_t c0 = cb + (gw / rtiles) * kChunk;
+    if (c0 >= ce) return;
+    const uint64_t c1 = min(c0 + (uint64_t)kChunk, (uint64_t)ce);
     const uint32_t r = rt * 32 + lane;
     if (r >= R) return;
     uint32_t cnt = 0;
@@ -336,7 +336,7 @@ void launch_sweep_jit(cudaKernel_t k, const DevFormula& F, const DevState& S, co
                       float wscale, double* terms, uint32_t terms_r, cudaStream_t st) {
     if (T.n_tiles == 0 || S.R == 0) return;
     const int kJitWarps = (int)(T.warps ? T.warps : 1);
-    constexpr int kVmax = 128;                                      // must match tiles.cpp (kTileVmax)
+    const int kVmax = (int)(T.vmax ? T.vmax : 128);                   // Plan::vmax
     const uint64_t nw = (uint64_t)T.n_tiles * ((S.R + 31) / 32);
     const unsigned blocks = (unsigned)((nw + kJitWarps - 1) / kJitWarps);
     const size_t smem = (size_t)kJitWarps * (kVmax * 32 * 4 + kVmax * 4);
@@ -350,11 +350,11 @@ void launch_sweep_jit(cudaKernel_t k, const DevFormula& F, const DevState& S, co
 
 void launch_sweep(const DevFormula& F, const DevState& S, float kappa, float wscale, double* terms, uint32_t terms_r,
                   cudaStream_t st) {
-    if (F.n_cons <= F.generic_begin || S.R == 0) return;
+    if (F.generic_end <= F.generic_begin || S.R == 0) return;
     const int warps = sweep_warps(F);
     const int smem = sweep_smem_bytes(F, warps);
     if (smem > 48 * 1024) cudaFuncSetAttribute(k1_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    const uint64_t chunks = (F.n_cons - F.generic_begin + kChunk - 1) / kChunk;
+    const uint64_t chunks = (F.generic_end - F.generic_begin + kChunk - 1) / kChunk;
     const uint64_t nw = chunks * ((S.R + 31) / 32);
     const uint64_t blocks = (nw + warps - 1) / warps;
     k1_sweep<<<(unsigned)blocks, warps * 32, smem, st>>>(F, S, kappa, wscale, terms, terms_r,
@@ -383,12 +383,13 @@ void launch_round(const DevFormula& F, const DevState& S, uint32_t rounding, uin
 }
 
 void launch_verify(const DevFormula& F, const DevState& S, const int8_t* x, const float* y, uint8_t* U_update,
-                   uint8_t* per_con, cudaStream_t st) {
-    if (F.n_cons == 0 || S.R == 0) return;
-    const uint64_t chunks = (F.n_cons + kChunk - 1) / kChunk;
+                   uint8_t* per_con, cudaStream_t st, uint32_t cb, uint32_t ce) {
+    if (ce == UINT32_MAX) ce = F.n_cons;
+    if (ce <= cb || S.R == 0) return;
+    const uint64_t chunks = (ce - cb + kChunk - 1) / kChunk;
     const uint64_t nw = chunks * ((S.R + 31) / 32);
     const uint64_t blocks = (nw + 7) / 8;
-    k5_verify<<<(unsigned)blocks, 256, 0, st>>>(F, S, x, y, U_update, per_con);
+    k5_verify<<<(unsigned)blocks, 256, 0, st>>>(F, S, x, y, U_update, per_con, cb, ce);
 }
 
 }  // namespace fsmt

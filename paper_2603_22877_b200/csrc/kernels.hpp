@@ -38,7 +38,8 @@ struct DevFormula {
     const float* hi;                // [n_real]
     const uint32_t* orig;           // [C] internal -> original constraint id (constraint arrays and U
                                     //     are in the internal, tile-sorted order; see tiles.cpp)
-    uint32_t generic_begin;         // internal [generic_begin, n_cons) run through the generic K1
+    uint32_t generic_begin;         // internal [generic_begin, generic_end) run through the generic K1
+    uint32_t generic_end;           //   (generic_end < n_cons only in constraint-sharded mode)
 };
 
 // Per-restart state, restart-minor (row = variable / constraint).
@@ -72,6 +73,7 @@ struct DevTiles {
     const void* recs;            // uint4 records
     const uint32_t* tile_vars;
     uint32_t warps;              // warps per CTA (Plan::jit_warps)
+    uint32_t vmax;               // local variables per tile (Plan::vmax)
 };
 void launch_sweep_jit(cudaKernel_t k, const DevFormula& F, const DevState& S, const DevTiles& T, float kappa,
                       float wscale, double* terms, uint32_t terms_r, cudaStream_t st);
@@ -87,7 +89,8 @@ void launch_update(const DevFormula& F, const DevState& S, float eta, float eps,
 void launch_round(const DevFormula& F, const DevState& S, uint32_t rounding, uint64_t seed, uint32_t restart_offset,
                   uint32_t stage, cudaStream_t st);
 // K5: exact verification + ERWA counter update (R18, R22).
+// K5 over internal constraints [cb, ce) (ce = UINT32_MAX: to the end).
 void launch_verify(const DevFormula& F, const DevState& S, const int8_t* x, const float* y, uint8_t* U_update,
-                   uint8_t* per_con, cudaStream_t st);
+                   uint8_t* per_con, cudaStream_t st, uint32_t cb = 0, uint32_t ce = UINT32_MAX);
 
 }  // namespace fsmt

@@ -33,6 +33,7 @@ constexpr uint64_t kJitMinCons = 32;      // specialise only classes with enough
 Plan make_plan(const Formula& f, const Built& b, bool enable_jit) {
     Plan p;
     if (const char* w = getenv("FSMT_JIT_WARPS")) p.jit_warps = std::max(1, std::min(8, atoi(w)));
+    if (const char* v = getenv("FSMT_TILE_VMAX")) p.vmax = (uint32_t)std::max(16, std::min(256, atoi(v)));
     const uint32_t C = (uint32_t)b.cons_tmpl.size();
     // 1. kernel classes
     std::map<std::vector<uint32_t>, uint32_t> kc_of;
@@ -132,7 +133,7 @@ Plan make_plan(const Formula& f, const Built& b, bool enable_jit) {
         for (uint32_t u : vars)
             if (group[u] == UINT32_MAX && std::find(batch.begin(), batch.end(), u) == batch.end()) batch.push_back(u);
         if (batch.empty()) continue;
-        if (cur_size > 0 && cur_size + batch.size() > kGroupVars) {
+        if (cur_size > 0 && cur_size + batch.size() > p.vmax / 2) {
             ++cur_group;
             cur_size = 0;
         }
@@ -189,8 +190,8 @@ Plan make_plan(const Formula& f, const Built& b, bool enable_jit) {
             size_t add = 0;
             for (uint32_t u : vars)
                 if (std::find(local.begin(), local.end(), u) == local.end()) ++add;
-            if (T.n_cons > 0 && local.size() + add > kTileVmax) break;
-            if (local.size() + add > kTileVmax) break;   // a single constraint over > VMAX vars: generic path
+            if (T.n_cons > 0 && local.size() + add > p.vmax) break;
+            if (local.size() + add > p.vmax) break;   // a single constraint over > VMAX vars: generic path
             for (uint32_t u : vars)
                 if (std::find(local.begin(), local.end(), u) == local.end()) local.push_back(u);
             // record
@@ -475,7 +476,7 @@ std::string jit_source(const Formula& f, const Built& b, const Plan& p) {
     o << "// generated by fsmt tiles.cpp: specialised K1 sweep for " << p.n_jit_kclasses << " kernel classes\n"
          "typedef unsigned int u32;\ntypedef unsigned long long u64;\n"
          "struct TileDesc { u32 kclass, cons_begin, n_cons, var_off, n_vars, rec_off, pad0, pad1; };\n"
-      << "#define VMAX " << kTileVmax << "\n#define WARPS " << p.jit_warps << "\n\n" << kErfcPrelude;
+      << "#define VMAX " << p.vmax << "\n#define WARPS " << p.jit_warps << "\n\n" << kErfcPrelude;
     for (uint32_t k = 0; k < p.n_jit_kclasses; ++k) emit_class(o, k, p.kclasses[k], b.tmpls[p.kclasses[k].tmpl]);
     const char* minb = getenv("FSMT_JIT_MINB");      // optional min CTAs/SM (register cap), A/B tuning
     o << "extern \"C\" __global__ void __launch_bounds__(WARPS * 32" << (minb && atoi(minb) > 0 ? std::string(", ") + minb : std::string())

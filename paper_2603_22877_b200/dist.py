@@ -72,3 +72,47 @@ def solve_restart_sharded(engine, n_bool: int, n_real: int, restarts_per_rank: i
             break
     return DistResult(SAT if best_key[0] == 0 else UNKNOWN, x_best.cpu().numpy(), y_best.cpu().numpy(),
                       best_key[2], best_key[1], best_key[0], stages)
+
+
+def solve_constraint_sharded(engine, n_bool: int, n_real: int, restarts: int, steps: int, seed: int, kappas,
+                             eta: float, eps: float, group=None) -> DistResult:
+    """Constraint-sharded solve (BASELINE config 5): every rank holds all R
+    restarts and sweeps only its share of the constraints (engine.shard(rank, world, 1)).
+    Per PGD step the partial gradients and objectives are all-reduced (C4: SUM over
+    R*(n_bool+n_real) f64 + R f64), then every rank applies the identical K3 update; per
+    stage the partial violation counts are all-reduced (C5: SUM over R u32).  All ranks
+    therefore keep bit-identical states and reach the same verdict.
+
+    engine: shard, begin, bind_buffers(ga, gb, obj, unsat), sweep(kappa, t), update(eta, eps),
+    stage_end(t, copy=False), get_model(r).
+    """
+    rank = dist.get_rank(group)
+    world = dist.get_world_size(group)
+    dev = _device_for_backend()
+    R = int(restarts)
+    engine.shard(rank, world, 1)
+    engine.begin(R, seed, 0)
+    ga = torch.zeros((n_bool, R), dtype=torch.float64, device=dev)
+    gb = torch.zeros((n_real, R), dtype=torch.float64, device=dev)
+    obj = torch.zeros(R, dtype=torch.float64, device=dev)
+    unsat = torch.zeros(R, dtype=torch.int32, device=dev)
+    engine.bind_buffers(ga, gb, obj, unsat)
+    best = None
+    stages = 0
+    for t, kappa in enumerate(kappas, start=1):
+        for _ in range(steps):
+            engine.sweep(float(kappa), t)
+            for buf in (ga, gb, obj):                                    # C4
+                dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
+            engine.update(eta, eps)
+        engine.stage_end(t, copy=False)
+        dist.all_reduce(unsat, op=dist.ReduceOp.SUM, group=group)          # C5
+        stages = t
+        u = unsat.cpu().numpy()
+        r = int(np.argmin(u))
+        if best is None or int(u[r]) < best[0]:
+            x, y = engine.get_model(r)
+            best = (int(u[r]), t, r, np.asarray(x, dtype=np.int8).copy(), np.asarray(y, dtype=np.float32).copy())
+        if best[0] == 0:
+            break
+    return DistResult(SAT if best[0] == 0 else UNKNOWN, best[3], best[4], best[2], best[1], best[0], stages)

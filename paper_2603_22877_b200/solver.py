@@ -150,7 +150,12 @@ class Solver:
         self._check(N.lib.fsmt_update(self._h, eta, eps, gm2.ctypes.data if want_gm2 else None))
         return gm2
 
-    def stage_end(self, stage_t: int):
+    def stage_end(self, stage_t: int, copy: bool = True):
+        """K4 + K5; returns unsat[R] (host) or None when copy=False (the result stays in the
+        device unsat buffer, e.g. a bound tensor to be all-reduced)."""
+        if not copy:
+            self._check(N.lib.fsmt_stage_end(self._h, stage_t, None))
+            return None
         u = np.empty(self.R, dtype=np.uint32)
         self._check(N.lib.fsmt_stage_end(self._h, stage_t, u.ctypes.data))
         return u
@@ -217,6 +222,15 @@ class Solver:
         buf = C.create_string_buffer(4096)
         self._check(N.lib.fsmt_jit_info(self._h, C.byref(n1), C.byref(n2), C.byref(n3), buf, 4096))
         return {"jit_classes": n1.value, "tiles": n2.value, "jit_cons": n3.value, "status": buf.value.decode()}
+
+    def shard(self, rank: int, world: int, mode: int):
+        """mode 0: restart-sharded (all constraints); 1: constraint-sharded (partial sums)."""
+        self._check(N.lib.fsmt_shard(self._h, rank, world, mode))
+
+    def bind_buffers(self, grad_a=None, grad_b=None, obj=None, unsat=None):
+        """Bind caller-owned device tensors (float64 [n_bool][R], [n_real][R], [R]; uint32/int32 [R])."""
+        ptr = lambda t: None if t is None else t.data_ptr()
+        self._check(N.lib.fsmt_bind_buffers(self._h, ptr(grad_a), ptr(grad_b), ptr(obj), ptr(unsat)))
 
     def jit_check(self):
         """NVRTC-compile the specialised sweep (no device needed): (cubin bytes, compiler log)."""
