@@ -50,6 +50,7 @@ class Params:
     eps: float = 1e-2            # P:165, R14
     rounding: str = "sign"       # "sign" | "philox"  (R17)
     erwa_mode: int = 0           # 0: Alg.2 verbatim (h <- 1); 1: reset-to-0 reading (R18)
+    eta_mode: int = 0            # step in stage t: eta / max(kappa_t, 1)^eta_mode (R13; 1/L ~ kappa^-2)
 
 
 # ----------------------------------------------------------------------------- projection bounds
@@ -195,8 +196,9 @@ def solve_restart(f, seed, r, params: Params, lo=None, hi=None):
     hist = []
     for t, kappa in enumerate(params.kappas, start=1):
         taken = 0
+        eta_t = params.eta / max(kappa, 1.0) ** params.eta_mode
         for _ in range(params.steps):
-            a2, b2, gm2, _ = pgd_step(f, a, b, kappa, w, params.eta, lo, hi)
+            a2, b2, gm2, _ = pgd_step(f, a, b, kappa, w, eta_t, lo, hi)
             if gm2 <= params.eps ** 2:
                 break
             a, b = a2, b2

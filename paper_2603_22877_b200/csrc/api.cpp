@@ -45,7 +45,7 @@ struct fsmt_ctx {
     // params
     std::vector<float> kappas;
     float eta = 0.05f, eps = 1e-2f;
-    uint32_t rounding = FSMT_ROUND_SIGN, erwa_mode = FSMT_ERWA_VERBATIM;
+    uint32_t rounding = FSMT_ROUND_SIGN, erwa_mode = FSMT_ERWA_VERBATIM, eta_mode = 0;
     double time_limit = 0.0;
     // run
     uint64_t seed = 0;
@@ -395,6 +395,11 @@ fsmt_status fsmt_build_xbdd(fsmt_ctx* ctx, uint64_t node_budget) {
             ctx->T.tile_vars = vp;
             ctx->T.warps = P.jit_warps;
             ctx->T.vmax = P.vmax;
+            ctx->T.rec_stage4 = P.rec_stage4;
+            const uint32_t* vr = nullptr;
+            s = upload(ctx, P.vrecs, vr, ctx->fallocs);
+            if (s) return s;
+            ctx->T.vrecs = vr;
             F.generic_begin = P.jit_cons_end;
         } else {
             ctx->jit_error = err;
@@ -465,6 +470,7 @@ fsmt_status fsmt_set_params(fsmt_ctx* ctx, const fsmt_params* p) {
         ctx->eps = 1e-2f;
         ctx->rounding = FSMT_ROUND_SIGN;
         ctx->erwa_mode = FSMT_ERWA_VERBATIM;
+        ctx->eta_mode = 0;
         ctx->time_limit = 0;
         return FSMT_OK;
     }
@@ -476,11 +482,13 @@ fsmt_status fsmt_set_params(fsmt_ctx* ctx, const fsmt_params* p) {
     } else {
         default_kappas(ctx->kappas);
     }
-    if (p->rounding > 1 || p->erwa_mode > 1) return fail(ctx, FSMT_ERR_ARG, "bad rounding / erwa_mode");
+    if (p->rounding > 1 || p->erwa_mode > 1 || p->eta_mode > 2)
+        return fail(ctx, FSMT_ERR_ARG, "bad rounding / erwa_mode / eta_mode");
     ctx->eta = p->eta > 0 ? p->eta : 0.05f;
     ctx->eps = p->eps > 0 ? p->eps : 1e-2f;
     ctx->rounding = p->rounding;
     ctx->erwa_mode = p->erwa_mode;
+    ctx->eta_mode = p->eta_mode;
     ctx->time_limit = p->time_limit_s;
     return FSMT_OK;
 }
@@ -649,11 +657,17 @@ static fsmt_status stage_end_impl(fsmt_ctx* ctx, uint32_t stage_t) {
         Timed tm(ctx, 2);
         launch_round(ctx->F, S, ctx->rounding, ctx->seed, ctx->restart_offset, stage_t, ctx->stream);
         ctx->launches += 1;
-        for (int k = 0; k < 2; ++k)                 // the constraint ranges this context owns
-            if (ctx->vrange[k][1] > ctx->vrange[k][0]) {
-                launch_verify(ctx->F, S, S.x, S.b, S.U, nullptr, ctx->stream, ctx->vrange[k][0], ctx->vrange[k][1]);
-                ctx->launches += 1;
-            }
+        if (ctx->T.n_tiles && ctx->jit.kernel5) {    // specialised check of this context's tiles
+            launch_verify_jit(ctx->jit.kernel5, ctx->F, S, ctx->T, S.x, S.b, S.U, nullptr, ctx->stream);
+            launch_verify(ctx->F, S, S.x, S.b, S.U, nullptr, ctx->stream, ctx->F.generic_begin, ctx->F.generic_end);
+            ctx->launches += 2;
+        } else {
+            for (int k = 0; k < 2; ++k)             // the constraint ranges this context owns
+                if (ctx->vrange[k][1] > ctx->vrange[k][0]) {
+                    launch_verify(ctx->F, S, S.x, S.b, S.U, nullptr, ctx->stream, ctx->vrange[k][0], ctx->vrange[k][1]);
+                    ctx->launches += 1;
+                }
+        }
     }
     CK(cudaMemsetAsync(S.frozen, 0, S.R, ctx->stream));
     fsmt_status s = check_launch(ctx);
@@ -780,9 +794,11 @@ fsmt_status fsmt_run_stage(fsmt_ctx* ctx, uint32_t stage_t, float kappa, uint32_
     if (!(kappa >= 0.f) || !std::isfinite(kappa)) return fail(ctx, FSMT_ERR_ARG, "kappa must be finite and >= 0");
     if (stage_t == 0) stage_t = 1;
     CK(cudaMemsetAsync(ctx->S.frozen, 0, ctx->S.R, ctx->stream));
+    const float kk = std::max(kappa, 1.0f);
+    const float eta_t = ctx->eta_mode == 1 ? ctx->eta / kk : ctx->eta_mode == 2 ? ctx->eta / (kk * kk) : ctx->eta;
     for (uint32_t k = 0; k < steps; ++k) {
         if ((s = sweep_impl(ctx, kappa, stage_t, nullptr, 0))) return s;
-        if ((s = update_impl(ctx, ctx->eta, ctx->eps))) return s;
+        if ((s = update_impl(ctx, eta_t, ctx->eps))) return s;
     }
     if ((s = stage_end_impl(ctx, stage_t))) return s;
     if (unsat_out || min_unsat) {
@@ -882,8 +898,14 @@ fsmt_status fsmt_verify_batch(fsmt_ctx* ctx, uint32_t R, const int8_t* x, const 
     if (e == cudaSuccess && nr) e = cudaMemcpyAsync(dy, y, nr * 4, k, ctx->stream);
     if (e == cudaSuccess) e = cudaMemsetAsync(T.unsat, 0, (size_t)R * 4, ctx->stream);
     if (e == cudaSuccess) {
-        launch_verify(F, T, dx, dy, nullptr, dpc, ctx->stream);
-        ctx->launches += 1;
+        if (ctx->T_all.n_tiles && ctx->jit.kernel5) {
+            launch_verify_jit(ctx->jit.kernel5, F, T, ctx->T_all, dx, dy, nullptr, dpc, ctx->stream);
+            launch_verify(F, T, dx, dy, nullptr, dpc, ctx->stream, ctx->plan.jit_cons_end, F.n_cons);
+            ctx->launches += 2;
+        } else {
+            launch_verify(F, T, dx, dy, nullptr, dpc, ctx->stream);
+            ctx->launches += 1;
+        }
         e = cudaGetLastError();
     }
     if (e == cudaSuccess) e = cudaMemcpyAsync(unsat_out, T.unsat, (size_t)R * 4, cudaMemcpyDeviceToHost, ctx->stream);

@@ -100,6 +100,7 @@ struct KClass {
     uint32_t n_refs;             // Boolean slots + sum nnz
     uint32_t words;              // record words before padding
     uint32_t stride4;            // record stride in uint4
+    uint32_t vstride4;           // K5 record stride in uint4 (atom id per atom slot)
     bool jit;
     uint64_t n_cons;
     std::vector<uint8_t> stream;  // per reference: 1 = changes most constraints (no run register)
@@ -117,10 +118,13 @@ struct Plan {
     std::vector<TileDesc> tiles;      // JIT tiles only, in internal order
     std::vector<uint32_t> tile_vars;  // unified var ids: Boolean i -> i, real j -> n_bool + j
     std::vector<uint32_t> recs;       // JIT records (uint32 words, stride4*4 per constraint)
+    std::vector<uint32_t> vrecs;      // K5 JIT records (atom ids, vstride4*4 per constraint); tile.pad1 = offset
     uint32_t jit_cons_end = 0;        // internal [0, jit_cons_end) are JIT constraints
     uint32_t n_jit_kclasses = 0;
     uint32_t jit_warps = 1;           // warps per CTA of the JIT sweep (A/B: profiles/README.md)
     uint32_t vmax = kTileVmaxDefault; // local variables per tile (on-chip accumulator rows)
+    uint32_t rec_stage4 = 0;          // per-warp shared-memory record stage, uint4 (0: not staged)
+    uint32_t cmax = kTileCmax;        // constraints per tile (FSMT_TILE_CMAX)
 };
 
 Plan make_plan(const Formula& f, const Built& b, bool enable_jit);

@@ -129,8 +129,16 @@ bool jit_compile(const std::string& src, JitKernel& out, std::string& err) {
         err = std::string("cudaLibraryGetKernel: ") + cudaGetErrorString(e);
         return false;
     }
+    cudaKernel_t k5 = nullptr;
+    e = cudaLibraryGetKernel(&k5, lib, "fsmt_k5_jit");
+    if (e != cudaSuccess) {
+        cudaLibraryUnload(lib);
+        err = std::string("cudaLibraryGetKernel(k5): ") + cudaGetErrorString(e);
+        return false;
+    }
     out.lib = lib;
     out.kernel = k;
+    out.kernel5 = k5;
     out.cubin_bytes = cubin.size();
     return true;
 }
@@ -139,6 +147,7 @@ void jit_release(JitKernel& k) {
     if (k.lib) cudaLibraryUnload((cudaLibrary_t)k.lib);
     k.lib = nullptr;
     k.kernel = nullptr;
+    k.kernel5 = nullptr;
 }
 
 }  // namespace fsmt

@@ -8,12 +8,13 @@ namespace fsmt {
 
 struct JitKernel {
     void* lib = nullptr;          // cudaLibrary_t
-    cudaKernel_t kernel = nullptr;
+    cudaKernel_t kernel = nullptr;     // fsmt_k1_jit (sweep)
+    cudaKernel_t kernel5 = nullptr;    // fsmt_k5_jit (exact check)
     size_t cubin_bytes = 0;
     std::string log;
 };
 
-// Compiles `src` for sm_100a with NVRTC and loads kernel "fsmt_k1_jit". false + err on failure.
+// Compiles `src` for sm_100a with NVRTC and loads kernels "fsmt_k1_jit" and "fsmt_k5_jit". false + err on failure.
 bool jit_compile(const std::string& src, JitKernel& out, std::string& err);
 // NVRTC only (no device needed): cubin + compiler log.
 bool jit_cubin(const std::string& src, std::vector<char>& cubin, std::string& log, std::string& err);

@@ -339,13 +339,29 @@ void launch_sweep_jit(cudaKernel_t k, const DevFormula& F, const DevState& S, co
     const int kVmax = (int)(T.vmax ? T.vmax : 128);                   // Plan::vmax
     const uint64_t nw = (uint64_t)T.n_tiles * ((S.R + 31) / 32);
     const unsigned blocks = (unsigned)((nw + kJitWarps - 1) / kJitWarps);
-    const size_t smem = (size_t)kJitWarps * (kVmax * 32 * 4 + kVmax * 4);
+    const size_t smem = (size_t)kJitWarps * (kVmax * 32 * 4 + kVmax * 4 + (size_t)T.rec_stage4 * 16);
     uint32_t n_tiles = T.n_tiles, R = S.R, n_bool = F.n_bool;
     const uint8_t* U = S.U;
     void* args[] = {(void*)&T.tiles, &n_tiles, (void*)&T.recs, (void*)&T.tile_vars, (void*)&S.a, (void*)&S.b,
                     (void*)&S.ga, (void*)&S.gb, (void*)&U, (void*)&S.obj, &R, &n_bool, &kappa, &wscale,
                     &terms, &terms_r, (void*)&F.orig};
     cudaLaunchKernel((const void*)k, dim3(blocks), dim3(kJitWarps * 32), args, smem, st);
+}
+
+void launch_verify_jit(cudaKernel_t k, const DevFormula& F, const DevState& S, const DevTiles& T, const int8_t* x,
+                       const float* y, uint8_t* U_update, uint8_t* per_con, cudaStream_t st) {
+    if (T.n_tiles == 0 || S.R == 0) return;
+    const int warps = (int)(T.warps ? T.warps : 1);
+    const int vmax = (int)(T.vmax ? T.vmax : 128);
+    const uint64_t nw = (uint64_t)T.n_tiles * ((S.R + 31) / 32);
+    const unsigned blocks = (unsigned)((nw + warps - 1) / warps);
+    const size_t smem = (size_t)warps * vmax * 4;
+    uint32_t n_tiles = T.n_tiles, R = S.R, n_bool = F.n_bool;
+    uint32_t* unsat = S.unsat;
+    void* args[] = {(void*)&T.tiles, &n_tiles, (void*)&T.recs, (void*)&T.vrecs, (void*)&T.tile_vars, (void*)&x,
+                    (void*)&y, (void*)&U_update, (void*)&unsat, (void*)&per_con, (void*)&F.orig, &R, &n_bool,
+                    (void*)&F.atom_rowptr, (void*)&F.atom_val64, (void*)&F.atom_rhs64, (void*)&F.atom_strict};
+    cudaLaunchKernel((const void*)k, dim3(blocks), dim3(warps * 32), args, smem, st);
 }
 
 void launch_sweep(const DevFormula& F, const DevState& S, float kappa, float wscale, double* terms, uint32_t terms_r,

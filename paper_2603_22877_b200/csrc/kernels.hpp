@@ -74,7 +74,12 @@ struct DevTiles {
     const uint32_t* tile_vars;
     uint32_t warps;              // warps per CTA (Plan::jit_warps)
     uint32_t vmax;               // local variables per tile (Plan::vmax)
+    uint32_t rec_stage4;         // per-warp record stage in uint4 (Plan::rec_stage4)
+    const void* vrecs;           // K5 records (atom ids), tile.pad1 = offset in uint4
 };
+// K5 (JIT-specialised, tiles): exact check over the tiles of T (+ ERWA counters / per_con).
+void launch_verify_jit(cudaKernel_t k, const DevFormula& F, const DevState& S, const DevTiles& T, const int8_t* x,
+                       const float* y, uint8_t* U_update, uint8_t* per_con, cudaStream_t st);
 void launch_sweep_jit(cudaKernel_t k, const DevFormula& F, const DevState& S, const DevTiles& T, float kappa,
                       float wscale, double* terms, uint32_t terms_r, cudaStream_t st);
 // row gather for u8 matrices: dst[i][:] = src[idx[i]][:]  (U between original and internal order)

@@ -34,6 +34,7 @@ Plan make_plan(const Formula& f, const Built& b, bool enable_jit) {
     Plan p;
     if (const char* w = getenv("FSMT_JIT_WARPS")) p.jit_warps = std::max(1, std::min(8, atoi(w)));
     if (const char* v = getenv("FSMT_TILE_VMAX")) p.vmax = (uint32_t)std::max(16, std::min(256, atoi(v)));
+    if (const char* v = getenv("FSMT_TILE_CMAX")) p.cmax = (uint32_t)std::max(1, std::min(1024, atoi(v)));
     const uint32_t C = (uint32_t)b.cons_tmpl.size();
     // 1. kernel classes
     std::map<std::vector<uint32_t>, uint32_t> kc_of;
@@ -69,6 +70,7 @@ Plan make_plan(const Formula& f, const Built& b, bool enable_jit) {
             }
             kc.words = 1 + (refs + 1) / 2 + atom_words;
             kc.stride4 = (kc.words + 3) / 4;
+            kc.vstride4 = std::max<uint32_t>(1, ((uint32_t)(key.size() - 1) + 3) / 4);
             kc.jit = enable_jit && small_nnz && t.nodes.size() <= kJitMaxNodes && refs <= kJitMaxRefs && t.root >= 0;
             kc.n_cons = 0;
             p.kclasses.push_back(kc);
@@ -180,10 +182,11 @@ Plan make_plan(const Formula& f, const Built& b, bool enable_jit) {
     while (i < C && p.kclasses[p.cons_kclass[i]].jit) {
         const uint32_t kc = p.cons_kclass[i];
         const KClass& K = p.kclasses[kc];
-        TileDesc T{kc, i, 0, (uint32_t)p.tile_vars.size(), 0, (uint32_t)(p.recs.size() / 4), 0, 0};
+        TileDesc T{kc, i, 0, (uint32_t)p.tile_vars.size(), 0, (uint32_t)(p.recs.size() / 4), 0,
+                   (uint32_t)(p.vrecs.size() / 4)};
         local.clear();
         const Key& k0 = keys[p.order[i]];
-        while (i < C && p.cons_kclass[i] == kc && T.n_cons < kTileCmax) {
+        while (i < C && p.cons_kclass[i] == kc && T.n_cons < p.cmax) {
             const Key& ki = keys[p.order[i]];
             if (T.n_cons > 0 && (memcmp(ki.g, k0.g, sizeof(k0.g)) != 0)) break;
             cons_vars(p.order[i], vars);
@@ -208,11 +211,14 @@ Plan make_plan(const Formula& f, const Built& b, bool enable_jit) {
                 ++ref;
             };
             uint32_t aw = 1 + (K.n_refs + 1) / 2;
+            std::vector<uint32_t> vrec(K.vstride4 * 4, 0);   // K5 record: atom id per atom slot
+            uint32_t va = 0;
             for (size_t s = 0; s < t.kinds.size(); ++s) {
                 if (t.kinds[s] == 0) {
                     put_ref(ids[s]);
                 } else {
                     uint32_t atom = ids[s];
+                    vrec[va++] = atom;
                     float rhs = (float)f.atom_rhs[atom];
                     double n2 = 0.0;
                     for (uint32_t kk = f.atom_rowptr[atom]; kk < f.atom_rowptr[atom + 1]; ++kk)
@@ -229,16 +235,24 @@ Plan make_plan(const Formula& f, const Built& b, bool enable_jit) {
                 }
             }
             p.recs.insert(p.recs.end(), rec.begin(), rec.end());
+            p.vrecs.insert(p.vrecs.end(), vrec.begin(), vrec.end());
             ++T.n_cons;
             ++i;
         }
         if (T.n_cons == 0) break;   // cannot tile (too many variables): rest is generic
         T.n_vars = (uint32_t)local.size();
+        T.pad0 = T.n_cons * K.stride4;           // record uint4s (shared-memory stage size)
         p.tile_vars.insert(p.tile_vars.end(), local.begin(), local.end());
         p.tiles.push_back(T);
     }
     p.jit_cons_end = i;
     // any JIT-class constraints after the cut run through the generic kernel
+    {
+        const char* e = getenv("FSMT_JIT_STAGE");
+        uint32_t ms = 0;
+        for (uint32_t k = 0; k < p.n_jit_kclasses; ++k) ms = std::max(ms, p.kclasses[k].stride4);
+        p.rec_stage4 = (e && e[0] == '1') ? p.cmax * ms : 0;
+    }
 
     // 5. per kernel class and reference position: does the local variable change from one
     //    constraint to the next within a tile most of the time ("stream": accumulate straight
@@ -282,6 +296,14 @@ std::string fnum(float v) {
 bool fast_erfc() {
     const char* e = getenv("FSMT_JIT_ERFC");
     return !(e && std::string(e) == "cuda");
+}
+
+// FSMT_JIT_STAGE=1: a tile's records are staged into shared memory at tile start and the
+// stream references' values are software-pipelined one constraint ahead.  Measured slower on
+// cfg4 (28.6 vs 22.6 ms: the extra shared memory costs occupancy), so off by default.
+bool stage_records() {
+    const char* e = getenv("FSMT_JIT_STAGE");
+    return e && e[0] == '1';
 }
 
 const char* kErfcPrelude =
@@ -340,7 +362,39 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
         if (!is_stream(i)) o << "  u32 cur" << i << " = 0xffffffffu; float val" << i << " = 0.f, acc" << i << " = 0.f;\n";
     const char* pf_env = getenv("FSMT_JIT_PREFETCH");
     const bool prefetch = pf_env && pf_env[0] == '1';
-    if (prefetch) {
+    const bool staged = stage_records();
+    auto ld_of = [&](size_t i) {
+        return ref_kind[i] == 0 ? std::string("a[(u64)vs[l] * R + rr]") : std::string("b[(u64)(vs[l] - n_bool) * R + rr]");
+    };
+    auto ext_of = [&](size_t i, const std::string& w) {
+        return "(" + w + " >> " + std::to_string(16 * (i % 2)) + ") & 0xffffu";
+    };
+    auto rec_word = [&](uint32_t wd, uint32_t off4) {   // word wd of the record rp + off4 (shared memory)
+        return "rp[" + std::to_string(off4 + wd / 4) + "]." + comp(wd);
+    };
+    if (staged) {
+        // records are in shared memory; the values of the stream references of constraint c+1
+        // are requested while c is evaluated (software pipeline of depth 1)
+        for (size_t i = 0; i < nr; ++i)
+            if (is_stream(i)) o << "  u32 nsl" << i << " = 0u; float nval" << i << " = 0.f;\n";
+        o << "  if (T.n_cons) {\n";
+        for (size_t i = 0; i < nr; ++i)
+            if (is_stream(i))
+                o << "    { const u32 l = " << ext_of(i, rec_word(1 + (uint32_t)i / 2, 0)) << "; nsl" << i << " = l; nval" << i
+                  << " = " << ld_of(i) << "; }\n";
+        o << "  }\n";
+        o << "  for (u32 c = 0; c < T.n_cons; ++c, rp += " << K.stride4 << ") {\n";
+        for (uint32_t q = 0; q < K.stride4; ++q) o << "    const uint4 q" << q << " = rp[" << q << "];\n";
+        o << "    const u32 uc = U ? (u32)U[(u64)(T.cons_begin + c) * R + rr] : 0u;\n";
+        for (size_t i = 0; i < nr; ++i)
+            if (is_stream(i)) o << "    const u32 sl" << i << " = nsl" << i << "; const float val" << i << " = nval" << i << ";\n";
+        o << "    if (c + 1 < T.n_cons) {\n";
+        for (size_t i = 0; i < nr; ++i)
+            if (is_stream(i))
+                o << "      { const u32 l = " << ext_of(i, rec_word(1 + (uint32_t)i / 2, K.stride4)) << "; nsl" << i
+                  << " = l; nval" << i << " = " << ld_of(i) << "; }\n";
+        o << "    }\n";
+    } else if (prefetch) {
         // software pipeline: the record and U counter of constraint c+1 are loaded while c is evaluated
         for (uint32_t q = 0; q < K.stride4; ++q) o << "  uint4 nq" << q << " = make_uint4(0u, 0u, 0u, 0u);\n";
         o << "  u32 nU = 0u;\n  if (T.n_cons) {\n";
@@ -364,8 +418,9 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
         const std::string ld = ref_kind[i] == 0 ? "a[(u64)vs[l] * R + rr]" : "b[(u64)(vs[l] - n_bool) * R + rr]";
         if (is_stream(i)) {
             // stream reference: new variable (almost) every constraint; no run register
-            o << "    const u32 sl" << i << " = " << ext << ";\n"
-              << "    float val" << i << ";\n    { const u32 l = sl" << i << "; val" << i << " = " << ld << "; }\n";
+            if (!staged)
+                o << "    const u32 sl" << i << " = " << ext << ";\n"
+                  << "    float val" << i << ";\n    { const u32 l = sl" << i << "; val" << i << " = " << ld << "; }\n";
         } else {
             o << "    { const u32 l = " << ext << "; if (l != cur" << i << ") { if (cur" << i
               << " != 0xffffffffu) accs[cur" << i << " * 32] += acc" << i << "; cur" << i << " = l; acc" << i
@@ -469,6 +524,62 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
     o << "}\n\n";
 }
 
+// K5 specialised: exact check of the rounded model (R22) for one kernel class.  Every slot's
+// truth value is computed, then the canonical xBDD is evaluated bottom-up with selects
+// (branch-free: lanes = restarts take different paths).  Atoms: s = 0; s += q_j y_j in stored
+// order in fp64 without FMA; s <= q0 (< q0 when strict).
+void emit_verify_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Template& t) {
+    const size_t ns = t.kinds.size();
+    o << "__device__ __forceinline__ u32 kv" << kid
+      << "(const TileDesc& T, const uint4* __restrict__ rp, const uint4* __restrict__ vp, const u32* __restrict__ vs,\n"
+         "    const signed char* __restrict__ x, const float* __restrict__ y, unsigned char* __restrict__ U,\n"
+         "    unsigned char* __restrict__ per_con, const u32* __restrict__ orig, u32 R, u64 rr, u32 r, bool live,\n"
+         "    u32 n_bool, const u32* __restrict__ arow, const double* __restrict__ aval,\n"
+         "    const double* __restrict__ arhs, const unsigned char* __restrict__ astrict) {\n"
+         "  u32 cnt = 0u;\n";
+    const uint32_t ref_words = 1 + (K.n_refs + 1) / 2;             // words 1.. hold the refs
+    const uint32_t q_needed = (ref_words + 3) / 4;
+    o << "  for (u32 c = 0; c < T.n_cons; ++c, rp += " << K.stride4 << ", vp += " << K.vstride4 << ") {\n";
+    for (uint32_t q = 0; q < q_needed; ++q) o << "    const uint4 q" << q << " = __ldg(rp + " << q << ");\n";
+    for (uint32_t q = 0; q < K.vstride4; ++q) o << "    const uint4 v" << q << " = __ldg(vp + " << q << ");\n";
+    uint32_t ref = 0, ai = 0;
+    auto ext = [&](uint32_t i) {
+        return "((" + word(1 + i / 2) + " >> " + std::to_string(16 * (i % 2)) + ") & 0xffffu)";
+    };
+    for (size_t s = 0; s < ns; ++s) {
+        if (t.kinds[s] == 0) {
+            o << "    const bool t" << s << " = x[(u64)vs[" << ext(ref) << "] * R + rr] == (signed char)-1;\n";
+            ++ref;
+        } else {
+            const uint32_t nnz = K.nnz[ai];
+            const std::string aid = "v" + std::to_string(ai / 4) + "." + comp(ai);
+            o << "    bool t" << s << ";\n    { const u32 aid = " << aid << "; const u32 k0 = arow[aid]; double sacc = 0.0;\n";
+            for (uint32_t k = 0; k < nnz; ++k) {
+                o << "      sacc = __dadd_rn(sacc, __dmul_rn(aval[k0 + " << k << "], (double)y[(u64)(vs[" << ext(ref)
+                  << "] - n_bool) * R + rr]));\n";
+                ++ref;
+            }
+            o << "      const double rhs = arhs[aid];\n      t" << s << " = astrict[aid] ? (sacc < rhs) : (sacc <= rhs); }\n";
+            ++ai;
+        }
+    }
+    auto sat = [&](int child) -> std::string {
+        if (child >= 0) return "s" + std::to_string(child);
+        return child == kTrue ? "true" : "false";
+    };
+    for (size_t vv = t.nodes.size(); vv-- > 0;) {
+        const TNode& nd = t.nodes[vv];
+        o << "    const bool s" << vv << " = t" << nd.level << " ? " << sat(nd.hi) << " : " << sat(nd.lo) << ";\n";
+    }
+    o << "    const u32 u = " << (t.root >= 0 ? "s" + std::to_string(t.root) : std::string(t.root == kTrue ? "true" : "false"))
+      << " ? 0u : 1u;\n"
+         "    if (live) {\n"
+         "      if (U) { unsigned char* cell = U + (u64)(T.cons_begin + c) * R + rr; const u32 nv = (u32)*cell + u; *cell = (unsigned char)(nv > 255u ? 255u : nv); }\n"
+         "      if (per_con) per_con[(u64)orig[T.cons_begin + c] * R + rr] = (unsigned char)u;\n"
+         "    }\n"
+         "    cnt += u;\n  }\n  return cnt;\n}\n\n";
+}
+
 }  // namespace
 
 std::string jit_source(const Formula& f, const Built& b, const Plan& p) {
@@ -504,9 +615,15 @@ std::string jit_source(const Formula& f, const Built& b, const Plan& p) {
          "  __syncwarp();\n"
          "  const float kq = kappa * 0.70710678118654752f;\n"
          "  const float dcoef = kappa * 0.79788456080286536f;\n"
-         "  double objacc = 0.0;\n"
-         "  const uint4* rp = recs + T.rec_off;\n"
-         "  switch (T.kclass) {\n";
+         "  double objacc = 0.0;\n";
+    if (stage_records())
+        o << "  uint4* rs = (uint4*)(smem + WARPS * VMAX * 33) + warp * " << p.rec_stage4 << ";\n"
+             "  for (u32 q = lane; q < T.pad0; q += 32) rs[q] = __ldg(recs + T.rec_off + q);   // pad0 = record uint4s\n"
+             "  __syncwarp();\n"
+             "  const uint4* rp = rs;\n";
+    else
+        o << "  const uint4* rp = recs + T.rec_off;\n";
+    o << "  switch (T.kclass) {\n";
     for (uint32_t k = 0; k < p.n_jit_kclasses; ++k)
         o << "    case " << k << ": kc" << k
           << "(T, rp, vs, acc + lane, a, b, U, R, rr, r, live, n_bool, kq, dcoef, wscale, objacc, terms, terms_r, orig); break;\n";
@@ -519,6 +636,39 @@ std::string jit_source(const Formula& f, const Built& b, const Plan& p) {
          "    if (g < n_bool) atomicAdd(ga + (u64)g * R + r, v); else atomicAdd(gb + (u64)(g - n_bool) * R + r, v);\n"
          "  }\n"
          "  atomicAdd(obj + r, objacc);\n"
+         "}\n\n";
+    // K5: exact verification of the rounded models + ERWA counters over the same tiles
+    for (uint32_t k = 0; k < p.n_jit_kclasses; ++k) emit_verify_class(o, k, p.kclasses[k], b.tmpls[p.kclasses[k].tmpl]);
+    o << "extern \"C\" __global__ void __launch_bounds__(WARPS * 32) fsmt_k5_jit(\n"
+         "    const TileDesc* __restrict__ tiles, u32 n_tiles, const uint4* __restrict__ recs,\n"
+         "    const uint4* __restrict__ vrecs, const u32* __restrict__ tile_vars, const signed char* __restrict__ x,\n"
+         "    const float* __restrict__ y, unsigned char* __restrict__ U, u32* __restrict__ unsat,\n"
+         "    unsigned char* __restrict__ per_con, const u32* __restrict__ orig, u32 R, u32 n_bool,\n"
+         "    const u32* __restrict__ arow, const double* __restrict__ aval, const double* __restrict__ arhs,\n"
+         "    const unsigned char* __restrict__ astrict) {\n"
+         "  extern __shared__ float smem[];\n"
+         "  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;\n"
+         "  u32* vs = (u32*)smem + warp * VMAX;\n"
+         "  const u32 rtiles = (R + 31) / 32;\n"
+         "  const u64 gw = (u64)blockIdx.x * WARPS + warp;\n"
+         "  const u32 rt = (u32)(gw % rtiles);\n"
+         "  const u64 ti = gw / rtiles;\n"
+         "  if (ti >= n_tiles) return;\n"
+         "  const TileDesc T = tiles[ti];\n"
+         "  const u32 r = rt * 32 + lane;\n"
+         "  const bool live = r < R;\n"
+         "  const u64 rr = live ? r : 0;\n"
+         "  for (u32 l = lane; l < T.n_vars; l += 32) vs[l] = tile_vars[T.var_off + l];\n"
+         "  __syncwarp();\n"
+         "  const uint4* rp = recs + T.rec_off;\n"
+         "  const uint4* vp = vrecs + T.pad1;\n"
+         "  u32 cnt = 0u;\n"
+         "  switch (T.kclass) {\n";
+    for (uint32_t k = 0; k < p.n_jit_kclasses; ++k)
+        o << "    case " << k << ": cnt = kv" << k
+          << "(T, rp, vp, vs, x, y, U, per_con, orig, R, rr, r, live, n_bool, arow, aval, arhs, astrict); break;\n";
+    o << "    default: break;\n  }\n"
+         "  if (live && cnt) atomicAdd(unsat + r, cnt);\n"
          "}\n";
     (void)f;
     return o.str();

@@ -82,13 +82,14 @@ class Solver:
 
     # ---------------------------------------------------------------- solve
     def set_params(self, kappas=None, eta=0.0, eps=0.0, rounding=N.ROUND_SIGN, erwa_mode=N.ERWA_VERBATIM,
-                   time_limit_s=0.0):
+                   time_limit_s=0.0, eta_mode=0):
         p = N.Params()
         if kappas is not None:
             self._kappas = np.ascontiguousarray(kappas, dtype=np.float32)
             p.kappas = self._kappas.ctypes.data_as(C.POINTER(C.c_float))
             p.n_stages = len(self._kappas)
         p.eta, p.eps, p.rounding, p.erwa_mode, p.time_limit_s = eta, eps, rounding, erwa_mode, time_limit_s
+        p.eta_mode = eta_mode
         self._check(N.lib.fsmt_set_params(self._h, C.byref(p)))
 
     def solve(self, restarts: int, steps: int, seed: int) -> SolveResult:

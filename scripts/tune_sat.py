@@ -37,6 +37,7 @@ def main():
     p.add_argument("--stages", type=int, default=20)
     p.add_argument("--erwa", type=int, nargs="+", default=[0, 1])
     p.add_argument("--rounding", type=int, nargs="+", default=[0])
+    p.add_argument("--eta-modes", type=int, nargs="+", default=[0])
     p.add_argument("--time-limit", type=float, default=120.0)
     p.add_argument("--only", default="")
     a = p.parse_args()
@@ -50,8 +51,9 @@ def main():
     sch = schedules(a.kmax, a.stages)
     if a.only:
         sch = {k: v for k, v in sch.items() if k in a.only.split(",")}
-    for (name, ks), steps, eta, erwa, rnd in itertools.product(sch.items(), a.steps, a.etas, a.erwa, a.rounding):
-        s.set_params(kappas=ks, eta=eta, erwa_mode=erwa, rounding=rnd, time_limit_s=a.time_limit)
+    for (name, ks), steps, eta, erwa, rnd, em in itertools.product(sch.items(), a.steps, a.etas, a.erwa, a.rounding,
+                                                                    a.eta_modes):
+        s.set_params(kappas=ks, eta=eta, erwa_mode=erwa, rounding=rnd, time_limit_s=a.time_limit, eta_mode=em)
         solved, times, best = 0, [], []
         t0 = time.perf_counter()
         for seed in a.seeds:
@@ -61,7 +63,7 @@ def main():
             times.append(res.stats["solve_ms"] / 1e3)
             best.append(res.stats["best_unsat"])
         print(json.dumps({"config": a.config, "schedule": name, "steps": steps, "eta": eta, "erwa": erwa,
-                          "rounding": rnd, "solved": solved, "runs": len(a.seeds), "best_unsat": best,
+                          "rounding": rnd, "eta_mode": em, "solved": solved, "runs": len(a.seeds), "best_unsat": best,
                           "solve_s": [round(x, 3) for x in times], "wall_s": round(time.perf_counter() - t0, 2)}),
               flush=True)
 
