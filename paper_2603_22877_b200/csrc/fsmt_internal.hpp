@@ -104,6 +104,11 @@ struct KClass {
     bool jit;
     uint64_t n_cons;
     std::vector<uint8_t> stream;  // per reference: 1 = changes most constraints (no run register)
+    // record compression: logical word w is stored at position wpos[w] of the compressed record,
+    // or (wpos[w] < 0) is the same for every constraint of the class and is emitted as the
+    // literal wconst[w] in the generated code (e.g. unit weights, +-1 coefficients, 1/||q||)
+    std::vector<int32_t> wpos;
+    std::vector<uint32_t> wconst;
 };
 
 struct TileDesc {                // mirrored in the JIT source (32 bytes)

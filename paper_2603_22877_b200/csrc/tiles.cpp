@@ -278,6 +278,62 @@ Plan make_plan(const Formula& f, const Built& b, bool enable_jit) {
         for (uint32_t r = 0; r < p.kclasses[k].n_refs; ++r)
             p.kclasses[k].stream[r] = seen[k] && 2 * changes[k][r] > seen[k];
     }
+
+    // 6. record compression: words equal across a whole class become literals in the code
+    const char* cz = getenv("FSMT_JIT_FOLD");
+    const bool fold = !(cz && cz[0] == '0');
+    std::vector<std::vector<uint8_t>> varies(p.n_jit_kclasses);
+    std::vector<std::vector<uint32_t>> first(p.n_jit_kclasses);
+    for (uint32_t k = 0; k < p.n_jit_kclasses; ++k) {
+        varies[k].assign(p.kclasses[k].words, fold ? 0 : 1);
+        first[k].assign(p.kclasses[k].words, 0);
+    }
+    std::vector<uint8_t> have(p.n_jit_kclasses, 0);
+    for (const TileDesc& T : p.tiles) {
+        const KClass& K = p.kclasses[T.kclass];
+        for (uint32_t c = 0; c < T.n_cons; ++c) {
+            const uint32_t* rec = p.recs.data() + ((size_t)T.rec_off + (size_t)c * K.stride4) * 4;
+            if (!have[T.kclass]) {
+                for (uint32_t w = 0; w < K.words; ++w) first[T.kclass][w] = rec[w];
+                have[T.kclass] = 1;
+            }
+            for (uint32_t w = 0; w < K.words; ++w) varies[T.kclass][w] |= rec[w] != first[T.kclass][w];
+        }
+    }
+    std::vector<uint32_t> old_stride(p.n_jit_kclasses);
+    for (uint32_t k = 0; k < p.n_jit_kclasses; ++k) {
+        KClass& K = p.kclasses[k];
+        old_stride[k] = K.stride4;
+        K.wpos.assign(K.words, -1);
+        K.wconst = first[k];
+        int32_t n = 0;
+        for (uint32_t w = 0; w < K.words; ++w)
+            if (varies[k][w]) K.wpos[w] = n++;
+        K.stride4 = std::max<uint32_t>(1, ((uint32_t)n + 3) / 4);
+    }
+    std::vector<uint32_t> packed;
+    packed.reserve(p.recs.size());
+    for (TileDesc& T : p.tiles) {
+        const KClass& K = p.kclasses[T.kclass];
+        const uint32_t os = old_stride[T.kclass];
+        const uint32_t new_off = (uint32_t)(packed.size() / 4);
+        for (uint32_t c = 0; c < T.n_cons; ++c) {
+            const uint32_t* rec = p.recs.data() + ((size_t)T.rec_off + (size_t)c * os) * 4;
+            std::vector<uint32_t> out(K.stride4 * 4, 0);
+            for (uint32_t w = 0; w < K.words; ++w)
+                if (K.wpos[w] >= 0) out[(size_t)K.wpos[w]] = rec[w];
+            packed.insert(packed.end(), out.begin(), out.end());
+        }
+        T.rec_off = new_off;
+        T.pad0 = T.n_cons * K.stride4;
+    }
+    p.recs.swap(packed);
+    {
+        const char* e = getenv("FSMT_JIT_STAGE");
+        uint32_t ms = 0;
+        for (uint32_t k = 0; k < p.n_jit_kclasses; ++k) ms = std::max(ms, p.kclasses[k].stride4);
+        p.rec_stage4 = (e && e[0] == '1') ? p.cmax * ms : 0;
+    }
     return p;
 }
 
@@ -333,9 +389,20 @@ const char* comp(uint32_t w) {
     return c[w % 4];
 }
 
-std::string word(uint32_t w) { return "q" + std::to_string(w / 4) + "." + comp(w); }
+// Record word w of the class being emitted (g_wk): a register of the loaded (compressed)
+// record, or a literal when the word is constant over the class (record compression).
+const KClass* g_wk = nullptr;
+std::string word(uint32_t w) {
+    if (g_wk && w < g_wk->wpos.size()) {
+        const int32_t p = g_wk->wpos[w];
+        if (p < 0) return "(" + std::to_string(g_wk->wconst[w]) + "u)";
+        return "q" + std::to_string(p / 4) + "." + comp((uint32_t)p);
+    }
+    return "q" + std::to_string(w / 4) + "." + comp(w);
+}
 
 void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Template& t) {
+    g_wk = &K;
     const size_t ns = t.kinds.size();
     o << "__device__ __forceinline__ void kc" << kid
       << "(const TileDesc& T, const uint4* __restrict__ rp, const u32* __restrict__ vs, float* __restrict__ accs,\n"
@@ -370,7 +437,9 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
         return "(" + w + " >> " + std::to_string(16 * (i % 2)) + ") & 0xffffu";
     };
     auto rec_word = [&](uint32_t wd, uint32_t off4) {   // word wd of the record rp + off4 (shared memory)
-        return "rp[" + std::to_string(off4 + wd / 4) + "]." + comp(wd);
+        const int32_t pw = K.wpos[wd];
+        if (pw < 0) return "(" + std::to_string(K.wconst[wd]) + "u)";
+        return "rp[" + std::to_string(off4 + (uint32_t)pw / 4) + "]." + comp((uint32_t)pw);
     };
     if (staged) {
         // records are in shared memory; the values of the stream references of constraint c+1
@@ -410,7 +479,7 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
         for (uint32_t q = 0; q < K.stride4; ++q) o << "    const uint4 q" << q << " = __ldg(rp + " << q << ");\n";
         o << "    const u32 uc = U ? (u32)U[(u64)(T.cons_begin + c) * R + rr] : 0u;\n";
     }
-    o << "    float w = __uint_as_float(q0.x) * wscale;\n"
+    o << "    float w = __uint_as_float(" << word(0) << ") * wscale;\n"
          "    if (U) w = ldexpf(w, (int)uc);\n";
     for (size_t i = 0; i < nr; ++i) {
         uint32_t wd = 1 + (uint32_t)i / 2;
@@ -485,7 +554,14 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
         else if (bl == "1.f") val = "fmaf(pt" + lv + ", " + bh + ", pf" + lv + ")";
         else if (bh == "0.f") val = "pf" + lv + " * " + bl;
         else if (bl == "0.f") val = "pt" + lv + " * " + bh;
-        else val = "fmaf(pt" + lv + ", " + bh + ", pf" + lv + " * " + bl + ")";
+        else {
+            // both children internal: d = m_bu[hi] - m_bu[lo]; m_bu[v] = m_bu[lo] + p d (p + (1-p) = 1),
+            // and d is reused by the gradient term below
+            o << "    const float d" << vv << " = " << bh << " - " << bl << ";\n";
+            o << "    const float bu" << vv << " = fmaf(pt" << lv << ", d" << vv << ", " << bl << ");\n";
+            o << "    G" << lv << " = fmaf(m" << vv << ", d" << vv << ", G" << lv << ");\n";
+            continue;
+        }
         o << "    const float bu" << vv << " = " << val << ";\n";
         std::string diff;
         if (bh == "1.f" && bl == "0.f") diff = "";
@@ -529,6 +605,7 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
 // (branch-free: lanes = restarts take different paths).  Atoms: s = 0; s += q_j y_j in stored
 // order in fp64 without FMA; s <= q0 (< q0 when strict).
 void emit_verify_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Template& t) {
+    g_wk = &K;
     const size_t ns = t.kinds.size();
     o << "__device__ __forceinline__ u32 kv" << kid
       << "(const TileDesc& T, const uint4* __restrict__ rp, const uint4* __restrict__ vp, const u32* __restrict__ vs,\n"
@@ -538,7 +615,9 @@ void emit_verify_class(std::ostringstream& o, uint32_t kid, const KClass& K, con
          "    const double* __restrict__ arhs, const unsigned char* __restrict__ astrict) {\n"
          "  u32 cnt = 0u;\n";
     const uint32_t ref_words = 1 + (K.n_refs + 1) / 2;             // words 1.. hold the refs
-    const uint32_t q_needed = (ref_words + 3) / 4;
+    uint32_t q_needed = 0;                                          // compressed uint4s holding them
+    for (uint32_t w = 1; w < ref_words; ++w)
+        if (K.wpos[w] >= 0) q_needed = std::max(q_needed, (uint32_t)K.wpos[w] / 4 + 1);
     o << "  for (u32 c = 0; c < T.n_cons; ++c, rp += " << K.stride4 << ", vp += " << K.vstride4 << ") {\n";
     for (uint32_t q = 0; q < q_needed; ++q) o << "    const uint4 q" << q << " = __ldg(rp + " << q << ");\n";
     for (uint32_t q = 0; q < K.vstride4; ++q) o << "    const uint4 v" << q << " = __ldg(vp + " << q << ");\n";

@@ -1,0 +1,111 @@
+"""GPU solve-loop pieces: step-size / ERWA readings, rounding modes inside the solve, and the two
+multi-GPU drivers run at world size 1 over NCCL must reproduce fsmt_solve exactly."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import fsmt_gen
+from fsmt_gen.points import random_points, random_counters
+from oracle import hsmt, objective, semantics
+from tests.helpers import check_gradient, check_objective
+
+pytestmark = pytest.mark.gpu
+
+
+def make(text):
+    import paper_2603_22877_b200 as P
+    s = P.Solver(0)
+    s.load_formula(text)
+    s.build_xbdd()
+    return s
+
+
+@pytest.mark.parametrize("eta_mode", [0, 1, 2])
+def test_run_stage_eta_mode_matches_manual_steps(eta_mode):
+    inst = fsmt_gen.config("cfg4s")
+    kappa, eta, steps = 3.0, 0.02, 4
+    s1, s2 = make(inst.text), make(inst.text)
+    s1.set_params(eta=eta, eps=1e-9, eta_mode=eta_mode)
+    s2.set_params(eta=eta, eps=1e-9)
+    for s in (s1, s2):
+        s.begin(48, 21)
+    u1, _ = s1.run_stage(2, kappa, steps)
+    kk = np.float32(max(kappa, 1.0))               # the library computes eta_t in fp32
+    eta_t = float(np.float32(eta) / (kk ** eta_mode if eta_mode < 2 else kk * kk)) if eta_mode else eta
+    for _ in range(steps):
+        s2.sweep(kappa, 2)
+        s2.update(eta_t, 1e-9)
+    u2 = s2.stage_end(2)
+    a1, b1 = s1.get_state()
+    a2, b2 = s2.get_state()
+    assert np.array_equal(a1, a2) and np.array_equal(b1, b2) and np.array_equal(u1, u2)
+
+
+def test_erwa_reset0_weights():
+    inst = fsmt_gen.config("cfg2s")
+    f = hsmt.parse(inst.text)
+    s = make(inst.text)
+    s.set_params(erwa_mode=1)
+    R = 33
+    a, b = random_points(f.n_bool, f.n_real, R, seed=2)
+    U = random_counters(len(f.constraints), R, seed=3, max_u=3)
+    s.begin(R, 1)
+    s.set_state(a, b)
+    s.set_counters(U)
+    s.sweep(1.0, 7)                       # reset-to-0 reading: w = w_c 2^U, no stage factor (R18)
+    obj, ga, gb = s.get_sweep()
+    for r in (0, 32):
+        w = np.array([c.weight for c in f.constraints]) * 2.0 ** U[:, r].astype(float)
+        C, oga, ogb = objective.objective_and_gradient(f, a[:, r], b[:, r], 1.0, w)
+        check_objective(obj[r], C, float(w.sum()))
+        check_gradient(np.concatenate([ga[:, r], gb[:, r]]), np.concatenate([oga, ogb]), scale_relative=True)
+
+
+@pytest.mark.parametrize("rounding", [0, 1])
+def test_solve_rounding_modes_sound(rounding):
+    inst = fsmt_gen.config("cfg4s")
+    f = hsmt.parse(inst.text)
+    s = make(inst.text)
+    s.set_params(eta=0.05, rounding=rounding)
+    res = s.solve(512, 40, 3)
+    _, sat = semantics.eval_formula(f, res.x, res.y)
+    assert (res.verdict == 10) == all(sat)
+    assert sum(not v for v in sat) == res.stats["best_unsat"]
+
+
+def _init_nccl():
+    import torch.distributed as dist
+    if not dist.is_initialized():
+        sock = socket.socket()
+        sock.bind(("127.0.0.1", 0))
+        port = sock.getsockname()[1]
+        sock.close()
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK="0", WORLD_SIZE="1")
+        dist.init_process_group("nccl", rank=0, world_size=1)
+
+
+@pytest.mark.parametrize("mode", ["restart", "constraint"])
+def test_dist_drivers_world1_reproduce_solve(mode):
+    import torch
+    from paper_2603_22877_b200 import dist as D
+    _init_nccl()
+    torch.cuda.set_device(0)
+    inst = fsmt_gen.config("cfg4s")
+    kappas = [0.5, 1.0, 2.0, 4.0, 8.0]
+    ref = make(inst.text)
+    ref.set_params(kappas=kappas, eta=0.05)
+    res = ref.solve(256, 20, 11)
+    s = make(inst.text)
+    s.set_params(kappas=kappas, eta=0.05)
+    s.bind_stream(torch.cuda.current_stream().cuda_stream)
+    d = s.get_dims()
+    if mode == "restart":
+        out = D.solve_restart_sharded(s, d["n_bool"], d["n_real"], 256, 20, 11, kappas)
+    else:
+        out = D.solve_constraint_sharded(s, d["n_bool"], d["n_real"], 256, 20, 11, kappas, 0.05, 1e-2)
+    assert out.verdict == res.verdict
+    assert (out.best_unsat, out.winner_stage, out.winner_restart) == (
+        res.stats["best_unsat"], res.stats["winner_stage"], res.stats["winner_restart"])
+    assert np.array_equal(out.x, res.x) and np.array_equal(out.y, res.y)
