@@ -71,7 +71,9 @@ typedef struct {
     uint32_t erwa_mode;        /* FSMT_ERWA_VERBATIM (Alg.2 h<-1) | FSMT_ERWA_RESET0 */
     double time_limit_s;       /* <= 0: none (P:696 uses 1000 s) */
     uint32_t eta_mode;         /* step size in stage t (R13): 0 eta; 1 eta/kappa_t; 2 eta/kappa_t^2 (the
-                                  kappa-scaling of 1/L) -- kappa_t < 1 counts as 1 */
+                                  kappa-scaling of 1/L); 3 block steps: eta for a, eta/kappa_t^2
+                                  for b (only the real block's Lipschitz term grows with kappa)
+                                  -- kappa_t < 1 counts as 1 */
 } fsmt_params;
 
 typedef struct {

@@ -50,7 +50,7 @@ class Params:
     eps: float = 1e-2            # P:165, R14
     rounding: str = "sign"       # "sign" | "philox"  (R17)
     erwa_mode: int = 0           # 0: Alg.2 verbatim (h <- 1); 1: reset-to-0 reading (R18)
-    eta_mode: int = 0            # step in stage t: eta / max(kappa_t, 1)^eta_mode (R13; 1/L ~ kappa^-2)
+    eta_mode: int = 0            # 0 eta; 1 eta/kappa; 2 eta/kappa^2; 3 eta for a, eta/kappa^2 for b (R13)
 
 
 # ----------------------------------------------------------------------------- projection bounds
@@ -164,11 +164,15 @@ def violations(f, x, y):
 # ----------------------------------------------------------------------------- PGD step (for replay)
 
 
-def pgd_step(f, a, b, kappa, w, eta, lo, hi):
-    """One Alg.1 iteration: returns (a', b', ||gm||^2, C) at (a, b) (Eq.11-14)."""
+def pgd_step(f, a, b, kappa, w, eta, lo, hi, eta_b=None):
+    """One Alg.1 iteration: returns (a', b', ||gm||^2, C) at (a, b) (Eq.11-14).
+
+    eta_b: optional separate step for the real block (eta_mode 3 reading); default eta.
+    """
+    eta_b = eta if eta_b is None else eta_b
     C, ga, gb = objective_and_gradient(f, a, b, kappa, w)
-    a2, b2 = project(np.asarray(a) - eta * ga, np.asarray(b) - eta * gb, lo, hi)
-    gm2 = float(np.sum(((np.asarray(a) - a2) / eta) ** 2) + np.sum(((np.asarray(b) - b2) / eta) ** 2))
+    a2, b2 = project(np.asarray(a) - eta * ga, np.asarray(b) - eta_b * gb, lo, hi)
+    gm2 = float(np.sum(((np.asarray(a) - a2) / eta) ** 2) + np.sum(((np.asarray(b) - b2) / eta_b) ** 2))
     return a2, b2, gm2, C
 
 
@@ -196,9 +200,13 @@ def solve_restart(f, seed, r, params: Params, lo=None, hi=None):
     hist = []
     for t, kappa in enumerate(params.kappas, start=1):
         taken = 0
-        eta_t = params.eta / max(kappa, 1.0) ** params.eta_mode
+        kk = max(kappa, 1.0)
+        eta_t = params.eta / kk ** min(params.eta_mode, 2)
+        eta_b = params.eta / kk ** 2 if params.eta_mode >= 2 else eta_t
+        if params.eta_mode == 3:
+            eta_t = params.eta
         for _ in range(params.steps):
-            a2, b2, gm2, _ = pgd_step(f, a, b, kappa, w, eta_t, lo, hi)
+            a2, b2, gm2, _ = pgd_step(f, a, b, kappa, w, eta_t, lo, hi, eta_b)
             if gm2 <= params.eps ** 2:
                 break
             a, b = a2, b2

@@ -482,7 +482,7 @@ fsmt_status fsmt_set_params(fsmt_ctx* ctx, const fsmt_params* p) {
     } else {
         default_kappas(ctx->kappas);
     }
-    if (p->rounding > 1 || p->erwa_mode > 1 || p->eta_mode > 2)
+    if (p->rounding > 1 || p->erwa_mode > 1 || p->eta_mode > 3)
         return fail(ctx, FSMT_ERR_ARG, "bad rounding / erwa_mode / eta_mode");
     ctx->eta = p->eta > 0 ? p->eta : 0.05f;
     ctx->eps = p->eps > 0 ? p->eps : 1e-2f;
@@ -641,10 +641,10 @@ static fsmt_status sweep_impl(fsmt_ctx* ctx, float kappa, uint32_t stage_t, doub
     return check_launch(ctx);
 }
 
-static fsmt_status update_impl(fsmt_ctx* ctx, float eta, float eps) {
+static fsmt_status update_impl(fsmt_ctx* ctx, float eta, float eps, float eta_b = 0.f) {
     {
         Timed tm(ctx, 1);
-        launch_update(ctx->F, ctx->S, eta, eps, ctx->stream);
+        launch_update(ctx->F, ctx->S, eta, eps, ctx->stream, eta_b);
     }
     ctx->launches += 3;
     return check_launch(ctx);
@@ -795,10 +795,13 @@ fsmt_status fsmt_run_stage(fsmt_ctx* ctx, uint32_t stage_t, float kappa, uint32_
     if (stage_t == 0) stage_t = 1;
     CK(cudaMemsetAsync(ctx->S.frozen, 0, ctx->S.R, ctx->stream));
     const float kk = std::max(kappa, 1.0f);
-    const float eta_t = ctx->eta_mode == 1 ? ctx->eta / kk : ctx->eta_mode == 2 ? ctx->eta / (kk * kk) : ctx->eta;
+    float eta_t = ctx->eta, eta_b = ctx->eta;      // eta_mode 0
+    if (ctx->eta_mode == 1) eta_t = eta_b = ctx->eta / kk;
+    if (ctx->eta_mode == 2) eta_t = eta_b = ctx->eta / (kk * kk);
+    if (ctx->eta_mode == 3) eta_b = ctx->eta / (kk * kk);   // block steps: a keeps eta, b gets eta/kappa^2
     for (uint32_t k = 0; k < steps; ++k) {
         if ((s = sweep_impl(ctx, kappa, stage_t, nullptr, 0))) return s;
-        if ((s = update_impl(ctx, eta_t, ctx->eps))) return s;
+        if ((s = update_impl(ctx, eta_t, ctx->eps, eta_b))) return s;
     }
     if ((s = stage_end_impl(ctx, stage_t))) return s;
     if (unsat_out || min_unsat) {

@@ -84,6 +84,11 @@ struct Built {
     std::vector<float> lo, hi;             // projection bounds (R15), f32
     uint32_t max_slots = 0, max_nodes = 0, n_bounded = 0;
     uint64_t n_nodes = 0;
+    // symmetric constraints over distinct variables (count-DP fast path):
+    // cons_sym = 1 + kind (OR, CARD, NAE, XOR) or 0; slot_neg = literal polarity per slot
+    std::vector<uint8_t> cons_sym;         // [C]
+    std::vector<uint16_t> cons_k;          // [C] CARD threshold
+    std::vector<uint8_t> slot_neg;         // parallel to slot_ids
 };
 
 // ---- device work plan (csrc/tiles.cpp) -----------------------------------------------------

@@ -175,7 +175,7 @@ __device__ __forceinline__ float step_value(float x, double g, float eta, float 
     return __double2float_rn(t);
 }
 
-__global__ void k3_norm(DevFormula F, DevState S, float eta) {
+__global__ void k3_norm(DevFormula F, DevState S, float eta, float eta_b) {
     const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= S.R) return;
     const uint32_t part = blockIdx.y;
@@ -190,9 +190,9 @@ __global__ void k3_norm(DevFormula F, DevState S, float eta) {
         } else {
             const uint32_t j = v - F.n_bool;
             x = S.b[(size_t)j * S.R + r];
-            xn = step_value(x, S.gb[(size_t)j * S.R + r], eta, F.lo[j], F.hi[j]);
+            xn = step_value(x, S.gb[(size_t)j * S.R + r], eta_b, F.lo[j], F.hi[j]);
         }
-        const double d = ((double)x - (double)xn) / (double)eta;
+        const double d = ((double)x - (double)xn) / (double)(v < F.n_bool ? eta : eta_b);
         acc += d * d;
     }
     S.gm2_part[(size_t)part * S.R + r] = acc;
@@ -207,7 +207,7 @@ __global__ void k3_final(DevState S, uint32_t n_parts, float eps) {
     if (!S.frozen[r] && acc <= (double)eps * (double)eps) S.frozen[r] = 1;   // Eq.14
 }
 
-__global__ void k3_apply(DevFormula F, DevState S, float eta) {
+__global__ void k3_apply(DevFormula F, DevState S, float eta, float eta_b) {
     const uint64_t n = (uint64_t)(F.n_bool + F.n_real) * S.R;
     for (uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t v = (uint32_t)(idx / S.R), r = (uint32_t)(idx % S.R);
@@ -218,7 +218,7 @@ __global__ void k3_apply(DevFormula F, DevState S, float eta) {
         } else {
             const uint32_t j = v - F.n_bool;
             float& x = S.b[(size_t)j * S.R + r];
-            x = step_value(x, S.gb[(size_t)j * S.R + r], eta, F.lo[j], F.hi[j]);
+            x = step_value(x, S.gb[(size_t)j * S.R + r], eta_b, F.lo[j], F.hi[j]);
         }
     }
 }
@@ -379,15 +379,16 @@ void launch_sweep(const DevFormula& F, const DevState& S, float kappa, float wsc
 
 int update_parts(const DevFormula& F) { return (int)((F.n_bool + F.n_real + kVarsPerPart - 1) / kVarsPerPart); }
 
-void launch_update(const DevFormula& F, const DevState& S, float eta, float eps, cudaStream_t st) {
+void launch_update(const DevFormula& F, const DevState& S, float eta, float eps, cudaStream_t st, float eta_b) {
+    if (!(eta_b > 0.f)) eta_b = eta;
     const uint32_t parts = (uint32_t)update_parts(F);
     if (parts == 0 || S.R == 0) return;
     dim3 g1((S.R + 127) / 128, parts);
-    k3_norm<<<g1, 128, 0, st>>>(F, S, eta);
+    k3_norm<<<g1, 128, 0, st>>>(F, S, eta, eta_b);
     k3_final<<<(S.R + 127) / 128, 128, 0, st>>>(S, parts, eps);
     const uint64_t n = (uint64_t)(F.n_bool + F.n_real) * S.R;
     const uint64_t blocks = std::min<uint64_t>((n + 255) / 256, 148ull * 16);
-    k3_apply<<<(unsigned)blocks, 256, 0, st>>>(F, S, eta);
+    k3_apply<<<(unsigned)blocks, 256, 0, st>>>(F, S, eta, eta_b);
 }
 
 void launch_round(const DevFormula& F, const DevState& S, uint32_t rounding, uint64_t seed, uint32_t off,

@@ -89,7 +89,8 @@ void launch_scatter_rows_u8(uint8_t* dst, const uint8_t* src, const uint32_t* id
                             cudaStream_t st);
 // K3: projected step (three launches: partial norms, finalize, apply).
 int update_parts(const DevFormula& F);
-void launch_update(const DevFormula& F, const DevState& S, float eta, float eps, cudaStream_t st);
+// eta: step for a (Booleans); eta_b: step for b (reals), <= 0 -> eta (Eq.11 uses one eta; R13).
+void launch_update(const DevFormula& F, const DevState& S, float eta, float eps, cudaStream_t st, float eta_b = 0.f);
 // K4: rounding (R17).
 void launch_round(const DevFormula& F, const DevState& S, uint32_t rounding, uint64_t seed, uint32_t restart_offset,
                   uint32_t stage, cudaStream_t st);

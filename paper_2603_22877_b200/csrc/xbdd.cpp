@@ -243,6 +243,8 @@ Built build_xbdds(const Formula& f, uint64_t node_budget) {
     b.cons_tmpl.resize(C);
     b.cons_slot_off.resize(C + 1);
     b.cons_w.resize(C);
+    b.cons_sym.assign(C, 0);
+    b.cons_k.assign(C, 0);
     b.lo.assign(f.n_real, -INFINITY);
     b.hi.assign(f.n_real, INFINITY);
     std::unordered_map<std::string, uint32_t> shape_to_tid;
@@ -293,6 +295,10 @@ Built build_xbdds(const Formula& f, uint64_t node_budget) {
         const Template& t = b.tmpls[tid];
         b.cons_tmpl[ci] = tid;
         b.cons_w[ci] = (float)c.weight;
+        const bool sym = c.kind != K_EXPR && sm.ids.size() == c.lit_n;   // distinct variables: slot i = literal i
+        b.cons_sym[ci] = sym ? (uint8_t)(1 + c.kind) : 0;
+        b.cons_k[ci] = (uint16_t)std::min<uint32_t>(c.k, 65535);
+        for (size_t s = 0; s < sm.ids.size(); ++s) b.slot_neg.push_back(sym ? f.lits[c.lit_first + s].neg : 0);
         b.slot_ids.insert(b.slot_ids.end(), sm.ids.begin(), sm.ids.end());
         b.cons_slot_off[ci + 1] = (uint32_t)b.slot_ids.size();
         b.max_slots = std::max<uint32_t>(b.max_slots, (uint32_t)t.kinds.size());

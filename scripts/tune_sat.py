@@ -23,6 +23,7 @@ def schedules(kmax_list, n_stages):
         g = [kmax ** (i / (n_stages - 1)) for i in range(n_stages)]          # geometric 1 .. kmax
         out[f"geo1-{kmax}"] = g
         out[f"geo0.1-{kmax}"] = [0.1 * (kmax / 0.1) ** (i / (n_stages - 1)) for i in range(n_stages)]
+        out[f"geo1-{kmax}-hold"] = g + [kmax] * n_stages                    # then hold kmax as long again
     return out
 
 
