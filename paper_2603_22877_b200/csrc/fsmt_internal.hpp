@@ -135,6 +135,7 @@ struct Plan {
     uint32_t vmax = kTileVmaxDefault; // local variables per tile (on-chip accumulator rows)
     uint32_t rec_stage4 = 0;          // per-warp shared-memory record stage, uint4 (0: not staged)
     uint32_t cmax = kTileCmax;        // constraints per tile (FSMT_TILE_CMAX)
+    uint32_t sval = 0;                // 1: tile variable values staged in shared memory (FSMT_JIT_SVAL)
 };
 
 Plan make_plan(const Formula& f, const Built& b, bool enable_jit);

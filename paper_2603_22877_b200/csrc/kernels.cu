@@ -42,6 +42,13 @@ __device__ __forceinline__ uint32_t draw24(uint64_t seed, uint32_t r, uint32_t v
 
 // ---------------------------------------------------------------------------------------- K0
 
+// w * 2^u, u in [0, 255]: exactly ldexpf(w, u) (powers of two <= 2^127, an overflow stays inf)
+__device__ __forceinline__ float pow2_u8(float w, uint32_t u) {
+    const float f1 = __uint_as_float((127u + (u & 127u)) << 23);
+    const float f2 = __uint_as_float((127u + ((u >> 7) << 6)) << 23);
+    return __fmul_rn(__fmul_rn(__fmul_rn(w, f1), f2), f2);
+}
+
 __global__ void k0_init(DevFormula F, DevState S, uint64_t seed, uint32_t off) {
     const uint64_t n = (uint64_t)(F.n_bool + F.n_real) * S.R;
     for (uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += (uint64_t)gridDim.x * blockDim.x) {
@@ -98,7 +105,7 @@ __global__ void __launch_bounds__(256) k1_sweep(DevFormula F, DevState S, float 
         const uint32_t nn = F.tmpl_node_off[tid + 1] - no;
         const int root = F.tmpl_root[tid];
         float w = F.cons_w[c] * wscale;                               // w_cr = w_c 2^(U + e_t)  (R18)
-        if (S.U) w = ldexpf(w, (int)S.U[(size_t)c * R + rr]);
+        if (S.U) w = pow2_u8(w, S.U[(size_t)c * R + rr]);
         // a1: slot probabilities (Eq.4 for Booleans, Eq.7 for atoms; erfc form, R28b)
         for (uint32_t s = 0; s < ns; ++s) {
             const uint32_t gid = F.slot_ids[so + s];
@@ -339,7 +346,8 @@ void launch_sweep_jit(cudaKernel_t k, const DevFormula& F, const DevState& S, co
     const int kVmax = (int)(T.vmax ? T.vmax : 128);                   // Plan::vmax
     const uint64_t nw = (uint64_t)T.n_tiles * ((S.R + 31) / 32);
     const unsigned blocks = (unsigned)((nw + kJitWarps - 1) / kJitWarps);
-    const size_t smem = (size_t)kJitWarps * (kVmax * 32 * 4 + kVmax * 4 + (size_t)T.rec_stage4 * 16);
+    const size_t smem = (size_t)kJitWarps * (kVmax * 32 * 4 * (T.sval ? 2 : 1) + kVmax * 4 + (size_t)T.rec_stage4 * 16);
+    if (smem > 48 * 1024) cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     uint32_t n_tiles = T.n_tiles, R = S.R, n_bool = F.n_bool;
     const uint8_t* U = S.U;
     void* args[] = {(void*)&T.tiles, &n_tiles, (void*)&T.recs, (void*)&T.tile_vars, (void*)&S.a, (void*)&S.b,

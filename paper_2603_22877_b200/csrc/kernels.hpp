@@ -76,6 +76,7 @@ struct DevTiles {
     uint32_t vmax;               // local variables per tile (Plan::vmax)
     uint32_t rec_stage4;         // per-warp record stage in uint4 (Plan::rec_stage4)
     const void* vrecs;           // K5 records (atom ids), tile.pad1 = offset in uint4
+    uint32_t sval;               // 1: tile variable values staged in shared memory (Plan::sval)
 };
 // K5 (JIT-specialised, tiles): exact check over the tiles of T (+ ERWA counters / per_con).
 void launch_verify_jit(cudaKernel_t k, const DevFormula& F, const DevState& S, const DevTiles& T, const int8_t* x,

@@ -35,6 +35,7 @@ Plan make_plan(const Formula& f, const Built& b, bool enable_jit) {
     if (const char* w = getenv("FSMT_JIT_WARPS")) p.jit_warps = std::max(1, std::min(8, atoi(w)));
     if (const char* v = getenv("FSMT_TILE_VMAX")) p.vmax = (uint32_t)std::max(16, std::min(256, atoi(v)));
     if (const char* v = getenv("FSMT_TILE_CMAX")) p.cmax = (uint32_t)std::max(1, std::min(1024, atoi(v)));
+    if (const char* v = getenv("FSMT_JIT_SVAL")) p.sval = v[0] == '1' ? 1u : 0u;
     const uint32_t C = (uint32_t)b.cons_tmpl.size();
     // 1. kernel classes
     std::map<std::vector<uint32_t>, uint32_t> kc_of;
@@ -364,6 +365,14 @@ bool stage_records() {
 }
 
 const char* kErfcPrelude =
+    "// w * 2^u for u in [0, 255], exactly ldexpf(w, u): every factor is a power of two <= 2^127,\n"
+    "// so each product is exact until it overflows, and an overflow stays inf (the exact value\n"
+    "// overflows too, all factors being >= 1)\n"
+    "__device__ __forceinline__ float fsmt_pow2_u8(float w, u32 u) {\n"
+    "  const float f1 = __uint_as_float((127u + (u & 127u)) << 23);\n"
+    "  const float f2 = __uint_as_float((127u + ((u >> 7) << 6)) << 23);\n"
+    "  return __fmul_rn(__fmul_rn(__fmul_rn(w, f1), f2), f2);\n"
+    "}\n"
     "__device__ __forceinline__ float fsmt_ex2(float x) { float r; asm(\"ex2.approx.ftz.f32 %0, %1;\" : \"=f\"(r) : \"f\"(x)); return r; }\n"
     "// 0.5*erfc(z) for z >= 0 and ez = exp(-z^2) (dd/db factor, P:1326-1327).\n"
     "// z < 0.75: 1 - erf(z) from the Maclaurin series of erf (10 terms); z >= 0.75: Numerical Recipes\n"
@@ -402,14 +411,14 @@ std::string word(uint32_t w) {
     return "q" + std::to_string(w / 4) + "." + comp(w);
 }
 
-void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Template& t) {
+void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Template& t, bool sval) {
     g_wk = &K;
     const size_t ns = t.kinds.size();
     o << "__device__ __forceinline__ void kc" << kid
       << "(const TileDesc& T, const uint4* __restrict__ rp, const u32* __restrict__ vs, float* __restrict__ accs,\n"
          "    const float* __restrict__ a, const float* __restrict__ b, const unsigned char* __restrict__ U,\n"
          "    u32 R, u64 rr, u32 r, bool live, u32 n_bool, float kq, float dcoef, float wscale, double& objacc,\n"
-         "    double* __restrict__ terms, u32 terms_r, const u32* __restrict__ orig) {\n";
+         "    double* __restrict__ terms, u32 terms_r, const u32* __restrict__ orig, const float* __restrict__ vals) {\n";
     // refs
     std::vector<int> ref_kind;      // 0 Boolean, 1 real
     std::vector<int> slot_ref0(ns);
@@ -432,6 +441,7 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
     const bool prefetch = pf_env && pf_env[0] == '1';
     const bool staged = stage_records();
     auto ld_of = [&](size_t i) {
+        if (sval) return std::string("vals[l * 32]");
         return ref_kind[i] == 0 ? std::string("a[(u64)vs[l] * R + rr]") : std::string("b[(u64)(vs[l] - n_bool) * R + rr]");
     };
     auto ext_of = [&](size_t i, const std::string& w) {
@@ -481,11 +491,11 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
         o << "    const u32 uc = U ? (u32)U[(u64)(T.cons_begin + c) * R + rr] : 0u;\n";
     }
     o << "    float w = __uint_as_float(" << word(0) << ") * wscale;\n"
-         "    if (U) w = ldexpf(w, (int)uc);\n";
+         "    if (U) w = fsmt_pow2_u8(w, uc);\n";
     for (size_t i = 0; i < nr; ++i) {
         uint32_t wd = 1 + (uint32_t)i / 2;
         const std::string ext = "(" + word(wd) + " >> " + std::to_string(16 * (i % 2)) + ") & 0xffffu";
-        const std::string ld = ref_kind[i] == 0 ? "a[(u64)vs[l] * R + rr]" : "b[(u64)(vs[l] - n_bool) * R + rr]";
+        const std::string ld = ld_of(i);
         if (is_stream(i)) {
             // stream reference: new variable (almost) every constraint; no run register
             if (!staged)
@@ -668,7 +678,7 @@ std::string jit_source(const Formula& f, const Built& b, const Plan& p) {
          "typedef unsigned int u32;\ntypedef unsigned long long u64;\n"
          "struct TileDesc { u32 kclass, cons_begin, n_cons, var_off, n_vars, rec_off, pad0, pad1; };\n"
       << "#define VMAX " << p.vmax << "\n#define WARPS " << p.jit_warps << "\n\n" << kErfcPrelude;
-    for (uint32_t k = 0; k < p.n_jit_kclasses; ++k) emit_class(o, k, p.kclasses[k], b.tmpls[p.kclasses[k].tmpl]);
+    for (uint32_t k = 0; k < p.n_jit_kclasses; ++k) emit_class(o, k, p.kclasses[k], b.tmpls[p.kclasses[k].tmpl], p.sval != 0);
     const char* minb = getenv("FSMT_JIT_MINB");      // optional min CTAs/SM (register cap), A/B tuning
     o << "extern \"C\" __global__ void __launch_bounds__(WARPS * 32" << (minb && atoi(minb) > 0 ? std::string(", ") + minb : std::string())
       << ") fsmt_k1_jit(\n"
@@ -692,7 +702,16 @@ std::string jit_source(const Formula& f, const Built& b, const Plan& p) {
          "  const u64 rr = live ? r : 0;\n"
          "  for (u32 l = lane; l < T.n_vars; l += 32) vs[l] = tile_vars[T.var_off + l];\n"
          "  for (u32 l = 0; l < T.n_vars; ++l) acc[l * 32 + lane] = 0.f;\n"
-         "  __syncwarp();\n"
+         "  __syncwarp();\n";
+    if (p.sval)
+        o << "  float* vals = smem + WARPS * VMAX * 33 + WARPS * " << p.rec_stage4 * 4 << " + warp * (VMAX * 32) + lane;\n"
+             "  for (u32 l = 0; l < T.n_vars; ++l) {   // tile variable values, staged once per tile\n"
+             "    const u32 g = vs[l];\n"
+             "    vals[l * 32] = g < n_bool ? a[(u64)g * R + rr] : b[(u64)(g - n_bool) * R + rr];\n"
+             "  }\n";
+    else
+        o << "  const float* vals = nullptr;\n";
+    o << ""
          "  const float kq = kappa * 0.70710678118654752f;\n"
          "  const float dcoef = kappa * 0.79788456080286536f;\n"
          "  double objacc = 0.0;\n";
@@ -706,7 +725,7 @@ std::string jit_source(const Formula& f, const Built& b, const Plan& p) {
     o << "  switch (T.kclass) {\n";
     for (uint32_t k = 0; k < p.n_jit_kclasses; ++k)
         o << "    case " << k << ": kc" << k
-          << "(T, rp, vs, acc + lane, a, b, U, R, rr, r, live, n_bool, kq, dcoef, wscale, objacc, terms, terms_r, orig); break;\n";
+          << "(T, rp, vs, acc + lane, a, b, U, R, rr, r, live, n_bool, kq, dcoef, wscale, objacc, terms, terms_r, orig, vals); break;\n";
     o << "    default: break;\n  }\n"
          "  __syncwarp();\n"
          "  if (!live) return;\n"

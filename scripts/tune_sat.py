@@ -17,13 +17,14 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
-def schedules(kmax_list, n_stages):
+def schedules(kmax_list, n_stages, holds=(1,)):
     out = {"default": [round(0.1 * i, 4) for i in range(1, 21)]}
     for kmax in kmax_list:
         g = [kmax ** (i / (n_stages - 1)) for i in range(n_stages)]          # geometric 1 .. kmax
         out[f"geo1-{kmax}"] = g
         out[f"geo0.1-{kmax}"] = [0.1 * (kmax / 0.1) ** (i / (n_stages - 1)) for i in range(n_stages)]
-        out[f"geo1-{kmax}-hold"] = g + [kmax] * n_stages                    # then hold kmax as long again
+        for m in holds:                                                      # then hold kmax m times as long
+            out[f"geo1-{kmax}-hold" + ("" if m == 1 else str(m))] = g + [kmax] * (m * n_stages)
     return out
 
 
@@ -36,6 +37,7 @@ def main():
     p.add_argument("--etas", type=float, nargs="+", default=[0.01, 0.05])
     p.add_argument("--kmax", type=float, nargs="+", default=[20.0, 100.0])
     p.add_argument("--stages", type=int, default=20)
+    p.add_argument("--holds", type=int, nargs="+", default=[1])
     p.add_argument("--erwa", type=int, nargs="+", default=[0, 1])
     p.add_argument("--rounding", type=int, nargs="+", default=[0])
     p.add_argument("--eta-modes", type=int, nargs="+", default=[0])
@@ -49,7 +51,7 @@ def main():
     s = P.Solver(0)
     s.load_formula(inst.text)
     s.build_xbdd()
-    sch = schedules(a.kmax, a.stages)
+    sch = schedules(a.kmax, a.stages, a.holds)
     if a.only:
         sch = {k: v for k, v in sch.items() if k in a.only.split(",")}
     for (name, ks), steps, eta, erwa, rnd, em in itertools.product(sch.items(), a.steps, a.etas, a.erwa, a.rounding,
