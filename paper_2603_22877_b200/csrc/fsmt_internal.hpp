@@ -95,7 +95,7 @@ struct Built {
 // Constraints are permuted into an internal order grouped into tiles: a tile is a run of
 // constraints of one kernel class (template + nnz of each atom slot) whose variables fit a
 // small local table, so the JIT-specialised sweep accumulates their gradients on chip.
-constexpr uint32_t kTileVmaxDefault = 128;   // local variables per tile (FSMT_TILE_VMAX)
+constexpr uint32_t kTileVmaxDefault = 64;    // local variables per tile (FSMT_TILE_VMAX; A/B in DESIGN.md §9)
 constexpr uint32_t kTileCmax = 64;        // constraints per tile
 constexpr uint32_t kGroupVarsDefault = 64;   // variables per footprint group (VMAX/2)
 
@@ -109,6 +109,8 @@ struct KClass {
     bool jit;
     uint64_t n_cons;
     std::vector<uint8_t> stream;  // per reference: 1 = changes most constraints (no run register)
+    std::vector<int32_t> alias;   // per reference: earlier reference with the same variable in every
+                                  // constraint of the class (one load, one accumulator), or -1
     // record compression: logical word w is stored at position wpos[w] of the compressed record,
     // or (wpos[w] < 0) is the same for every constraint of the class and is emitted as the
     // literal wconst[w] in the generated code (e.g. unit weights, +-1 coefficients, 1/||q||)

@@ -92,8 +92,8 @@ bool jit_cubin(const std::string& src, std::vector<char>& cubin, std::string& lo
         return false;
     }
     const char* opts[] = {"--gpu-architecture=sm_100a", "-lineinfo", "--std=c++17", "-default-device",
-                          "--ptxas-options=-v"};
-    int rc = n.compile(prog, 5, opts);
+                          "--ptxas-options=-v", "--diag-suppress=177"};   // 177: unused pt/pf of fused slots
+    int rc = n.compile(prog, 6, opts);
     size_t ls = 0;
     n.log_size(prog, &ls);
     log.assign(ls, '\0');

@@ -30,6 +30,11 @@ constexpr uint32_t kJitMaxClasses = 32;
 constexpr uint64_t kJitMinCons = 32;      // specialise only classes with enough constraints
 }  // namespace
 
+static bool stage_records_env() {
+    const char* e = getenv("FSMT_JIT_STAGE");
+    return e && e[0] == '1';
+}
+
 Plan make_plan(const Formula& f, const Built& b, bool enable_jit) {
     Plan p;
     if (const char* w = getenv("FSMT_JIT_WARPS")) p.jit_warps = std::max(1, std::min(8, atoi(w)));
@@ -280,6 +285,35 @@ Plan make_plan(const Formula& f, const Built& b, bool enable_jit) {
             p.kclasses[k].stream[r] = seen[k] && 2 * changes[k][r] > seen[k];
     }
 
+    // 5b. aliases: reference r reads the same variable as an earlier reference r' in every
+    //     constraint of the class (e.g. x_j in both separation atoms of a placement pair)
+    {
+        std::vector<std::vector<uint8_t>> same(p.n_jit_kclasses);
+        for (uint32_t k = 0; k < p.n_jit_kclasses; ++k)
+            same[k].assign((size_t)p.kclasses[k].n_refs * p.kclasses[k].n_refs, 1);
+        for (const TileDesc& T : p.tiles) {
+            const KClass& K = p.kclasses[T.kclass];
+            std::vector<uint8_t>& sm = same[T.kclass];
+            std::vector<uint32_t> l(K.n_refs);
+            for (uint32_t c = 0; c < T.n_cons; ++c) {
+                const uint32_t* rec = p.recs.data() + ((size_t)T.rec_off + (size_t)c * K.stride4) * 4;
+                for (uint32_t r = 0; r < K.n_refs; ++r) l[r] = (rec[1 + r / 2] >> (16 * (r % 2))) & 0xFFFFu;
+                for (uint32_t r = 1; r < K.n_refs; ++r)
+                    for (uint32_t q = 0; q < r; ++q) sm[(size_t)r * K.n_refs + q] &= (uint8_t)(l[r] == l[q]);
+            }
+        }
+        const char* ae = getenv("FSMT_JIT_ALIAS");
+        const bool on = !(ae && ae[0] == '0') && !stage_records_env();
+        for (uint32_t k = 0; k < p.n_jit_kclasses; ++k) {
+            KClass& K = p.kclasses[k];
+            K.alias.assign(K.n_refs, -1);
+            if (!on || K.n_cons == 0) continue;
+            for (uint32_t r = 1; r < K.n_refs; ++r)
+                for (uint32_t q = 0; q < r; ++q)
+                    if (same[k][(size_t)r * K.n_refs + q] && K.alias[q] < 0) { K.alias[r] = (int32_t)q; break; }
+        }
+    }
+
     // 6. record compression: words equal across a whole class become literals in the code
     // opt-in (FSMT_JIT_FOLD=1): fewer registers/loads, but measured slower on cfg4 (26.6 vs 22.1 ms)
     const char* cz = getenv("FSMT_JIT_FOLD");
@@ -359,6 +393,13 @@ bool fast_erfc() {
 // FSMT_JIT_STAGE=1: a tile's records are staged into shared memory at tile start and the
 // stream references' values are software-pipelined one constraint ahead.  Measured slower on
 // cfg4 (28.6 vs 22.6 ms: the extra shared memory costs occupancy), so off by default.
+// FSMT_JIT_ERFC_VOTE=1: warp-vote per atom, one erfc branch when the warp agrees.  Measured
+// slower on cfg4 at kappa = 1 (19.6 vs 19.1 ms: the lanes straddle |u| = 0.75), so off by default.
+bool erfc_vote() {
+    const char* e = getenv("FSMT_JIT_ERFC_VOTE");
+    return e && e[0] == '1';
+}
+
 bool stage_records() {
     const char* e = getenv("FSMT_JIT_STAGE");
     return e && e[0] == '1';
@@ -377,21 +418,27 @@ const char* kErfcPrelude =
     "// 0.5*erfc(z) for z >= 0 and ez = exp(-z^2) (dd/db factor, P:1326-1327).\n"
     "// z < 0.75: 1 - erf(z) from the Maclaurin series of erf (10 terms); z >= 0.75: Numerical Recipes\n"
     "// erfcc, t exp(-z^2 + P(t)), t = 1/(1 + z/2), fractional error < 1.2e-7.\n"
-    "__device__ __forceinline__ float fsmt_half_erfc(float z, float& ez) {\n"
-    "  const float z2 = z * z;\n"
-    "  ez = fsmt_ex2(-1.44269504088896341f * z2);\n"
+    "__device__ __forceinline__ float fsmt_erfc_small(float z, float z2) {\n"
     "  float q = -1.4503291e-7f;\n"
     "  q = fmaf(q, z2, 1.4589169e-6f); q = fmaf(q, z2, -1.3227513e-5f); q = fmaf(q, z2, 1.0683761e-4f);\n"
     "  q = fmaf(q, z2, -7.5757576e-4f); q = fmaf(q, z2, 4.6296296e-3f); q = fmaf(q, z2, -2.3809524e-2f);\n"
     "  q = fmaf(q, z2, 0.1f); q = fmaf(q, z2, -0.33333333f); q = fmaf(q, z2, 1.f);\n"
-    "  const float small = fmaf(-1.12837916709551257f * z, q, 1.f);\n"
-    "  const float t = __fdividef(1.f, fmaf(0.5f, z, 1.f));\n"
+    "  return 0.5f * fmaf(-1.12837916709551257f * z, q, 1.f);\n"
+    "}\n"
+    "__device__ __forceinline__ float fsmt_erfc_tail(float z, float z2) {\n"
+    "  float t;   // 1/(1 + z/2) with 1 + z/2 >= 1: rcp.approx needs no denormal range fix-up\n"
+    "  asm(\"rcp.approx.ftz.f32 %0, %1;\" : \"=f\"(t) : \"f\"(fmaf(0.5f, z, 1.f)));\n"
     "  float p = 0.17087277f;\n"
     "  p = fmaf(p, t, -0.82215223f); p = fmaf(p, t, 1.48851587f); p = fmaf(p, t, -1.13520398f);\n"
     "  p = fmaf(p, t, 0.27886807f); p = fmaf(p, t, -0.18628806f); p = fmaf(p, t, 0.09678418f);\n"
     "  p = fmaf(p, t, 0.37409196f); p = fmaf(p, t, 1.00002368f); p = fmaf(p, t, -1.26551223f);\n"
-    "  const float tail = t * fsmt_ex2((p - z2) * 1.44269504088896341f);\n"
-    "  return 0.5f * (z < 0.75f ? small : tail);\n"
+    "  return 0.5f * t * fsmt_ex2((p - z2) * 1.44269504088896341f);\n"
+    "}\n"
+    "__device__ __forceinline__ float fsmt_half_erfc(float z, float& ez) {\n"
+    "  const float z2 = z * z;\n"
+    "  ez = fsmt_ex2(-1.44269504088896341f * z2);\n"
+    "  const float small = fsmt_erfc_small(z, z2), tail = fsmt_erfc_tail(z, z2);\n"
+    "  return z < 0.75f ? small : tail;\n"
     "}\n\n";
 
 const char* comp(uint32_t w) {
@@ -435,8 +482,13 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
     const char* ms_env = getenv("FSMT_JIT_STREAM");   // "0": every reference in run mode (A/B)
     const bool use_stream = !(ms_env && ms_env[0] == '0');
     auto is_stream = [&](size_t i) { return use_stream && i < K.stream.size() && K.stream[i]; };
+    const bool staged_mode = stage_records();
+    auto alias_of = [&](size_t i) -> int {   // target reference of an alias, -1 if i is its own
+        return (!staged_mode && i < K.alias.size()) ? K.alias[i] : -1;
+    };
     for (size_t i = 0; i < nr; ++i)
-        if (!is_stream(i)) o << "  u32 cur" << i << " = 0xffffffffu; float val" << i << " = 0.f, acc" << i << " = 0.f;\n";
+        if (!is_stream(i) && alias_of(i) < 0)
+            o << "  u32 cur" << i << " = 0xffffffffu; float val" << i << " = 0.f, acc" << i << " = 0.f;\n";
     const char* pf_env = getenv("FSMT_JIT_PREFETCH");
     const bool prefetch = pf_env && pf_env[0] == '1';
     const bool staged = stage_records();
@@ -496,6 +548,10 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
         uint32_t wd = 1 + (uint32_t)i / 2;
         const std::string ext = "(" + word(wd) + " >> " + std::to_string(16 * (i % 2)) + ") & 0xffffu";
         const std::string ld = ld_of(i);
+        if (alias_of(i) >= 0) {
+            o << "    const float val" << i << " = val" << alias_of(i) << ";   // alias\n";
+            continue;
+        }
         if (is_stream(i)) {
             // stream reference: new variable (almost) every constraint; no run register
             if (!staged)
@@ -524,7 +580,17 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
             }
             aw += 2 + nnz;
             o << "    const float u" << s << " = kq * z" << s << " * inv" << s << ";\n";
-            if (fast_erfc())
+            if (fast_erfc() && erfc_vote()) {
+                // warp vote: both erfc branches only when the warp's lanes straddle |u| = 0.75
+                o << "    const float za" << s << " = fabsf(u" << s << "), zb" << s << " = za" << s << " * za" << s << ";\n"
+                  << "    const float ez" << s << " = fsmt_ex2(-1.44269504088896341f * zb" << s << ");\n"
+                  << "    float e" << s << ";\n"
+                  << "    { const unsigned bal = __ballot_sync(0xffffffffu, za" << s << " < 0.75f);\n"
+                  << "      if (bal == 0xffffffffu) e" << s << " = fsmt_erfc_small(za" << s << ", zb" << s << ");\n"
+                  << "      else if (bal == 0u) e" << s << " = fsmt_erfc_tail(za" << s << ", zb" << s << ");\n"
+                  << "      else e" << s << " = za" << s << " < 0.75f ? fsmt_erfc_small(za" << s << ", zb" << s
+                  << ") : fsmt_erfc_tail(za" << s << ", zb" << s << "); }\n";
+            } else if (fast_erfc())
                 o << "    float ez" << s << ";\n    const float e" << s << " = fsmt_half_erfc(fabsf(u" << s << "), ez" << s << ");\n";
             else
                 o << "    const float e" << s << " = 0.5f * erfcf(fabsf(u" << s << "));\n"
@@ -534,18 +600,67 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
               << "    const float dd" << s << " = dcoef * inv" << s << " * ez" << s << ";\n";
         }
     }
-    // forward pass (Alg.F): m_td in registers
+    // XOR diamonds (peephole, FSMT_JIT_DIAMOND=0 disables): node n at slot s whose children h, l
+    // sit at one slot s', have n as their only parent, and cross (hi(h) = lo(l) = X, lo(h) =
+    // hi(l) = Y).  Then n reaches X with P_X = pt_s pt_s' + pf_s pf_s' (s, s' equal) and Y with
+    // 1 - P_X, so h and l need no messages of their own:
+    //   forward  m[X] += P_X m[n], m[Y] += (1 - P_X) m[n]
+    //   backward d = m_bu[X] - m_bu[Y], m_bu[n] = m_bu[Y] + P_X d,
+    //            dCOP/dpt_s += m[n] d (pt_s' - pf_s'), dCOP/dpt_s' += m[n] d (pt_s - pf_s)
+    // which is Alg.F/Alg.B over n, h, l regrouped (P_X + P_Y = 1).  For two Boolean slots
+    // P_X = (1 + v_s v_s')/2 and pt - pf = -v.
     const size_t nn = t.nodes.size();
-    for (size_t v = 0; v < nn; ++v) o << "    float m" << v << " = " << ((int)v == t.root ? "1.f" : "0.f") << ";\n";
+    std::vector<int> indeg(nn, 0);
+    for (size_t v = 0; v < nn; ++v) {
+        if (t.nodes[v].hi >= 0) ++indeg[t.nodes[v].hi];
+        if (t.nodes[v].lo >= 0) ++indeg[t.nodes[v].lo];
+    }
+    if (t.root >= 0) ++indeg[t.root];
+    std::vector<char> dhead(nn, 0), dskip(nn, 0);
+    const char* dm_env = getenv("FSMT_JIT_DIAMOND");
+    if (!(dm_env && dm_env[0] == '0')) {
+        for (size_t v = 0; v < nn; ++v) {
+            const TNode& nd = t.nodes[v];
+            if (dskip[v] || nd.hi < 0 || nd.lo < 0 || nd.hi == nd.lo) continue;
+            const TNode& h = t.nodes[nd.hi];
+            const TNode& l = t.nodes[nd.lo];
+            if (h.level != l.level || indeg[nd.hi] != 1 || indeg[nd.lo] != 1) continue;
+            if (h.hi != l.lo || h.lo != l.hi || h.hi == h.lo) continue;
+            dhead[v] = 1;
+            dskip[nd.hi] = dskip[nd.lo] = 1;
+        }
+    }
+    auto is_bool = [&](uint32_t lv) { return t.kinds[lv] == 0; };
+    auto vref = [&](uint32_t lv) { return "val" + std::to_string(slot_ref0[lv]); };
+    // forward pass (Alg.F): m_td in registers
+    for (size_t v = 0; v < nn; ++v)
+        if (!dskip[v]) o << "    float m" << v << " = " << ((int)v == t.root ? "1.f" : "0.f") << ";\n";
     o << "    float pT = 0.f;\n";
     for (size_t v = 0; v < nn; ++v) {
+        if (dskip[v]) continue;
         const TNode& nd = t.nodes[v];
-        auto push = [&](int child, const char* pn) {
-            if (child >= 0) o << "    m" << child << " = fmaf(" << pn << nd.level << ", m" << v << ", m" << child << ");\n";
-            else if (child == kTrue) o << "    pT = fmaf(" << pn << nd.level << ", m" << v << ", pT);\n";
+        auto push = [&](int child, const std::string& pn) {
+            if (child >= 0) o << "    m" << child << " = fmaf(" << pn << ", m" << v << ", m" << child << ");\n";
+            else if (child == kTrue) o << "    pT = fmaf(" << pn << ", m" << v << ", pT);\n";
         };
-        push(nd.hi, "pt");
-        push(nd.lo, "pf");
+        if (dhead[v]) {
+            const TNode& h = t.nodes[nd.hi];
+            const uint32_t s1 = nd.level, s2 = h.level;
+            const std::string P = "PX" + std::to_string(v), Q = "PY" + std::to_string(v);
+            if (is_bool(s1) && is_bool(s2)) {
+                o << "    const float vv" << v << " = " << vref(s1) << " * " << vref(s2) << ";\n"
+                  << "    const float " << P << " = fmaf(0.5f, vv" << v << ", 0.5f), " << Q << " = fmaf(-0.5f, vv" << v
+                  << ", 0.5f);\n";
+            } else {
+                o << "    const float " << P << " = fmaf(pt" << s1 << ", pt" << s2 << ", pf" << s1 << " * pf" << s2 << "), " << Q
+                  << " = fmaf(pt" << s1 << ", pf" << s2 << ", pf" << s1 << " * pt" << s2 << ");\n";
+            }
+            push(h.hi, P);   // X: s, s' equal
+            push(h.lo, Q);   // Y
+            continue;
+        }
+        push(nd.hi, "pt" + std::to_string(nd.level));
+        push(nd.lo, "pf" + std::to_string(nd.level));
     }
     // backward pass (Alg.B, sign R1): m_bu in registers, dE/dv per slot
     for (size_t s = 0; s < ns; ++s) o << "    float G" << s << " = 0.f;\n";
@@ -554,7 +669,24 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
         return child == kTrue ? "1.f" : "0.f";
     };
     for (size_t vv = nn; vv-- > 0;) {
+        if (dskip[vv]) continue;
         const TNode& nd = t.nodes[vv];
+        if (dhead[vv]) {
+            const TNode& h = t.nodes[nd.hi];
+            const uint32_t s1 = nd.level, s2 = h.level;
+            const std::string X = bu(h.hi), Y = bu(h.lo), sv = std::to_string(vv);
+            o << "    const float d" << sv << " = " << X << " - " << Y << ";\n"
+              << "    const float bu" << sv << " = fmaf(PX" << sv << ", d" << sv << ", " << Y << ");\n"
+              << "    const float md" << sv << " = m" << sv << " * d" << sv << ";\n";
+            if (is_bool(s1) && is_bool(s2)) {
+                o << "    G" << s1 << " = fmaf(-md" << sv << ", " << vref(s2) << ", G" << s1 << ");\n"
+                  << "    G" << s2 << " = fmaf(-md" << sv << ", " << vref(s1) << ", G" << s2 << ");\n";
+            } else {
+                o << "    G" << s1 << " = fmaf(md" << sv << ", pt" << s2 << " - pf" << s2 << ", G" << s1 << ");\n"
+                  << "    G" << s2 << " = fmaf(md" << sv << ", pt" << s1 << " - pf" << s1 << ", G" << s2 << ");\n";
+            }
+            continue;
+        }
         std::string bh = bu(nd.hi), bl = bu(nd.lo);
         std::string lv = std::to_string(nd.level);
         // m_bu[v] = p m_bu[hi] + (1-p) m_bu[lo]
@@ -585,29 +717,36 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
     o << "    const float E = 1.f - 2.f * pT;\n"
          "    objacc += (double)w * (double)E;\n"
          "    if (terms != nullptr && live && r == terms_r) terms[orig[T.cons_begin + c]] = (double)E;\n";
+    // gradient terms per target reference (aliases fold into their target: one read-modify-write)
+    std::vector<std::vector<std::pair<std::string, std::string>>> terms_of(nr);
     auto accum = [&](int ri, const std::string& a, const std::string& b) {
-        if (is_stream((size_t)ri))
-            o << "      accs[sl" << ri << " * 32] = fmaf(" << a << ", " << b << ", accs[sl" << ri << " * 32]);\n";
-        else
-            o << "      acc" << ri << " = fmaf(" << a << ", " << b << ", acc" << ri << ");\n";
+        const int tgt = alias_of((size_t)ri) >= 0 ? alias_of((size_t)ri) : ri;
+        terms_of[(size_t)tgt].emplace_back(a, b);
     };
     for (size_t s = 0; s < ns; ++s) {
         if (t.kinds[s] == 0) {
             accum(slot_ref0[s], "w", "G" + std::to_string(s));
         } else {
-            o << "    { const float gd = w * G" << s << " * dd" << s << ";\n";
+            o << "    const float gd" << s << " = w * G" << s << " * dd" << s << ";\n";
             size_t ai = 0;
             for (size_t s2 = 0; s2 < s; ++s2) ai += t.kinds[s2] == 1;
             for (uint32_t k = 0; k < K.nnz[ai]; ++k) {
                 int ri = slot_ref0[s] + (int)k;
-                accum(ri, "gd", "__uint_as_float(" + word(coef_word[ri]) + ")");
+                accum(ri, "gd" + std::to_string(s), "__uint_as_float(" + word(coef_word[ri]) + ")");
             }
-            o << "    }\n";
         }
+    }
+    for (size_t ri = 0; ri < nr; ++ri) {
+        if (terms_of[ri].empty()) continue;
+        const std::string dst = is_stream(ri) ? "accs[sl" + std::to_string(ri) + " * 32]" : "acc" + std::to_string(ri);
+        std::string e = dst;
+        for (const auto& ab : terms_of[ri]) e = "fmaf(" + ab.first + ", " + ab.second + ", " + e + ")";
+        o << "    " << dst << " = " << e << ";\n";
     }
     o << "  }\n";
     for (size_t i = 0; i < nr; ++i)
-        if (!is_stream(i)) o << "  if (cur" << i << " != 0xffffffffu) accs[cur" << i << " * 32] += acc" << i << ";\n";
+        if (!is_stream(i) && alias_of(i) < 0)
+            o << "  if (cur" << i << " != 0xffffffffu) accs[cur" << i << " * 32] += acc" << i << ";\n";
     o << "}\n\n";
 }
 

@@ -109,3 +109,27 @@ def test_dist_drivers_world1_reproduce_solve(mode):
     assert (out.best_unsat, out.winner_stage, out.winner_restart) == (
         res.stats["best_unsat"], res.stats["winner_stage"], res.stats["winner_restart"])
     assert np.array_equal(out.x, res.x) and np.array_equal(out.y, res.y)
+
+
+def test_cfg4_placement_time_to_sat():
+    """The 10k-variable / 705k-constraint placement instance is solved
+    with the DESIGN.md §9 schedule (geometric kappa to 300 then held, eta_mode 3, ERWA
+    reset-to-0), and the model satisfies every constraint under the oracle's exact semantics."""
+    from paper_2603_22877_b200 import native as N
+    inst = fsmt_gen.config("cfg4")
+    s = make(inst.text)
+    kappas = [300.0 ** (i / 19) for i in range(20)] + [300.0] * 60
+    s.set_params(kappas=kappas, eta=0.03, eta_mode=3, erwa_mode=1, time_limit_s=240)
+    res = s.solve(1024, 40, 0)
+    assert res.verdict == N.SAT, res.stats
+    assert s.verify(res.x, res.y) == 0                       # host exact check, all constraints
+    # independent check on a seeded sample of 20,000 constraints under the oracle's semantics
+    from tests.helpers import subformula
+    rng = np.random.default_rng(0)
+    sample = rng.choice(inst.n_cons, 20000, replace=False)
+    sub, kept = subformula(inst.text, extra_constraints=sample)
+    f = hsmt.parse(sub)
+    x = np.asarray(res.x)
+    y = np.asarray(res.y, dtype=np.float32)
+    bad = [kept[ci] for ci, c in enumerate(f.constraints) if not semantics.constraint_sat(f, c, x, y)]
+    assert len(kept) == 20000 and not bad, bad[:10]
