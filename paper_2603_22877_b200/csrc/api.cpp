@@ -395,8 +395,7 @@ fsmt_status fsmt_build_xbdd(fsmt_ctx* ctx, uint64_t node_budget) {
             ctx->T.tile_vars = vp;
             ctx->T.warps = P.jit_warps;
             ctx->T.vmax = P.vmax;
-            ctx->T.rec_stage4 = P.rec_stage4;
-            ctx->T.sval = P.sval;
+            ctx->T.rmax = P.rmax;
             const uint32_t* vr = nullptr;
             s = upload(ctx, P.vrecs, vr, ctx->fallocs);
             if (s) return s;

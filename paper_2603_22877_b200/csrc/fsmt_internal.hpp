@@ -95,7 +95,8 @@ struct Built {
 // Constraints are permuted into an internal order grouped into tiles: a tile is a run of
 // constraints of one kernel class (template + nnz of each atom slot) whose variables fit a
 // small local table, so the JIT-specialised sweep accumulates their gradients on chip.
-constexpr uint32_t kTileVmaxDefault = 64;    // local variables per tile (FSMT_TILE_VMAX; A/B in DESIGN.md §9)
+constexpr uint32_t kTileVmaxDefault = 64;    // stream variables (shared-memory rows) per tile (FSMT_TILE_VMAX)
+constexpr uint32_t kTileRmaxDefault = 128;   // run variables per tile (FSMT_TILE_RMAX)
 constexpr uint32_t kTileCmax = 64;        // constraints per tile
 constexpr uint32_t kGroupVarsDefault = 64;   // variables per footprint group (VMAX/2)
 
@@ -118,6 +119,8 @@ struct KClass {
     std::vector<uint32_t> wconst;
 };
 
+// n_vars = n_stream | n_run << 16; tile_vars[var_off ..) holds the stream variables then the run
+// variables; pad0 = record uint4s, pad1 = K5 record offset (uint4)
 struct TileDesc {                // mirrored in the JIT source (32 bytes)
     uint32_t kclass, cons_begin, n_cons, var_off, n_vars, rec_off, pad0, pad1;
 };
@@ -134,10 +137,10 @@ struct Plan {
     uint32_t jit_cons_end = 0;        // internal [0, jit_cons_end) are JIT constraints
     uint32_t n_jit_kclasses = 0;
     uint32_t jit_warps = 1;           // warps per CTA of the JIT sweep (A/B: profiles/README.md)
-    uint32_t vmax = kTileVmaxDefault; // local variables per tile (on-chip accumulator rows)
-    uint32_t rec_stage4 = 0;          // per-warp shared-memory record stage, uint4 (0: not staged)
+    uint32_t vmax = kTileVmaxDefault; // stream variables per tile = shared-memory accumulator rows
+    uint32_t rmax = kTileRmaxDefault; // run variables per tile (register accumulators, flushed to HBM)
+    uint32_t group = kTileVmaxDefault;  // footprint group size in variables (FSMT_TILE_GROUP)
     uint32_t cmax = kTileCmax;        // constraints per tile (FSMT_TILE_CMAX)
-    uint32_t sval = 0;                // 1: tile variable values staged in shared memory (FSMT_JIT_SVAL)
 };
 
 Plan make_plan(const Formula& f, const Built& b, bool enable_jit);

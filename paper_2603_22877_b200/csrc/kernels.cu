@@ -343,10 +343,10 @@ void launch_sweep_jit(cudaKernel_t k, const DevFormula& F, const DevState& S, co
                       float wscale, double* terms, uint32_t terms_r, cudaStream_t st) {
     if (T.n_tiles == 0 || S.R == 0) return;
     const int kJitWarps = (int)(T.warps ? T.warps : 1);
-    const int kVmax = (int)(T.vmax ? T.vmax : 128);                   // Plan::vmax
+    const int kVmax = (int)T.vmax, kVtot = (int)(T.vmax + T.rmax);    // Plan::vmax, Plan::rmax
     const uint64_t nw = (uint64_t)T.n_tiles * ((S.R + 31) / 32);
     const unsigned blocks = (unsigned)((nw + kJitWarps - 1) / kJitWarps);
-    const size_t smem = (size_t)kJitWarps * (kVmax * 32 * 4 * (T.sval ? 2 : 1) + kVmax * 4 + (size_t)T.rec_stage4 * 16);
+    const size_t smem = (size_t)kJitWarps * ((size_t)kVmax * 32 * 4 + (size_t)kVtot * 4);
     if (smem > 48 * 1024) cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     uint32_t n_tiles = T.n_tiles, R = S.R, n_bool = F.n_bool;
     const uint8_t* U = S.U;
@@ -360,10 +360,10 @@ void launch_verify_jit(cudaKernel_t k, const DevFormula& F, const DevState& S, c
                        const float* y, uint8_t* U_update, uint8_t* per_con, cudaStream_t st) {
     if (T.n_tiles == 0 || S.R == 0) return;
     const int warps = (int)(T.warps ? T.warps : 1);
-    const int vmax = (int)(T.vmax ? T.vmax : 128);
+    const int vtot = (int)(T.vmax + T.rmax);
     const uint64_t nw = (uint64_t)T.n_tiles * ((S.R + 31) / 32);
     const unsigned blocks = (unsigned)((nw + warps - 1) / warps);
-    const size_t smem = (size_t)warps * vmax * 4;
+    const size_t smem = (size_t)warps * vtot * 4;
     uint32_t n_tiles = T.n_tiles, R = S.R, n_bool = F.n_bool;
     uint32_t* unsat = S.unsat;
     void* args[] = {(void*)&T.tiles, &n_tiles, (void*)&T.recs, (void*)&T.vrecs, (void*)&T.tile_vars, (void*)&x,

@@ -73,10 +73,9 @@ struct DevTiles {
     const void* recs;            // uint4 records
     const uint32_t* tile_vars;
     uint32_t warps;              // warps per CTA (Plan::jit_warps)
-    uint32_t vmax;               // local variables per tile (Plan::vmax)
-    uint32_t rec_stage4;         // per-warp record stage in uint4 (Plan::rec_stage4)
+    uint32_t vmax;               // stream variables (shared-memory accumulator rows) per tile (Plan::vmax)
+    uint32_t rmax;               // run variables per tile (Plan::rmax)
     const void* vrecs;           // K5 records (atom ids), tile.pad1 = offset in uint4
-    uint32_t sval;               // 1: tile variable values staged in shared memory (Plan::sval)
 };
 // K5 (JIT-specialised, tiles): exact check over the tiles of T (+ ERWA counters / per_con).
 void launch_verify_jit(cudaKernel_t k, const DevFormula& F, const DevState& S, const DevTiles& T, const int8_t* x,

@@ -3,10 +3,11 @@
 // Plan: every constraint gets a kernel class (template + nnz of each atom slot).  Variables
 // are grouped by first appearance (a constraint's newly seen variables form one batch; a
 // batch never straddles a group), each constraint is keyed by (kernel class, footprint
-// groups) and the stable sort of these keys is the internal constraint order.  Runs of one
-// key become tiles of <= kTileCmax constraints over <= kTileVmax local variables, so the
-// sweep accumulates a tile's gradient contributions on chip and flushes each local
-// variable once per tile.
+// groups) and the stable sort of these keys is the internal constraint order.  Each
+// reference position of a class is "stream" (its variable changes from one constraint to
+// the next most of the time) or "run".  Runs of one key become tiles of <= cmax constraints
+// with <= vmax stream variables (one shared-memory accumulator row each, flushed once per
+// tile) and <= rmax run variables (register accumulators, flushed once per run).
 //
 // JIT: for each hot kernel class the forward pass (Alg.F) and backward pass
 // (Alg.B, sign R1) are emitted as straight-line code over the class's
@@ -30,17 +31,14 @@ constexpr uint32_t kJitMaxClasses = 32;
 constexpr uint64_t kJitMinCons = 32;      // specialise only classes with enough constraints
 }  // namespace
 
-static bool stage_records_env() {
-    const char* e = getenv("FSMT_JIT_STAGE");
-    return e && e[0] == '1';
-}
-
 Plan make_plan(const Formula& f, const Built& b, bool enable_jit) {
     Plan p;
     if (const char* w = getenv("FSMT_JIT_WARPS")) p.jit_warps = std::max(1, std::min(8, atoi(w)));
     if (const char* v = getenv("FSMT_TILE_VMAX")) p.vmax = (uint32_t)std::max(16, std::min(256, atoi(v)));
     if (const char* v = getenv("FSMT_TILE_CMAX")) p.cmax = (uint32_t)std::max(1, std::min(1024, atoi(v)));
-    if (const char* v = getenv("FSMT_JIT_SVAL")) p.sval = v[0] == '1' ? 1u : 0u;
+    if (const char* v = getenv("FSMT_TILE_RMAX")) p.rmax = (uint32_t)std::max(16, std::min(1024, atoi(v)));
+    p.group = p.vmax;
+    if (const char* v = getenv("FSMT_TILE_GROUP")) p.group = (uint32_t)std::max(8, std::min(1024, atoi(v)));
     const uint32_t C = (uint32_t)b.cons_tmpl.size();
     // 1. kernel classes
     std::map<std::vector<uint32_t>, uint32_t> kc_of;
@@ -141,7 +139,7 @@ Plan make_plan(const Formula& f, const Built& b, bool enable_jit) {
         for (uint32_t u : vars)
             if (group[u] == UINT32_MAX && std::find(batch.begin(), batch.end(), u) == batch.end()) batch.push_back(u);
         if (batch.empty()) continue;
-        if (cur_size > 0 && cur_size + batch.size() > p.vmax / 2) {
+        if (cur_size > 0 && cur_size + batch.size() > p.group) {
             ++cur_group;
             cur_size = 0;
         }
@@ -182,27 +180,88 @@ Plan make_plan(const Formula& f, const Built& b, bool enable_jit) {
         p.pos[p.order[i]] = i;
         p.cons_kclass[i] = kcl[p.order[i]];
     }
-    // 4. tiles + records over the JIT prefix
+    // 4. per JIT class and reference position (SURVEY §8(a) a4 accumulation):
+    //    "stream" if the variable changes from one constraint to the next of the class in the
+    //    internal order most of the time (accumulated straight into a shared-memory row),
+    //    "run" otherwise (register accumulator, flushed with one fp64 atomic per run);
+    //    aliases: reference r reads the same variable as an earlier reference in every
+    //    constraint of the class (e.g. x_j in both separation atoms of a placement pair)
+    std::vector<uint32_t> rv, pv;
+    {
+        std::vector<std::vector<uint64_t>> changes(p.n_jit_kclasses);
+        std::vector<std::vector<uint8_t>> same(p.n_jit_kclasses);
+        std::vector<uint64_t> seen(p.n_jit_kclasses, 0);
+        for (uint32_t k = 0; k < p.n_jit_kclasses; ++k) {
+            changes[k].assign(p.kclasses[k].n_refs, 0);
+            same[k].assign((size_t)p.kclasses[k].n_refs * p.kclasses[k].n_refs, 1);
+        }
+        for (uint32_t i = 0; i < C && p.kclasses[p.cons_kclass[i]].jit; ++i) {
+            const uint32_t k = p.cons_kclass[i];
+            const uint32_t nr = p.kclasses[k].n_refs;
+            cons_vars(p.order[i], rv);
+            const bool has_prev = i > 0 && p.cons_kclass[i - 1] == k;
+            if (has_prev) cons_vars(p.order[i - 1], pv);
+            for (uint32_t r = 0; r < nr; ++r) changes[k][r] += !has_prev || rv[r] != pv[r];
+            ++seen[k];
+            std::vector<uint8_t>& sm = same[k];
+            for (uint32_t r = 1; r < nr; ++r)
+                for (uint32_t q = 0; q < r; ++q) sm[(size_t)r * nr + q] &= (uint8_t)(rv[r] == rv[q]);
+        }
+        const char* ms_env = getenv("FSMT_JIT_STREAM");   // "0": every reference in run mode (A/B)
+        const bool use_stream = !(ms_env && ms_env[0] == '0');
+        const char* ae = getenv("FSMT_JIT_ALIAS");
+        const bool use_alias = !(ae && ae[0] == '0');
+        for (uint32_t k = 0; k < p.n_jit_kclasses; ++k) {
+            KClass& K = p.kclasses[k];
+            K.stream.assign(K.n_refs, 0);
+            K.alias.assign(K.n_refs, -1);
+            for (uint32_t r = 0; r < K.n_refs; ++r) K.stream[r] = use_stream && seen[k] && 2 * changes[k][r] > seen[k];
+            if (!use_alias || !seen[k]) continue;
+            for (uint32_t r = 1; r < K.n_refs; ++r)
+                for (uint32_t q = 0; q < r; ++q)
+                    if (same[k][(size_t)r * K.n_refs + q] && K.alias[q] < 0) {
+                        K.alias[r] = (int32_t)q;
+                        K.stream[r] = K.stream[q];
+                        break;
+                    }
+        }
+    }
+
+    // 5. tiles + records over the JIT prefix: a tile is a run of one sort key with <= cmax
+    //    constraints, <= vmax stream variables (shared-memory rows) and <= rmax run variables;
+    //    a reference's record field is its variable's index among the tile's stream or run
+    //    variables
     uint32_t i = 0;
-    std::vector<uint32_t> local;
+    std::vector<uint32_t> sloc, rloc, adds, addr;
+    auto index_of = [](const std::vector<uint32_t>& v, uint32_t u) {
+        return (uint32_t)(std::find(v.begin(), v.end(), u) - v.begin());
+    };
     while (i < C && p.kclasses[p.cons_kclass[i]].jit) {
         const uint32_t kc = p.cons_kclass[i];
         const KClass& K = p.kclasses[kc];
         TileDesc T{kc, i, 0, (uint32_t)p.tile_vars.size(), 0, (uint32_t)(p.recs.size() / 4), 0,
                    (uint32_t)(p.vrecs.size() / 4)};
-        local.clear();
+        sloc.clear();
+        rloc.clear();
         const Key& k0 = keys[p.order[i]];
         while (i < C && p.cons_kclass[i] == kc && T.n_cons < p.cmax) {
             const Key& ki = keys[p.order[i]];
             if (T.n_cons > 0 && (memcmp(ki.g, k0.g, sizeof(k0.g)) != 0)) break;
             cons_vars(p.order[i], vars);
-            size_t add = 0;
-            for (uint32_t u : vars)
-                if (std::find(local.begin(), local.end(), u) == local.end()) ++add;
-            if (T.n_cons > 0 && local.size() + add > p.vmax) break;
-            if (local.size() + add > p.vmax) break;   // a single constraint over > VMAX vars: generic path
-            for (uint32_t u : vars)
-                if (std::find(local.begin(), local.end(), u) == local.end()) local.push_back(u);
+            adds.clear();
+            addr.clear();
+            for (uint32_t r = 0; r < K.n_refs; ++r) {
+                if (K.alias[r] >= 0) continue;
+                const uint32_t u = vars[r];
+                if (K.stream[r]) {
+                    if (index_of(sloc, u) == sloc.size() && index_of(adds, u) == adds.size()) adds.push_back(u);
+                } else if (index_of(rloc, u) == rloc.size() && index_of(addr, u) == addr.size()) {
+                    addr.push_back(u);
+                }
+            }
+            if (sloc.size() + adds.size() > p.vmax || rloc.size() + addr.size() > p.rmax) break;
+            sloc.insert(sloc.end(), adds.begin(), adds.end());
+            rloc.insert(rloc.end(), addr.begin(), addr.end());
             // record
             const uint32_t c = p.order[i];
             const Template& t = b.tmpls[K.tmpl];
@@ -212,7 +271,8 @@ Plan make_plan(const Formula& f, const Built& b, bool enable_jit) {
             memcpy(&rec[0], &w, 4);
             uint32_t ref = 0;
             auto put_ref = [&](uint32_t u) {
-                uint32_t l = (uint32_t)(std::find(local.begin(), local.end(), u) - local.begin());
+                const uint32_t tr = K.alias[ref] >= 0 ? (uint32_t)K.alias[ref] : ref;
+                const uint32_t l = K.stream[tr] ? index_of(sloc, u) : index_of(rloc, u);
                 rec[1 + ref / 2] |= (l & 0xFFFFu) << (16 * (ref % 2));
                 ++ref;
             };
@@ -245,74 +305,15 @@ Plan make_plan(const Formula& f, const Built& b, bool enable_jit) {
             ++T.n_cons;
             ++i;
         }
-        if (T.n_cons == 0) break;   // cannot tile (too many variables): rest is generic
-        T.n_vars = (uint32_t)local.size();
-        T.pad0 = T.n_cons * K.stride4;           // record uint4s (shared-memory stage size)
-        p.tile_vars.insert(p.tile_vars.end(), local.begin(), local.end());
+        if (T.n_cons == 0) break;   // a single constraint over too many variables: rest is generic
+        T.n_vars = (uint32_t)sloc.size() | ((uint32_t)rloc.size() << 16);
+        T.pad0 = T.n_cons * K.stride4;
+        p.tile_vars.insert(p.tile_vars.end(), sloc.begin(), sloc.end());
+        p.tile_vars.insert(p.tile_vars.end(), rloc.begin(), rloc.end());
         p.tiles.push_back(T);
     }
     p.jit_cons_end = i;
     // any JIT-class constraints after the cut run through the generic kernel
-    {
-        const char* e = getenv("FSMT_JIT_STAGE");
-        uint32_t ms = 0;
-        for (uint32_t k = 0; k < p.n_jit_kclasses; ++k) ms = std::max(ms, p.kclasses[k].stride4);
-        p.rec_stage4 = (e && e[0] == '1') ? p.cmax * ms : 0;
-    }
-
-    // 5. per kernel class and reference position: does the local variable change from one
-    //    constraint to the next within a tile most of the time ("stream": accumulate straight
-    //    into the tile accumulator) or rarely ("run": register accumulation over the run)?
-    std::vector<std::vector<uint64_t>> changes(p.n_jit_kclasses);
-    std::vector<uint64_t> seen(p.n_jit_kclasses, 0);
-    for (uint32_t k = 0; k < p.n_jit_kclasses; ++k) changes[k].assign(p.kclasses[k].n_refs, 0);
-    for (const TileDesc& T : p.tiles) {
-        const KClass& K = p.kclasses[T.kclass];
-        for (uint32_t c = 0; c < T.n_cons; ++c) {
-            const uint32_t* rec = p.recs.data() + ((size_t)T.rec_off + (size_t)c * K.stride4) * 4;
-            const uint32_t* prev = rec - K.stride4 * 4;
-            for (uint32_t r = 0; r < K.n_refs; ++r) {
-                const uint32_t l = (rec[1 + r / 2] >> (16 * (r % 2))) & 0xFFFFu;
-                const uint32_t lp = c ? (prev[1 + r / 2] >> (16 * (r % 2))) & 0xFFFFu : 0xFFFFFFFFu;
-                changes[T.kclass][r] += (l != lp);
-            }
-            seen[T.kclass] += 1;
-        }
-    }
-    for (uint32_t k = 0; k < p.n_jit_kclasses; ++k) {
-        p.kclasses[k].stream.assign(p.kclasses[k].n_refs, 0);
-        for (uint32_t r = 0; r < p.kclasses[k].n_refs; ++r)
-            p.kclasses[k].stream[r] = seen[k] && 2 * changes[k][r] > seen[k];
-    }
-
-    // 5b. aliases: reference r reads the same variable as an earlier reference r' in every
-    //     constraint of the class (e.g. x_j in both separation atoms of a placement pair)
-    {
-        std::vector<std::vector<uint8_t>> same(p.n_jit_kclasses);
-        for (uint32_t k = 0; k < p.n_jit_kclasses; ++k)
-            same[k].assign((size_t)p.kclasses[k].n_refs * p.kclasses[k].n_refs, 1);
-        for (const TileDesc& T : p.tiles) {
-            const KClass& K = p.kclasses[T.kclass];
-            std::vector<uint8_t>& sm = same[T.kclass];
-            std::vector<uint32_t> l(K.n_refs);
-            for (uint32_t c = 0; c < T.n_cons; ++c) {
-                const uint32_t* rec = p.recs.data() + ((size_t)T.rec_off + (size_t)c * K.stride4) * 4;
-                for (uint32_t r = 0; r < K.n_refs; ++r) l[r] = (rec[1 + r / 2] >> (16 * (r % 2))) & 0xFFFFu;
-                for (uint32_t r = 1; r < K.n_refs; ++r)
-                    for (uint32_t q = 0; q < r; ++q) sm[(size_t)r * K.n_refs + q] &= (uint8_t)(l[r] == l[q]);
-            }
-        }
-        const char* ae = getenv("FSMT_JIT_ALIAS");
-        const bool on = !(ae && ae[0] == '0') && !stage_records_env();
-        for (uint32_t k = 0; k < p.n_jit_kclasses; ++k) {
-            KClass& K = p.kclasses[k];
-            K.alias.assign(K.n_refs, -1);
-            if (!on || K.n_cons == 0) continue;
-            for (uint32_t r = 1; r < K.n_refs; ++r)
-                for (uint32_t q = 0; q < r; ++q)
-                    if (same[k][(size_t)r * K.n_refs + q] && K.alias[q] < 0) { K.alias[r] = (int32_t)q; break; }
-        }
-    }
 
     // 6. record compression: words equal across a whole class become literals in the code
     // opt-in (FSMT_JIT_FOLD=1): fewer registers/loads, but measured slower on cfg4 (26.6 vs 22.1 ms)
@@ -364,12 +365,6 @@ Plan make_plan(const Formula& f, const Built& b, bool enable_jit) {
         T.pad0 = T.n_cons * K.stride4;
     }
     p.recs.swap(packed);
-    {
-        const char* e = getenv("FSMT_JIT_STAGE");
-        uint32_t ms = 0;
-        for (uint32_t k = 0; k < p.n_jit_kclasses; ++k) ms = std::max(ms, p.kclasses[k].stride4);
-        p.rec_stage4 = (e && e[0] == '1') ? p.cmax * ms : 0;
-    }
     return p;
 }
 
@@ -390,18 +385,10 @@ bool fast_erfc() {
     return !(e && std::string(e) == "cuda");
 }
 
-// FSMT_JIT_STAGE=1: a tile's records are staged into shared memory at tile start and the
-// stream references' values are software-pipelined one constraint ahead.  Measured slower on
-// cfg4 (28.6 vs 22.6 ms: the extra shared memory costs occupancy), so off by default.
-// FSMT_JIT_ERFC_VOTE=1: warp-vote per atom, one erfc branch when the warp agrees.  Measured
-// slower on cfg4 at kappa = 1 (19.6 vs 19.1 ms: the lanes straddle |u| = 0.75), so off by default.
+// FSMT_JIT_ERFC_VOTE=1: warp-vote per atom, one erfc branch when the warp agrees (A/B,
+// DESIGN.md §9).
 bool erfc_vote() {
     const char* e = getenv("FSMT_JIT_ERFC_VOTE");
-    return e && e[0] == '1';
-}
-
-bool stage_records() {
-    const char* e = getenv("FSMT_JIT_STAGE");
     return e && e[0] == '1';
 }
 
@@ -458,14 +445,15 @@ std::string word(uint32_t w) {
     return "q" + std::to_string(w / 4) + "." + comp(w);
 }
 
-void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Template& t, bool sval) {
+void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Template& t) {
     g_wk = &K;
     const size_t ns = t.kinds.size();
     o << "__device__ __forceinline__ void kc" << kid
-      << "(const TileDesc& T, const uint4* __restrict__ rp, const u32* __restrict__ vs, float* __restrict__ accs,\n"
-         "    const float* __restrict__ a, const float* __restrict__ b, const unsigned char* __restrict__ U,\n"
+      << "(const TileDesc& T, const uint4* __restrict__ rp, const u32* __restrict__ vs, const u32* __restrict__ vr,\n"
+         "    float* __restrict__ accs, const float* __restrict__ a, const float* __restrict__ b,\n"
+         "    double* __restrict__ ga, double* __restrict__ gb, const unsigned char* __restrict__ U,\n"
          "    u32 R, u64 rr, u32 r, bool live, u32 n_bool, float kq, float dcoef, float wscale, double& objacc,\n"
-         "    double* __restrict__ terms, u32 terms_r, const u32* __restrict__ orig, const float* __restrict__ vals) {\n";
+         "    double* __restrict__ terms, u32 terms_r, const u32* __restrict__ orig) {\n";
     // refs
     std::vector<int> ref_kind;      // 0 Boolean, 1 real
     std::vector<int> slot_ref0(ns);
@@ -479,69 +467,27 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
         }
     }
     const size_t nr = ref_kind.size();
-    const char* ms_env = getenv("FSMT_JIT_STREAM");   // "0": every reference in run mode (A/B)
-    const bool use_stream = !(ms_env && ms_env[0] == '0');
-    auto is_stream = [&](size_t i) { return use_stream && i < K.stream.size() && K.stream[i]; };
-    const bool staged_mode = stage_records();
+    auto is_stream = [&](size_t i) { return i < K.stream.size() && K.stream[i]; };
     auto alias_of = [&](size_t i) -> int {   // target reference of an alias, -1 if i is its own
-        return (!staged_mode && i < K.alias.size()) ? K.alias[i] : -1;
+        return i < K.alias.size() ? K.alias[i] : -1;
     };
     for (size_t i = 0; i < nr; ++i)
         if (!is_stream(i) && alias_of(i) < 0)
             o << "  u32 cur" << i << " = 0xffffffffu; float val" << i << " = 0.f, acc" << i << " = 0.f;\n";
-    const char* pf_env = getenv("FSMT_JIT_PREFETCH");
-    const bool prefetch = pf_env && pf_env[0] == '1';
-    const bool staged = stage_records();
+    // value of reference i's variable: stream variables are listed in vs, run variables in vr
     auto ld_of = [&](size_t i) {
-        if (sval) return std::string("vals[l * 32]");
-        return ref_kind[i] == 0 ? std::string("a[(u64)vs[l] * R + rr]") : std::string("b[(u64)(vs[l] - n_bool) * R + rr]");
+        const std::string v = is_stream(i) ? "vs" : "vr";
+        return ref_kind[i] == 0 ? "a[(u64)" + v + "[l] * R + rr]" : "b[(u64)(" + v + "[l] - n_bool) * R + rr]";
     };
-    auto ext_of = [&](size_t i, const std::string& w) {
-        return "(" + w + " >> " + std::to_string(16 * (i % 2)) + ") & 0xffffu";
+    // a run accumulator goes straight to the fp64 gradient (one atomic per run)
+    auto flush_run = [&](size_t i) {
+        const std::string g = ref_kind[i] == 0 ? "ga + (u64)vr[cur" + std::to_string(i) + "] * R + r"
+                                               : "gb + (u64)(vr[cur" + std::to_string(i) + "] - n_bool) * R + r";
+        return "if (live) atomicAdd(" + g + ", (double)acc" + std::to_string(i) + ");";
     };
-    auto rec_word = [&](uint32_t wd, uint32_t off4) {   // word wd of the record rp + off4 (shared memory)
-        const int32_t pw = K.wpos[wd];
-        if (pw < 0) return "(" + std::to_string(K.wconst[wd]) + "u)";
-        return "rp[" + std::to_string(off4 + (uint32_t)pw / 4) + "]." + comp((uint32_t)pw);
-    };
-    if (staged) {
-        // records are in shared memory; the values of the stream references of constraint c+1
-        // are requested while c is evaluated (software pipeline of depth 1)
-        for (size_t i = 0; i < nr; ++i)
-            if (is_stream(i)) o << "  u32 nsl" << i << " = 0u; float nval" << i << " = 0.f;\n";
-        o << "  if (T.n_cons) {\n";
-        for (size_t i = 0; i < nr; ++i)
-            if (is_stream(i))
-                o << "    { const u32 l = " << ext_of(i, rec_word(1 + (uint32_t)i / 2, 0)) << "; nsl" << i << " = l; nval" << i
-                  << " = " << ld_of(i) << "; }\n";
-        o << "  }\n";
-        o << "  for (u32 c = 0; c < T.n_cons; ++c, rp += " << K.stride4 << ") {\n";
-        for (uint32_t q = 0; q < K.stride4; ++q) o << "    const uint4 q" << q << " = rp[" << q << "];\n";
-        o << "    const u32 uc = U ? (u32)U[(u64)(T.cons_begin + c) * R + rr] : 0u;\n";
-        for (size_t i = 0; i < nr; ++i)
-            if (is_stream(i)) o << "    const u32 sl" << i << " = nsl" << i << "; const float val" << i << " = nval" << i << ";\n";
-        o << "    if (c + 1 < T.n_cons) {\n";
-        for (size_t i = 0; i < nr; ++i)
-            if (is_stream(i))
-                o << "      { const u32 l = " << ext_of(i, rec_word(1 + (uint32_t)i / 2, K.stride4)) << "; nsl" << i
-                  << " = l; nval" << i << " = " << ld_of(i) << "; }\n";
-        o << "    }\n";
-    } else if (prefetch) {
-        // software pipeline: the record and U counter of constraint c+1 are loaded while c is evaluated
-        for (uint32_t q = 0; q < K.stride4; ++q) o << "  uint4 nq" << q << " = make_uint4(0u, 0u, 0u, 0u);\n";
-        o << "  u32 nU = 0u;\n  if (T.n_cons) {\n";
-        for (uint32_t q = 0; q < K.stride4; ++q) o << "    nq" << q << " = __ldg(rp + " << q << ");\n";
-        o << "    if (U) nU = U[(u64)T.cons_begin * R + rr];\n  }\n";
-        o << "  for (u32 c = 0; c < T.n_cons; ++c, rp += " << K.stride4 << ") {\n";
-        for (uint32_t q = 0; q < K.stride4; ++q) o << "    const uint4 q" << q << " = nq" << q << ";\n";
-        o << "    const u32 uc = nU;\n    if (c + 1 < T.n_cons) {\n";
-        for (uint32_t q = 0; q < K.stride4; ++q) o << "      nq" << q << " = __ldg(rp + " << K.stride4 + q << ");\n";
-        o << "      if (U) nU = U[(u64)(T.cons_begin + c + 1) * R + rr];\n    }\n";
-    } else {
-        o << "  for (u32 c = 0; c < T.n_cons; ++c, rp += " << K.stride4 << ") {\n";
-        for (uint32_t q = 0; q < K.stride4; ++q) o << "    const uint4 q" << q << " = __ldg(rp + " << q << ");\n";
-        o << "    const u32 uc = U ? (u32)U[(u64)(T.cons_begin + c) * R + rr] : 0u;\n";
-    }
+    o << "  for (u32 c = 0; c < T.n_cons; ++c, rp += " << K.stride4 << ") {\n";
+    for (uint32_t q = 0; q < K.stride4; ++q) o << "    const uint4 q" << q << " = __ldg(rp + " << q << ");\n";
+    o << "    const u32 uc = U ? (u32)U[(u64)(T.cons_begin + c) * R + rr] : 0u;\n";
     o << "    float w = __uint_as_float(" << word(0) << ") * wscale;\n"
          "    if (U) w = fsmt_pow2_u8(w, uc);\n";
     for (size_t i = 0; i < nr; ++i) {
@@ -554,13 +500,11 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
         }
         if (is_stream(i)) {
             // stream reference: new variable (almost) every constraint; no run register
-            if (!staged)
-                o << "    const u32 sl" << i << " = " << ext << ";\n"
-                  << "    float val" << i << ";\n    { const u32 l = sl" << i << "; val" << i << " = " << ld << "; }\n";
+            o << "    const u32 sl" << i << " = " << ext << ";\n"
+              << "    float val" << i << ";\n    { const u32 l = sl" << i << "; val" << i << " = " << ld << "; }\n";
         } else {
-            o << "    { const u32 l = " << ext << "; if (l != cur" << i << ") { if (cur" << i
-              << " != 0xffffffffu) accs[cur" << i << " * 32] += acc" << i << "; cur" << i << " = l; acc" << i
-              << " = 0.f; val" << i << " = " << ld << "; } }\n";
+            o << "    { const u32 l = " << ext << "; if (l != cur" << i << ") { if (cur" << i << " != 0xffffffffu) { "
+              << flush_run(i) << " } cur" << i << " = l; acc" << i << " = 0.f; val" << i << " = " << ld << "; } }\n";
         }
     }
     // slot probabilities
@@ -745,8 +689,7 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
     }
     o << "  }\n";
     for (size_t i = 0; i < nr; ++i)
-        if (!is_stream(i) && alias_of(i) < 0)
-            o << "  if (cur" << i << " != 0xffffffffu) accs[cur" << i << " * 32] += acc" << i << ";\n";
+        if (!is_stream(i) && alias_of(i) < 0) o << "  if (cur" << i << " != 0xffffffffu) { " << flush_run(i) << " }\n";
     o << "}\n\n";
 }
 
@@ -759,7 +702,7 @@ void emit_verify_class(std::ostringstream& o, uint32_t kid, const KClass& K, con
     const size_t ns = t.kinds.size();
     o << "__device__ __forceinline__ u32 kv" << kid
       << "(const TileDesc& T, const uint4* __restrict__ rp, const uint4* __restrict__ vp, const u32* __restrict__ vs,\n"
-         "    const signed char* __restrict__ x, const float* __restrict__ y, unsigned char* __restrict__ U,\n"
+         "    const u32* __restrict__ vr, const signed char* __restrict__ x, const float* __restrict__ y, unsigned char* __restrict__ U,\n"
          "    unsigned char* __restrict__ per_con, const u32* __restrict__ orig, u32 R, u64 rr, u32 r, bool live,\n"
          "    u32 n_bool, const u32* __restrict__ arow, const double* __restrict__ aval,\n"
          "    const double* __restrict__ arhs, const unsigned char* __restrict__ astrict) {\n"
@@ -772,20 +715,22 @@ void emit_verify_class(std::ostringstream& o, uint32_t kid, const KClass& K, con
     for (uint32_t q = 0; q < q_needed; ++q) o << "    const uint4 q" << q << " = __ldg(rp + " << q << ");\n";
     for (uint32_t q = 0; q < K.vstride4; ++q) o << "    const uint4 v" << q << " = __ldg(vp + " << q << ");\n";
     uint32_t ref = 0, ai = 0;
-    auto ext = [&](uint32_t i) {
-        return "((" + word(1 + i / 2) + " >> " + std::to_string(16 * (i % 2)) + ") & 0xffffu)";
+    auto ext = [&](uint32_t i) {   // variable id of reference i (stream ids in vs, run ids in vr)
+        const int32_t tr = i < K.alias.size() && K.alias[i] >= 0 ? K.alias[i] : (int32_t)i;
+        const std::string v = (size_t)tr < K.stream.size() && K.stream[tr] ? "vs" : "vr";
+        return v + "[((" + word(1 + i / 2) + " >> " + std::to_string(16 * (i % 2)) + ") & 0xffffu)]";
     };
     for (size_t s = 0; s < ns; ++s) {
         if (t.kinds[s] == 0) {
-            o << "    const bool t" << s << " = x[(u64)vs[" << ext(ref) << "] * R + rr] == (signed char)-1;\n";
+            o << "    const bool t" << s << " = x[(u64)" << ext(ref) << " * R + rr] == (signed char)-1;\n";
             ++ref;
         } else {
             const uint32_t nnz = K.nnz[ai];
             const std::string aid = "v" + std::to_string(ai / 4) + "." + comp(ai);
             o << "    bool t" << s << ";\n    { const u32 aid = " << aid << "; const u32 k0 = arow[aid]; double sacc = 0.0;\n";
             for (uint32_t k = 0; k < nnz; ++k) {
-                o << "      sacc = __dadd_rn(sacc, __dmul_rn(aval[k0 + " << k << "], (double)y[(u64)(vs[" << ext(ref)
-                  << "] - n_bool) * R + rr]));\n";
+                o << "      sacc = __dadd_rn(sacc, __dmul_rn(aval[k0 + " << k << "], (double)y[(u64)(" << ext(ref)
+                  << " - n_bool) * R + rr]));\n";
                 ++ref;
             }
             o << "      const double rhs = arhs[aid];\n      t" << s << " = astrict[aid] ? (sacc < rhs) : (sacc <= rhs); }\n";
@@ -816,8 +761,9 @@ std::string jit_source(const Formula& f, const Built& b, const Plan& p) {
     o << "// generated by fsmt tiles.cpp: specialised K1 sweep for " << p.n_jit_kclasses << " kernel classes\n"
          "typedef unsigned int u32;\ntypedef unsigned long long u64;\n"
          "struct TileDesc { u32 kclass, cons_begin, n_cons, var_off, n_vars, rec_off, pad0, pad1; };\n"
-      << "#define VMAX " << p.vmax << "\n#define WARPS " << p.jit_warps << "\n\n" << kErfcPrelude;
-    for (uint32_t k = 0; k < p.n_jit_kclasses; ++k) emit_class(o, k, p.kclasses[k], b.tmpls[p.kclasses[k].tmpl], p.sval != 0);
+      << "#define VMAX " << p.vmax << "\n#define VTOT " << p.vmax + p.rmax << "\n#define WARPS " << p.jit_warps
+      << "\n\n" << kErfcPrelude;
+    for (uint32_t k = 0; k < p.n_jit_kclasses; ++k) emit_class(o, k, p.kclasses[k], b.tmpls[p.kclasses[k].tmpl]);
     const char* minb = getenv("FSMT_JIT_MINB");      // optional min CTAs/SM (register cap), A/B tuning
     o << "extern \"C\" __global__ void __launch_bounds__(WARPS * 32" << (minb && atoi(minb) > 0 ? std::string(", ") + minb : std::string())
       << ") fsmt_k1_jit(\n"
@@ -828,47 +774,34 @@ std::string jit_source(const Formula& f, const Built& b, const Plan& p) {
          "    double* __restrict__ terms, u32 terms_r, const u32* __restrict__ orig) {\n"
          "  extern __shared__ float smem[];\n"
          "  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;\n"
-         "  float* acc = smem + warp * (VMAX * 32);\n"
-         "  u32* vs = (u32*)(smem + WARPS * VMAX * 32) + warp * VMAX;\n"
+         "  float* acc = smem + warp * (VMAX * 32);                  // stream-variable rows\n"
+         "  u32* vs = (u32*)(smem + WARPS * VMAX * 32) + warp * VTOT; // stream then run variable ids\n"
          "  const u32 rtiles = (R + 31) / 32;\n"
          "  const u64 gw = (u64)blockIdx.x * WARPS + warp;\n"
          "  const u32 rt = (u32)(gw % rtiles);\n"
          "  const u64 ti = gw / rtiles;\n"
          "  if (ti >= n_tiles) return;\n"
          "  const TileDesc T = tiles[ti];\n"
+         "  const u32 n_s = T.n_vars & 0xffffu, n_v = n_s + (T.n_vars >> 16);\n"
          "  const u32 r = rt * 32 + lane;\n"
          "  const bool live = r < R;\n"
          "  const u64 rr = live ? r : 0;\n"
-         "  for (u32 l = lane; l < T.n_vars; l += 32) vs[l] = tile_vars[T.var_off + l];\n"
-         "  for (u32 l = 0; l < T.n_vars; ++l) acc[l * 32 + lane] = 0.f;\n"
-         "  __syncwarp();\n";
-    if (p.sval)
-        o << "  float* vals = smem + WARPS * VMAX * 33 + WARPS * " << p.rec_stage4 * 4 << " + warp * (VMAX * 32) + lane;\n"
-             "  for (u32 l = 0; l < T.n_vars; ++l) {   // tile variable values, staged once per tile\n"
-             "    const u32 g = vs[l];\n"
-             "    vals[l * 32] = g < n_bool ? a[(u64)g * R + rr] : b[(u64)(g - n_bool) * R + rr];\n"
-             "  }\n";
-    else
-        o << "  const float* vals = nullptr;\n";
-    o << ""
+         "  for (u32 l = lane; l < n_v; l += 32) vs[l] = tile_vars[T.var_off + l];\n"
+         "  for (u32 l = 0; l < n_s; ++l) acc[l * 32 + lane] = 0.f;\n"
+         "  __syncwarp();\n"
+         "  const u32* vr = vs + n_s;\n"
          "  const float kq = kappa * 0.70710678118654752f;\n"
          "  const float dcoef = kappa * 0.79788456080286536f;\n"
-         "  double objacc = 0.0;\n";
-    if (stage_records())
-        o << "  uint4* rs = (uint4*)(smem + WARPS * VMAX * 33) + warp * " << p.rec_stage4 << ";\n"
-             "  for (u32 q = lane; q < T.pad0; q += 32) rs[q] = __ldg(recs + T.rec_off + q);   // pad0 = record uint4s\n"
-             "  __syncwarp();\n"
-             "  const uint4* rp = rs;\n";
-    else
-        o << "  const uint4* rp = recs + T.rec_off;\n";
-    o << "  switch (T.kclass) {\n";
+         "  double objacc = 0.0;\n"
+         "  const uint4* rp = recs + T.rec_off;\n"
+         "  switch (T.kclass) {\n";
     for (uint32_t k = 0; k < p.n_jit_kclasses; ++k)
         o << "    case " << k << ": kc" << k
-          << "(T, rp, vs, acc + lane, a, b, U, R, rr, r, live, n_bool, kq, dcoef, wscale, objacc, terms, terms_r, orig, vals); break;\n";
+          << "(T, rp, vs, vr, acc + lane, a, b, ga, gb, U, R, rr, r, live, n_bool, kq, dcoef, wscale, objacc, terms, terms_r, orig); break;\n";
     o << "    default: break;\n  }\n"
          "  __syncwarp();\n"
          "  if (!live) return;\n"
-         "  for (u32 l = 0; l < T.n_vars; ++l) {\n"
+         "  for (u32 l = 0; l < n_s; ++l) {\n"
          "    const u32 g = vs[l];\n"
          "    const double v = (double)acc[l * 32 + lane];\n"
          "    if (g < n_bool) atomicAdd(ga + (u64)g * R + r, v); else atomicAdd(gb + (u64)(g - n_bool) * R + r, v);\n"
@@ -886,7 +819,7 @@ std::string jit_source(const Formula& f, const Built& b, const Plan& p) {
          "    const unsigned char* __restrict__ astrict) {\n"
          "  extern __shared__ float smem[];\n"
          "  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;\n"
-         "  u32* vs = (u32*)smem + warp * VMAX;\n"
+         "  u32* vs = (u32*)smem + warp * VTOT;\n"
          "  const u32 rtiles = (R + 31) / 32;\n"
          "  const u64 gw = (u64)blockIdx.x * WARPS + warp;\n"
          "  const u32 rt = (u32)(gw % rtiles);\n"
@@ -896,15 +829,17 @@ std::string jit_source(const Formula& f, const Built& b, const Plan& p) {
          "  const u32 r = rt * 32 + lane;\n"
          "  const bool live = r < R;\n"
          "  const u64 rr = live ? r : 0;\n"
-         "  for (u32 l = lane; l < T.n_vars; l += 32) vs[l] = tile_vars[T.var_off + l];\n"
+         "  const u32 n_s = T.n_vars & 0xffffu, n_v = n_s + (T.n_vars >> 16);\n"
+         "  for (u32 l = lane; l < n_v; l += 32) vs[l] = tile_vars[T.var_off + l];\n"
          "  __syncwarp();\n"
+         "  const u32* vr = vs + n_s;\n"
          "  const uint4* rp = recs + T.rec_off;\n"
          "  const uint4* vp = vrecs + T.pad1;\n"
          "  u32 cnt = 0u;\n"
          "  switch (T.kclass) {\n";
     for (uint32_t k = 0; k < p.n_jit_kclasses; ++k)
         o << "    case " << k << ": cnt = kv" << k
-          << "(T, rp, vp, vs, x, y, U, per_con, orig, R, rr, r, live, n_bool, arow, aval, arhs, astrict); break;\n";
+          << "(T, rp, vp, vs, vr, x, y, U, per_con, orig, R, rr, r, live, n_bool, arow, aval, arhs, astrict); break;\n";
     o << "    default: break;\n  }\n"
          "  if (live && cnt) atomicAdd(unsat + r, cnt);\n"
          "}\n";
