@@ -95,7 +95,7 @@ struct Built {
 // Constraints are permuted into an internal order grouped into tiles: a tile is a run of
 // constraints of one kernel class (template + nnz of each atom slot) whose variables fit a
 // small local table, so the JIT-specialised sweep accumulates their gradients on chip.
-constexpr uint32_t kTileVmaxDefault = 64;    // stream variables (shared-memory rows) per tile (FSMT_TILE_VMAX)
+constexpr uint32_t kTileVmaxDefault = 48;    // stream variables (shared-memory rows) per tile (FSMT_TILE_VMAX)
 constexpr uint32_t kTileRmaxDefault = 128;   // run variables per tile (FSMT_TILE_RMAX)
 constexpr uint32_t kTileCmax = 64;        // constraints per tile
 constexpr uint32_t kGroupVarsDefault = 64;   // variables per footprint group (VMAX/2)

@@ -316,9 +316,9 @@ Plan make_plan(const Formula& f, const Built& b, bool enable_jit) {
     // any JIT-class constraints after the cut run through the generic kernel
 
     // 6. record compression: words equal across a whole class become literals in the code
-    // opt-in (FSMT_JIT_FOLD=1): fewer registers/loads, but measured slower on cfg4 (26.6 vs 22.1 ms)
+    // (FSMT_JIT_FOLD=0 disables; cfg4: 7 -> 4 uint4 per record, 13.7 vs 14.0 ms at vmax 48)
     const char* cz = getenv("FSMT_JIT_FOLD");
-    const bool fold = cz && cz[0] == '1';
+    const bool fold = !(cz && cz[0] == '0');
     std::vector<std::vector<uint8_t>> varies(p.n_jit_kclasses);
     std::vector<std::vector<uint32_t>> first(p.n_jit_kclasses);
     for (uint32_t k = 0; k < p.n_jit_kclasses; ++k) {
@@ -384,6 +384,10 @@ bool fast_erfc() {
     const char* e = getenv("FSMT_JIT_ERFC");
     return !(e && std::string(e) == "cuda");
 }
+const char* erfc_fn() {
+    const char* e = getenv("FSMT_JIT_ERFC");
+    return (e && std::string(e) == "nr") ? "fsmt_half_erfc_nr" : "fsmt_half_erfc";
+}
 
 // FSMT_JIT_ERFC_VOTE=1: warp-vote per atom, one erfc branch when the warp agrees (A/B,
 // DESIGN.md §9).
@@ -402,9 +406,27 @@ const char* kErfcPrelude =
     "  return __fmul_rn(__fmul_rn(__fmul_rn(w, f1), f2), f2);\n"
     "}\n"
     "__device__ __forceinline__ float fsmt_ex2(float x) { float r; asm(\"ex2.approx.ftz.f32 %0, %1;\" : \"=f\"(r) : \"f\"(x)); return r; }\n"
-    "// 0.5*erfc(z) for z >= 0 and ez = exp(-z^2) (dd/db factor, P:1326-1327).\n"
-    "// z < 0.75: 1 - erf(z) from the Maclaurin series of erf (10 terms); z >= 0.75: Numerical Recipes\n"
-    "// erfcc, t exp(-z^2 + P(t)), t = 1/(1 + z/2), fractional error < 1.2e-7.\n"
+    "// 0.5*erfc(z) for z >= 0 and ez = exp(-z^2) (dd/db factor, P:1326-1327).  Coefficients from\n"
+    "// scripts/fit_erfc.py: z < 0.75: 0.5 (1 - z P(z^2)), P ~ erf(z)/z (degree 5);\n"
+    "// z >= 0.75: t Q(t) ez, t = 1/(1 + z/2), Q ~ 0.5 erfcx(z)/t (degree 7), reusing ez.\n"
+    "// Max abs error 5.3e-8 in fp32 (with exact exp).  FSMT_JIT_ERFC=nr: the previous\n"
+    "// Maclaurin + Numerical Recipes erfcc pair; =cuda: erfcf + expf (A/B).\n"
+    "__device__ __forceinline__ float fsmt_half_erfc(float z, float& ez) {\n"
+    "  const float z2 = z * z;\n"
+    "  ez = fsmt_ex2(-1.44269504088896341f * z2);\n"
+    "  float p = -6.760858814e-04f;\n"
+    "  p = fmaf(p, z2, 5.115946755e-03f); p = fmaf(p, z2, -2.683541551e-02f); p = fmaf(p, z2, 1.128339246e-01f);\n"
+    "  p = fmaf(p, z2, -3.761262000e-01f); p = fmaf(p, z2, 1.128379107e+00f);\n"
+    "  const float small = 0.5f * fmaf(-z, p, 1.f);\n"
+    "  float t;   // 1/(1 + z/2) with 1 + z/2 >= 1: rcp.approx needs no denormal range fix-up\n"
+    "  asm(\"rcp.approx.ftz.f32 %0, %1;\" : \"=f\"(t) : \"f\"(fmaf(0.5f, z, 1.f)));\n"
+    "  float q = 4.469624162e-02f;\n"
+    "  q = fmaf(q, t, -1.088827997e-01f); q = fmaf(q, t, 3.824992850e-02f); q = fmaf(q, t, 3.101851977e-02f);\n"
+    "  q = fmaf(q, t, 8.971593529e-02f); q = fmaf(q, t, 1.233071312e-01f); q = fmaf(q, t, 1.410502791e-01f);\n"
+    "  q = fmaf(q, t, 1.410473883e-01f);\n"
+    "  const float tail = t * q * ez;\n"
+    "  return z < 0.75f ? small : tail;\n"
+    "}\n"
     "__device__ __forceinline__ float fsmt_erfc_small(float z, float z2) {\n"
     "  float q = -1.4503291e-7f;\n"
     "  q = fmaf(q, z2, 1.4589169e-6f); q = fmaf(q, z2, -1.3227513e-5f); q = fmaf(q, z2, 1.0683761e-4f);\n"
@@ -413,7 +435,7 @@ const char* kErfcPrelude =
     "  return 0.5f * fmaf(-1.12837916709551257f * z, q, 1.f);\n"
     "}\n"
     "__device__ __forceinline__ float fsmt_erfc_tail(float z, float z2) {\n"
-    "  float t;   // 1/(1 + z/2) with 1 + z/2 >= 1: rcp.approx needs no denormal range fix-up\n"
+    "  float t;\n"
     "  asm(\"rcp.approx.ftz.f32 %0, %1;\" : \"=f\"(t) : \"f\"(fmaf(0.5f, z, 1.f)));\n"
     "  float p = 0.17087277f;\n"
     "  p = fmaf(p, t, -0.82215223f); p = fmaf(p, t, 1.48851587f); p = fmaf(p, t, -1.13520398f);\n"
@@ -421,7 +443,7 @@ const char* kErfcPrelude =
     "  p = fmaf(p, t, 0.37409196f); p = fmaf(p, t, 1.00002368f); p = fmaf(p, t, -1.26551223f);\n"
     "  return 0.5f * t * fsmt_ex2((p - z2) * 1.44269504088896341f);\n"
     "}\n"
-    "__device__ __forceinline__ float fsmt_half_erfc(float z, float& ez) {\n"
+    "__device__ __forceinline__ float fsmt_half_erfc_nr(float z, float& ez) {\n"
     "  const float z2 = z * z;\n"
     "  ez = fsmt_ex2(-1.44269504088896341f * z2);\n"
     "  const float small = fsmt_erfc_small(z, z2), tail = fsmt_erfc_tail(z, z2);\n"
@@ -535,7 +557,7 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
                   << "      else e" << s << " = za" << s << " < 0.75f ? fsmt_erfc_small(za" << s << ", zb" << s
                   << ") : fsmt_erfc_tail(za" << s << ", zb" << s << "); }\n";
             } else if (fast_erfc())
-                o << "    float ez" << s << ";\n    const float e" << s << " = fsmt_half_erfc(fabsf(u" << s << "), ez" << s << ");\n";
+                o << "    float ez" << s << ";\n    const float e" << s << " = " << erfc_fn() << "(fabsf(u" << s << "), ez" << s << ");\n";
             else
                 o << "    const float e" << s << " = 0.5f * erfcf(fabsf(u" << s << "));\n"
                   << "    const float ez" << s << " = expf(-u" << s << " * u" << s << ");\n";
