@@ -51,6 +51,7 @@ class Params:
     rounding: str = "sign"       # "sign" | "philox"  (R17)
     erwa_mode: int = 0           # 0: Alg.2 verbatim (h <- 1); 1: reset-to-0 reading (R18)
     eta_mode: int = 0            # 0 eta; 1 eta/kappa; 2 eta/kappa^2; 3 eta for a, eta/kappa^2 for b (R13)
+    proj_iters: int = 0          # 0: R15 interval clamps; > 0: Prop.1 QP by that many Dykstra sweeps (R33)
 
 
 # ----------------------------------------------------------------------------- projection bounds
@@ -114,15 +115,20 @@ def bounds(f):
     return np.array(lo, dtype=np.float32), np.array(hi, dtype=np.float32)
 
 
-def project(a, b, lo, hi):
-    """Def.1 / Prop.1 with reading R15: separable clamps."""
-    return np.clip(a, -1.0, 1.0), np.minimum(np.maximum(b, lo.astype(np.float64)), hi.astype(np.float64))
+def project(a, b, lo, hi, H=None, proj_iters=0):
+    """Def.1 / Prop.1: a clamped to [-1, 1]; b clamped to the R15 intervals, or (R33, proj_iters > 0
+    and multi-variable unit atoms present) projected by Dykstra onto intervals and halfspaces."""
+    a2 = np.clip(a, -1.0, 1.0)
+    if H and proj_iters > 0:
+        from .projection import dykstra
+        return a2, dykstra(np.asarray(b, dtype=np.float64), lo, hi, H, proj_iters)
+    return a2, np.minimum(np.maximum(b, lo.astype(np.float64)), hi.astype(np.float64))
 
 
 # ----------------------------------------------------------------------------- init / rounding
 
 
-def init_point(f, seed, r, lo, hi):
+def init_point(f, seed, r, lo, hi, H=None, proj_iters=0):
     """Reading R20; returns fp32-representable (a, b) as fp64 arrays."""
     a = np.empty(f.n_bool)
     for i in range(f.n_bool):
@@ -138,7 +144,7 @@ def init_point(f, seed, r, lo, hi):
         else:
             v = 2.0 * u - 1.0
         b[j] = float(np.float32(v))
-    a, b = project(a, b, lo, hi)
+    a, b = project(a, b, lo, hi, H, proj_iters)
     return a, b
 
 
@@ -164,14 +170,15 @@ def violations(f, x, y):
 # ----------------------------------------------------------------------------- PGD step (for replay)
 
 
-def pgd_step(f, a, b, kappa, w, eta, lo, hi, eta_b=None):
+def pgd_step(f, a, b, kappa, w, eta, lo, hi, eta_b=None, H=None, proj_iters=0):
     """One Alg.1 iteration: returns (a', b', ||gm||^2, C) at (a, b) (Eq.11-14).
 
     eta_b: optional separate step for the real block (eta_mode 3 reading); default eta.
+    H, proj_iters: the R33 projection (oracle/projection.py); default the R15 clamps.
     """
     eta_b = eta if eta_b is None else eta_b
     C, ga, gb = objective_and_gradient(f, a, b, kappa, w)
-    a2, b2 = project(np.asarray(a) - eta * ga, np.asarray(b) - eta_b * gb, lo, hi)
+    a2, b2 = project(np.asarray(a) - eta * ga, np.asarray(b) - eta_b * gb, lo, hi, H, proj_iters)
     gm2 = float(np.sum(((np.asarray(a) - a2) / eta) ** 2) + np.sum(((np.asarray(b) - b2) / eta_b) ** 2))
     return a2, b2, gm2, C
 
@@ -192,7 +199,9 @@ class RestartResult:
 def solve_restart(f, seed, r, params: Params, lo=None, hi=None):
     if lo is None:
         lo, hi = bounds(f)
-    a, b = init_point(f, seed, r, lo, hi)
+    from .projection import halfspaces
+    H = halfspaces(f) if params.proj_iters > 0 else None
+    a, b = init_point(f, seed, r, lo, hi, H, params.proj_iters)
     C_n = len(f.constraints)
     h = np.zeros(C_n)
     w = np.array([c.weight for c in f.constraints], dtype=np.float64)   # initial w_c (Alg.2 input)
@@ -206,7 +215,7 @@ def solve_restart(f, seed, r, params: Params, lo=None, hi=None):
         if params.eta_mode == 3:
             eta_t = params.eta
         for _ in range(params.steps):
-            a2, b2, gm2, _ = pgd_step(f, a, b, kappa, w, eta_t, lo, hi, eta_b)
+            a2, b2, gm2, _ = pgd_step(f, a, b, kappa, w, eta_t, lo, hi, eta_b, H, params.proj_iters)
             if gm2 <= params.eps ** 2:
                 break
             a, b = a2, b2
