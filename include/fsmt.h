@@ -60,6 +60,7 @@ typedef struct {
     uint32_t n_bounded;        /* reals with a finite projection bound (R15) */
     uint64_t n_nodes;          /* sum over constraints of |V_c| */
     uint64_t n_slot_refs;      /* sum over constraints of slot count */
+    uint32_t n_halfspaces;     /* multi-variable unit atom literals (projection halfspaces, R33) */
 } fsmt_dims;
 
 typedef struct {
@@ -74,6 +75,11 @@ typedef struct {
                                   kappa-scaling of 1/L); 3 block steps: eta for a, eta/kappa_t^2
                                   for b (only the real block's Lipschitz term grows with kappa)
                                   -- kappa_t < 1 counts as 1 */
+    uint32_t proj_iters;       /* projection of the real block (Def.1/Prop.1): 0 = R15 (interval
+                                  clamps from single-variable unit atoms; multi-variable unit atoms stay
+                                  soft); N > 0 = R33: the QP with every unit atom, by N sweeps of Dykstra's
+                                  algorithm over the halfspaces g.b <= h then the box, at init and after every
+                                  gradient step (<= 100000; FSMT_ERR_ARG above) */
 } fsmt_params;
 
 typedef struct {

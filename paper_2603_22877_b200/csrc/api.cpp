@@ -370,6 +370,28 @@ fsmt_status fsmt_build_xbdd(fsmt_ctx* ctx, uint64_t node_budget) {
     UP(ainv, atom_invnorm);
     UP(b.lo, lo);
     UP(b.hi, hi);
+    {   // R33 halfspaces (multi-variable unit atoms)
+        std::vector<float> hg(b.h_g.begin(), b.h_g.end()), hh(b.h_h.begin(), b.h_h.end()), inv2;
+        std::vector<uint8_t> in_h(f.n_real, 0);
+        std::vector<uint32_t> hv;
+        for (size_t k = 0; k + 1 < b.h_rowptr.size(); ++k) {
+            double n2 = 0.0;
+            for (uint32_t t = b.h_rowptr[k]; t < b.h_rowptr[k + 1]; ++t) n2 += (double)hg[t] * (double)hg[t];
+            inv2.push_back((float)(1.0 / n2));
+        }
+        for (uint32_t j : b.h_col) in_h[j] = 1;
+        for (uint32_t j = 0; j < f.n_real; ++j)
+            if (in_h[j]) hv.push_back(j);
+        F.n_half = (uint32_t)(b.h_rowptr.size() - 1);
+        F.n_hvars = (uint32_t)hv.size();
+        UP(b.h_rowptr, h_rowptr);
+        UP(b.h_col, h_col);
+        UP(hg, h_g);
+        UP(hh, h_h);
+        UP(inv2, h_inv2);
+        UP(hv, hvars);
+        UP(in_h, in_h);
+    }
 #undef UP
     s = upload(ctx, P.pos, ctx->d_pos, ctx->fallocs);
     if (s) return s;
@@ -431,6 +453,7 @@ fsmt_status fsmt_get_dims(const fsmt_ctx* ctx, fsmt_dims* out) {
         d.n_bounded = ctx->b.n_bounded;
         d.n_nodes = ctx->b.n_nodes;
         d.n_slot_refs = ctx->b.slot_ids.size();
+        d.n_halfspaces = (uint32_t)(ctx->b.h_rowptr.size() - 1);
     }
     *out = d;
     return FSMT_OK;
@@ -471,6 +494,7 @@ fsmt_status fsmt_set_params(fsmt_ctx* ctx, const fsmt_params* p) {
         ctx->rounding = FSMT_ROUND_SIGN;
         ctx->erwa_mode = FSMT_ERWA_VERBATIM;
         ctx->eta_mode = 0;
+        ctx->F.proj_iters = 0;
         ctx->time_limit = 0;
         return FSMT_OK;
     }
@@ -482,8 +506,9 @@ fsmt_status fsmt_set_params(fsmt_ctx* ctx, const fsmt_params* p) {
     } else {
         default_kappas(ctx->kappas);
     }
-    if (p->rounding > 1 || p->erwa_mode > 1 || p->eta_mode > 3)
-        return fail(ctx, FSMT_ERR_ARG, "bad rounding / erwa_mode / eta_mode");
+    if (p->rounding > 1 || p->erwa_mode > 1 || p->eta_mode > 3 || p->proj_iters > 100000)
+        return fail(ctx, FSMT_ERR_ARG, "bad rounding / erwa_mode / eta_mode / proj_iters");
+    ctx->F.proj_iters = p->proj_iters;
     ctx->eta = p->eta > 0 ? p->eta : 0.05f;
     ctx->eps = p->eps > 0 ? p->eps : 1e-2f;
     ctx->rounding = p->rounding;
@@ -519,13 +544,23 @@ fsmt_status fsmt_begin(fsmt_ctx* ctx, uint32_t R, uint64_t seed, uint32_t restar
         drop_state(ctx);
         return s;
     }
+    S.bn = S.ph = S.pb = nullptr;
+    if (F.n_half) {   // R33 projection buffers (small: halfspace variables only, plus the candidate b)
+        const size_t hn = (size_t)ctx->b.h_col.size() * R;
+        if ((s = alloc((void**)&S.bn, nr * 4)) || (s = alloc((void**)&S.ph, hn * 4)) ||
+            (s = alloc((void**)&S.pb, (size_t)F.n_hvars * R * 4))) {
+            drop_state(ctx);
+            return s;
+        }
+    }
     CK(cudaMemsetAsync(S.U, 0, nc, ctx->stream));
     CK(cudaMemsetAsync(S.frozen, 0, R, ctx->stream));
     CK(cudaMemsetAsync(S.ga, 0, nb * 8, ctx->stream));
     CK(cudaMemsetAsync(S.gb, 0, nr * 8, ctx->stream));
     CK(cudaMemsetAsync(S.obj, 0, (size_t)R * 8, ctx->stream));
     launch_init(F, S, seed, restart_offset, ctx->stream);
-    ctx->launches += 1;
+    launch_project(F, S, S.b, false, ctx->stream);     // R33: init is projected like every step
+    ctx->launches += 1 + (F.proj_iters && F.n_half ? 1 : 0);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(ctx->stream));
     ctx->seed = seed;
@@ -646,7 +681,7 @@ static fsmt_status update_impl(fsmt_ctx* ctx, float eta, float eps, float eta_b 
         Timed tm(ctx, 1);
         launch_update(ctx->F, ctx->S, eta, eps, ctx->stream, eta_b);
     }
-    ctx->launches += 3;
+    ctx->launches += 3 + (ctx->F.proj_iters && ctx->F.n_half && ctx->S.bn ? 2 : 0);
     return check_launch(ctx);
 }
 

@@ -89,6 +89,9 @@ struct Built {
     std::vector<uint8_t> cons_sym;         // [C]
     std::vector<uint16_t> cons_k;          // [C] CARD threshold
     std::vector<uint8_t> slot_neg;         // parallel to slot_ids
+    // multi-variable unit atom literals as halfspaces g.b <= h (Prop.1, reading R33)
+    std::vector<uint32_t> h_rowptr{0}, h_col;
+    std::vector<double> h_g, h_h;
 };
 
 // ---- device work plan (csrc/tiles.cpp) -----------------------------------------------------

@@ -67,7 +67,9 @@ __global__ void k0_init(DevFormula F, DevState S, uint64_t seed, uint32_t off) {
                 val = __dadd_rn((double)lo, __dmul_rn(__dsub_rn((double)hi, (double)lo), u));
             else
                 val = __dsub_rn(__dmul_rn(2.0, u), 1.0);
-            S.b[(size_t)j * S.R + r] = fminf(fmaxf(__double2float_rn(val), lo), hi);
+            const float bv = __double2float_rn(val);
+            // with the R33 projection the halfspace variables start unclamped (Dykstra owns their box)
+            S.b[(size_t)j * S.R + r] = (F.proj_iters && F.in_h[j]) ? bv : fminf(fmaxf(bv, lo), hi);
         }
     }
 }
@@ -182,6 +184,54 @@ __device__ __forceinline__ float step_value(float x, double g, float eta, float 
     return __double2float_rn(t);
 }
 
+// candidate b' of the projected step (R33): halfspace variables unclamped (Dykstra projects
+// them), the others clamped to their interval (their exact projection)
+__global__ void k3_cand(DevFormula F, DevState S, float eta_b) {
+    const uint64_t n = (uint64_t)F.n_real * S.R;
+    for (uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t j = (uint32_t)(idx / S.R);
+        const bool h = F.in_h[j];
+        S.bn[idx] = step_value(S.b[idx], S.gb[idx], eta_b, h ? -INFINITY : F.lo[j], h ? INFINITY : F.hi[j]);
+    }
+}
+
+// Dykstra's algorithm per restart (thread = restart; every access is a coalesced row segment):
+// sets C_1..C_K = halfspaces g_k.b <= h_k in order, then C_0 = the box of the halfspace
+// variables, each with its own correction (ph, pb), F.proj_iters sweeps (R33).
+__global__ void k_dykstra(DevFormula F, DevState S, float* __restrict__ X, bool skip_frozen) {
+    const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t R = S.R;
+    if (r >= R) return;
+    if (skip_frozen && S.frozen[r]) return;
+    const uint32_t nnz = F.h_rowptr[F.n_half];
+    for (uint32_t k = 0; k < nnz; ++k) S.ph[(size_t)k * R + r] = 0.f;
+    for (uint32_t v = 0; v < F.n_hvars; ++v) S.pb[(size_t)v * R + r] = 0.f;
+    for (uint32_t it = 0; it < F.proj_iters; ++it) {
+        for (uint32_t h = 0; h < F.n_half; ++h) {
+            const uint32_t k0 = F.h_rowptr[h], k1 = F.h_rowptr[h + 1];
+            float v = -F.h_h[h];
+            for (uint32_t k = k0; k < k1; ++k)
+                v = fmaf(F.h_g[k], X[(size_t)F.h_col[k] * R + r] + S.ph[(size_t)k * R + r], v);
+            const float t = fmaxf(v, 0.f) * F.h_inv2[h];
+            for (uint32_t k = k0; k < k1; ++k) {
+                float* xp = X + (size_t)F.h_col[k] * R + r;
+                const float y = *xp + S.ph[(size_t)k * R + r];
+                const float xn = fmaf(-t, F.h_g[k], y);
+                S.ph[(size_t)k * R + r] = y - xn;
+                *xp = xn;
+            }
+        }
+        for (uint32_t v = 0; v < F.n_hvars; ++v) {
+            const uint32_t j = F.hvars[v];
+            float* xp = X + (size_t)j * R + r;
+            const float y = *xp + S.pb[(size_t)v * R + r];
+            const float xn = fminf(fmaxf(y, F.lo[j]), F.hi[j]);
+            S.pb[(size_t)v * R + r] = y - xn;
+            *xp = xn;
+        }
+    }
+}
+
 __global__ void k3_norm(DevFormula F, DevState S, float eta, float eta_b) {
     const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= S.R) return;
@@ -197,7 +247,7 @@ __global__ void k3_norm(DevFormula F, DevState S, float eta, float eta_b) {
         } else {
             const uint32_t j = v - F.n_bool;
             x = S.b[(size_t)j * S.R + r];
-            xn = step_value(x, S.gb[(size_t)j * S.R + r], eta_b, F.lo[j], F.hi[j]);
+            xn = S.bn ? S.bn[(size_t)j * S.R + r] : step_value(x, S.gb[(size_t)j * S.R + r], eta_b, F.lo[j], F.hi[j]);
         }
         const double d = ((double)x - (double)xn) / (double)(v < F.n_bool ? eta : eta_b);
         acc += d * d;
@@ -225,7 +275,7 @@ __global__ void k3_apply(DevFormula F, DevState S, float eta, float eta_b) {
         } else {
             const uint32_t j = v - F.n_bool;
             float& x = S.b[(size_t)j * S.R + r];
-            x = step_value(x, S.gb[(size_t)j * S.R + r], eta_b, F.lo[j], F.hi[j]);
+            x = S.bn ? S.bn[(size_t)j * S.R + r] : step_value(x, S.gb[(size_t)j * S.R + r], eta_b, F.lo[j], F.hi[j]);
         }
     }
 }
@@ -391,12 +441,25 @@ void launch_update(const DevFormula& F, const DevState& S, float eta, float eps,
     if (!(eta_b > 0.f)) eta_b = eta;
     const uint32_t parts = (uint32_t)update_parts(F);
     if (parts == 0 || S.R == 0) return;
+    DevState Sp = S;
+    if (F.proj_iters && F.n_half && S.bn) {       // Prop.1 with halfspaces (R33): candidate + Dykstra
+        const uint64_t n = (uint64_t)F.n_real * S.R;
+        k3_cand<<<(unsigned)std::min<uint64_t>((n + 255) / 256, 148ull * 16), 256, 0, st>>>(F, S, eta_b);
+        launch_project(F, S, S.bn, true, st);
+    } else {
+        Sp.bn = nullptr;
+    }
     dim3 g1((S.R + 127) / 128, parts);
-    k3_norm<<<g1, 128, 0, st>>>(F, S, eta, eta_b);
+    k3_norm<<<g1, 128, 0, st>>>(F, Sp, eta, eta_b);
     k3_final<<<(S.R + 127) / 128, 128, 0, st>>>(S, parts, eps);
     const uint64_t n = (uint64_t)(F.n_bool + F.n_real) * S.R;
     const uint64_t blocks = std::min<uint64_t>((n + 255) / 256, 148ull * 16);
-    k3_apply<<<(unsigned)blocks, 256, 0, st>>>(F, S, eta, eta_b);
+    k3_apply<<<(unsigned)blocks, 256, 0, st>>>(F, Sp, eta, eta_b);
+}
+
+void launch_project(const DevFormula& F, const DevState& S, float* X, bool skip_frozen, cudaStream_t st) {
+    if (!F.proj_iters || !F.n_half || S.R == 0) return;
+    k_dykstra<<<(S.R + 63) / 64, 64, 0, st>>>(F, S, X, skip_frozen);
 }
 
 void launch_round(const DevFormula& F, const DevState& S, uint32_t rounding, uint64_t seed, uint32_t off,

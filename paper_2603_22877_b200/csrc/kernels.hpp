@@ -38,6 +38,15 @@ struct DevFormula {
     const float* hi;                // [n_real]
     const uint32_t* orig;           // [C] internal -> original constraint id (constraint arrays and U
                                     //     are in the internal, tile-sorted order; see tiles.cpp)
+    // Prop.1 projection with multi-variable unit atoms (R33): halfspaces g.b <= h, Dykstra sweeps
+    uint32_t n_half = 0, n_hvars = 0, proj_iters = 0;
+    const uint32_t* h_rowptr = nullptr;  // [n_half+1]
+    const uint32_t* h_col = nullptr;     // [nnz] real index
+    const float* h_g = nullptr;          // [nnz]
+    const float* h_h = nullptr;          // [n_half]
+    const float* h_inv2 = nullptr;       // [n_half] 1/||g||^2
+    const uint32_t* hvars = nullptr;     // [n_hvars] reals in some halfspace (box corrections)
+    const uint8_t* in_h = nullptr;       // [n_real] 1 if in some halfspace
     uint32_t generic_begin;         // internal [generic_begin, generic_end) run through the generic K1
     uint32_t generic_end;           //   (generic_end < n_cons only in constraint-sharded mode)
 };
@@ -56,6 +65,9 @@ struct DevState {
     uint8_t* frozen;   // [R]
     double* gm2;       // [R]
     double* gm2_part;  // [n_parts][R]
+    float* bn;         // [n_real][R] candidate b of the projected step (R33), or null
+    float* ph;         // [nnz of halfspaces][R] Dykstra corrections
+    float* pb;         // [n_hvars][R] Dykstra box corrections
 };
 
 int sweep_smem_bytes(const DevFormula& F, int warps);
@@ -91,6 +103,9 @@ void launch_scatter_rows_u8(uint8_t* dst, const uint8_t* src, const uint32_t* id
 int update_parts(const DevFormula& F);
 // eta: step for a (Booleans); eta_b: step for b (reals), <= 0 -> eta (Eq.11 uses one eta; R13).
 void launch_update(const DevFormula& F, const DevState& S, float eta, float eps, cudaStream_t st, float eta_b = 0.f);
+// Dykstra projection (R33) of X [n_real][R] in place: F.proj_iters sweeps over the halfspaces then
+// the box, per restart (skips frozen restarts when skip_frozen).
+void launch_project(const DevFormula& F, const DevState& S, float* X, bool skip_frozen, cudaStream_t st);
 // K4: rounding (R17).
 void launch_round(const DevFormula& F, const DevState& S, uint32_t rounding, uint64_t seed, uint32_t restart_offset,
                   uint32_t stage, cudaStream_t st);

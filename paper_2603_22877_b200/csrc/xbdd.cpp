@@ -311,7 +311,21 @@ Built build_xbdds(const Formula& f, uint64_t node_budget) {
             bool positive = (nd.hi == kTrue && nd.lo == kFalse);
             bool negative = (nd.hi == kFalse && nd.lo == kTrue);
             uint32_t r0 = f.atom_rowptr[atom];
-            if ((positive || negative) && f.atom_rowptr[atom + 1] - r0 == 1) {
+            const uint32_t nnz = f.atom_rowptr[atom + 1] - r0;
+            if ((positive || negative) && nnz >= 2) {
+                // R33: g = +-q, h = +-q0 - delta, delta = 2^-17 (|q0| + ||q||_1)
+                double l1 = 0.0;
+                for (uint32_t k = r0; k < r0 + nnz; ++k) l1 += std::fabs(f.atom_val[k]);
+                const double delta = std::ldexp(std::fabs(f.atom_rhs[atom]) + l1, -17);
+                const double sg = positive ? 1.0 : -1.0;
+                for (uint32_t k = r0; k < r0 + nnz; ++k) {
+                    b.h_col.push_back(f.atom_col[k]);
+                    b.h_g.push_back(sg * f.atom_val[k]);
+                }
+                b.h_h.push_back(sg * f.atom_rhs[atom] - delta);
+                b.h_rowptr.push_back((uint32_t)b.h_col.size());
+            }
+            if ((positive || negative) && nnz == 1) {
                 uint32_t j = f.atom_col[r0];
                 double q = f.atom_val[r0];
                 bool upper = (q > 0) == positive;

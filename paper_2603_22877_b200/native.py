@@ -26,13 +26,14 @@ ERWA_VERBATIM, ERWA_RESET0 = 0, 1
 class Dims(C.Structure):
     _fields_ = [("n_bool", C.c_uint32), ("n_real", C.c_uint32), ("n_atoms", C.c_uint32), ("n_cons", C.c_uint32),
                 ("n_templates", C.c_uint32), ("max_slots", C.c_uint32), ("max_nodes", C.c_uint32),
-                ("n_bounded", C.c_uint32), ("n_nodes", C.c_uint64), ("n_slot_refs", C.c_uint64)]
+                ("n_bounded", C.c_uint32), ("n_nodes", C.c_uint64), ("n_slot_refs", C.c_uint64),
+                ("n_halfspaces", C.c_uint32)]
 
 
 class Params(C.Structure):
     _fields_ = [("kappas", C.POINTER(C.c_float)), ("n_stages", C.c_uint32), ("eta", C.c_float), ("eps", C.c_float),
                 ("rounding", C.c_uint32), ("erwa_mode", C.c_uint32), ("time_limit_s", C.c_double),
-                ("eta_mode", C.c_uint32)]
+                ("eta_mode", C.c_uint32), ("proj_iters", C.c_uint32)]
 
 
 class Stats(C.Structure):

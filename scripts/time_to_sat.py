@@ -30,6 +30,7 @@ def main():
                    help="geo1-<kmax>[-hold<m>]: <stages> geometric kappas 1..kmax, then kmax m*<stages> more times")
     p.add_argument("--stages", type=int, default=20)
     p.add_argument("--eta-mode", type=int, default=0)
+    p.add_argument("--proj-iters", type=int, default=0)
     p.add_argument("--erwa", type=int, default=0)
     p.add_argument("--rounding", type=int, default=0)
     p.add_argument("--time-limit", type=float, default=1000.0)
@@ -51,7 +52,7 @@ def main():
         hold = int(parts[2][4:] or 1) if len(parts) > 2 else 0
         kappas = [kmax ** (i / (a.stages - 1)) for i in range(a.stages)] + [kmax] * (hold * a.stages)
     s.set_params(kappas=kappas, eta=a.eta, erwa_mode=a.erwa, rounding=a.rounding, time_limit_s=a.time_limit,
-                 eta_mode=a.eta_mode)
+                 eta_mode=a.eta_mode, proj_iters=a.proj_iters)
     runs = []
     for seed in a.seeds:
         res = s.solve(a.restarts, a.steps, seed)
@@ -63,7 +64,7 @@ def main():
     times = [r["solve_s"] if r["verdict"] == "SAT" else float("inf") for r in runs]
     med = statistics.median(times)
     print(json.dumps({"config": a.config, "restarts": a.restarts, "steps_per_stage": a.steps, "eta": a.eta,
-                      "eta_mode": a.eta_mode, "erwa": a.erwa, "schedule": a.schedule or a.kappas or "default",
+                      "eta_mode": a.eta_mode, "proj_iters": a.proj_iters, "erwa": a.erwa, "schedule": a.schedule or a.kappas or "default",
                       "build_s": build_s, "median_time_to_sat_s": med if med != float("inf") else None,
                       "solved": sum(r["verdict"] == "SAT" for r in runs), "runs": len(runs),
                       "jit": s.jit_info()}))
