@@ -37,6 +37,8 @@ struct fsmt_ctx {
     std::string jit_src, jit_error;
     JitKernel jit;
     DevTiles T{};
+    DevSlots slots{};                  // slot tables of the symmetric JIT classes (has_sym)
+    bool has_sym = false;
     const uint32_t* d_pos = nullptr;   // original -> internal constraint index (device)
     // constraint sharding (fsmt_shard): this context's part of the sweep and of the check
     DevTiles T_all{};                  // every JIT tile
@@ -144,6 +146,9 @@ void free_list(std::vector<void*>& v) {
 void drop_state(fsmt_ctx* ctx) {
     free_list(ctx->sallocs);
     ctx->S = DevState{};
+    ctx->slots.PT = ctx->slots.PF = ctx->slots.DD = nullptr;
+    ctx->slots.GU = nullptr;
+    ctx->slots.TT = nullptr;
     ctx->rounded = false;
     if (ctx->terms) { cudaFree(ctx->terms); ctx->terms = nullptr; }
 }
@@ -155,6 +160,8 @@ void drop_formula(fsmt_ctx* ctx) {
     jit_release(ctx->jit);
     ctx->T = DevTiles{};
     ctx->T_all = DevTiles{};
+    ctx->slots = DevSlots{};
+    ctx->has_sym = false;
     ctx->d_pos = nullptr;
 }
 
@@ -423,6 +430,16 @@ fsmt_status fsmt_build_xbdd(fsmt_ctx* ctx, uint64_t node_budget) {
             if (s) return s;
             ctx->T.vrecs = vr;
             F.generic_begin = P.jit_cons_end;
+            if (P.has_sym) {
+                const uint32_t* sa = nullptr;
+                s = upload(ctx, P.sym_atoms, sa, ctx->fallocs);
+                if (s) return s;
+                ctx->slots = DevSlots{};
+                ctx->slots.atoms = sa;
+                ctx->slots.n_sa = (uint32_t)P.sym_atoms.size();
+                ctx->slots.nv = f.n_bool + f.n_real;
+                ctx->has_sym = true;
+            }
         } else {
             ctx->jit_error = err;
         }
@@ -544,6 +561,16 @@ fsmt_status fsmt_begin(fsmt_ctx* ctx, uint32_t R, uint64_t seed, uint32_t restar
         drop_state(ctx);
         return s;
     }
+    if (ctx->has_sym) {   // slot tables (rows: Booleans, reals (unused), table atoms)
+        DevSlots& D = ctx->slots;
+        const size_t rows = (size_t)D.nv + D.n_sa;
+        if ((s = alloc((void**)&D.PT, rows * R * 4)) || (s = alloc((void**)&D.PF, rows * R * 4)) ||
+            (s = alloc((void**)&D.DD, (size_t)D.n_sa * R * 4)) || (s = alloc((void**)&D.GU, rows * R * 8)) ||
+            (s = alloc((void**)&D.TT, rows * R))) {
+            drop_state(ctx);
+            return s;
+        }
+    }
     S.bn = S.ph = S.pb = nullptr;
     if (F.n_half) {   // R33 projection buffers (small: halfspace variables only, plus the candidate b)
         const size_t hn = (size_t)ctx->b.h_col.size() * R;
@@ -664,12 +691,23 @@ static fsmt_status sweep_impl(fsmt_ctx* ctx, float kappa, uint32_t stage_t, doub
     {
         Timed tm(ctx, 0);
         const float ws = wscale_of(stage_t, ctx->erwa_mode);
+        const bool sym = ctx->has_sym && ctx->T.n_tiles;
+        if (sym) {   // shared slot probabilities for the symmetric classes
+            const DevSlots& D = ctx->slots;
+            CK(cudaMemsetAsync(D.GU, 0, ((size_t)D.nv + D.n_sa) * S.R * 8, ctx->stream));
+            launch_slot_prob(ctx->jit.kprob, F, S, D, kappa, ctx->stream);
+            ctx->launches += 1;
+        }
         if (ctx->T.n_tiles) {
-            launch_sweep_jit(ctx->jit.kernel, F, S, ctx->T, kappa, ws, terms, terms_r, ctx->stream);
+            launch_sweep_jit(ctx->jit.kernel, F, S, ctx->T, kappa, ws, terms, terms_r, ctx->stream, &ctx->slots);
             ctx->launches += 1;
         }
         if (F.generic_begin < F.generic_end) {
             launch_sweep(F, S, kappa, ws, terms, terms_r, ctx->stream);
+            ctx->launches += 1;
+        }
+        if (sym) {
+            launch_slot_chain(ctx->jit.kchain, F, S, ctx->slots, ctx->stream);
             ctx->launches += 1;
         }
     }
@@ -693,7 +731,11 @@ static fsmt_status stage_end_impl(fsmt_ctx* ctx, uint32_t stage_t) {
         launch_round(ctx->F, S, ctx->rounding, ctx->seed, ctx->restart_offset, stage_t, ctx->stream);
         ctx->launches += 1;
         if (ctx->T.n_tiles && ctx->jit.kernel5) {    // specialised check of this context's tiles
-            launch_verify_jit(ctx->jit.kernel5, ctx->F, S, ctx->T, S.x, S.b, S.U, nullptr, ctx->stream);
+            if (ctx->has_sym) {
+                launch_slot_truth(ctx->jit.ktruth, ctx->F, S, ctx->slots, S.x, S.b, ctx->stream);
+                ctx->launches += 1;
+            }
+            launch_verify_jit(ctx->jit.kernel5, ctx->F, S, ctx->T, S.x, S.b, S.U, nullptr, ctx->stream, ctx->slots.TT);
             launch_verify(ctx->F, S, S.x, S.b, S.U, nullptr, ctx->stream, ctx->F.generic_begin, ctx->F.generic_end);
             ctx->launches += 2;
         } else {
@@ -925,8 +967,10 @@ fsmt_status fsmt_verify_batch(fsmt_ctx* ctx, uint32_t R, const int8_t* x, const 
         return true;
     };
     const size_t nb = (size_t)F.n_bool * R, nr = (size_t)F.n_real * R, nc = (size_t)F.n_cons * R;
+    uint8_t* dtt = nullptr;
+    const size_t tt_rows = ctx->has_sym ? (size_t)ctx->slots.nv + ctx->slots.n_sa : 0;
     if (!alloc((void**)&dx, nb) || !alloc((void**)&dy, nr * 4) || !alloc((void**)&T.unsat, (size_t)R * 4) ||
-        (per_con && !alloc((void**)&dpc, nc))) {
+        (per_con && !alloc((void**)&dpc, nc)) || (tt_rows && !alloc((void**)&dtt, tt_rows * R))) {
         free_list(tmp);
         return fail(ctx, FSMT_ERR_OOM, "cudaMalloc failed in fsmt_verify_batch");
     }
@@ -937,7 +981,13 @@ fsmt_status fsmt_verify_batch(fsmt_ctx* ctx, uint32_t R, const int8_t* x, const 
     if (e == cudaSuccess) e = cudaMemsetAsync(T.unsat, 0, (size_t)R * 4, ctx->stream);
     if (e == cudaSuccess) {
         if (ctx->T_all.n_tiles && ctx->jit.kernel5) {
-            launch_verify_jit(ctx->jit.kernel5, F, T, ctx->T_all, dx, dy, nullptr, dpc, ctx->stream);
+            if (dtt) {
+                DevSlots D2 = ctx->slots;
+                D2.TT = dtt;
+                launch_slot_truth(ctx->jit.ktruth, F, T, D2, dx, dy, ctx->stream);
+                ctx->launches += 1;
+            }
+            launch_verify_jit(ctx->jit.kernel5, F, T, ctx->T_all, dx, dy, nullptr, dpc, ctx->stream, dtt);
             launch_verify(F, T, dx, dy, nullptr, dpc, ctx->stream, ctx->plan.jit_cons_end, F.n_cons);
             ctx->launches += 2;
         } else {

@@ -120,6 +120,12 @@ struct KClass {
     // literal wconst[w] in the generated code (e.g. unit weights, +-1 coefficients, 1/||q||)
     std::vector<int32_t> wpos;
     std::vector<uint32_t> wconst;
+    // symmetric class: every OR/CARD/NAE/XOR constraint of one (kind, L, k) over
+    // distinct variables shares the all-positive diagram stmpl; slots read shared probability
+    // tables (Booleans and the symmetric classes' atoms), literal polarities are record sign bits
+    bool sym = false;
+    uint32_t sym_kind = 0, sym_L = 0, sym_k = 0;
+    Template stmpl;
 };
 
 // n_vars = n_stream | n_run << 16; tile_vars[var_off ..) holds the stream variables then the run
@@ -144,6 +150,10 @@ struct Plan {
     uint32_t rmax = kTileRmaxDefault; // run variables per tile (register accumulators, flushed to HBM)
     uint32_t group = kTileVmaxDefault;  // footprint group size in variables (FSMT_TILE_GROUP)
     uint32_t cmax = kTileCmax;        // constraints per tile (FSMT_TILE_CMAX)
+    // atoms read through the slot tables by symmetric JIT classes; table row of atom sym_atoms[t]
+    // is n_bool + n_real + t (rows [0, n_bool) are the Booleans, the real rows are unused)
+    std::vector<uint32_t> sym_atoms;
+    bool has_sym = false;
 };
 
 Plan make_plan(const Formula& f, const Built& b, bool enable_jit);
@@ -154,6 +164,11 @@ struct BuildError {
     std::string msg;
     bool budget;
 };
+
+// Canonical xBDD of the all-positive symmetric constraint kind (OR/CARD/NAE/XOR) over L slots
+// (slot kinds 2 = "table slot", see tiles.cpp); a constraint's literal polarities act on it as
+// per-slot swaps of p_true / p_false.
+Template symmetric_template(uint32_t kind, uint32_t L, uint32_t k);
 
 // Compiles every constraint (a0 of SURVEY §8(a)). Throws BuildError.
 Built build_xbdds(const Formula& f, uint64_t node_budget);

@@ -136,9 +136,19 @@ bool jit_compile(const std::string& src, JitKernel& out, std::string& err) {
         err = std::string("cudaLibraryGetKernel(k5): ") + cudaGetErrorString(e);
         return false;
     }
+    cudaKernel_t kp = nullptr, kc = nullptr, kt = nullptr;
+    if (cudaLibraryGetKernel(&kp, lib, "fsmt_kp_jit") != cudaSuccess || cudaLibraryGetKernel(&kc, lib, "fsmt_kc_jit") != cudaSuccess ||
+        cudaLibraryGetKernel(&kt, lib, "fsmt_kt_jit") != cudaSuccess) {
+        cudaLibraryUnload(lib);
+        err = "cudaLibraryGetKernel(slot-table kernels) failed";
+        return false;
+    }
     out.lib = lib;
     out.kernel = k;
     out.kernel5 = k5;
+    out.kprob = kp;
+    out.kchain = kc;
+    out.ktruth = kt;
     out.cubin_bytes = cubin.size();
     return true;
 }
@@ -148,6 +158,7 @@ void jit_release(JitKernel& k) {
     k.lib = nullptr;
     k.kernel = nullptr;
     k.kernel5 = nullptr;
+    k.kprob = k.kchain = k.ktruth = nullptr;
 }
 
 }  // namespace fsmt

@@ -10,6 +10,9 @@ struct JitKernel {
     void* lib = nullptr;          // cudaLibrary_t
     cudaKernel_t kernel = nullptr;     // fsmt_k1_jit (sweep)
     cudaKernel_t kernel5 = nullptr;    // fsmt_k5_jit (exact check)
+    cudaKernel_t kprob = nullptr;      // fsmt_kp_jit (shared slot probability tables; symmetric classes)
+    cudaKernel_t kchain = nullptr;     // fsmt_kc_jit (slot-table gradients -> grad_a / grad_b)
+    cudaKernel_t ktruth = nullptr;     // fsmt_kt_jit (slot truth table for the exact check)
     size_t cubin_bytes = 0;
     std::string log;
 };

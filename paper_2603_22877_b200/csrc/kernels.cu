@@ -390,7 +390,7 @@ void launch_scatter_rows_u8(uint8_t* dst, const uint8_t* src, const uint32_t* id
 }
 
 void launch_sweep_jit(cudaKernel_t k, const DevFormula& F, const DevState& S, const DevTiles& T, float kappa,
-                      float wscale, double* terms, uint32_t terms_r, cudaStream_t st) {
+                      float wscale, double* terms, uint32_t terms_r, cudaStream_t st, const DevSlots* D) {
     if (T.n_tiles == 0 || S.R == 0) return;
     const int kJitWarps = (int)(T.warps ? T.warps : 1);
     const int kVmax = (int)T.vmax, kVtot = (int)(T.vmax + T.rmax);    // Plan::vmax, Plan::rmax
@@ -400,14 +400,45 @@ void launch_sweep_jit(cudaKernel_t k, const DevFormula& F, const DevState& S, co
     if (smem > 48 * 1024) cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     uint32_t n_tiles = T.n_tiles, R = S.R, n_bool = F.n_bool;
     const uint8_t* U = S.U;
+    const float* PT = D ? D->PT : nullptr;
+    const float* PF = D ? D->PF : nullptr;
+    double* GU = D ? D->GU : nullptr;
     void* args[] = {(void*)&T.tiles, &n_tiles, (void*)&T.recs, (void*)&T.tile_vars, (void*)&S.a, (void*)&S.b,
                     (void*)&S.ga, (void*)&S.gb, (void*)&U, (void*)&S.obj, &R, &n_bool, &kappa, &wscale,
-                    &terms, &terms_r, (void*)&F.orig};
+                    &terms, &terms_r, (void*)&F.orig, (void*)&PT, (void*)&PF, (void*)&GU};
     cudaLaunchKernel((const void*)k, dim3(blocks), dim3(kJitWarps * 32), args, smem, st);
 }
 
+void launch_slot_prob(cudaKernel_t k, const DevFormula& F, const DevState& S, const DevSlots& D, float kappa, cudaStream_t st) {
+    uint32_t n_bool = F.n_bool, nv = D.nv, n_sa = D.n_sa, R = S.R;
+    const uint64_t n = (uint64_t)(n_bool + n_sa) * R;
+    if (!n) return;
+    void* args[] = {&n_bool, &nv, &n_sa, (void*)&D.atoms, (void*)&S.a, (void*)&S.b, (void*)&F.atom_rowptr,
+                    (void*)&F.atom_col, (void*)&F.atom_val, (void*)&F.atom_rhs, (void*)&F.atom_invnorm, &R, &kappa,
+                    (void*)&D.PT, (void*)&D.PF, (void*)&D.DD};
+    cudaLaunchKernel((const void*)k, dim3((unsigned)std::min<uint64_t>((n + 255) / 256, 148ull * 16)), dim3(256), args, 0, st);
+}
+
+void launch_slot_chain(cudaKernel_t k, const DevFormula& F, const DevState& S, const DevSlots& D, cudaStream_t st) {
+    uint32_t n_bool = F.n_bool, nv = D.nv, n_sa = D.n_sa, R = S.R;
+    if (!R) return;
+    void* args[] = {&n_bool, &nv, &n_sa, (void*)&D.atoms, (void*)&F.atom_rowptr, (void*)&F.atom_col, (void*)&F.atom_val,
+                    &R, (void*)&D.GU, (void*)&D.DD, (void*)&S.ga, (void*)&S.gb};
+    cudaLaunchKernel((const void*)k, dim3((R + 63) / 64), dim3(64), args, 0, st);
+}
+
+void launch_slot_truth(cudaKernel_t k, const DevFormula& F, const DevState& S, const DevSlots& D, const int8_t* x,
+                       const float* y, cudaStream_t st) {
+    uint32_t n_bool = F.n_bool, nv = D.nv, n_sa = D.n_sa, R = S.R;
+    const uint64_t n = (uint64_t)(n_bool + n_sa) * R;
+    if (!n) return;
+    void* args[] = {&n_bool, &nv, &n_sa, (void*)&D.atoms, (void*)&x, (void*)&y, (void*)&F.atom_rowptr, (void*)&F.atom_col,
+                    (void*)&F.atom_val64, (void*)&F.atom_rhs64, (void*)&F.atom_strict, &R, (void*)&D.TT};
+    cudaLaunchKernel((const void*)k, dim3((unsigned)std::min<uint64_t>((n + 255) / 256, 148ull * 16)), dim3(256), args, 0, st);
+}
+
 void launch_verify_jit(cudaKernel_t k, const DevFormula& F, const DevState& S, const DevTiles& T, const int8_t* x,
-                       const float* y, uint8_t* U_update, uint8_t* per_con, cudaStream_t st) {
+                       const float* y, uint8_t* U_update, uint8_t* per_con, cudaStream_t st, const uint8_t* TT) {
     if (T.n_tiles == 0 || S.R == 0) return;
     const int warps = (int)(T.warps ? T.warps : 1);
     const int vtot = (int)(T.vmax + T.rmax);
@@ -418,7 +449,7 @@ void launch_verify_jit(cudaKernel_t k, const DevFormula& F, const DevState& S, c
     uint32_t* unsat = S.unsat;
     void* args[] = {(void*)&T.tiles, &n_tiles, (void*)&T.recs, (void*)&T.vrecs, (void*)&T.tile_vars, (void*)&x,
                     (void*)&y, (void*)&U_update, (void*)&unsat, (void*)&per_con, (void*)&F.orig, &R, &n_bool,
-                    (void*)&F.atom_rowptr, (void*)&F.atom_val64, (void*)&F.atom_rhs64, (void*)&F.atom_strict};
+                    (void*)&F.atom_rowptr, (void*)&F.atom_val64, (void*)&F.atom_rhs64, (void*)&F.atom_strict, (void*)&TT};
     cudaLaunchKernel((const void*)k, dim3(blocks), dim3(warps * 32), args, smem, st);
 }
 

@@ -89,11 +89,25 @@ struct DevTiles {
     uint32_t rmax;               // run variables per tile (Plan::rmax)
     const void* vrecs;           // K5 records (atom ids), tile.pad1 = offset in uint4
 };
+// Slot tables of the symmetric JIT classes (rows: Booleans [0, n_bool), table atom t at nv + t).
+struct DevSlots {
+    uint32_t n_sa = 0, nv = 0;          // table atoms; nv = n_bool + n_real
+    const uint32_t* atoms = nullptr;    // [n_sa] atom ids
+    float* PT = nullptr;                // [nv + n_sa][R] p_true of the row
+    float* PF = nullptr;                // [nv + n_sa][R] p_false
+    float* DD = nullptr;                // [n_sa][R] dd/dz factor
+    double* GU = nullptr;               // [nv + n_sa][R] dE/dp_true of the row (weighted)
+    uint8_t* TT = nullptr;              // [nv + n_sa][R] exact truth of the row (K5)
+};
+void launch_slot_prob(cudaKernel_t k, const DevFormula& F, const DevState& S, const DevSlots& D, float kappa, cudaStream_t st);
+void launch_slot_chain(cudaKernel_t k, const DevFormula& F, const DevState& S, const DevSlots& D, cudaStream_t st);
+void launch_slot_truth(cudaKernel_t k, const DevFormula& F, const DevState& S, const DevSlots& D, const int8_t* x,
+                       const float* y, cudaStream_t st);
 // K5 (JIT-specialised, tiles): exact check over the tiles of T (+ ERWA counters / per_con).
 void launch_verify_jit(cudaKernel_t k, const DevFormula& F, const DevState& S, const DevTiles& T, const int8_t* x,
-                       const float* y, uint8_t* U_update, uint8_t* per_con, cudaStream_t st);
+                       const float* y, uint8_t* U_update, uint8_t* per_con, cudaStream_t st, const uint8_t* TT = nullptr);
 void launch_sweep_jit(cudaKernel_t k, const DevFormula& F, const DevState& S, const DevTiles& T, float kappa,
-                      float wscale, double* terms, uint32_t terms_r, cudaStream_t st);
+                      float wscale, double* terms, uint32_t terms_r, cudaStream_t st, const DevSlots* D = nullptr);
 // row gather for u8 matrices: dst[i][:] = src[idx[i]][:]  (U between original and internal order)
 void launch_gather_rows_u8(uint8_t* dst, const uint8_t* src, const uint32_t* idx, uint32_t rows, uint32_t R,
                            cudaStream_t st);

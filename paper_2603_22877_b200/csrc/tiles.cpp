@@ -29,6 +29,8 @@ constexpr uint32_t kJitMaxNodes = 96;
 constexpr uint32_t kJitMaxRefs = 64;
 constexpr uint32_t kJitMaxClasses = 32;
 constexpr uint64_t kJitMinCons = 32;      // specialise only classes with enough constraints
+constexpr uint32_t kJitMaxNodesSym = 160; // symmetric classes (messages only, no inline atom math)
+constexpr uint32_t kSymMark = 0xFFFFFFF0u;
 }  // namespace
 
 Plan make_plan(const Formula& f, const Built& b, bool enable_jit) {
@@ -43,8 +45,40 @@ Plan make_plan(const Formula& f, const Built& b, bool enable_jit) {
     // 1. kernel classes
     std::map<std::vector<uint32_t>, uint32_t> kc_of;
     std::vector<uint32_t> kcl(C);
+    const char* sym_env = getenv("FSMT_JIT_SYM");        // "0": symmetric classes off (A/B)
+    const bool sym_on = !(sym_env && sym_env[0] == '0');
     for (uint32_t c = 0; c < C; ++c) {
         const Template& t = b.tmpls[b.cons_tmpl[c]];
+        const uint32_t Ls = b.cons_slot_off[c + 1] - b.cons_slot_off[c];
+        if (sym_on && b.cons_sym[c] && Ls >= 2) {
+            const uint32_t kind = b.cons_sym[c] - 1u, kk = kind == 1 ? b.cons_k[c] : 0u;
+            std::vector<uint32_t> key{kSymMark, kind, Ls, kk};
+            auto it = kc_of.find(key);
+            uint32_t k;
+            if (it == kc_of.end()) {
+                k = (uint32_t)p.kclasses.size();
+                kc_of.emplace(key, k);
+                KClass kc;
+                kc.sym = true;
+                kc.sym_kind = kind;
+                kc.sym_L = Ls;
+                kc.sym_k = kk;
+                kc.stmpl = symmetric_template(kind, Ls, kk);
+                kc.tmpl = UINT32_MAX;
+                kc.n_refs = Ls;
+                kc.words = 1 + (Ls + 1) / 2 + (Ls + 31) / 32;   // weight, slot refs, sign bits
+                kc.stride4 = (kc.words + 3) / 4;
+                kc.vstride4 = 1;
+                kc.jit = enable_jit && kc.stmpl.nodes.size() <= kJitMaxNodesSym && Ls <= kJitMaxRefs && kc.stmpl.root >= 0;
+                kc.n_cons = 0;
+                p.kclasses.push_back(kc);
+            } else {
+                k = it->second;
+            }
+            kcl[c] = k;
+            p.kclasses[k].n_cons++;
+            continue;
+        }
         std::vector<uint32_t> key{b.cons_tmpl[c]};
         const uint32_t* ids = b.slot_ids.data() + b.cons_slot_off[c];
         uint32_t refs = 0;
@@ -88,7 +122,8 @@ Plan make_plan(const Formula& f, const Built& b, bool enable_jit) {
     std::vector<uint32_t> idx(p.kclasses.size());
     for (size_t i = 0; i < idx.size(); ++i) idx[i] = (uint32_t)i;
     auto work = [&](uint32_t k) {
-        return p.kclasses[k].n_cons * (uint64_t)(b.tmpls[p.kclasses[k].tmpl].nodes.size() + p.kclasses[k].n_refs);
+        const KClass& K = p.kclasses[k];
+        return K.n_cons * (uint64_t)((K.sym ? K.stmpl : b.tmpls[K.tmpl]).nodes.size() + K.n_refs);
     };
     std::stable_sort(idx.begin(), idx.end(), [&](uint32_t x, uint32_t y) {
         if (p.kclasses[x].jit != p.kclasses[y].jit) return p.kclasses[x].jit;
@@ -116,15 +151,37 @@ Plan make_plan(const Formula& f, const Built& b, bool enable_jit) {
     for (uint32_t& k : kcl) k = ren[k];
     p.n_jit_kclasses = njit;
 
+    // 1b. atoms read through the slot tables (symmetric JIT classes), by first appearance
+    std::vector<int32_t> sym_row(f.n_atoms(), -1);
+    for (uint32_t c = 0; c < C; ++c) {
+        const KClass& K = p.kclasses[kcl[c]];
+        if (!(K.sym && K.jit)) continue;
+        p.has_sym = true;
+        const Template& t = b.tmpls[b.cons_tmpl[c]];
+        const uint32_t* ids = b.slot_ids.data() + b.cons_slot_off[c];
+        for (size_t s = 0; s < t.kinds.size(); ++s)
+            if (t.kinds[s] == 1 && sym_row[ids[s]] < 0) {
+                sym_row[ids[s]] = (int32_t)p.sym_atoms.size();
+                p.sym_atoms.push_back(ids[s]);
+            }
+    }
+
     // 2. footprint groups by first-appearance batches
     const uint32_t NV = f.n_bool + f.n_real;
-    std::vector<uint32_t> group(NV, UINT32_MAX);
+    std::vector<uint32_t> group(NV + p.sym_atoms.size(), UINT32_MAX);
     uint32_t cur_group = 0, cur_size = 0;
     std::vector<uint32_t> batch;
+    // variables of constraint c in reference order; a symmetric JIT class's references are its
+    // slots' table rows (Boolean i -> i, table atom t -> NV + t)
     auto cons_vars = [&](uint32_t c, std::vector<uint32_t>& out) {
         out.clear();
         const Template& t = b.tmpls[b.cons_tmpl[c]];
         const uint32_t* ids = b.slot_ids.data() + b.cons_slot_off[c];
+        const KClass& K = p.kclasses[kcl[c]];
+        if (K.sym && K.jit) {
+            for (size_t s = 0; s < t.kinds.size(); ++s) out.push_back(t.kinds[s] == 0 ? ids[s] : NV + (uint32_t)sym_row[ids[s]]);
+            return;
+        }
         for (size_t s = 0; s < t.kinds.size(); ++s) {
             if (t.kinds[s] == 0) out.push_back(ids[s]);
             else
@@ -264,6 +321,23 @@ Plan make_plan(const Formula& f, const Built& b, bool enable_jit) {
             rloc.insert(rloc.end(), addr.begin(), addr.end());
             // record
             const uint32_t c = p.order[i];
+            if (K.sym) {
+                // weight, one table-row ref per slot, then the slots' literal signs (1 = negated)
+                std::vector<uint32_t> rec(K.stride4 * 4, 0);
+                float w = b.cons_w[c];
+                memcpy(&rec[0], &w, 4);
+                const uint32_t L = K.n_refs, so = b.cons_slot_off[c];
+                for (uint32_t r = 0; r < L; ++r) {
+                    const uint32_t l = K.stream[r] ? index_of(sloc, vars[r]) : index_of(rloc, vars[r]);
+                    rec[1 + r / 2] |= (l & 0xFFFFu) << (16 * (r % 2));
+                    rec[1 + (L + 1) / 2 + r / 32] |= (uint32_t)(b.slot_neg[so + r] != 0) << (r % 32);
+                }
+                p.recs.insert(p.recs.end(), rec.begin(), rec.end());
+                p.vrecs.insert(p.vrecs.end(), (size_t)K.vstride4 * 4, 0u);
+                ++T.n_cons;
+                ++i;
+                continue;
+            }
             const Template& t = b.tmpls[K.tmpl];
             const uint32_t* ids = b.slot_ids.data() + b.cons_slot_off[c];
             std::vector<uint32_t> rec(K.stride4 * 4, 0);
@@ -475,14 +549,15 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
          "    float* __restrict__ accs, const float* __restrict__ a, const float* __restrict__ b,\n"
          "    double* __restrict__ ga, double* __restrict__ gb, const unsigned char* __restrict__ U,\n"
          "    u32 R, u64 rr, u32 r, bool live, u32 n_bool, float kq, float dcoef, float wscale, double& objacc,\n"
-         "    double* __restrict__ terms, u32 terms_r, const u32* __restrict__ orig) {\n";
+         "    double* __restrict__ terms, u32 terms_r, const u32* __restrict__ orig,\n"
+         "    const float* __restrict__ PT, const float* __restrict__ PF, double* __restrict__ gu) {\n";
     // refs
-    std::vector<int> ref_kind;      // 0 Boolean, 1 real
+    std::vector<int> ref_kind;      // 0 Boolean, 1 real, 2 slot-table row (symmetric classes)
     std::vector<int> slot_ref0(ns);
     for (size_t s = 0, ai = 0; s < ns; ++s) {
         slot_ref0[s] = (int)ref_kind.size();
-        if (t.kinds[s] == 0) {
-            ref_kind.push_back(0);
+        if (t.kinds[s] == 0 || t.kinds[s] == 2) {
+            ref_kind.push_back(t.kinds[s]);
         } else {
             const uint32_t nz = K.nnz[ai++];
             for (uint32_t k = 0; k < nz; ++k) ref_kind.push_back(1);
@@ -495,16 +570,24 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
     };
     for (size_t i = 0; i < nr; ++i)
         if (!is_stream(i) && alias_of(i) < 0)
-            o << "  u32 cur" << i << " = 0xffffffffu; float val" << i << " = 0.f, acc" << i << " = 0.f;\n";
-    // value of reference i's variable: stream variables are listed in vs, run variables in vr
+            o << "  u32 cur" << i << " = 0xffffffffu; float val" << i << " = 0.f, acc" << i << " = 0.f"
+              << (ref_kind[i] == 2 ? ", vaf" + std::to_string(i) + " = 0.f" : std::string()) << ";\n";
+    // value of reference i's variable: stream variables are listed in vs, run variables in vr;
+    // a table slot reads (p_true, p_false) of its row into (val, vaf)
     auto ld_of = [&](size_t i) {
         const std::string v = is_stream(i) ? "vs" : "vr";
-        return ref_kind[i] == 0 ? "a[(u64)" + v + "[l] * R + rr]" : "b[(u64)(" + v + "[l] - n_bool) * R + rr]";
+        if (ref_kind[i] == 2)
+            return "{ const u64 o_ = (u64)" + v + "[l] * R + rr; val" + std::to_string(i) + " = PT[o_]; vaf" +
+                   std::to_string(i) + " = PF[o_]; }";
+        return "val" + std::to_string(i) + " = " +
+               (ref_kind[i] == 0 ? "a[(u64)" + v + "[l] * R + rr]" : "b[(u64)(" + v + "[l] - n_bool) * R + rr]") + ";";
     };
     // a run accumulator goes straight to the fp64 gradient (one atomic per run)
     auto flush_run = [&](size_t i) {
-        const std::string g = ref_kind[i] == 0 ? "ga + (u64)vr[cur" + std::to_string(i) + "] * R + r"
-                                               : "gb + (u64)(vr[cur" + std::to_string(i) + "] - n_bool) * R + r";
+        const std::string cur = "vr[cur" + std::to_string(i) + "]";
+        const std::string g = ref_kind[i] == 0 ? "ga + (u64)" + cur + " * R + r"
+                            : ref_kind[i] == 2 ? "gu + (u64)" + cur + " * R + r"
+                                               : "gb + (u64)(" + cur + " - n_bool) * R + r";
         return "if (live) atomicAdd(" + g + ", (double)acc" + std::to_string(i) + ");";
     };
     o << "  for (u32 c = 0; c < T.n_cons; ++c, rp += " << K.stride4 << ") {\n";
@@ -523,19 +606,27 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
         if (is_stream(i)) {
             // stream reference: new variable (almost) every constraint; no run register
             o << "    const u32 sl" << i << " = " << ext << ";\n"
-              << "    float val" << i << ";\n    { const u32 l = sl" << i << "; val" << i << " = " << ld << "; }\n";
+              << "    float val" << i << (ref_kind[i] == 2 ? ", vaf" + std::to_string(i) : std::string()) << ";\n    { const u32 l = sl"
+              << i << "; " << ld << " }\n";
         } else {
             o << "    { const u32 l = " << ext << "; if (l != cur" << i << ") { if (cur" << i << " != 0xffffffffu) { "
-              << flush_run(i) << " } cur" << i << " = l; acc" << i << " = 0.f; val" << i << " = " << ld << "; } }\n";
+              << flush_run(i) << " } cur" << i << " = l; acc" << i << " = 0.f; " << ld << " } }\n";
         }
     }
     // slot probabilities
     uint32_t aw = 1 + ((uint32_t)nr + 1) / 2;
     std::vector<uint32_t> coef_word(nr, 0);
+    const uint32_t sign_word = 1 + ((uint32_t)nr + 1) / 2;   // symmetric classes: literal signs
     for (size_t s = 0, ai = 0; s < ns; ++s) {
         if (t.kinds[s] == 0) {
             o << "    const float pt" << s << " = 0.5f * (1.f - val" << slot_ref0[s] << "), pf" << s << " = 0.5f * (1.f + val"
               << slot_ref0[s] << ");\n";
+        } else if (t.kinds[s] == 2) {
+            // negated literal: p_true and p_false of its row swap (Eq.4 / Eq.7 of the literal)
+            const int ri = slot_ref0[s];
+            o << "    const bool sg" << s << " = (" << word(sign_word + (uint32_t)s / 32) << " >> " << s % 32 << ") & 1u;\n"
+              << "    const float pt" << s << " = sg" << s << " ? vaf" << ri << " : val" << ri << ", pf" << s << " = sg" << s
+              << " ? val" << ri << " : vaf" << ri << ";\n";
         } else {
             const uint32_t nnz = K.nnz[ai++];
             o << "    float z" << s << " = -__uint_as_float(" << word(aw) << ");\n";
@@ -692,6 +783,9 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
     for (size_t s = 0; s < ns; ++s) {
         if (t.kinds[s] == 0) {
             accum(slot_ref0[s], "w", "G" + std::to_string(s));
+        } else if (t.kinds[s] == 2) {
+            // dCOP/dp_true of the row = -dCOP/dp_true of a negated literal
+            accum(slot_ref0[s], "w", "(sg" + std::to_string(s) + " ? -G" + std::to_string(s) + " : G" + std::to_string(s) + ")");
         } else {
             o << "    const float gd" << s << " = w * G" << s << " * dd" << s << ";\n";
             size_t ai = 0;
@@ -727,9 +821,11 @@ void emit_verify_class(std::ostringstream& o, uint32_t kid, const KClass& K, con
          "    const u32* __restrict__ vr, const signed char* __restrict__ x, const float* __restrict__ y, unsigned char* __restrict__ U,\n"
          "    unsigned char* __restrict__ per_con, const u32* __restrict__ orig, u32 R, u64 rr, u32 r, bool live,\n"
          "    u32 n_bool, const u32* __restrict__ arow, const double* __restrict__ aval,\n"
-         "    const double* __restrict__ arhs, const unsigned char* __restrict__ astrict) {\n"
+         "    const double* __restrict__ arhs, const unsigned char* __restrict__ astrict,\n"
+         "    const unsigned char* __restrict__ TT) {\n"
          "  u32 cnt = 0u;\n";
-    const uint32_t ref_words = 1 + (K.n_refs + 1) / 2;             // words 1.. hold the refs
+    // words 1.. hold the refs (symmetric classes: then the sign words)
+    const uint32_t ref_words = 1 + (K.n_refs + 1) / 2 + (K.sym ? (K.n_refs + 31) / 32 : 0);
     uint32_t q_needed = 0;                                          // compressed uint4s holding them
     for (uint32_t w = 1; w < ref_words; ++w)
         if (K.wpos[w] >= 0) q_needed = std::max(q_needed, (uint32_t)K.wpos[w] / 4 + 1);
@@ -743,6 +839,12 @@ void emit_verify_class(std::ostringstream& o, uint32_t kid, const KClass& K, con
         return v + "[((" + word(1 + i / 2) + " >> " + std::to_string(16 * (i % 2)) + ") & 0xffffu)]";
     };
     for (size_t s = 0; s < ns; ++s) {
+        if (t.kinds[s] == 2) {   // table slot: truth of the row (fsmt_kt_jit) xor the literal's sign
+            o << "    const bool t" << s << " = (TT[(u64)" << ext(ref) << " * R + rr] != 0) != (bool)((" << word(1 + ((uint32_t)ns + 1) / 2 + (uint32_t)s / 32)
+              << " >> " << s % 32 << ") & 1u);\n";
+            ++ref;
+            continue;
+        }
         if (t.kinds[s] == 0) {
             o << "    const bool t" << s << " = x[(u64)" << ext(ref) << " * R + rr] == (signed char)-1;\n";
             ++ref;
@@ -785,7 +887,8 @@ std::string jit_source(const Formula& f, const Built& b, const Plan& p) {
          "struct TileDesc { u32 kclass, cons_begin, n_cons, var_off, n_vars, rec_off, pad0, pad1; };\n"
       << "#define VMAX " << p.vmax << "\n#define VTOT " << p.vmax + p.rmax << "\n#define WARPS " << p.jit_warps
       << "\n\n" << kErfcPrelude;
-    for (uint32_t k = 0; k < p.n_jit_kclasses; ++k) emit_class(o, k, p.kclasses[k], b.tmpls[p.kclasses[k].tmpl]);
+    auto tmpl_of = [&](const KClass& K) -> const Template& { return K.sym ? K.stmpl : b.tmpls[K.tmpl]; };
+    for (uint32_t k = 0; k < p.n_jit_kclasses; ++k) emit_class(o, k, p.kclasses[k], tmpl_of(p.kclasses[k]));
     const char* minb = getenv("FSMT_JIT_MINB");      // optional min CTAs/SM (register cap), A/B tuning
     o << "extern \"C\" __global__ void __launch_bounds__(WARPS * 32" << (minb && atoi(minb) > 0 ? std::string(", ") + minb : std::string())
       << ") fsmt_k1_jit(\n"
@@ -793,7 +896,8 @@ std::string jit_source(const Formula& f, const Built& b, const Plan& p) {
          "    const u32* __restrict__ tile_vars, const float* __restrict__ a, const float* __restrict__ b,\n"
          "    double* __restrict__ ga, double* __restrict__ gb, const unsigned char* __restrict__ U,\n"
          "    double* __restrict__ obj, u32 R, u32 n_bool, float kappa, float wscale,\n"
-         "    double* __restrict__ terms, u32 terms_r, const u32* __restrict__ orig) {\n"
+         "    double* __restrict__ terms, u32 terms_r, const u32* __restrict__ orig,\n"
+         "    const float* __restrict__ PT, const float* __restrict__ PF, double* __restrict__ gu) {\n"
          "  extern __shared__ float smem[];\n"
          "  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;\n"
          "  float* acc = smem + warp * (VMAX * 32);                  // stream-variable rows\n"
@@ -816,29 +920,32 @@ std::string jit_source(const Formula& f, const Built& b, const Plan& p) {
          "  const float dcoef = kappa * 0.79788456080286536f;\n"
          "  double objacc = 0.0;\n"
          "  const uint4* rp = recs + T.rec_off;\n"
+         "  bool symt = false;   // symmetric class: the tile's variables are slot-table rows\n"
          "  switch (T.kclass) {\n";
     for (uint32_t k = 0; k < p.n_jit_kclasses; ++k)
         o << "    case " << k << ": kc" << k
-          << "(T, rp, vs, vr, acc + lane, a, b, ga, gb, U, R, rr, r, live, n_bool, kq, dcoef, wscale, objacc, terms, terms_r, orig); break;\n";
+          << "(T, rp, vs, vr, acc + lane, a, b, ga, gb, U, R, rr, r, live, n_bool, kq, dcoef, wscale, objacc, terms, terms_r, orig, PT, PF, gu); "
+          << (p.kclasses[k].sym ? "symt = true; " : "") << "break;\n";
     o << "    default: break;\n  }\n"
          "  __syncwarp();\n"
          "  if (!live) return;\n"
          "  for (u32 l = 0; l < n_s; ++l) {\n"
          "    const u32 g = vs[l];\n"
          "    const double v = (double)acc[l * 32 + lane];\n"
-         "    if (g < n_bool) atomicAdd(ga + (u64)g * R + r, v); else atomicAdd(gb + (u64)(g - n_bool) * R + r, v);\n"
+         "    if (symt) atomicAdd(gu + (u64)g * R + r, v);\n"
+         "    else if (g < n_bool) atomicAdd(ga + (u64)g * R + r, v); else atomicAdd(gb + (u64)(g - n_bool) * R + r, v);\n"
          "  }\n"
          "  atomicAdd(obj + r, objacc);\n"
          "}\n\n";
     // K5: exact verification of the rounded models + ERWA counters over the same tiles
-    for (uint32_t k = 0; k < p.n_jit_kclasses; ++k) emit_verify_class(o, k, p.kclasses[k], b.tmpls[p.kclasses[k].tmpl]);
+    for (uint32_t k = 0; k < p.n_jit_kclasses; ++k) emit_verify_class(o, k, p.kclasses[k], tmpl_of(p.kclasses[k]));
     o << "extern \"C\" __global__ void __launch_bounds__(WARPS * 32) fsmt_k5_jit(\n"
          "    const TileDesc* __restrict__ tiles, u32 n_tiles, const uint4* __restrict__ recs,\n"
          "    const uint4* __restrict__ vrecs, const u32* __restrict__ tile_vars, const signed char* __restrict__ x,\n"
          "    const float* __restrict__ y, unsigned char* __restrict__ U, u32* __restrict__ unsat,\n"
          "    unsigned char* __restrict__ per_con, const u32* __restrict__ orig, u32 R, u32 n_bool,\n"
          "    const u32* __restrict__ arow, const double* __restrict__ aval, const double* __restrict__ arhs,\n"
-         "    const unsigned char* __restrict__ astrict) {\n"
+         "    const unsigned char* __restrict__ astrict, const unsigned char* __restrict__ TT) {\n"
          "  extern __shared__ float smem[];\n"
          "  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;\n"
          "  u32* vs = (u32*)smem + warp * VTOT;\n"
@@ -861,9 +968,63 @@ std::string jit_source(const Formula& f, const Built& b, const Plan& p) {
          "  switch (T.kclass) {\n";
     for (uint32_t k = 0; k < p.n_jit_kclasses; ++k)
         o << "    case " << k << ": cnt = kv" << k
-          << "(T, rp, vp, vs, vr, x, y, U, per_con, orig, R, rr, r, live, n_bool, arow, aval, arhs, astrict); break;\n";
+          << "(T, rp, vp, vs, vr, x, y, U, per_con, orig, R, rr, r, live, n_bool, arow, aval, arhs, astrict, TT); break;\n";
     o << "    default: break;\n  }\n"
          "  if (live && cnt) atomicAdd(unsat + r, cnt);\n"
+         "}\n";
+    // slot tables for the symmetric classes: probabilities of every Boolean and
+    // table atom once per sweep, the row gradients chained back to grad_a / grad_b, and the rows'
+    // exact truth values for K5
+    o << "extern \"C\" __global__ void fsmt_kp_jit(u32 n_bool, u32 nv, u32 n_sa, const u32* __restrict__ satoms,\n"
+         "    const float* __restrict__ a, const float* __restrict__ b, const u32* __restrict__ arow,\n"
+         "    const u32* __restrict__ acol, const float* __restrict__ aval, const float* __restrict__ arhs,\n"
+         "    const float* __restrict__ ainv, u32 R, float kappa, float* __restrict__ PT, float* __restrict__ PF,\n"
+         "    float* __restrict__ DD) {\n"
+         "  const u64 n = (u64)(n_bool + n_sa) * R;\n"
+         "  const float kq = kappa * 0.70710678118654752f, dcoef = kappa * 0.79788456080286536f;\n"
+         "  for (u64 idx = (u64)blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += (u64)gridDim.x * blockDim.x) {\n"
+         "    const u32 row = (u32)(idx / R), r = (u32)(idx % R);\n"
+         "    if (row < n_bool) {                       // Eq.4: p_true = (1 - a)/2\n"
+         "      const float v = a[idx];\n"
+         "      PT[idx] = 0.5f * (1.f - v); PF[idx] = 0.5f * (1.f + v);\n"
+         "    } else {                                  // Eq.7 with the erfc form (R28b)\n"
+         "      const u32 t = row - n_bool, at = satoms[t];\n"
+         "      float z = -arhs[at];\n"
+         "      for (u32 k = arow[at]; k < arow[at + 1]; ++k) z = fmaf(aval[k], b[(u64)acol[k] * R + r], z);\n"
+         "      const float inv = ainv[at], u = kq * z * inv;\n"
+         "      float ez;\n"
+         "      const float e = " << erfc_fn() << "(fabsf(u), ez);\n"
+         "      const u64 o = (u64)(nv + t) * R + r;\n"
+         "      PT[o] = u >= 0.f ? e : 1.f - e; PF[o] = u >= 0.f ? 1.f - e : e;\n"
+         "      DD[(u64)t * R + r] = dcoef * inv * ez;\n"
+         "    }\n"
+         "  }\n"
+         "}\n\n"
+         "extern \"C\" __global__ void fsmt_kc_jit(u32 n_bool, u32 nv, u32 n_sa, const u32* __restrict__ satoms,\n"
+         "    const u32* __restrict__ arow, const u32* __restrict__ acol, const float* __restrict__ aval, u32 R,\n"
+         "    const double* __restrict__ gu, const float* __restrict__ DD, double* __restrict__ ga, double* __restrict__ gb) {\n"
+         "  const u32 r = blockIdx.x * blockDim.x + threadIdx.x;\n"
+         "  if (r >= R) return;\n"
+         "  for (u32 i = 0; i < n_bool; ++i) ga[(u64)i * R + r] += gu[(u64)i * R + r];\n"
+         "  for (u32 t = 0; t < n_sa; ++t) {               // dE/db_j = sum over rows of G dd q_j (P:1326-1327)\n"
+         "    const double g = gu[(u64)(nv + t) * R + r] * (double)DD[(u64)t * R + r];\n"
+         "    const u32 at = satoms[t];\n"
+         "    for (u32 k = arow[at]; k < arow[at + 1]; ++k) gb[(u64)acol[k] * R + r] += g * (double)aval[k];\n"
+         "  }\n"
+         "}\n\n"
+         "extern \"C\" __global__ void fsmt_kt_jit(u32 n_bool, u32 nv, u32 n_sa, const u32* __restrict__ satoms,\n"
+         "    const signed char* __restrict__ x, const float* __restrict__ y, const u32* __restrict__ arow,\n"
+         "    const u32* __restrict__ acol, const double* __restrict__ aval, const double* __restrict__ arhs,\n"
+         "    const unsigned char* __restrict__ astrict, u32 R, unsigned char* __restrict__ TT) {\n"
+         "  const u64 n = (u64)(n_bool + n_sa) * R;\n"
+         "  for (u64 idx = (u64)blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += (u64)gridDim.x * blockDim.x) {\n"
+         "    const u32 row = (u32)(idx / R), r = (u32)(idx % R);\n"
+         "    if (row < n_bool) { TT[idx] = x[idx] == (signed char)-1; continue; }\n"
+         "    const u32 t = row - n_bool, at = satoms[t];\n"
+         "    double s = 0.0;                           // exact check (R22): fp64, stored order, no FMA\n"
+         "    for (u32 k = arow[at]; k < arow[at + 1]; ++k) s = __dadd_rn(s, __dmul_rn(aval[k], (double)y[(u64)acol[k] * R + r]));\n"
+         "    TT[(u64)(nv + t) * R + r] = astrict[at] ? (s < arhs[at]) : (s <= arhs[at]);\n"
+         "  }\n"
          "}\n";
     (void)f;
     return o.str();

@@ -131,13 +131,9 @@ int compile_expr(const Formula& f, uint32_t v, const SlotMap& sm, Mgr& m) {
     return acc;
 }
 
-int compile_symmetric(const Formula& f, const Constraint& c, const SlotMap& sm, Mgr& m) {
-    std::vector<int> lit(c.lit_n);
-    for (uint32_t t = 0; t < c.lit_n; ++t) {
-        const Lit& l = f.lits[c.lit_first + t];
-        lit[t] = m.var(sm.pos.at(((uint64_t)l.kind << 32) | l.idx), l.neg != 0);
-    }
-    switch (c.kind) {
+// Symmetric constraint over literal diagrams lit[0..L) (slot order): OR, CARD (#true <= k), NAE, XOR.
+int combine_symmetric(Mgr& m, uint32_t kind, uint32_t k, const std::vector<int>& lit) {
+    switch (kind) {
         case K_OR: {
             int acc = 0;
             for (int x : lit) acc = m.apply(Mgr::OR, acc, x);
@@ -157,7 +153,6 @@ int compile_symmetric(const Formula& f, const Constraint& c, const SlotMap& sm, 
             return m.neg(m.apply(Mgr::OR, all_t, all_f));
         }
         default: {                                     // CARD: #true <= k (count DP, saturating at k+1)
-            uint32_t k = c.k;
             std::vector<int> S(k + 2, 0);
             S[0] = 1;
             for (int x : lit) {
@@ -174,6 +169,15 @@ int compile_symmetric(const Formula& f, const Constraint& c, const SlotMap& sm, 
             return m.neg(S[k + 1]);
         }
     }
+}
+
+int compile_symmetric(const Formula& f, const Constraint& c, const SlotMap& sm, Mgr& m) {
+    std::vector<int> lit(c.lit_n);
+    for (uint32_t t = 0; t < c.lit_n; ++t) {
+        const Lit& l = f.lits[c.lit_first + t];
+        lit[t] = m.var(sm.pos.at(((uint64_t)l.kind << 32) | l.idx), l.neg != 0);
+    }
+    return combine_symmetric(m, c.kind, c.k, lit);
 }
 
 // Canonical numbering (R7) of the diagram rooted at `root` (manager ids).
@@ -218,6 +222,17 @@ std::string template_key(const Template& t) {
     k += std::to_string(t.root);
     return k;
 }
+
+}  // namespace
+
+Template symmetric_template(uint32_t kind, uint32_t L, uint32_t k) {
+    Mgr m(1u << 21);
+    std::vector<int> lit(L);
+    for (uint32_t t = 0; t < L; ++t) lit[t] = m.var(t, false);
+    return canonicalise(m, combine_symmetric(m, kind, k, lit), std::vector<uint8_t>(L, 2));
+}
+
+namespace {
 
 bool unit_holds(const Formula& f, uint32_t atom, bool positive, float y) {
     uint32_t r0 = f.atom_rowptr[atom];

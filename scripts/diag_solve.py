@@ -73,6 +73,8 @@ def main():
                     "bins_over_area_1": int((area > 1.0).sum()),
                     "violated_nonoverlap": int((viol < M * (M - 1) // 2).sum()),
                     "violated_bounds": int((viol >= M * (M - 1) // 2).sum())})
+    cons_lines = [ln for ln in inst.text.splitlines() if ln[:2] in ("c ", "e ")]
+    out["violated_lines"] = [cons_lines[i][:120] for i in viol[:12]]
     print(json.dumps(out))
 
 
