@@ -423,7 +423,7 @@ fsmt_status fsmt_build_xbdd(fsmt_ctx* ctx, uint64_t node_budget) {
             ctx->T.recs = rp;
             ctx->T.tile_vars = vp;
             ctx->T.warps = P.jit_warps;
-            ctx->T.vmax = P.vmax;
+            ctx->T.vmax = P.kernel_vmax();
             ctx->T.rmax = P.rmax;
             const uint32_t* vr = nullptr;
             s = upload(ctx, P.vrecs, vr, ctx->fallocs);

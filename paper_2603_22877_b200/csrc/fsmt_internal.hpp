@@ -154,6 +154,9 @@ struct Plan {
     // is n_bool + n_real + t (rows [0, n_bool) are the Booleans, the real rows are unused)
     std::vector<uint32_t> sym_atoms;
     bool has_sym = false;
+    uint32_t vmax_sym = 128;          // stream rows of symmetric-class tiles (FSMT_TILE_VMAX_SYM)
+    // shared-memory rows per warp of the JIT sweep: the largest tile limit in use
+    uint32_t kernel_vmax() const { return has_sym ? std::max(vmax, vmax_sym) : vmax; }
 };
 
 Plan make_plan(const Formula& f, const Built& b, bool enable_jit);

@@ -40,6 +40,7 @@ Plan make_plan(const Formula& f, const Built& b, bool enable_jit) {
     if (const char* v = getenv("FSMT_TILE_CMAX")) p.cmax = (uint32_t)std::max(1, std::min(1024, atoi(v)));
     if (const char* v = getenv("FSMT_TILE_RMAX")) p.rmax = (uint32_t)std::max(16, std::min(1024, atoi(v)));
     p.group = p.vmax;
+    if (const char* v = getenv("FSMT_TILE_VMAX_SYM")) p.vmax_sym = (uint32_t)std::max(16, std::min(512, atoi(v)));
     if (const char* v = getenv("FSMT_TILE_GROUP")) p.group = (uint32_t)std::max(8, std::min(1024, atoi(v)));
     const uint32_t C = (uint32_t)b.cons_tmpl.size();
     // 1. kernel classes
@@ -47,10 +48,24 @@ Plan make_plan(const Formula& f, const Built& b, bool enable_jit) {
     std::vector<uint32_t> kcl(C);
     const char* sym_env = getenv("FSMT_JIT_SYM");        // "0": symmetric classes off (A/B)
     const bool sym_on = !(sym_env && sym_env[0] == '0');
+    // a symmetric constraint reads its atoms through the slot tables only when they are shared
+    // (each referenced by >= 2 constraints): unique atoms are cheaper inline
+    std::vector<uint32_t> atom_refs(f.n_atoms(), 0);
+    for (uint32_t c = 0; c < C; ++c) {
+        const Template& t = b.tmpls[b.cons_tmpl[c]];
+        for (size_t s = 0; s < t.kinds.size(); ++s)
+            if (t.kinds[s] == 1) ++atom_refs[b.slot_ids[b.cons_slot_off[c] + s]];
+    }
+    auto sym_ok = [&](uint32_t c) {
+        const Template& t = b.tmpls[b.cons_tmpl[c]];
+        for (size_t s = 0; s < t.kinds.size(); ++s)
+            if (t.kinds[s] == 1 && atom_refs[b.slot_ids[b.cons_slot_off[c] + s]] < 2) return false;
+        return true;
+    };
     for (uint32_t c = 0; c < C; ++c) {
         const Template& t = b.tmpls[b.cons_tmpl[c]];
         const uint32_t Ls = b.cons_slot_off[c + 1] - b.cons_slot_off[c];
-        if (sym_on && b.cons_sym[c] && Ls >= 2) {
+        if (sym_on && b.cons_sym[c] && Ls >= 2 && sym_ok(c)) {
             const uint32_t kind = b.cons_sym[c] - 1u, kk = kind == 1 ? b.cons_k[c] : 0u;
             std::vector<uint32_t> key{kSymMark, kind, Ls, kk};
             auto it = kc_of.find(key);
@@ -316,7 +331,7 @@ Plan make_plan(const Formula& f, const Built& b, bool enable_jit) {
                     addr.push_back(u);
                 }
             }
-            if (sloc.size() + adds.size() > p.vmax || rloc.size() + addr.size() > p.rmax) break;
+            if (sloc.size() + adds.size() > (K.sym ? p.vmax_sym : p.vmax) || rloc.size() + addr.size() > p.rmax) break;
             sloc.insert(sloc.end(), adds.begin(), adds.end());
             rloc.insert(rloc.end(), addr.begin(), addr.end());
             // record
@@ -885,7 +900,7 @@ std::string jit_source(const Formula& f, const Built& b, const Plan& p) {
     o << "// generated by fsmt tiles.cpp: specialised K1 sweep for " << p.n_jit_kclasses << " kernel classes\n"
          "typedef unsigned int u32;\ntypedef unsigned long long u64;\n"
          "struct TileDesc { u32 kclass, cons_begin, n_cons, var_off, n_vars, rec_off, pad0, pad1; };\n"
-      << "#define VMAX " << p.vmax << "\n#define VTOT " << p.vmax + p.rmax << "\n#define WARPS " << p.jit_warps
+      << "#define VMAX " << p.kernel_vmax() << "\n#define VTOT " << p.kernel_vmax() + p.rmax << "\n#define WARPS " << p.jit_warps
       << "\n\n" << kErfcPrelude;
     auto tmpl_of = [&](const KClass& K) -> const Template& { return K.sym ? K.stmpl : b.tmpls[K.tmpl]; };
     for (uint32_t k = 0; k < p.n_jit_kclasses; ++k) emit_class(o, k, p.kclasses[k], tmpl_of(p.kclasses[k]));
