@@ -52,6 +52,7 @@ class Params:
     erwa_mode: int = 0           # 0: Alg.2 verbatim (h <- 1); 1: reset-to-0 reading (R18)
     eta_mode: int = 0            # 0 eta; 1 eta/kappa; 2 eta/kappa^2; 3 eta for a, eta/kappa^2 for b (R13)
     proj_iters: int = 0          # 0: R15 interval clamps; > 0: Prop.1 QP by that many Dykstra sweeps (R33)
+    n_roundings: int = 1         # R34: draws of R(a) per stage with Philox rounding; the best one is kept
 
 
 # ----------------------------------------------------------------------------- projection bounds
@@ -154,7 +155,9 @@ def round_sign(a):
 
 
 def round_philox(a, seed, r, t):
-    """Randomised rounding R(a) (Eq.4; reading R17): -1 iff a < 1 - k 2^-23."""
+    """Randomised rounding R(a) (Eq.4; reading R17): -1 iff a < 1 - k 2^-23.
+
+    t is the Philox stage word: stage t's m-th draw (R34) uses t + (m << 16)."""
     x = np.empty(len(a), dtype=np.int8)
     for i, ai in enumerate(a):
         k = philox.draw24(seed, r, i, t, philox.TAG_ROUND)
@@ -220,9 +223,18 @@ def solve_restart(f, seed, r, params: Params, lo=None, hi=None):
                 break
             a, b = a2, b2
             taken += 1
-        x = round_sign(a) if params.rounding == "sign" else round_philox(a, seed, r, t)
         y = np.asarray(b, dtype=np.float32)
-        u = violations(f, x, y)
+        if params.rounding == "sign":
+            x = round_sign(a)
+            u = violations(f, x, y)
+        else:
+            # R34: n_roundings draws of R(a), the first with the fewest violations kept
+            x, u = None, None
+            for m in range(max(1, params.n_roundings)):
+                xm = round_philox(a, seed, r, t + (m << 16))
+                um = violations(f, xm, y)
+                if u is None or um.sum() < u.sum():
+                    x, u = xm, um
         n_unsat = int(u.sum())
         for c in range(C_n):
             h[c] = RHO * h[c] + u[c]

@@ -577,3 +577,27 @@ def test_grouped_sparse_path_matches_enumeration(name):
     assert abs(C1 - C2) < 1e-10 * max(1, abs(C1))
     assert np.allclose(ga1, ga2, atol=1e-12) and np.allclose(gb1, gb2, atol=1e-12)
     assert all(abs(t1[i] - t2[i]) < 1e-13 for i in t1)
+
+
+def test_multiple_roundings_reading_r34():
+    """R34: with n_roundings = M the stage keeps the first of M Philox draws with the fewest
+    violations; M = 1 is the single draw of R17 (draw m uses stage word t + (m << 16))."""
+    inst = fsmt_gen.config("cfg1")
+    f = hsmt.parse(inst.text)
+    lo, hi = solve.bounds(f)
+    base = solve.Params(rounding="philox", steps=3, kappas=[0.5, 1.0, 1.5])
+    r1 = solve.solve_restart(f, 7, 3, base, lo, hi)
+    base.n_roundings = 1
+    assert solve.solve_restart(f, 7, 3, base, lo, hi).history == r1.history
+    # the M-draw stage-1 choice equals the brute-force minimum over the M draws
+    a, b = solve.init_point(f, 7, 3, lo, hi)
+    w = [c.weight for c in f.constraints]
+    for _ in range(3):
+        a, b, _, _ = solve.pgd_step(f, a, b, 0.5, w, base.eta, lo, hi)
+    y = np.asarray(b, dtype=np.float32)
+    draws = [solve.violations(f, solve.round_philox(a, 7, 3, 1 + (m << 16)), y).sum() for m in range(6)]
+    assert draws[0] == solve.violations(f, solve.round_philox(a, 7, 3, 1), y).sum()
+    base.n_roundings = 6
+    base.kappas = [0.5]
+    res = solve.solve_restart(f, 7, 3, base, lo, hi)
+    assert res.history[0][2] == min(draws)
