@@ -48,6 +48,7 @@ struct fsmt_ctx {
     std::vector<float> kappas;
     float eta = 0.05f, eps = 1e-2f;
     uint32_t rounding = FSMT_ROUND_SIGN, erwa_mode = FSMT_ERWA_VERBATIM, eta_mode = 0;
+    uint32_t n_roundings = 1;          // R34
     double time_limit = 0.0;
     // run
     uint64_t seed = 0;
@@ -509,6 +510,7 @@ fsmt_status fsmt_set_params(fsmt_ctx* ctx, const fsmt_params* p) {
         ctx->eta = 0.05f;
         ctx->eps = 1e-2f;
         ctx->rounding = FSMT_ROUND_SIGN;
+        ctx->n_roundings = 1;
         ctx->erwa_mode = FSMT_ERWA_VERBATIM;
         ctx->eta_mode = 0;
         ctx->F.proj_iters = 0;
@@ -523,8 +525,9 @@ fsmt_status fsmt_set_params(fsmt_ctx* ctx, const fsmt_params* p) {
     } else {
         default_kappas(ctx->kappas);
     }
-    if (p->rounding > 1 || p->erwa_mode > 1 || p->eta_mode > 3 || p->proj_iters > 100000)
-        return fail(ctx, FSMT_ERR_ARG, "bad rounding / erwa_mode / eta_mode / proj_iters");
+    if (p->rounding > 1 || p->erwa_mode > 1 || p->eta_mode > 3 || p->proj_iters > 100000 || p->n_roundings > 4096)
+        return fail(ctx, FSMT_ERR_ARG, "bad rounding / erwa_mode / eta_mode / proj_iters / n_roundings");
+    ctx->n_roundings = std::max<uint32_t>(1, p->n_roundings);
     ctx->F.proj_iters = p->proj_iters;
     ctx->eta = p->eta > 0 ? p->eta : 0.05f;
     ctx->eps = p->eps > 0 ? p->eps : 1e-2f;
@@ -570,6 +573,11 @@ fsmt_status fsmt_begin(fsmt_ctx* ctx, uint32_t R, uint64_t seed, uint32_t restar
             drop_state(ctx);
             return s;
         }
+    }
+    if ((s = alloc((void**)&S.x_best, nb)) || (s = alloc((void**)&S.unsat_m, (size_t)R * 4)) ||
+        (s = alloc((void**)&S.unsat_best, (size_t)R * 4)) || (s = alloc((void**)&S.better, R))) {
+        drop_state(ctx);
+        return s;
     }
     S.bn = S.ph = S.pb = nullptr;
     if (F.n_half) {   // R33 projection buffers (small: halfspace variables only, plus the candidate b)
@@ -723,28 +731,49 @@ static fsmt_status update_impl(fsmt_ctx* ctx, float eta, float eps, float eta_b 
     return check_launch(ctx);
 }
 
-static fsmt_status stage_end_impl(fsmt_ctx* ctx, uint32_t stage_t) {
-    const DevState& S = ctx->S;
-    CK(cudaMemsetAsync(S.unsat, 0, (size_t)S.R * 4, ctx->stream));
-    {
-        Timed tm(ctx, 2);
-        launch_round(ctx->F, S, ctx->rounding, ctx->seed, ctx->restart_offset, stage_t, ctx->stream);
-        ctx->launches += 1;
-        if (ctx->T.n_tiles && ctx->jit.kernel5) {    // specialised check of this context's tiles
-            if (ctx->has_sym) {
-                launch_slot_truth(ctx->jit.ktruth, ctx->F, S, ctx->slots, S.x, S.b, ctx->stream);
+// K5 over this context's constraints for the rounded model in S2.x (unsat into S2.unsat)
+static void verify_rounded(fsmt_ctx* ctx, const DevState& S2, uint8_t* U_update) {
+    if (ctx->T.n_tiles && ctx->jit.kernel5) {    // specialised check of this context's tiles
+        if (ctx->has_sym) {
+            launch_slot_truth(ctx->jit.ktruth, ctx->F, S2, ctx->slots, S2.x, S2.b, ctx->stream);
+            ctx->launches += 1;
+        }
+        launch_verify_jit(ctx->jit.kernel5, ctx->F, S2, ctx->T, S2.x, S2.b, U_update, nullptr, ctx->stream, ctx->slots.TT);
+        launch_verify(ctx->F, S2, S2.x, S2.b, U_update, nullptr, ctx->stream, ctx->F.generic_begin, ctx->F.generic_end);
+        ctx->launches += 2;
+    } else {
+        for (int k = 0; k < 2; ++k)             // the constraint ranges this context owns
+            if (ctx->vrange[k][1] > ctx->vrange[k][0]) {
+                launch_verify(ctx->F, S2, S2.x, S2.b, U_update, nullptr, ctx->stream, ctx->vrange[k][0], ctx->vrange[k][1]);
                 ctx->launches += 1;
             }
-            launch_verify_jit(ctx->jit.kernel5, ctx->F, S, ctx->T, S.x, S.b, S.U, nullptr, ctx->stream, ctx->slots.TT);
-            launch_verify(ctx->F, S, S.x, S.b, S.U, nullptr, ctx->stream, ctx->F.generic_begin, ctx->F.generic_end);
-            ctx->launches += 2;
+    }
+}
+
+static fsmt_status stage_end_impl(fsmt_ctx* ctx, uint32_t stage_t) {
+    const DevState& S = ctx->S;
+    const uint32_t M = ctx->rounding == FSMT_ROUND_PHILOX ? ctx->n_roundings : 1;
+    if (M > 1 && ctx->shard_mode != 0)
+        return fail(ctx, FSMT_ERR_STATE, "n_roundings > 1 needs the unsharded mode (the choice needs global counts)");
+    {
+        Timed tm(ctx, 2);
+        if (M > 1) {   // R34: M draws of R(a), keep the one with the fewest violations per restart
+            DevState S2 = S;
+            S2.unsat = S.unsat_m;
+            for (uint32_t m = 0; m < M; ++m) {
+                CK(cudaMemsetAsync(S.unsat_m, 0, (size_t)S.R * 4, ctx->stream));
+                launch_round(ctx->F, S, ctx->rounding, ctx->seed, ctx->restart_offset, stage_t + (m << 16), ctx->stream);
+                verify_rounded(ctx, S2, nullptr);
+                launch_keep_best(ctx->F, S, S.unsat_m, S.unsat_best, S.x_best, S.better, m, ctx->stream);
+                ctx->launches += 3;
+            }
+            CK(cudaMemcpyAsync(S.x, S.x_best, (size_t)ctx->F.n_bool * S.R, cudaMemcpyDeviceToDevice, ctx->stream));
         } else {
-            for (int k = 0; k < 2; ++k)             // the constraint ranges this context owns
-                if (ctx->vrange[k][1] > ctx->vrange[k][0]) {
-                    launch_verify(ctx->F, S, S.x, S.b, S.U, nullptr, ctx->stream, ctx->vrange[k][0], ctx->vrange[k][1]);
-                    ctx->launches += 1;
-                }
+            launch_round(ctx->F, S, ctx->rounding, ctx->seed, ctx->restart_offset, stage_t, ctx->stream);
+            ctx->launches += 1;
         }
+        CK(cudaMemsetAsync(S.unsat, 0, (size_t)S.R * 4, ctx->stream));
+        verify_rounded(ctx, S, S.U);
     }
     CK(cudaMemsetAsync(S.frozen, 0, S.R, ctx->stream));
     fsmt_status s = check_launch(ctx);

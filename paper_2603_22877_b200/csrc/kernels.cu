@@ -493,6 +493,29 @@ void launch_project(const DevFormula& F, const DevState& S, float* X, bool skip_
     k_dykstra<<<(S.R + 63) / 64, 64, 0, st>>>(F, S, X, skip_frozen);
 }
 
+__global__ void k_best_flag(uint32_t R, const uint32_t* __restrict__ um, uint32_t* __restrict__ ub, uint8_t* __restrict__ flag,
+                            uint32_t m) {
+    const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= R) return;
+    const bool better = m == 0 || um[r] < ub[r];
+    flag[r] = better;
+    if (better) ub[r] = um[r];
+}
+
+__global__ void k_copy_cols(uint64_t n, uint32_t R, const int8_t* __restrict__ x, int8_t* __restrict__ xb,
+                            const uint8_t* __restrict__ flag) {
+    for (uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += (uint64_t)gridDim.x * blockDim.x)
+        if (flag[idx % R]) xb[idx] = x[idx];
+}
+
+void launch_keep_best(const DevFormula& F, const DevState& S, const uint32_t* unsat_m, uint32_t* unsat_best,
+                      int8_t* x_best, uint8_t* flag, uint32_t m, cudaStream_t st) {
+    if (!S.R) return;
+    k_best_flag<<<(S.R + 255) / 256, 256, 0, st>>>(S.R, unsat_m, unsat_best, flag, m);
+    const uint64_t n = (uint64_t)F.n_bool * S.R;
+    if (n) k_copy_cols<<<(unsigned)std::min<uint64_t>((n + 255) / 256, 148ull * 16), 256, 0, st>>>(n, S.R, S.x, x_best, flag);
+}
+
 void launch_round(const DevFormula& F, const DevState& S, uint32_t rounding, uint64_t seed, uint32_t off,
                   uint32_t stage, cudaStream_t st) {
     const uint64_t n = (uint64_t)F.n_bool * S.R;

@@ -68,6 +68,10 @@ struct DevState {
     float* bn;         // [n_real][R] candidate b of the projected step (R33), or null
     float* ph;         // [nnz of halfspaces][R] Dykstra corrections
     float* pb;         // [n_hvars][R] Dykstra box corrections
+    int8_t* x_best;    // [n_bool][R] best rounding of the stage (R34), or null
+    uint32_t* unsat_m; // [R]
+    uint32_t* unsat_best;  // [R]
+    uint8_t* better;   // [R]
 };
 
 int sweep_smem_bytes(const DevFormula& F, int warps);
@@ -120,6 +124,10 @@ void launch_update(const DevFormula& F, const DevState& S, float eta, float eps,
 // Dykstra projection (R33) of X [n_real][R] in place: F.proj_iters sweeps over the halfspaces then
 // the box, per restart (skips frozen restarts when skip_frozen).
 void launch_project(const DevFormula& F, const DevState& S, float* X, bool skip_frozen, cudaStream_t st);
+// R34: keep, per restart, the rounding with the fewest violations: restarts whose unsat_m beats
+// unsat_best (or m == 0) copy x into x_best.
+void launch_keep_best(const DevFormula& F, const DevState& S, const uint32_t* unsat_m, uint32_t* unsat_best,
+                      int8_t* x_best, uint8_t* flag, uint32_t m, cudaStream_t st);
 // K4: rounding (R17).
 void launch_round(const DevFormula& F, const DevState& S, uint32_t rounding, uint64_t seed, uint32_t restart_offset,
                   uint32_t stage, cudaStream_t st);

@@ -33,7 +33,8 @@ class Dims(C.Structure):
 class Params(C.Structure):
     _fields_ = [("kappas", C.POINTER(C.c_float)), ("n_stages", C.c_uint32), ("eta", C.c_float), ("eps", C.c_float),
                 ("rounding", C.c_uint32), ("erwa_mode", C.c_uint32), ("time_limit_s", C.c_double),
-                ("eta_mode", C.c_uint32), ("proj_iters", C.c_uint32)]
+                ("eta_mode", C.c_uint32), ("proj_iters", C.c_uint32),
+                ("n_roundings", C.c_uint32)]
 
 
 class Stats(C.Structure):

@@ -82,7 +82,7 @@ class Solver:
 
     # ---------------------------------------------------------------- solve
     def set_params(self, kappas=None, eta=0.0, eps=0.0, rounding=N.ROUND_SIGN, erwa_mode=N.ERWA_VERBATIM,
-                   time_limit_s=0.0, eta_mode=0, proj_iters=0):
+                   time_limit_s=0.0, eta_mode=0, proj_iters=0, n_roundings=1):
         p = N.Params()
         if kappas is not None:
             self._kappas = np.ascontiguousarray(kappas, dtype=np.float32)
@@ -91,6 +91,7 @@ class Solver:
         p.eta, p.eps, p.rounding, p.erwa_mode, p.time_limit_s = eta, eps, rounding, erwa_mode, time_limit_s
         p.eta_mode = eta_mode
         p.proj_iters = proj_iters
+        p.n_roundings = n_roundings
         self._check(N.lib.fsmt_set_params(self._h, C.byref(p)))
 
     def solve(self, restarts: int, steps: int, seed: int) -> SolveResult:

@@ -42,6 +42,7 @@ def main():
     p.add_argument("--rounding", type=int, nargs="+", default=[0])
     p.add_argument("--eta-modes", type=int, nargs="+", default=[0])
     p.add_argument("--proj-iters", type=int, nargs="+", default=[0])
+    p.add_argument("--n-roundings", type=int, nargs="+", default=[1])
     p.add_argument("--time-limit", type=float, default=120.0)
     p.add_argument("--only", default="")
     a = p.parse_args()
@@ -55,10 +56,13 @@ def main():
     sch = schedules(a.kmax, a.stages, a.holds)
     if a.only:
         sch = {k: v for k, v in sch.items() if k in a.only.split(",")}
-    for (name, ks), steps, eta, erwa, rnd, em, pi in itertools.product(sch.items(), a.steps, a.etas, a.erwa, a.rounding,
-                                                                        a.eta_modes, a.proj_iters):
+    for (name, ks), steps, eta, erwa, rnd, em, pi, nr in itertools.product(sch.items(), a.steps, a.etas, a.erwa,
+                                                                            a.rounding, a.eta_modes, a.proj_iters,
+                                                                            a.n_roundings):
+        if nr > 1 and rnd == 0:
+            continue
         s.set_params(kappas=ks, eta=eta, erwa_mode=erwa, rounding=rnd, time_limit_s=a.time_limit, eta_mode=em,
-                     proj_iters=pi)
+                     proj_iters=pi, n_roundings=nr)
         solved, times, best = 0, [], []
         t0 = time.perf_counter()
         for seed in a.seeds:
@@ -68,7 +72,7 @@ def main():
             times.append(res.stats["solve_ms"] / 1e3)
             best.append(res.stats["best_unsat"])
         print(json.dumps({"config": a.config, "schedule": name, "steps": steps, "eta": eta, "erwa": erwa,
-                          "rounding": rnd, "eta_mode": em, "proj_iters": pi, "solved": solved, "runs": len(a.seeds), "best_unsat": best,
+                          "rounding": rnd, "eta_mode": em, "proj_iters": pi, "n_roundings": nr, "solved": solved, "runs": len(a.seeds), "best_unsat": best,
                           "solve_s": [round(x, 3) for x in times], "wall_s": round(time.perf_counter() - t0, 2)}),
               flush=True)
 

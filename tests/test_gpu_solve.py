@@ -133,3 +133,45 @@ def test_cfg4_placement_time_to_sat():
     y = np.asarray(res.y, dtype=np.float32)
     bad = [kept[ci] for ci, c in enumerate(f.constraints) if not semantics.constraint_sat(f, c, x, y)]
     assert len(kept) == 20000 and not bad, bad[:10]
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg4s"])
+def test_multiple_roundings_r34_match_oracle(name):
+    """R34: with n_roundings = M each restart keeps the first of its M Philox draws with the
+    fewest violations; the kept model, its unsat count and the ERWA counters match the oracle."""
+    from oracle import solve as osolve
+    inst = fsmt_gen.config(name)
+    f = hsmt.parse(inst.text)
+    M, R, seed = 6, 70, 9
+    s = make(inst.text)
+    s.set_params(eta=0.05, eps=1e-12, rounding=1, n_roundings=M)
+    s.begin(R, seed)
+    for _ in range(3):
+        s.sweep(1.0, 2)
+        s.update(0.05, 1e-12)
+    a, b = s.get_state()
+    unsat = s.stage_end(2)
+    x = s.get_rounded()
+    U = s.get_counters()
+    y = b.astype(np.float32)
+    for r in range(0, R, 7):
+        best = None
+        for m in range(M):
+            xm = osolve.round_philox(a[:, r].astype(np.float64), seed, r, 2 + (m << 16))
+            um = osolve.violations(f, xm, y[:, r])
+            if best is None or um.sum() < best[1].sum():
+                best = (xm, um)
+        assert np.array_equal(x[:, r], best[0]), r
+        assert unsat[r] == best[1].sum()
+        assert np.array_equal(U[:, r].astype(int), best[1])
+
+
+def test_multiple_roundings_solve_sound():
+    inst = fsmt_gen.config("cfg4s")
+    f = hsmt.parse(inst.text)
+    s = make(inst.text)
+    s.set_params(eta=0.05, rounding=1, n_roundings=4)
+    res = s.solve(256, 20, 5)
+    _, sat = semantics.eval_formula(f, res.x, res.y)
+    assert (res.verdict == 10) == all(sat)
+    assert sum(not v for v in sat) == res.stats["best_unsat"]
