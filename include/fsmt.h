@@ -79,7 +79,9 @@ typedef struct {
                                   clamps from single-variable unit atoms; multi-variable unit atoms stay
                                   soft); N > 0 = R33: the QP with every unit atom, by N sweeps of Dykstra's
                                   algorithm over the halfspaces g.b <= h then the box, at init and after every
-                                  gradient step (<= 100000; FSMT_ERR_ARG above) */
+                                  gradient step (<= 100000; FSMT_ERR_ARG above; fsmt_begin fails with
+                                  FSMT_ERR_ARG when the halfspace variables and corrections exceed the 227 KB
+                                  of shared memory of one CTA) */
     uint32_t n_roundings;      /* R34 (FSMT_ROUND_PHILOX only): draws of R(a) per stage, the first with the
                                   fewest violated constraints kept per restart (0/1 = one draw; <= 4096);
                                   needs the unsharded mode (fsmt_stage_end fails with FSMT_ERR_STATE) */

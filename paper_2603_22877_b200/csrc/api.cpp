@@ -378,27 +378,55 @@ fsmt_status fsmt_build_xbdd(fsmt_ctx* ctx, uint64_t node_budget) {
     UP(ainv, atom_invnorm);
     UP(b.lo, lo);
     UP(b.hi, hi);
-    {   // R33 halfspaces (multi-variable unit atoms)
-        std::vector<float> hg(b.h_g.begin(), b.h_g.end()), hh(b.h_h.begin(), b.h_h.end()), inv2;
+    {   // R33 halfspaces (multi-variable unit atoms), reordered by dependency level: a halfspace's
+        // level is one more than the last earlier halfspace sharing a variable, so one level's
+        // halfspaces touch disjoint variables and the level-by-level sweep performs exactly the
+        // sequential Dykstra sweep of constraint order (k_dykstra)
+        const size_t K = b.h_rowptr.size() - 1;
         std::vector<uint8_t> in_h(f.n_real, 0);
-        std::vector<uint32_t> hv;
-        for (size_t k = 0; k + 1 < b.h_rowptr.size(); ++k) {
-            double n2 = 0.0;
-            for (uint32_t t = b.h_rowptr[k]; t < b.h_rowptr[k + 1]; ++t) n2 += (double)hg[t] * (double)hg[t];
-            inv2.push_back((float)(1.0 / n2));
-        }
+        std::vector<uint32_t> hv, lidx(f.n_real, 0);
         for (uint32_t j : b.h_col) in_h[j] = 1;
         for (uint32_t j = 0; j < f.n_real; ++j)
-            if (in_h[j]) hv.push_back(j);
-        F.n_half = (uint32_t)(b.h_rowptr.size() - 1);
+            if (in_h[j]) { lidx[j] = (uint32_t)hv.size(); hv.push_back(j); }
+        std::vector<uint32_t> level(K, 0), last(f.n_real, 0);
+        uint32_t n_levels = 0;
+        for (size_t k = 0; k < K; ++k) {
+            uint32_t l = 0;
+            for (uint32_t t = b.h_rowptr[k]; t < b.h_rowptr[k + 1]; ++t) l = std::max(l, last[b.h_col[t]]);
+            level[k] = l;
+            for (uint32_t t = b.h_rowptr[k]; t < b.h_rowptr[k + 1]; ++t) last[b.h_col[t]] = l + 1;
+            n_levels = std::max(n_levels, l + 1);
+        }
+        std::vector<uint32_t> order(K);
+        for (size_t k = 0; k < K; ++k) order[k] = (uint32_t)k;
+        std::stable_sort(order.begin(), order.end(), [&](uint32_t x, uint32_t y) { return level[x] < level[y]; });
+        std::vector<uint32_t> rowptr{0}, lcol, loff(n_levels + 1, 0);
+        std::vector<float> hg, hh, inv2;
+        for (uint32_t k : order) {
+            double n2 = 0.0;
+            for (uint32_t t = b.h_rowptr[k]; t < b.h_rowptr[k + 1]; ++t) {
+                lcol.push_back(lidx[b.h_col[t]]);
+                hg.push_back((float)b.h_g[t]);
+                n2 += (double)(float)b.h_g[t] * (double)(float)b.h_g[t];
+            }
+            rowptr.push_back((uint32_t)lcol.size());
+            hh.push_back((float)b.h_h[k]);
+            inv2.push_back((float)(1.0 / n2));
+            ++loff[level[k] + 1];
+        }
+        for (uint32_t l = 0; l < n_levels; ++l) loff[l + 1] += loff[l];
+        F.n_half = (uint32_t)K;
         F.n_hvars = (uint32_t)hv.size();
-        UP(b.h_rowptr, h_rowptr);
-        UP(b.h_col, h_col);
+        F.n_hlevels = n_levels;
+        F.h_nnz = (uint32_t)lcol.size();
+        UP(rowptr, h_rowptr);
+        UP(lcol, h_col);
         UP(hg, h_g);
         UP(hh, h_h);
         UP(inv2, h_inv2);
         UP(hv, hvars);
         UP(in_h, in_h);
+        UP(loff, h_level_off);
     }
 #undef UP
     s = upload(ctx, P.pos, ctx->d_pos, ctx->fallocs);
@@ -543,6 +571,8 @@ fsmt_status fsmt_begin(fsmt_ctx* ctx, uint32_t R, uint64_t seed, uint32_t restar
     if (s) return s;
     if (ctx->host_only) return fail(ctx, FSMT_ERR_CUDA, "fsmt_begin: host-only context has no device");
     if (R == 0) return fail(ctx, FSMT_ERR_ARG, "restarts must be > 0");
+    if (ctx->F.proj_iters && ctx->F.n_half && project_smem_bytes(ctx->F, ctx->F.h_nnz) > 227 * 1024)
+        return fail(ctx, FSMT_ERR_ARG, "too many multi-variable unit atoms for the on-chip Dykstra projection (R33)");
     cudaSetDevice(ctx->device);
     drop_state(ctx);
     const DevFormula& F = ctx->F;
@@ -579,11 +609,9 @@ fsmt_status fsmt_begin(fsmt_ctx* ctx, uint32_t R, uint64_t seed, uint32_t restar
         drop_state(ctx);
         return s;
     }
-    S.bn = S.ph = S.pb = nullptr;
-    if (F.n_half) {   // R33 projection buffers (small: halfspace variables only, plus the candidate b)
-        const size_t hn = (size_t)ctx->b.h_col.size() * R;
-        if ((s = alloc((void**)&S.bn, nr * 4)) || (s = alloc((void**)&S.ph, hn * 4)) ||
-            (s = alloc((void**)&S.pb, (size_t)F.n_hvars * R * 4))) {
+    S.bn = nullptr;
+    if (F.n_half) {   // R33: the candidate b of the projected step
+        if ((s = alloc((void**)&S.bn, nr * 4))) {
             drop_state(ctx);
             return s;
         }

@@ -195,41 +195,52 @@ __global__ void k3_cand(DevFormula F, DevState S, float eta_b) {
     }
 }
 
-// Dykstra's algorithm per restart (thread = restart; every access is a coalesced row segment):
-// sets C_1..C_K = halfspaces g_k.b <= h_k in order, then C_0 = the box of the halfspace
-// variables, each with its own correction (ph, pb), F.proj_iters sweeps (R33).
-__global__ void k_dykstra(DevFormula F, DevState S, float* __restrict__ X, bool skip_frozen) {
-    const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
-    const uint32_t R = S.R;
-    if (r >= R) return;
+// Dykstra's algorithm (R33), one CTA per restart, the restart's halfspace variables and all
+// corrections in shared memory: sets C_1..C_K = halfspaces g_k.b <= h_k in constraint order,
+// then C_0 = the box of the halfspace variables, F.proj_iters sweeps.  The halfspaces are
+// stored by dependency level (api.cpp): within a level they touch disjoint variables, so the
+// threads of the CTA project them concurrently and the level barrier reproduces the sequential
+// sweep exactly.
+__global__ void __launch_bounds__(128) k_dykstra(DevFormula F, DevState S, float* __restrict__ X, bool skip_frozen) {
+    extern __shared__ float sh[];
+    const uint32_t r = blockIdx.x, R = S.R;
     if (skip_frozen && S.frozen[r]) return;
-    const uint32_t nnz = F.h_rowptr[F.n_half];
-    for (uint32_t k = 0; k < nnz; ++k) S.ph[(size_t)k * R + r] = 0.f;
-    for (uint32_t v = 0; v < F.n_hvars; ++v) S.pb[(size_t)v * R + r] = 0.f;
-    for (uint32_t it = 0; it < F.proj_iters; ++it) {
-        for (uint32_t h = 0; h < F.n_half; ++h) {
-            const uint32_t k0 = F.h_rowptr[h], k1 = F.h_rowptr[h + 1];
-            float v = -F.h_h[h];
-            for (uint32_t k = k0; k < k1; ++k)
-                v = fmaf(F.h_g[k], X[(size_t)F.h_col[k] * R + r] + S.ph[(size_t)k * R + r], v);
-            const float t = fmaxf(v, 0.f) * F.h_inv2[h];
-            for (uint32_t k = k0; k < k1; ++k) {
-                float* xp = X + (size_t)F.h_col[k] * R + r;
-                const float y = *xp + S.ph[(size_t)k * R + r];
-                const float xn = fmaf(-t, F.h_g[k], y);
-                S.ph[(size_t)k * R + r] = y - xn;
-                *xp = xn;
-            }
-        }
-        for (uint32_t v = 0; v < F.n_hvars; ++v) {
-            const uint32_t j = F.hvars[v];
-            float* xp = X + (size_t)j * R + r;
-            const float y = *xp + S.pb[(size_t)v * R + r];
-            const float xn = fminf(fmaxf(y, F.lo[j]), F.hi[j]);
-            S.pb[(size_t)v * R + r] = y - xn;
-            *xp = xn;
-        }
+    const uint32_t nv = F.n_hvars, nnz = F.h_rowptr[F.n_half];
+    float* xs = sh;                 // [nv] iterate
+    float* pb = xs + nv;            // [nv] box corrections
+    float* ph = pb + nv;            // [nnz] halfspace corrections
+    for (uint32_t v = threadIdx.x; v < nv; v += blockDim.x) {
+        xs[v] = X[(size_t)F.hvars[v] * R + r];
+        pb[v] = 0.f;
     }
+    for (uint32_t k = threadIdx.x; k < nnz; k += blockDim.x) ph[k] = 0.f;
+    __syncthreads();
+    for (uint32_t it = 0; it < F.proj_iters; ++it) {
+        for (uint32_t l = 0; l < F.n_hlevels; ++l) {
+            for (uint32_t h = F.h_level_off[l] + threadIdx.x; h < F.h_level_off[l + 1]; h += blockDim.x) {
+                const uint32_t k0 = F.h_rowptr[h], k1 = F.h_rowptr[h + 1];
+                float v = -F.h_h[h];
+                for (uint32_t k = k0; k < k1; ++k) v = fmaf(F.h_g[k], xs[F.h_col[k]] + ph[k], v);
+                const float t = fmaxf(v, 0.f) * F.h_inv2[h];
+                for (uint32_t k = k0; k < k1; ++k) {
+                    const float y = xs[F.h_col[k]] + ph[k];
+                    const float xn = fmaf(-t, F.h_g[k], y);
+                    ph[k] = y - xn;
+                    xs[F.h_col[k]] = xn;
+                }
+            }
+            __syncthreads();
+        }
+        for (uint32_t v = threadIdx.x; v < nv; v += blockDim.x) {
+            const uint32_t j = F.hvars[v];
+            const float y = xs[v] + pb[v];
+            const float xn = fminf(fmaxf(y, F.lo[j]), F.hi[j]);
+            pb[v] = y - xn;
+            xs[v] = xn;
+        }
+        __syncthreads();
+    }
+    for (uint32_t v = threadIdx.x; v < nv; v += blockDim.x) X[(size_t)F.hvars[v] * R + r] = xs[v];
 }
 
 __global__ void k3_norm(DevFormula F, DevState S, float eta, float eta_b) {
@@ -488,9 +499,13 @@ void launch_update(const DevFormula& F, const DevState& S, float eta, float eps,
     k3_apply<<<(unsigned)blocks, 256, 0, st>>>(F, Sp, eta, eta_b);
 }
 
+size_t project_smem_bytes(const DevFormula& F, uint32_t nnz) { return ((size_t)2 * F.n_hvars + nnz) * 4; }
+
 void launch_project(const DevFormula& F, const DevState& S, float* X, bool skip_frozen, cudaStream_t st) {
     if (!F.proj_iters || !F.n_half || S.R == 0) return;
-    k_dykstra<<<(S.R + 63) / 64, 64, 0, st>>>(F, S, X, skip_frozen);
+    const size_t smem = project_smem_bytes(F, F.h_nnz);
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k_dykstra, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_dykstra<<<S.R, 128, smem, st>>>(F, S, X, skip_frozen);
 }
 
 __global__ void k_best_flag(uint32_t R, const uint32_t* __restrict__ um, uint32_t* __restrict__ ub, uint8_t* __restrict__ flag,

@@ -39,14 +39,15 @@ struct DevFormula {
     const uint32_t* orig;           // [C] internal -> original constraint id (constraint arrays and U
                                     //     are in the internal, tile-sorted order; see tiles.cpp)
     // Prop.1 projection with multi-variable unit atoms (R33): halfspaces g.b <= h, Dykstra sweeps
-    uint32_t n_half = 0, n_hvars = 0, proj_iters = 0;
-    const uint32_t* h_rowptr = nullptr;  // [n_half+1]
-    const uint32_t* h_col = nullptr;     // [nnz] real index
+    uint32_t n_half = 0, n_hvars = 0, proj_iters = 0, n_hlevels = 0, h_nnz = 0;
+    const uint32_t* h_rowptr = nullptr;  // [n_half+1], halfspaces in dependency-level order
+    const uint32_t* h_col = nullptr;     // [nnz] index into hvars
     const float* h_g = nullptr;          // [nnz]
     const float* h_h = nullptr;          // [n_half]
     const float* h_inv2 = nullptr;       // [n_half] 1/||g||^2
     const uint32_t* hvars = nullptr;     // [n_hvars] reals in some halfspace (box corrections)
     const uint8_t* in_h = nullptr;       // [n_real] 1 if in some halfspace
+    const uint32_t* h_level_off = nullptr;  // [n_hlevels+1] halfspace range of each level
     uint32_t generic_begin;         // internal [generic_begin, generic_end) run through the generic K1
     uint32_t generic_end;           //   (generic_end < n_cons only in constraint-sharded mode)
 };
@@ -66,8 +67,6 @@ struct DevState {
     double* gm2;       // [R]
     double* gm2_part;  // [n_parts][R]
     float* bn;         // [n_real][R] candidate b of the projected step (R33), or null
-    float* ph;         // [nnz of halfspaces][R] Dykstra corrections
-    float* pb;         // [n_hvars][R] Dykstra box corrections
     int8_t* x_best;    // [n_bool][R] best rounding of the stage (R34), or null
     uint32_t* unsat_m; // [R]
     uint32_t* unsat_best;  // [R]
@@ -124,6 +123,7 @@ void launch_update(const DevFormula& F, const DevState& S, float eta, float eps,
 // Dykstra projection (R33) of X [n_real][R] in place: F.proj_iters sweeps over the halfspaces then
 // the box, per restart (skips frozen restarts when skip_frozen).
 void launch_project(const DevFormula& F, const DevState& S, float* X, bool skip_frozen, cudaStream_t st);
+size_t project_smem_bytes(const DevFormula& F, uint32_t nnz);   // k_dykstra shared memory (<= 227 KB)
 // R34: keep, per restart, the rounding with the fewest violations: restarts whose unsat_m beats
 // unsat_best (or m == 0) copy x into x_best.
 void launch_keep_best(const DevFormula& F, const DevState& S, const uint32_t* unsat_m, uint32_t* unsat_best,
