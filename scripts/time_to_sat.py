@@ -27,10 +27,11 @@ def main():
     p.add_argument("--eta", type=float, default=0.05)
     p.add_argument("--kappas", type=str, default="")
     p.add_argument("--schedule", type=str, default="",
-                   help="geo1-<kmax>[-hold<m>]: <stages> geometric kappas 1..kmax, then kmax m*<stages> more times")
+                   help="geo<kmin>-<kmax>[-hold<m>]: <stages> geometric kappas kmin..kmax, then kmax m*<stages> more times")
     p.add_argument("--stages", type=int, default=20)
     p.add_argument("--eta-mode", type=int, default=0)
     p.add_argument("--proj-iters", type=int, default=0)
+    p.add_argument("--n-roundings", type=int, default=1)
     p.add_argument("--erwa", type=int, default=0)
     p.add_argument("--rounding", type=int, default=0)
     p.add_argument("--time-limit", type=float, default=1000.0)
@@ -50,9 +51,10 @@ def main():
         parts = a.schedule.split("-")
         kmax = float(parts[1])
         hold = int(parts[2][4:] or 1) if len(parts) > 2 else 0
-        kappas = [kmax ** (i / (a.stages - 1)) for i in range(a.stages)] + [kmax] * (hold * a.stages)
+        kmin = float(parts[0][3:]) if parts[0].startswith("geo") and len(parts[0]) > 3 else 1.0
+        kappas = [kmin * (kmax / kmin) ** (i / (a.stages - 1)) for i in range(a.stages)] + [kmax] * (hold * a.stages)
     s.set_params(kappas=kappas, eta=a.eta, erwa_mode=a.erwa, rounding=a.rounding, time_limit_s=a.time_limit,
-                 eta_mode=a.eta_mode, proj_iters=a.proj_iters)
+                 eta_mode=a.eta_mode, proj_iters=a.proj_iters, n_roundings=a.n_roundings)
     runs = []
     for seed in a.seeds:
         res = s.solve(a.restarts, a.steps, seed)
@@ -64,7 +66,7 @@ def main():
     times = [r["solve_s"] if r["verdict"] == "SAT" else float("inf") for r in runs]
     med = statistics.median(times)
     print(json.dumps({"config": a.config, "restarts": a.restarts, "steps_per_stage": a.steps, "eta": a.eta,
-                      "eta_mode": a.eta_mode, "proj_iters": a.proj_iters, "erwa": a.erwa, "schedule": a.schedule or a.kappas or "default",
+                      "eta_mode": a.eta_mode, "proj_iters": a.proj_iters, "n_roundings": a.n_roundings, "rounding": a.rounding, "erwa": a.erwa, "schedule": a.schedule or a.kappas or "default",
                       "build_s": build_s, "median_time_to_sat_s": med if med != float("inf") else None,
                       "solved": sum(r["verdict"] == "SAT" for r in runs), "runs": len(runs),
                       "jit": s.jit_info()}))
