@@ -9,7 +9,7 @@ from fsmt_gen.points import random_points
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("name,world", [("cfg4s", 2), ("cfg3s", 3), ("cfg2s", 2)])
+@pytest.mark.parametrize("name,world", [("cfg4s", 2), ("cfg3s", 3), ("cfg2s", 2), ("cfg2", 2)])
 def test_constraint_shards_sum_to_full(name, world):
     import torch
     import paper_2603_22877_b200 as P
