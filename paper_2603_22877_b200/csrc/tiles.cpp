@@ -494,6 +494,7 @@ const char* kErfcPrelude =
     "  const float f2 = __uint_as_float((127u + ((u >> 7) << 6)) << 23);\n"
     "  return __fmul_rn(__fmul_rn(__fmul_rn(w, f1), f2), f2);\n"
     "}\n"
+    "#define FSMT_AT(base, off) (*(const float*)((const char*)(base) + (off)))\n"
     "__device__ __forceinline__ float fsmt_ex2(float x) { float r; asm(\"ex2.approx.ftz.f32 %0, %1;\" : \"=f\"(r) : \"f\"(x)); return r; }\n"
     "// 0.5*erfc(z) for z >= 0 and ez = exp(-z^2) (dd/db factor, P:1326-1327).  Coefficients from\n"
     "// scripts/fit_erfc.py: z < 0.75: 0.5 (1 - z P(z^2)), P ~ erf(z)/z (degree 5);\n"
@@ -561,11 +562,11 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
     const size_t ns = t.kinds.size();
     o << "__device__ __forceinline__ void kc" << kid
       << "(const TileDesc& T, const uint4* __restrict__ rp, const u32* __restrict__ vs, const u32* __restrict__ vr,\n"
-         "    float* __restrict__ accs, const float* __restrict__ a, const float* __restrict__ b,\n"
+         "    float* __restrict__ accs, const float* __restrict__ ab, const float* __restrict__ bb,\n"
          "    double* __restrict__ ga, double* __restrict__ gb, const unsigned char* __restrict__ U,\n"
-         "    u32 R, u64 rr, u32 r, bool live, u32 n_bool, float kq, float dcoef, float wscale, double& objacc,\n"
+         "    u32 R, u32 R4, u64 rr, u32 r, bool live, u32 n_bool, float kq, float dcoef, float wscale, double& objacc,\n"
          "    double* __restrict__ terms, u32 terms_r, const u32* __restrict__ orig,\n"
-         "    const float* __restrict__ PT, const float* __restrict__ PF, double* __restrict__ gu) {\n";
+         "    const float* __restrict__ PTl, const float* __restrict__ PFl, double* __restrict__ gu) {\n";
     // refs
     std::vector<int> ref_kind;      // 0 Boolean, 1 real, 2 slot-table row (symmetric classes)
     std::vector<int> slot_ref0(ns);
@@ -589,13 +590,13 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
               << (ref_kind[i] == 2 ? ", vaf" + std::to_string(i) + " = 0.f" : std::string()) << ";\n";
     // value of reference i's variable: stream variables are listed in vs, run variables in vr;
     // a table slot reads (p_true, p_false) of its row into (val, vaf)
+    // (ab, bb, PTl, PFl are the lane's column bases: one IMAD.WIDE per address)
     auto ld_of = [&](size_t i) {
         const std::string v = is_stream(i) ? "vs" : "vr";
         if (ref_kind[i] == 2)
-            return "{ const u64 o_ = (u64)" + v + "[l] * R + rr; val" + std::to_string(i) + " = PT[o_]; vaf" +
-                   std::to_string(i) + " = PF[o_]; }";
-        return "val" + std::to_string(i) + " = " +
-               (ref_kind[i] == 0 ? "a[(u64)" + v + "[l] * R + rr]" : "b[(u64)(" + v + "[l] - n_bool) * R + rr]") + ";";
+            return "{ const u64 o_ = (u64)" + v + "[l] * R4; val" + std::to_string(i) + " = FSMT_AT(PTl, o_); vaf" +
+                   std::to_string(i) + " = FSMT_AT(PFl, o_); }";
+        return "val" + std::to_string(i) + " = FSMT_AT(" + (ref_kind[i] == 0 ? "ab" : "bb") + ", (u64)" + v + "[l] * R4);";
     };
     // a run accumulator goes straight to the fp64 gradient (one atomic per run)
     auto flush_run = [&](size_t i) {
@@ -935,11 +936,17 @@ std::string jit_source(const Formula& f, const Built& b, const Plan& p) {
          "  const float dcoef = kappa * 0.79788456080286536f;\n"
          "  double objacc = 0.0;\n"
          "  const uint4* rp = recs + T.rec_off;\n"
+         "  // the lane's column bases: element (v, restart rr) of a [var][R] array at base + v * 4R bytes\n"
+         "  const u32 R4 = R * 4u;\n"
+         "  const float* ab = a + rr;\n"
+         "  const float* bb = b + (rr - (u64)n_bool * R);   // reals are addressed by their unified id\n"
+         "  const float* PTl = PT ? PT + rr : nullptr;\n"
+         "  const float* PFl = PF ? PF + rr : nullptr;\n"
          "  bool symt = false;   // symmetric class: the tile's variables are slot-table rows\n"
          "  switch (T.kclass) {\n";
     for (uint32_t k = 0; k < p.n_jit_kclasses; ++k)
         o << "    case " << k << ": kc" << k
-          << "(T, rp, vs, vr, acc + lane, a, b, ga, gb, U, R, rr, r, live, n_bool, kq, dcoef, wscale, objacc, terms, terms_r, orig, PT, PF, gu); "
+          << "(T, rp, vs, vr, acc + lane, ab, bb, ga, gb, U, R, R4, rr, r, live, n_bool, kq, dcoef, wscale, objacc, terms, terms_r, orig, PTl, PFl, gu); "
           << (p.kclasses[k].sym ? "symt = true; " : "") << "break;\n";
     o << "    default: break;\n  }\n"
          "  __syncwarp();\n"
