@@ -839,7 +839,11 @@ void emit_verify_class(std::ostringstream& o, uint32_t kid, const KClass& K, con
          "    u32 n_bool, const u32* __restrict__ arow, const double* __restrict__ aval,\n"
          "    const double* __restrict__ arhs, const unsigned char* __restrict__ astrict,\n"
          "    const unsigned char* __restrict__ TT) {\n"
-         "  u32 cnt = 0u;\n";
+         "  u32 cnt = 0u;\n"
+         "  const u32 R4 = R * 4u;\n"
+         "  const signed char* xb = x + rr;                          // the lane's column bases\n"
+         "  const float* yb = y + (rr - (u64)n_bool * R);             // reals by their unified id\n"
+         "  const unsigned char* TTl = TT ? TT + rr : nullptr;\n";
     // words 1.. hold the refs (symmetric classes: then the sign words)
     const uint32_t ref_words = 1 + (K.n_refs + 1) / 2 + (K.sym ? (K.n_refs + 31) / 32 : 0);
     uint32_t q_needed = 0;                                          // compressed uint4s holding them
@@ -856,21 +860,21 @@ void emit_verify_class(std::ostringstream& o, uint32_t kid, const KClass& K, con
     };
     for (size_t s = 0; s < ns; ++s) {
         if (t.kinds[s] == 2) {   // table slot: truth of the row (fsmt_kt_jit) xor the literal's sign
-            o << "    const bool t" << s << " = (TT[(u64)" << ext(ref) << " * R + rr] != 0) != (bool)((" << word(1 + ((uint32_t)ns + 1) / 2 + (uint32_t)s / 32)
+            o << "    const bool t" << s << " = (TTl[(u64)" << ext(ref) << " * R] != 0) != (bool)((" << word(1 + ((uint32_t)ns + 1) / 2 + (uint32_t)s / 32)
               << " >> " << s % 32 << ") & 1u);\n";
             ++ref;
             continue;
         }
         if (t.kinds[s] == 0) {
-            o << "    const bool t" << s << " = x[(u64)" << ext(ref) << " * R + rr] == (signed char)-1;\n";
+            o << "    const bool t" << s << " = xb[(u64)" << ext(ref) << " * R] == (signed char)-1;\n";
             ++ref;
         } else {
             const uint32_t nnz = K.nnz[ai];
             const std::string aid = "v" + std::to_string(ai / 4) + "." + comp(ai);
             o << "    bool t" << s << ";\n    { const u32 aid = " << aid << "; const u32 k0 = arow[aid]; double sacc = 0.0;\n";
             for (uint32_t k = 0; k < nnz; ++k) {
-                o << "      sacc = __dadd_rn(sacc, __dmul_rn(aval[k0 + " << k << "], (double)y[(u64)(" << ext(ref)
-                  << " - n_bool) * R + rr]));\n";
+                o << "      sacc = __dadd_rn(sacc, __dmul_rn(aval[k0 + " << k << "], (double)FSMT_AT(yb, (u64)" << ext(ref)
+                  << " * R4)));\n";
                 ++ref;
             }
             o << "      const double rhs = arhs[aid];\n      t" << s << " = astrict[aid] ? (sacc < rhs) : (sacc <= rhs); }\n";
