@@ -126,6 +126,12 @@ struct KClass {
     bool sym = false;
     uint32_t sym_kind = 0, sym_L = 0, sym_k = 0;
     Template stmpl;
+    // K5 record folding: every constraint of the class has the same coefficients and strictness
+    // at each atom slot (kept here, emitted as exact fp64 literals); the K5 record then holds only
+    // the atoms' fp64 right-hand sides
+    bool vfold = false;
+    std::vector<std::vector<double>> vcoef;   // per atom slot
+    std::vector<uint8_t> vstrict;             // per atom slot
 };
 
 // n_vars = n_stream | n_run << 16; tile_vars[var_off ..) holds the stream variables then the run

@@ -299,6 +299,40 @@ Plan make_plan(const Formula& f, const Built& b, bool enable_jit) {
         }
     }
 
+    // 4b. K5 record folding (see KClass::vfold)
+    {
+        const char* ve = getenv("FSMT_JIT_VFOLD");
+        const bool von = !(ve && ve[0] == '0');
+        std::vector<uint8_t> seen_k(p.n_jit_kclasses, 0);
+        for (uint32_t k = 0; k < p.n_jit_kclasses; ++k) p.kclasses[k].vfold = von && !p.kclasses[k].sym;
+        for (uint32_t i2 = 0; i2 < C && p.kclasses[p.cons_kclass[i2]].jit; ++i2) {
+            KClass& K = p.kclasses[p.cons_kclass[i2]];
+            if (!K.vfold) continue;
+            const uint32_t c = p.order[i2];
+            const Template& t = b.tmpls[K.tmpl];
+            const uint32_t* ids = b.slot_ids.data() + b.cons_slot_off[c];
+            std::vector<std::vector<double>> co;
+            std::vector<uint8_t> st;
+            for (size_t sl = 0; sl < t.kinds.size(); ++sl)
+                if (t.kinds[sl] == 1) {
+                    const uint32_t at = ids[sl];
+                    co.emplace_back(f.atom_val.begin() + f.atom_rowptr[at], f.atom_val.begin() + f.atom_rowptr[at + 1]);
+                    st.push_back(f.atom_strict[at]);
+                }
+            if (!seen_k[p.cons_kclass[i2]]) {
+                seen_k[p.cons_kclass[i2]] = 1;
+                K.vcoef = co;
+                K.vstrict = st;
+            } else if (co != K.vcoef || st != K.vstrict) {
+                K.vfold = false;
+            }
+        }
+        for (uint32_t k = 0; k < p.n_jit_kclasses; ++k) {
+            KClass& K = p.kclasses[k];
+            if (K.vfold) K.vstride4 = std::max<uint32_t>(1, (2 * (uint32_t)K.vcoef.size() + 3) / 4);
+        }
+    }
+
     // 5. tiles + records over the JIT prefix: a tile is a run of one sort key with <= cmax
     //    constraints, <= vmax stream variables (shared-memory rows) and <= rmax run variables;
     //    a reference's record field is its variable's index among the tile's stream or run
@@ -373,7 +407,14 @@ Plan make_plan(const Formula& f, const Built& b, bool enable_jit) {
                     put_ref(ids[s]);
                 } else {
                     uint32_t atom = ids[s];
-                    vrec[va++] = atom;
+                    if (K.vfold) {   // the atom's fp64 right-hand side (lo, hi words)
+                        uint64_t bits;
+                        memcpy(&bits, &f.atom_rhs[atom], 8);
+                        vrec[va++] = (uint32_t)bits;
+                        vrec[va++] = (uint32_t)(bits >> 32);
+                    } else {
+                        vrec[va++] = atom;
+                    }
                     float rhs = (float)f.atom_rhs[atom];
                     double n2 = 0.0;
                     for (uint32_t kk = f.atom_rowptr[atom]; kk < f.atom_rowptr[atom + 1]; ++kk)
@@ -870,6 +911,21 @@ void emit_verify_class(std::ostringstream& o, uint32_t kid, const KClass& K, con
             ++ref;
         } else {
             const uint32_t nnz = K.nnz[ai];
+            if (K.vfold) {   // class-constant coefficients / strictness as exact literals, rhs from the record
+                auto vw = [&](uint32_t w) { return "v" + std::to_string(w / 4) + "." + comp(w); };
+                o << "    bool t" << s << ";\n    { double sacc = 0.0;\n";
+                for (uint32_t k = 0; k < nnz; ++k) {
+                    uint64_t bits;
+                    memcpy(&bits, &K.vcoef[ai][k], 8);
+                    o << "      sacc = __dadd_rn(sacc, __dmul_rn(__longlong_as_double(" << (long long)bits << "LL), (double)FSMT_AT(yb, (u64)"
+                      << ext(ref) << " * R4)));\n";
+                    ++ref;
+                }
+                o << "      const double rhs = __hiloint2double((int)" << vw(2 * ai + 1) << ", (int)" << vw(2 * ai) << ");\n"
+                  << "      t" << s << " = " << (K.vstrict[ai] ? "sacc < rhs" : "sacc <= rhs") << "; }\n";
+                ++ai;
+                continue;
+            }
             const std::string aid = "v" + std::to_string(ai / 4) + "." + comp(ai);
             o << "    bool t" << s << ";\n    { const u32 aid = " << aid << "; const u32 k0 = arow[aid]; double sacc = 0.0;\n";
             for (uint32_t k = 0; k < nnz; ++k) {
