@@ -38,6 +38,7 @@ struct fsmt_ctx {
     JitKernel jit;
     DevTiles T{};
     DevSlots slots{};                  // slot tables of the symmetric JIT classes (has_sym)
+    cudaGraphExec_t gexec = nullptr;   // fsmt_run_stage's PGD steps as one CUDA graph (re-used, updated)
     bool has_sym = false;
     const uint32_t* d_pos = nullptr;   // original -> internal constraint index (device)
     // constraint sharding (fsmt_shard): this context's part of the sweep and of the check
@@ -145,6 +146,7 @@ void free_list(std::vector<void*>& v) {
 }
 
 void drop_state(fsmt_ctx* ctx) {
+    if (ctx->gexec) { cudaGraphExecDestroy(ctx->gexec); ctx->gexec = nullptr; }
     free_list(ctx->sallocs);
     ctx->S = DevState{};
     ctx->slots.PT = ctx->slots.PF = ctx->slots.DD = nullptr;
@@ -933,9 +935,44 @@ fsmt_status fsmt_run_stage(fsmt_ctx* ctx, uint32_t stage_t, float kappa, uint32_
     if (ctx->eta_mode == 1) eta_t = eta_b = ctx->eta / kk;
     if (ctx->eta_mode == 2) eta_t = eta_b = ctx->eta / (kk * kk);
     if (ctx->eta_mode == 3) eta_b = ctx->eta / (kk * kk);   // block steps: a keeps eta, b gets eta/kappa^2
-    for (uint32_t k = 0; k < steps; ++k) {
-        if ((s = sweep_impl(ctx, kappa, stage_t, nullptr, 0))) return s;
-        if ((s = update_impl(ctx, eta_t, ctx->eps, eta_b))) return s;
+    // FSMT_GRAPH=1: the S PGD steps are captured into one CUDA graph (one graph launch instead of
+    // ~5 S kernel launches); the executable graph is kept and updated in place with the next
+    // stage's parameters.  Opt-in: capture + update cost about what the launches cost on the
+    // configs measured; never with per-kernel timing (events).
+    const char* ge = getenv("FSMT_GRAPH");
+    if (ge && ge[0] == '1' && !ctx->timing && steps >= 2) {
+        cudaGraph_t g = nullptr;
+        CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+        fsmt_status s2 = FSMT_OK;
+        for (uint32_t k = 0; k < steps && !s2; ++k) {
+            s2 = sweep_impl(ctx, kappa, stage_t, nullptr, 0);
+            if (!s2) s2 = update_impl(ctx, eta_t, ctx->eps, eta_b);
+        }
+        const cudaError_t ee = cudaStreamEndCapture(ctx->stream, &g);
+        if (s2 || ee != cudaSuccess) {
+            if (g) cudaGraphDestroy(g);
+            cudaGetLastError();
+            if (s2) return s2;
+            CK(ee);
+        }
+        if (ctx->gexec) {
+            cudaGraphExecUpdateResultInfo info;
+            if (cudaGraphExecUpdate(ctx->gexec, g, &info) != cudaSuccess) {
+                cudaGetLastError();
+                cudaGraphExecDestroy(ctx->gexec);
+                ctx->gexec = nullptr;
+            }
+        }
+        cudaError_t ei = cudaSuccess;
+        if (!ctx->gexec) ei = cudaGraphInstantiate(&ctx->gexec, g, 0);
+        cudaGraphDestroy(g);
+        CK(ei);
+        CK(cudaGraphLaunch(ctx->gexec, ctx->stream));
+    } else {
+        for (uint32_t k = 0; k < steps; ++k) {
+            if ((s = sweep_impl(ctx, kappa, stage_t, nullptr, 0))) return s;
+            if ((s = update_impl(ctx, eta_t, ctx->eps, eta_b))) return s;
+        }
     }
     if ((s = stage_end_impl(ctx, stage_t))) return s;
     if (unsat_out || min_unsat) {

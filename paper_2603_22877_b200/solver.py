@@ -102,6 +102,7 @@ class Solver:
         s = N.lib.fsmt_solve(self._h, restarts, steps, seed, C.byref(v), x.ctypes.data, y.ctypes.data, C.byref(st))
         if s not in (N.OK, N.ERR_TIMEOUT):
             self._check(s)
+        self.R = restarts                 # fsmt_solve leaves its R-restart state in the context
         stats = {k: getattr(st, k) for k, _ in st._fields_}
         stats["timeout"] = s == N.ERR_TIMEOUT
         return SolveResult(v.value, x, y, stats)

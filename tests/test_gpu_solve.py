@@ -175,3 +175,23 @@ def test_multiple_roundings_solve_sound():
     _, sat = semantics.eval_formula(f, res.x, res.y)
     assert (res.verdict == 10) == all(sat)
     assert sum(not v for v in sat) == res.stats["best_unsat"]
+
+
+def test_graph_captured_stages_reproduce_solve():
+    """FSMT_GRAPH=1 (the PGD steps of a stage as one CUDA graph, updated in place across stages)
+    launches the same kernels with the same parameters: the solve is bit-identical."""
+    inst = fsmt_gen.config("cfg4s")
+    out = []
+    for g in ("0", "1"):
+        os.environ["FSMT_GRAPH"] = g
+        try:
+            s = make(inst.text)
+            s.set_params(eta=0.05, rounding=1, kappas=[0.5, 1.0, 2.0, 4.0])
+            res = s.solve(128, 12, 4)
+            a, b = s.get_state()
+            out.append((res.verdict, res.stats["best_unsat"], np.asarray(res.x).copy(), np.asarray(res.y).copy(), a, b))
+        finally:
+            os.environ.pop("FSMT_GRAPH", None)
+    assert out[0][0] == out[1][0] and out[0][1] == out[1][1]
+    for k in (2, 3, 4, 5):
+        assert np.array_equal(out[0][k], out[1][k])
