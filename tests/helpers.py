@@ -49,8 +49,13 @@ def subformula(text, bool_vars=(), real_vars=(), extra_constraints=()):
     rset = set(int(j) for j in real_vars)
     hot_atoms = {aid for aid, p in atoms.items() if any(int(t.split(":")[0]) in rset for t in p[4:])}
     keep = []
-    extra = set(extra_constraints)
-    for ci, ln in enumerate(cons):
+    extra = set(int(c) for c in extra_constraints)
+    if not bset and not rset:                    # constraints by index only: no scan
+        keep = sorted(extra)
+        cons_iter = ()
+    else:
+        cons_iter = enumerate(cons)
+    for ci, ln in cons_iter:
         toks = re.findall(r"[+-]?[ab]\d+", ln)
         hit = ci in extra
         for t in toks:

@@ -174,6 +174,27 @@ def test_k1_full_size_sampled(gpu_mod, name, R):
         check_gradient(gb[rsel, r], ogb[rsel], what=f"{name} grad_b")
 
 
+@pytest.mark.parametrize("name,R", [("cfg3", 1024), ("cfg4", 1024)])
+def test_k5_full_size_sampled(gpu_mod, name, R):
+    """K5 (specialised check) at the bench launch configuration: per-constraint verdicts of
+    sampled constraints for sampled restarts are bit-exact against the oracle's exact semantics
+    (R22), and the unsat counts equal the per-constraint sums."""
+    inst = fsmt_gen.config(name)
+    s = make(gpu_mod, inst.text)
+    d = s.get_dims()
+    rng = np.random.default_rng(11)
+    x = np.where(rng.random((d["n_bool"], R)) < 0.5, -1, 1).astype(np.int8)
+    _, y = random_points(0, d["n_real"], R, seed=12, b_lo=0.0, b_hi=1.0)
+    unsat, pc = s.verify_batch(x, y, per_con=True)
+    assert np.array_equal(unsat.astype(np.int64), pc.sum(axis=0).astype(np.int64))
+    csel = np.sort(rng.choice(d["n_cons"], 3000, replace=False))
+    sub, keep = subformula(inst.text, extra_constraints=csel)
+    fs = hsmt.parse(sub)
+    for r in (0, 517, R - 1):
+        want = np.array([0 if semantics.constraint_sat(fs, c, x[:, r], y[:, r]) else 1 for c in fs.constraints])
+        assert np.array_equal(pc[keep, r].astype(int), want), r
+
+
 # ------------------------------------------------------------------------------------- K3 (P3)
 
 @pytest.mark.parametrize("name", ["cfg1", "cfg4s", "cfg3s"])
