@@ -113,6 +113,10 @@ struct KClass {
     bool jit;
     uint64_t n_cons;
     std::vector<uint8_t> stream;  // per reference: 1 = changes most constraints (no run register)
+    // affine groups: reference r with aff_head[r] = q >= 0 reads, in every constraint of the
+    // class, the variable of q plus aff_dg[r] at the local (tile) index of q plus aff_dl[r]
+    // (e.g. the 7 bits and 2 coordinates of one placement module): q's check / lookup serves all
+    std::vector<int32_t> aff_head, aff_dg, aff_dl;
     std::vector<int32_t> alias;   // per reference: earlier reference with the same variable in every
                                   // constraint of the class (one load, one accumulator), or -1
     // record compression: logical word w is stored at position wpos[w] of the compressed record,

@@ -445,6 +445,79 @@ Plan make_plan(const Formula& f, const Built& b, bool enable_jit) {
     p.jit_cons_end = i;
     // any JIT-class constraints after the cut run through the generic kernel
 
+    // 5c. affine reference groups (KClass::aff_head): from the tile records (local indices) and
+    //     the constraints' variables, per class; a group's members must share the head's kind
+    //     (Boolean / real / table row) and stream flag.  FSMT_JIT_AFFINE=0 disables.
+    {
+        const char* ae = getenv("FSMT_JIT_AFFINE");
+        const bool on = !(ae && ae[0] == '0');
+        std::vector<std::vector<uint8_t>> ok(p.n_jit_kclasses);
+        std::vector<std::vector<int32_t>> dg(p.n_jit_kclasses), dl(p.n_jit_kclasses);
+        std::vector<uint8_t> init(p.n_jit_kclasses, 0);
+        std::vector<int> rkind;
+        for (const TileDesc& T : p.tiles) {
+            const KClass& K = p.kclasses[T.kclass];
+            const uint32_t nr = K.n_refs;
+            std::vector<uint8_t>& okk = ok[T.kclass];
+            for (uint32_t c = 0; c < T.n_cons; ++c) {
+                const uint32_t* rec = p.recs.data() + ((size_t)T.rec_off + (size_t)c * K.stride4) * 4;
+                cons_vars(p.order[T.cons_begin + c], vars);
+                auto lref = [&](uint32_t r) { return (int32_t)((rec[1 + r / 2] >> (16 * (r % 2))) & 0xFFFFu); };
+                if (!init[T.kclass]) {
+                    init[T.kclass] = 1;
+                    okk.assign((size_t)nr * nr, 0);
+                    dg[T.kclass].assign((size_t)nr * nr, 0);
+                    dl[T.kclass].assign((size_t)nr * nr, 0);
+                    for (uint32_t r = 1; r < nr; ++r)
+                        for (uint32_t q = 0; q < r; ++q) {
+                            okk[(size_t)r * nr + q] = 1;
+                            dg[T.kclass][(size_t)r * nr + q] = (int32_t)vars[r] - (int32_t)vars[q];
+                            dl[T.kclass][(size_t)r * nr + q] = lref(r) - lref(q);
+                        }
+                    continue;
+                }
+                for (uint32_t r = 1; r < nr; ++r)
+                    for (uint32_t q = 0; q < r; ++q) {
+                        const size_t ix = (size_t)r * nr + q;
+                        if (okk[ix] && ((int32_t)vars[r] - (int32_t)vars[q] != dg[T.kclass][ix] || lref(r) - lref(q) != dl[T.kclass][ix]))
+                            okk[ix] = 0;
+                    }
+            }
+        }
+        for (uint32_t k = 0; k < p.n_jit_kclasses; ++k) {
+            KClass& K = p.kclasses[k];
+            const uint32_t nr = K.n_refs;
+            K.aff_head.assign(nr, -1);
+            K.aff_dg.assign(nr, 0);
+            K.aff_dl.assign(nr, 0);
+            if (!on || !init[k]) continue;
+            // reference kinds in reference order
+            rkind.clear();
+            const Template& t = K.sym ? K.stmpl : b.tmpls[K.tmpl];
+            for (size_t sl = 0, ai = 0; sl < t.kinds.size(); ++sl) {
+                if (t.kinds[sl] == 1) {
+                    for (uint32_t z = 0; z < K.nnz[ai]; ++z) rkind.push_back(1);
+                    ++ai;
+                } else {
+                    rkind.push_back(t.kinds[sl]);
+                }
+            }
+            for (uint32_t r = 1; r < nr; ++r) {
+                if (K.alias[r] >= 0) continue;
+                for (uint32_t q = 0; q < r; ++q) {
+                    if (K.alias[q] >= 0 || K.aff_head[q] >= 0) continue;
+                    if (rkind[q] != rkind[r] || K.stream[q] != K.stream[r]) continue;
+                    const size_t ix = (size_t)r * nr + q;
+                    if (!ok[k][ix] || dl[k][ix] == 0) continue;
+                    K.aff_head[r] = (int32_t)q;
+                    K.aff_dg[r] = dg[k][ix];
+                    K.aff_dl[r] = dl[k][ix];
+                    break;
+                }
+            }
+        }
+    }
+
     // 6. record compression: words equal across a whole class become literals in the code
     // (FSMT_JIT_FOLD=0 disables; cfg4: 7 -> 4 uint4 per record, 13.7 vs 14.0 ms at vmax 48)
     const char* cz = getenv("FSMT_JIT_FOLD");
@@ -625,28 +698,35 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
     auto alias_of = [&](size_t i) -> int {   // target reference of an alias, -1 if i is its own
         return i < K.alias.size() ? K.alias[i] : -1;
     };
+    auto head_of = [&](size_t i) -> int {   // affine group head (-1: i is a head or ungrouped)
+        return i < K.aff_head.size() ? K.aff_head[i] : -1;
+    };
+    std::vector<std::vector<size_t>> members(nr);
     for (size_t i = 0; i < nr; ++i)
-        if (!is_stream(i) && alias_of(i) < 0)
-            o << "  u32 cur" << i << " = 0xffffffffu; float val" << i << " = 0.f, acc" << i << " = 0.f"
-              << (ref_kind[i] == 2 ? ", vaf" + std::to_string(i) + " = 0.f" : std::string()) << ";\n";
-    // value of reference i's variable: stream variables are listed in vs, run variables in vr;
-    // a table slot reads (p_true, p_false) of its row into (val, vaf)
-    // (ab, bb, PTl, PFl are the lane's column bases: one IMAD.WIDE per address)
-    auto ld_of = [&](size_t i) {
-        const std::string v = is_stream(i) ? "vs" : "vr";
-        if (ref_kind[i] == 2)
-            return "{ const u64 o_ = (u64)" + v + "[l] * R4; val" + std::to_string(i) + " = FSMT_AT(PTl, o_); vaf" +
-                   std::to_string(i) + " = FSMT_AT(PFl, o_); }";
-        return "val" + std::to_string(i) + " = FSMT_AT(" + (ref_kind[i] == 0 ? "ab" : "bb") + ", (u64)" + v + "[l] * R4);";
+        if (alias_of(i) < 0 && head_of(i) >= 0) members[(size_t)head_of(i)].push_back(i);
+    const std::string I = "";
+    for (size_t i = 0; i < nr; ++i) {
+        if (is_stream(i) || alias_of(i) >= 0) continue;
+        if (head_of(i) < 0) o << "  u32 cur" << i << " = 0xffffffffu, gcur" << i << " = 0u;";
+        o << " float val" << i << " = 0.f, acc" << i << " = 0.f"
+          << (ref_kind[i] == 2 ? ", vaf" + std::to_string(i) + " = 0.f" : std::string()) << ";\n";
+    }
+    // value of reference i at byte offset `off` of its column base: Booleans in a (ab), reals
+    // by unified id in b (bb), table rows in PT / PF (PTl / PFl)
+    auto ld_at = [&](size_t i, const std::string& off) {
+        const std::string is = std::to_string(i);
+        if (ref_kind[i] == 2) return "val" + is + " = FSMT_AT(PTl, " + off + "); vaf" + is + " = FSMT_AT(PFl, " + off + ");";
+        return "val" + is + " = FSMT_AT(" + (ref_kind[i] == 0 ? "ab" : "bb") + ", " + off + ");";
     };
-    // a run accumulator goes straight to the fp64 gradient (one atomic per run)
-    auto flush_run = [&](size_t i) {
-        const std::string cur = "vr[cur" + std::to_string(i) + "]";
-        const std::string g = ref_kind[i] == 0 ? "ga + (u64)" + cur + " * R + r"
-                            : ref_kind[i] == 2 ? "gu + (u64)" + cur + " * R + r"
-                                               : "gb + (u64)(" + cur + " - n_bool) * R + r";
-        return "if (live) atomicAdd(" + g + ", (double)acc" + std::to_string(i) + ");";
+    auto dgoff = [&](size_t m) { return "(u64)(" + std::to_string(K.aff_dg[m]) + " * (long long)R4)"; };
+    // a run accumulator goes straight to the fp64 gradient (one atomic per run); g = the variable
+    auto flush_run = [&](size_t i, const std::string& g) {
+        const std::string dst = ref_kind[i] == 0 ? "ga + (u64)(" + g + ") * R + r"
+                              : ref_kind[i] == 2 ? "gu + (u64)(" + g + ") * R + r"
+                                                 : "gb + (u64)(" + g + " - n_bool) * R + r";
+        return "if (live) atomicAdd(" + dst + ", (double)acc" + std::to_string(i) + ");";
     };
+    auto gm = [&](size_t h, size_t m) { return "gcur" + std::to_string(h) + " + (" + std::to_string(K.aff_dg[m]) + ")"; };
     o << "  for (u32 c = 0; c < T.n_cons; ++c, rp += " << K.stride4 << ") {\n";
     for (uint32_t q = 0; q < K.stride4; ++q) o << "    const uint4 q" << q << " = __ldg(rp + " << q << ");\n";
     o << "    const u32 uc = U ? (u32)U[(u64)(T.cons_begin + c) * R + rr] : 0u;\n";
@@ -655,19 +735,27 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
     for (size_t i = 0; i < nr; ++i) {
         uint32_t wd = 1 + (uint32_t)i / 2;
         const std::string ext = "(" + word(wd) + " >> " + std::to_string(16 * (i % 2)) + ") & 0xffffu";
-        const std::string ld = ld_of(i);
         if (alias_of(i) >= 0) {
             o << "    const float val" << i << " = val" << alias_of(i) << ";   // alias\n";
             continue;
         }
+        if (head_of(i) >= 0) continue;   // loaded with its group head
         if (is_stream(i)) {
             // stream reference: new variable (almost) every constraint; no run register
             o << "    const u32 sl" << i << " = " << ext << ";\n"
-              << "    float val" << i << (ref_kind[i] == 2 ? ", vaf" + std::to_string(i) : std::string()) << ";\n    { const u32 l = sl"
-              << i << "; " << ld << " }\n";
+              << "    const u64 so" << i << " = (u64)vs[sl" << i << "] * R4;\n";
+            o << "    float val" << i << (ref_kind[i] == 2 ? ", vaf" + std::to_string(i) : std::string()) << "; " << ld_at(i, "so" + std::to_string(i)) << "\n";
+            for (size_t m : members[i])
+                o << "    float val" << m << (ref_kind[m] == 2 ? ", vaf" + std::to_string(m) : std::string()) << "; "
+                  << ld_at(m, "so" + std::to_string(i) + " + " + dgoff(m)) << "   // affine\n";
         } else {
             o << "    { const u32 l = " << ext << "; if (l != cur" << i << ") { if (cur" << i << " != 0xffffffffu) { "
-              << flush_run(i) << " } cur" << i << " = l; acc" << i << " = 0.f; " << ld << " } }\n";
+              << flush_run(i, "gcur" + std::to_string(i));
+            for (size_t m : members[i]) o << " " << flush_run(m, gm(i, m));
+            o << " } cur" << i << " = l; gcur" << i << " = vr[l]; acc" << i << " = 0.f; "
+              << ld_at(i, "(u64)gcur" + std::to_string(i) + " * R4");
+            for (size_t m : members[i]) o << " acc" << m << " = 0.f; " << ld_at(m, "(u64)gcur" + std::to_string(i) + " * R4 + " + dgoff(m));
+            o << " } }\n";
         }
     }
     // slot probabilities
@@ -855,14 +943,21 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
     }
     for (size_t ri = 0; ri < nr; ++ri) {
         if (terms_of[ri].empty()) continue;
-        const std::string dst = is_stream(ri) ? "accs[sl" + std::to_string(ri) + " * 32]" : "acc" + std::to_string(ri);
+        std::string dst = "acc" + std::to_string(ri);
+        if (is_stream(ri))
+            dst = head_of(ri) >= 0 ? "accs[(sl" + std::to_string(head_of(ri)) + " + " + std::to_string(K.aff_dl[ri]) + ") * 32]"
+                                   : "accs[sl" + std::to_string(ri) + " * 32]";
         std::string e = dst;
         for (const auto& ab : terms_of[ri]) e = "fmaf(" + ab.first + ", " + ab.second + ", " + e + ")";
         o << "    " << dst << " = " << e << ";\n";
     }
     o << "  }\n";
     for (size_t i = 0; i < nr; ++i)
-        if (!is_stream(i) && alias_of(i) < 0) o << "  if (cur" << i << " != 0xffffffffu) { " << flush_run(i) << " }\n";
+        if (!is_stream(i) && alias_of(i) < 0 && head_of(i) < 0) {
+            o << "  if (cur" << i << " != 0xffffffffu) { " << flush_run(i, "gcur" + std::to_string(i));
+            for (size_t m : members[i]) o << " " << flush_run(m, gm(i, m));
+            o << " }\n";
+        }
     o << "}\n\n";
 }
 
