@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <sstream>
 #include <unordered_map>
@@ -518,6 +519,21 @@ Plan make_plan(const Formula& f, const Built& b, bool enable_jit) {
         }
     }
 
+    // 5d. alias and affine-member references need no record field (K1 and K5 derive them from
+    //     their target / head).  FSMT_JIT_DROPREF=1 zeroes the fields so words holding only such
+    //     fields fold away (cfg4: 4 -> 2 uint4 per record); measured slower for K1 (10.58 vs
+    //     10.36 ms) though faster for K5, and slower overall, so the fields stay by default
+    const char* dre = getenv("FSMT_JIT_DROPREF");
+    if (dre && dre[0] == '1')
+        for (const TileDesc& T : p.tiles) {
+            const KClass& K = p.kclasses[T.kclass];
+            for (uint32_t c = 0; c < T.n_cons; ++c) {
+                uint32_t* rec = p.recs.data() + ((size_t)T.rec_off + (size_t)c * K.stride4) * 4;
+                for (uint32_t r = 0; r < K.n_refs; ++r)
+                    if (K.alias[r] >= 0 || K.aff_head[r] >= 0) rec[1 + r / 2] &= ~(0xFFFFu << (16 * (r % 2)));
+            }
+        }
+
     // 6. record compression: words equal across a whole class become literals in the code
     // (FSMT_JIT_FOLD=0 disables; cfg4: 7 -> 4 uint4 per record, 13.7 vs 14.0 ms at vmax 48)
     const char* cz = getenv("FSMT_JIT_FOLD");
@@ -989,10 +1005,22 @@ void emit_verify_class(std::ostringstream& o, uint32_t kid, const KClass& K, con
     for (uint32_t q = 0; q < q_needed; ++q) o << "    const uint4 q" << q << " = __ldg(rp + " << q << ");\n";
     for (uint32_t q = 0; q < K.vstride4; ++q) o << "    const uint4 v" << q << " = __ldg(vp + " << q << ");\n";
     uint32_t ref = 0, ai = 0;
-    auto ext = [&](uint32_t i) {   // variable id of reference i (stream ids in vs, run ids in vr)
-        const int32_t tr = i < K.alias.size() && K.alias[i] >= 0 ? K.alias[i] : (int32_t)i;
-        const std::string v = (size_t)tr < K.stream.size() && K.stream[tr] ? "vs" : "vr";
-        return v + "[((" + word(1 + i / 2) + " >> " + std::to_string(16 * (i % 2)) + ") & 0xffffu)]";
+    // variable id of each reference: own references look theirs up (stream ids in vs, run ids in
+    // vr); an alias takes its target's, an affine member its head's plus the group offset (the
+    // records carry neither field: KClass::aff_head, step 5d)
+    const uint32_t nref = K.n_refs;
+    auto own = [&](uint32_t i) {
+        return !(i < K.alias.size() && K.alias[i] >= 0) && !(i < K.aff_head.size() && K.aff_head[i] >= 0);
+    };
+    for (uint32_t i = 0; i < nref; ++i)
+        if (own(i))
+            o << "    const u32 gv" << i << " = " << (i < K.stream.size() && K.stream[i] ? "vs" : "vr") << "[((" << word(1 + i / 2)
+              << " >> " << 16 * (i % 2) << ") & 0xffffu)];\n";
+    std::function<std::string(uint32_t)> ext = [&](uint32_t i) -> std::string {
+        if (i < K.alias.size() && K.alias[i] >= 0) return ext((uint32_t)K.alias[i]);
+        if (i < K.aff_head.size() && K.aff_head[i] >= 0)
+            return "(gv" + std::to_string(K.aff_head[i]) + " + (" + std::to_string(K.aff_dg[i]) + "))";
+        return "gv" + std::to_string(i);
     };
     for (size_t s = 0; s < ns; ++s) {
         if (t.kinds[s] == 2) {   // table slot: truth of the row (fsmt_kt_jit) xor the literal's sign
