@@ -634,10 +634,10 @@ const char* kErfcPrelude =
     "__device__ __forceinline__ float fsmt_half_erfc(float z, float& ez) {\n"
     "  const float z2 = z * z;\n"
     "  ez = fsmt_ex2(-1.44269504088896341f * z2);\n"
-    "  float p = -6.760858814e-04f;\n"
-    "  p = fmaf(p, z2, 5.115946755e-03f); p = fmaf(p, z2, -2.683541551e-02f); p = fmaf(p, z2, 1.128339246e-01f);\n"
-    "  p = fmaf(p, z2, -3.761262000e-01f); p = fmaf(p, z2, 1.128379107e+00f);\n"
-    "  const float small = 0.5f * fmaf(-z, p, 1.f);\n"
+    "  float p = -3.380429407e-04f;   // 0.5 P (exact halving of the fitted coefficients)\n"
+    "  p = fmaf(p, z2, 2.5579733775e-03f); p = fmaf(p, z2, -1.3417707755e-02f); p = fmaf(p, z2, 5.64169623e-02f);\n"
+    "  p = fmaf(p, z2, -1.880631e-01f); p = fmaf(p, z2, 5.641895535e-01f);\n"
+    "  const float small = fmaf(-z, p, 0.5f);\n"
     "  float t;   // 1/(1 + z/2) with 1 + z/2 >= 1: rcp.approx needs no denormal range fix-up\n"
     "  asm(\"rcp.approx.ftz.f32 %0, %1;\" : \"=f\"(t) : \"f\"(fmaf(0.5f, z, 1.f)));\n"
     "  float q = 4.469624162e-02f;\n"
@@ -797,7 +797,12 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
                 o << "    z" << s << " = fmaf(__uint_as_float(" << word(aw + 2 + k) << "), val" << slot_ref0[s] + k << ", z" << s << ");\n";
             }
             aw += 2 + nnz;
-            o << "    const float u" << s << " = kq * z" << s << " * inv" << s << ";\n";
+            // inv class-constant (folded): kappa/sqrt2 * inv and the dd factor are loop-invariant
+            const bool inv_const = K.wpos[aw - 2 - nnz + 1] < 0;
+            if (inv_const)
+                o << "    const float u" << s << " = z" << s << " * (kq * inv" << s << ");\n";
+            else
+                o << "    const float u" << s << " = kq * z" << s << " * inv" << s << ";\n";
             if (fast_erfc() && erfc_vote()) {
                 // warp vote: both erfc branches only when the warp's lanes straddle |u| = 0.75
                 o << "    const float za" << s << " = fabsf(u" << s << "), zb" << s << " = za" << s << " * za" << s << ";\n"
@@ -815,7 +820,7 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
                   << "    const float ez" << s << " = expf(-u" << s << " * u" << s << ");\n";
             o << "    const float pt" << s << " = u" << s << " >= 0.f ? e" << s << " : 1.f - e" << s << ";\n"
               << "    const float pf" << s << " = u" << s << " >= 0.f ? 1.f - e" << s << " : e" << s << ";\n"
-              << "    const float dd" << s << " = dcoef * inv" << s << " * ez" << s << ";\n";
+              << "    const float dd" << s << " = (dcoef * inv" << s << ") * ez" << s << ";\n";
         }
     }
     // XOR diamonds (peephole, FSMT_JIT_DIAMOND=0 disables): node n at slot s whose children h, l
