@@ -1006,36 +1006,67 @@ void emit_verify_class(std::ostringstream& o, uint32_t kid, const KClass& K, con
     uint32_t q_needed = 0;                                          // compressed uint4s holding them
     for (uint32_t w = 1; w < ref_words; ++w)
         if (K.wpos[w] >= 0) q_needed = std::max(q_needed, (uint32_t)K.wpos[w] / 4 + 1);
+    // reference kinds in reference order (0 Boolean, 1 real, 2 table row)
+    const uint32_t nref = K.n_refs;
+    std::vector<int> rk;
+    for (size_t sl = 0, a2 = 0; sl < ns; ++sl) {
+        if (t.kinds[sl] == 1) {
+            for (uint32_t z = 0; z < K.nnz[a2]; ++z) rk.push_back(1);
+            ++a2;
+        } else {
+            rk.push_back(t.kinds[sl]);
+        }
+    }
+    auto is_alias = [&](uint32_t i) { return i < K.alias.size() && K.alias[i] >= 0; };
+    auto head_of = [&](uint32_t i) -> int { return i < K.aff_head.size() ? K.aff_head[i] : -1; };
+    auto is_stream = [&](uint32_t i) { return i < K.stream.size() && K.stream[i]; };
+    std::vector<std::vector<uint32_t>> members(nref);
+    for (uint32_t i = 0; i < nref; ++i)
+        if (!is_alias(i) && head_of(i) >= 0) members[(uint32_t)head_of(i)].push_back(i);
+    auto ty = [&](uint32_t i) { return std::string(rk[i] == 1 ? "double" : "bool"); };
+    auto load = [&](uint32_t i, const std::string& g) {
+        if (rk[i] == 0) return "xb[(u64)(" + g + ") * R] == (signed char)-1";
+        if (rk[i] == 1) return "(double)FSMT_AT(yb, (u64)(" + g + ") * R4)";
+        return "TTl[(u64)(" + g + ") * R] != 0";
+    };
+    // run groups keep their values while the head's variable does not change (one check per
+    // group); stream groups load every constraint (one lookup per group)
+    for (uint32_t i = 0; i < nref; ++i)
+        if (!is_alias(i) && head_of(i) < 0 && !is_stream(i)) {
+            o << "  u32 kc" << i << " = 0xffffffffu; " << ty(i) << " kv" << i << " = 0;";
+            for (uint32_t m : members[i]) o << " " << ty(m) << " kv" << m << " = 0;";
+            o << "\n";
+        }
     o << "  for (u32 c = 0; c < T.n_cons; ++c, rp += " << K.stride4 << ", vp += " << K.vstride4 << ") {\n";
     for (uint32_t q = 0; q < q_needed; ++q) o << "    const uint4 q" << q << " = __ldg(rp + " << q << ");\n";
     for (uint32_t q = 0; q < K.vstride4; ++q) o << "    const uint4 v" << q << " = __ldg(vp + " << q << ");\n";
     uint32_t ref = 0, ai = 0;
-    // variable id of each reference: own references look theirs up (stream ids in vs, run ids in
-    // vr); an alias takes its target's, an affine member its head's plus the group offset (the
-    // records carry neither field: KClass::aff_head, step 5d)
-    const uint32_t nref = K.n_refs;
-    auto own = [&](uint32_t i) {
-        return !(i < K.alias.size() && K.alias[i] >= 0) && !(i < K.aff_head.size() && K.aff_head[i] >= 0);
-    };
+    for (uint32_t i = 0; i < nref; ++i) {
+        if (is_alias(i) || head_of(i) >= 0) continue;
+        const std::string ext = "((" + word(1 + i / 2) + " >> " + std::to_string(16 * (i % 2)) + ") & 0xffffu)";
+        if (is_stream(i)) {
+            o << "    const u32 gv" << i << " = vs[" << ext << "];\n";
+            o << "    const " << ty(i) << " kv" << i << " = " << load(i, "gv" + std::to_string(i)) << ";\n";
+            for (uint32_t m : members[i])
+                o << "    const " << ty(m) << " kv" << m << " = " << load(m, "gv" + std::to_string(i) + " + (" + std::to_string(K.aff_dg[m]) + ")") << ";\n";
+        } else {
+            o << "    { const u32 l = " << ext << "; if (l != kc" << i << ") { kc" << i << " = l; const u32 g = vr[l]; kv" << i << " = "
+              << load(i, "g") << ";";
+            for (uint32_t m : members[i]) o << " kv" << m << " = " << load(m, "g + (" + std::to_string(K.aff_dg[m]) + ")") << ";";
+            o << " } }\n";
+        }
+    }
     for (uint32_t i = 0; i < nref; ++i)
-        if (own(i))
-            o << "    const u32 gv" << i << " = " << (i < K.stream.size() && K.stream[i] ? "vs" : "vr") << "[((" << word(1 + i / 2)
-              << " >> " << 16 * (i % 2) << ") & 0xffffu)];\n";
-    std::function<std::string(uint32_t)> ext = [&](uint32_t i) -> std::string {
-        if (i < K.alias.size() && K.alias[i] >= 0) return ext((uint32_t)K.alias[i]);
-        if (i < K.aff_head.size() && K.aff_head[i] >= 0)
-            return "(gv" + std::to_string(K.aff_head[i]) + " + (" + std::to_string(K.aff_dg[i]) + "))";
-        return "gv" + std::to_string(i);
-    };
+        if (is_alias(i)) o << "    const " << ty(i) << " kv" << i << " = kv" << K.alias[i] << ";\n";
     for (size_t s = 0; s < ns; ++s) {
         if (t.kinds[s] == 2) {   // table slot: truth of the row (fsmt_kt_jit) xor the literal's sign
-            o << "    const bool t" << s << " = (TTl[(u64)" << ext(ref) << " * R] != 0) != (bool)((" << word(1 + ((uint32_t)ns + 1) / 2 + (uint32_t)s / 32)
+            o << "    const bool t" << s << " = kv" << ref << " != (bool)((" << word(1 + ((uint32_t)ns + 1) / 2 + (uint32_t)s / 32)
               << " >> " << s % 32 << ") & 1u);\n";
             ++ref;
             continue;
         }
         if (t.kinds[s] == 0) {
-            o << "    const bool t" << s << " = xb[(u64)" << ext(ref) << " * R] == (signed char)-1;\n";
+            o << "    const bool t" << s << " = kv" << ref << ";\n";
             ++ref;
         } else {
             const uint32_t nnz = K.nnz[ai];
@@ -1045,8 +1076,7 @@ void emit_verify_class(std::ostringstream& o, uint32_t kid, const KClass& K, con
                 for (uint32_t k = 0; k < nnz; ++k) {
                     uint64_t bits;
                     memcpy(&bits, &K.vcoef[ai][k], 8);
-                    o << "      sacc = __dadd_rn(sacc, __dmul_rn(__longlong_as_double(" << (long long)bits << "LL), (double)FSMT_AT(yb, (u64)"
-                      << ext(ref) << " * R4)));\n";
+                    o << "      sacc = __dadd_rn(sacc, __dmul_rn(__longlong_as_double(" << (long long)bits << "LL), kv" << ref << "));\n";
                     ++ref;
                 }
                 o << "      const double rhs = __hiloint2double((int)" << vw(2 * ai + 1) << ", (int)" << vw(2 * ai) << ");\n"
@@ -1057,8 +1087,7 @@ void emit_verify_class(std::ostringstream& o, uint32_t kid, const KClass& K, con
             const std::string aid = "v" + std::to_string(ai / 4) + "." + comp(ai);
             o << "    bool t" << s << ";\n    { const u32 aid = " << aid << "; const u32 k0 = arow[aid]; double sacc = 0.0;\n";
             for (uint32_t k = 0; k < nnz; ++k) {
-                o << "      sacc = __dadd_rn(sacc, __dmul_rn(aval[k0 + " << k << "], (double)FSMT_AT(yb, (u64)" << ext(ref)
-                  << " * R4)));\n";
+                o << "      sacc = __dadd_rn(sacc, __dmul_rn(aval[k0 + " << k << "], kv" << ref << "));\n";
                 ++ref;
             }
             o << "      const double rhs = arhs[aid];\n      t" << s << " = astrict[aid] ? (sacc < rhs) : (sacc <= rhs); }\n";
