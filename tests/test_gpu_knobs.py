@@ -1,0 +1,80 @@
+"""The JIT planner's and emitter's optional transformations (DESIGN.md §7, §9 A/B table) each
+keep the sweep and the exact check in parity with the oracle: objective, gradients and
+per-constraint verdicts on cfg3s / cfg4s / cfg2 under every knob setting."""
+import os
+
+import numpy as np
+import pytest
+
+import fsmt_gen
+from fsmt_gen.points import random_points
+from oracle import hsmt, objective, semantics
+from tests.helpers import check_gradient, check_objective
+
+pytestmark = pytest.mark.gpu
+
+KNOBS = [
+    {},
+    {"FSMT_JIT_AFFINE": "0"},
+    {"FSMT_JIT_DIAMOND": "0", "FSMT_JIT_ALIAS": "0"},
+    {"FSMT_JIT_FOLD": "0", "FSMT_JIT_VFOLD": "0"},
+    {"FSMT_JIT_DROPREF": "1"},
+    {"FSMT_JIT_SYM": "0"},
+    {"FSMT_JIT_ERFC": "nr", "FSMT_JIT_ERFC_VOTE": "1"},
+    {"FSMT_JIT_ERFC": "cuda"},
+    {"FSMT_JIT_STREAM": "0"},
+    {"FSMT_TILE_VMAX": "16", "FSMT_TILE_RMAX": "16", "FSMT_TILE_CMAX": "3"},
+]
+
+
+_ORC = {}
+
+
+def oracle_case(name):
+    """Formula, points and oracle values for restarts 0 and 44 (cached across knob settings)."""
+    if name not in _ORC:
+        inst = fsmt_gen.config(name)
+        f = hsmt.parse(inst.text)
+        a, b = random_points(f.n_bool, f.n_real, 45, seed=21, b_lo=0.0, b_hi=1.0)
+        w = [c.weight for c in f.constraints]
+        x = np.where(a < 0, -1, 1).astype(np.int8)
+        vals = {}
+        for r in (0, 44):
+            C, oga, ogb = objective.objective_and_gradient(f, a[:, r], b[:, r], 1.3, w)
+            want = np.array([0 if semantics.constraint_sat(f, c, x[:, r], b[:, r]) else 1 for c in f.constraints])
+            vals[r] = (C, oga, ogb, want)
+        _ORC[name] = (inst, f, a, b, x, w, vals)
+    return _ORC[name]
+
+
+@pytest.mark.parametrize("knobs", KNOBS, ids=lambda k: ",".join(f"{a}={b}" for a, b in k.items()) or "default")
+@pytest.mark.parametrize("name", ["cfg3s", "cfg4s", "cfg2"])
+def test_knob_parity(name, knobs):
+    import paper_2603_22877_b200 as P
+    inst = fsmt_gen.config(name)
+    old = {k: os.environ.get(k) for k in knobs}
+    os.environ.update(knobs)
+    try:
+        s = P.Solver(0)
+        s.load_formula(inst.text)
+        s.build_xbdd()                       # the knobs are read here
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    assert s.jit_info()["jit_classes"] > 0 or (name == "cfg2" and knobs.get("FSMT_JIT_SYM") == "0")
+    _, f, a, b, x, w, vals = oracle_case(name)
+    R = 45
+    s.begin(R, 3)
+    s.set_state(a, b)
+    s.sweep(1.3, 1)
+    obj, ga, gb = s.get_sweep()
+    _, pc = s.verify_batch(x, b, per_con=True)
+    for r in (0, 44):
+        C, oga, ogb, want = vals[r]
+        check_objective(obj[r], C, float(sum(w)), what=f"{name} {knobs}")
+        check_gradient(ga[:, r], oga, what=f"{name} grad_a {knobs}")
+        check_gradient(gb[:, r], ogb, what=f"{name} grad_b {knobs}")
+        assert np.array_equal(pc[:, r].astype(int), want)
