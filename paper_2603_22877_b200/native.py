@@ -44,6 +44,16 @@ class Stats(C.Structure):
 
 
 if not os.path.exists(LIB_PATH):
+    # A fresh checkout: compile it (nvcc, sm_100a) rather than fall back to anything.
+    import importlib.util as _ilu
+    _spec = _ilu.spec_from_file_location("_fsmt_build", os.path.join(HERE, "build.py"))
+    _b = _ilu.module_from_spec(_spec)
+    _spec.loader.exec_module(_b)
+    try:
+        _b.build()
+    except Exception as _e:  # noqa: BLE001
+        raise ImportError(f"libfsmt.so could not be built: {_e}") from _e
+if not os.path.exists(LIB_PATH):
     raise ImportError(f"libfsmt.so not built at {LIB_PATH}: run `python -c 'import __graft_entry__ as g; g.build()'` "
                       "(there is no CPU fallback)")
 lib = C.CDLL(LIB_PATH)
