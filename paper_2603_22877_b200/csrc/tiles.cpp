@@ -608,6 +608,13 @@ const char* erfc_fn() {
     return (e && std::string(e) == "nr") ? "fsmt_half_erfc_nr" : "fsmt_half_erfc";
 }
 
+// FSMT_JIT_PAIR=0: atoms one at a time on the scalar FP32 pipe instead of in pairs on the
+// packed f32x2 pipe (A/B; both bit-identical).
+bool jit_pair() {
+    const char* e = getenv("FSMT_JIT_PAIR");
+    return !(e && e[0] == '0');
+}
+
 // FSMT_JIT_ERFC_VOTE=1: warp-vote per atom, one erfc branch when the warp agrees (A/B,
 // DESIGN.md §9).
 bool erfc_vote() {
@@ -662,6 +669,31 @@ const char* kErfcPrelude =
     "  p = fmaf(p, t, 0.27886807f); p = fmaf(p, t, -0.18628806f); p = fmaf(p, t, 0.09678418f);\n"
     "  p = fmaf(p, t, 0.37409196f); p = fmaf(p, t, 1.00002368f); p = fmaf(p, t, -1.26551223f);\n"
     "  return 0.5f * t * fsmt_ex2((p - z2) * 1.44269504088896341f);\n"
+    "}\n"
+    "// Two atoms at once on the packed fp32x2 pipe (FFMA2/FMUL2, sm_100): per component exactly\n"
+    "// the operations of fsmt_half_erfc (each f32x2 lane rounds like the scalar op), so the\n"
+    "// result is bit-identical while the issue count of the polynomial halves.\n"
+    "#define FSMT_C2(v) make_float2(v, v)\n"
+    "__device__ __forceinline__ float2 fsmt_half_erfc2(float2 z, float2& ez) {\n"
+    "  const float2 z2 = __fmul2_rn(z, z);\n"
+    "  const float2 ea = __fmul2_rn(FSMT_C2(-1.44269504088896341f), z2);\n"
+    "  ez = make_float2(fsmt_ex2(ea.x), fsmt_ex2(ea.y));\n"
+    "  float2 p = FSMT_C2(-3.380429407e-04f);\n"
+    "  p = __ffma2_rn(p, z2, FSMT_C2(2.5579733775e-03f)); p = __ffma2_rn(p, z2, FSMT_C2(-1.3417707755e-02f));\n"
+    "  p = __ffma2_rn(p, z2, FSMT_C2(5.64169623e-02f)); p = __ffma2_rn(p, z2, FSMT_C2(-1.880631e-01f));\n"
+    "  p = __ffma2_rn(p, z2, FSMT_C2(5.641895535e-01f));\n"
+    "  const float2 small = __ffma2_rn(make_float2(-z.x, -z.y), p, FSMT_C2(0.5f));\n"
+    "  const float2 den = __ffma2_rn(FSMT_C2(0.5f), z, FSMT_C2(1.f));\n"
+    "  float2 t;\n"
+    "  asm(\"rcp.approx.ftz.f32 %0, %1;\" : \"=f\"(t.x) : \"f\"(den.x));\n"
+    "  asm(\"rcp.approx.ftz.f32 %0, %1;\" : \"=f\"(t.y) : \"f\"(den.y));\n"
+    "  float2 q = FSMT_C2(4.469624162e-02f);\n"
+    "  q = __ffma2_rn(q, t, FSMT_C2(-1.088827997e-01f)); q = __ffma2_rn(q, t, FSMT_C2(3.824992850e-02f));\n"
+    "  q = __ffma2_rn(q, t, FSMT_C2(3.101851977e-02f)); q = __ffma2_rn(q, t, FSMT_C2(8.971593529e-02f));\n"
+    "  q = __ffma2_rn(q, t, FSMT_C2(1.233071312e-01f)); q = __ffma2_rn(q, t, FSMT_C2(1.410502791e-01f));\n"
+    "  q = __ffma2_rn(q, t, FSMT_C2(1.410473883e-01f));\n"
+    "  const float2 tail = __fmul2_rn(__fmul2_rn(t, q), ez);\n"
+    "  return make_float2(z.x < 0.75f ? small.x : tail.x, z.y < 0.75f ? small.y : tail.y);\n"
     "}\n"
     "__device__ __forceinline__ float fsmt_half_erfc_nr(float z, float& ez) {\n"
     "  const float z2 = z * z;\n"
@@ -778,7 +810,63 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
     uint32_t aw = 1 + ((uint32_t)nr + 1) / 2;
     std::vector<uint32_t> coef_word(nr, 0);
     const uint32_t sign_word = 1 + ((uint32_t)nr + 1) / 2;   // symmetric classes: literal signs
+    // atom pairs for the packed f32x2 pipe: consecutive atom slots with equal nnz and equal
+    // class-constant status of 1/||q|| (their words are consecutive in the record)
+    std::vector<int> pair_with(ns, -1), pair_second(ns, 0);
+    if (jit_pair() && fast_erfc() && !erfc_vote() && std::string(erfc_fn()) == "fsmt_half_erfc") {
+        int pend = -1;
+        uint32_t awp = 1 + ((uint32_t)nr + 1) / 2, pend_aw = 0;
+        for (size_t s = 0, ai = 0; s < ns; ++s) {
+            if (t.kinds[s] != 1) continue;
+            const uint32_t nz = K.nnz[ai];
+            const bool ic = K.wpos[awp + 1] < 0;
+            if (pend >= 0 && K.nnz[ai - 1] == nz && (K.wpos[pend_aw + 1] < 0) == ic) {
+                pair_with[(size_t)pend] = (int)s;
+                pair_second[s] = 1;
+                pend = -1;
+            } else {
+                pend = (int)s;
+                pend_aw = awp;
+            }
+            awp += 2 + nz;
+            ++ai;
+        }
+    }
     for (size_t s = 0, ai = 0; s < ns; ++s) {
+        if (t.kinds[s] == 1 && pair_second[s]) {   // emitted with its partner
+            aw += 2 + K.nnz[ai++];
+            continue;
+        }
+        if (t.kinds[s] == 1 && pair_with[s] >= 0) {
+            const size_t b = (size_t)pair_with[s];
+            const uint32_t nnz = K.nnz[ai++], awb = aw + 2 + nnz;
+            const std::string sa = std::to_string(s), sb = std::to_string(b);
+            o << "    float2 zp" << sa << " = make_float2(-__uint_as_float(" << word(aw) << "), -__uint_as_float(" << word(awb) << "));\n";
+            o << "    const float inv" << sa << " = __uint_as_float(" << word(aw + 1) << "), inv" << sb << " = __uint_as_float("
+              << word(awb + 1) << ");\n";
+            for (uint32_t k = 0; k < nnz; ++k) {
+                coef_word[slot_ref0[s] + k] = aw + 2 + k;
+                coef_word[slot_ref0[b] + k] = awb + 2 + k;
+                o << "    zp" << sa << " = __ffma2_rn(make_float2(__uint_as_float(" << word(aw + 2 + k) << "), __uint_as_float("
+                  << word(awb + 2 + k) << ")), make_float2(val" << slot_ref0[s] + k << ", val" << slot_ref0[b] + k << "), zp" << sa << ");\n";
+            }
+            if (K.wpos[aw + 1] < 0)
+                o << "    const float2 up" << sa << " = __fmul2_rn(zp" << sa << ", make_float2(kq * inv" << sa << ", kq * inv" << sb << "));\n";
+            else
+                o << "    const float2 up" << sa << " = __fmul2_rn(__fmul2_rn(FSMT_C2(kq), zp" << sa << "), make_float2(inv" << sa
+                  << ", inv" << sb << "));\n";
+            o << "    const float u" << sa << " = up" << sa << ".x, u" << sb << " = up" << sa << ".y;\n"
+              << "    float2 ezp" << sa << ";\n"
+              << "    const float2 ep" << sa << " = fsmt_half_erfc2(make_float2(fabsf(u" << sa << "), fabsf(u" << sb << ")), ezp" << sa << ");\n"
+              << "    const float2 omp" << sa << " = __fadd2_rn(FSMT_C2(1.f), make_float2(-ep" << sa << ".x, -ep" << sa << ".y));\n"
+              << "    const float pt" << sa << " = u" << sa << " >= 0.f ? ep" << sa << ".x : omp" << sa << ".x;\n"
+              << "    const float pf" << sa << " = u" << sa << " >= 0.f ? omp" << sa << ".x : ep" << sa << ".x;\n"
+              << "    const float pt" << sb << " = u" << sb << " >= 0.f ? ep" << sa << ".y : omp" << sa << ".y;\n"
+              << "    const float pf" << sb << " = u" << sb << " >= 0.f ? omp" << sa << ".y : ep" << sa << ".y;\n"
+              << "    const float2 ddp" << sa << " = __fmul2_rn(make_float2(dcoef * inv" << sa << ", dcoef * inv" << sb << "), ezp" << sa << ");\n";
+            aw += 2 + nnz;
+            continue;
+        }
         if (t.kinds[s] == 0) {
             o << "    const float pt" << s << " = 0.5f * (1.f - val" << slot_ref0[s] << "), pf" << s << " = 0.5f * (1.f + val"
               << slot_ref0[s] << ");\n";
@@ -953,7 +1041,14 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
             // dCOP/dp_true of the row = -dCOP/dp_true of a negated literal
             accum(slot_ref0[s], "w", "(sg" + std::to_string(s) + " ? -G" + std::to_string(s) + " : G" + std::to_string(s) + ")");
         } else {
-            o << "    const float gd" << s << " = w * G" << s << " * dd" << s << ";\n";
+            if (pair_with[s] >= 0) {
+                const std::string sa = std::to_string(s), sb = std::to_string(pair_with[s]);
+                o << "    const float2 gdp" << sa << " = __fmul2_rn(__fmul2_rn(FSMT_C2(w), make_float2(G" << sa << ", G" << sb
+                  << ")), ddp" << sa << ");\n"
+                  << "    const float gd" << sa << " = gdp" << sa << ".x, gd" << sb << " = gdp" << sa << ".y;\n";
+            } else if (!pair_second[s]) {
+                o << "    const float gd" << s << " = w * G" << s << " * dd" << s << ";\n";
+            }
             size_t ai = 0;
             for (size_t s2 = 0; s2 < s; ++s2) ai += t.kinds[s2] == 1;
             for (uint32_t k = 0; k < K.nnz[ai]; ++k) {
