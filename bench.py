@@ -46,6 +46,7 @@ def parse_args():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-prepare", action="store_true", help="generic kernels (no fsmt_prepare(R))")
     return p.parse_args()
 
 
@@ -190,9 +191,11 @@ def main():
     t0 = time.perf_counter()
     s.load_formula(inst.text)
     s.build_xbdd()
+    R = args.restarts
+    if not args.no_prepare:
+        s.prepare(R)                  # kernels specialised for R restarts (part of the build)
     build_s = time.perf_counter() - t0
     dims = s.get_dims()
-    R = args.restarts
     S = args.pgd_steps
     s.set_params(eta=0.01, eps=1e-2)
     stream = torch.cuda.current_stream()
@@ -287,7 +290,8 @@ def main():
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": f"{args.config}: placement-10k, {dims['n_bool'] + dims['n_real']} vars / "
                                    f"{dims['n_cons']} constraints" if args.config == "cfg4" else args.config,
-                       "restarts_per_gpu": R, "global_restarts": R * world, "pgd_steps_per_stage": S,
+                       "restarts_per_gpu": R, "global_restarts": R * world,
+                       "kernels": "generic" if args.no_prepare else "specialised for R (fsmt_prepare)", "pgd_steps_per_stage": S,
                        "kappa": KAPPA, "parallelism": f"restart-sharded x{world}",
                        "l2": "inputs exceed L2 (U counters %.0f MB + structure + state per step)" % (dims["n_cons"] * R / 1e6),
                        "accumulation": "fp64", "build_s": round(build_s, 2)},

@@ -123,6 +123,15 @@ fsmt_status fsmt_load_formula(fsmt_ctx* ctx, const char* hsmt, size_t len);
  * node_budget: max decision nodes per constraint (0 -> 32767, also the encoding limit). */
 fsmt_status fsmt_build_xbdd(fsmt_ctx* ctx, uint64_t node_budget);
 
+/* Optional, after fsmt_build_xbdd: compile a second copy of the specialised sweep/check
+ * kernels (K1, K5; DESIGN.md §7 item 10) with the restart count R as a compile-time
+ * constant (NVRTC, about 1-3 s, host only).  Every later launch over a state of exactly R
+ * restarts (fsmt_begin / fsmt_solve with restarts == R) uses it; other R keep the generic
+ * kernels.  Results are bit-identical to the generic kernels.  R == 0 drops the copy.
+ * FSMT_ERR_STATE before build; FSMT_ERR_CUDA if the compile fails (the generic kernels stay
+ * in use); OK and no effect when the formula has no specialised kernel classes. */
+fsmt_status fsmt_prepare(fsmt_ctx* ctx, uint32_t R);
+
 fsmt_status fsmt_get_dims(const fsmt_ctx* ctx, fsmt_dims* out);
 /* Projection bounds lo[n_real], hi[n_real] (host, f32; +-inf when unbounded). */
 fsmt_status fsmt_get_bounds(const fsmt_ctx* ctx, float* lo, float* hi);

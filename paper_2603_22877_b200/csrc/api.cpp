@@ -36,6 +36,8 @@ struct fsmt_ctx {
     Plan plan;
     std::string jit_src, jit_error;
     JitKernel jit;
+    JitKernel jit_r;            // fsmt_prepare(R): the same module with R a compile-time constant
+    uint32_t jit_r_R = 0;
     DevTiles T{};
     DevSlots slots{};                  // slot tables of the symmetric JIT classes (has_sym)
     cudaGraphExec_t gexec = nullptr;   // fsmt_run_stage's PGD steps as one CUDA graph (re-used, updated)
@@ -161,6 +163,8 @@ void drop_formula(fsmt_ctx* ctx) {
     free_list(ctx->fallocs);
     ctx->F = DevFormula{};
     jit_release(ctx->jit);
+    jit_release(ctx->jit_r);
+    ctx->jit_r_R = 0;
     ctx->T = DevTiles{};
     ctx->T_all = DevTiles{};
     ctx->slots = DevSlots{};
@@ -714,10 +718,41 @@ fsmt_status fsmt_jit_check(fsmt_ctx* ctx, size_t* cubin_bytes, char* log, size_t
     return FSMT_OK;
 }
 
+fsmt_status fsmt_prepare(fsmt_ctx* ctx, uint32_t R) {
+    fsmt_status s = need(ctx, 2, "fsmt_prepare");
+    if (s) return s;
+    if (R == 0 || !ctx->jit.kernel || ctx->host_only) {
+        jit_release(ctx->jit_r);
+        ctx->jit_r_R = 0;
+        return FSMT_OK;
+    }
+    if (ctx->jit_r.kernel && ctx->jit_r_R == R) return FSMT_OK;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);   // the previous copy may still be in flight
+    jit_release(ctx->jit_r);
+    ctx->jit_r_R = 0;
+    // U[c][r] (1 B per constraint and restart) larger than ~1.5x the 126 MB L2 comes from HBM
+    // every sweep: the sweep then loads it 3 constraints ahead (cfg4 9.78 ->
+    // 8.85 ms; cfg3, whose 117 MB of U stays in L2, is faster without)
+    const int upf = (double)ctx->plan.jit_cons_end * R > 192e6 ? 3 : 0;
+    const std::string src = upf ? jit_source(ctx->f, ctx->b, ctx->plan, upf) : ctx->jit_src;
+    std::string err;
+    if (!jit_compile("#define FSMT_RC " + std::to_string(R) + "u\n" + src, ctx->jit_r, err))
+        return fail(ctx, FSMT_ERR_CUDA, "fsmt_prepare: " + err);
+    ctx->jit_r_R = R;
+    return FSMT_OK;
+}
+
 size_t fsmt_jit_source(const fsmt_ctx* ctx, char* buf, size_t len) {
     if (!ctx || ctx->stage < 2) return 0;
     if (buf && len) snprintf(buf, len, "%s", ctx->jit_src.c_str());
     return ctx->jit_src.size() + 1;
+}
+
+// the JIT module for a launch over R restarts: the R-specialised copy when fsmt_prepare(R)
+// built one, else the generic module
+static const JitKernel& jk(const fsmt_ctx* ctx, uint32_t R) {
+    return (ctx->jit_r.kernel && ctx->jit_r_R == R) ? ctx->jit_r : ctx->jit;
 }
 
 static fsmt_status sweep_impl(fsmt_ctx* ctx, float kappa, uint32_t stage_t, double* terms, uint32_t terms_r) {
@@ -733,11 +768,11 @@ static fsmt_status sweep_impl(fsmt_ctx* ctx, float kappa, uint32_t stage_t, doub
         if (sym) {   // shared slot probabilities for the symmetric classes
             const DevSlots& D = ctx->slots;
             CK(cudaMemsetAsync(D.GU, 0, ((size_t)D.nv + D.n_sa) * S.R * 8, ctx->stream));
-            launch_slot_prob(ctx->jit.kprob, F, S, D, kappa, ctx->stream);
+            launch_slot_prob(jk(ctx, S.R).kprob, F, S, D, kappa, ctx->stream);
             ctx->launches += 1;
         }
         if (ctx->T.n_tiles) {
-            launch_sweep_jit(ctx->jit.kernel, F, S, ctx->T, kappa, ws, terms, terms_r, ctx->stream, &ctx->slots);
+            launch_sweep_jit(jk(ctx, S.R).kernel, F, S, ctx->T, kappa, ws, terms, terms_r, ctx->stream, &ctx->slots);
             ctx->launches += 1;
         }
         if (F.generic_begin < F.generic_end) {
@@ -745,7 +780,7 @@ static fsmt_status sweep_impl(fsmt_ctx* ctx, float kappa, uint32_t stage_t, doub
             ctx->launches += 1;
         }
         if (sym) {
-            launch_slot_chain(ctx->jit.kchain, F, S, ctx->slots, ctx->stream);
+            launch_slot_chain(jk(ctx, S.R).kchain, F, S, ctx->slots, ctx->stream);
             ctx->launches += 1;
         }
     }
@@ -765,10 +800,10 @@ static fsmt_status update_impl(fsmt_ctx* ctx, float eta, float eps, float eta_b 
 static void verify_rounded(fsmt_ctx* ctx, const DevState& S2, uint8_t* U_update) {
     if (ctx->T.n_tiles && ctx->jit.kernel5) {    // specialised check of this context's tiles
         if (ctx->has_sym) {
-            launch_slot_truth(ctx->jit.ktruth, ctx->F, S2, ctx->slots, S2.x, S2.b, ctx->stream);
+            launch_slot_truth(jk(ctx, S2.R).ktruth, ctx->F, S2, ctx->slots, S2.x, S2.b, ctx->stream);
             ctx->launches += 1;
         }
-        launch_verify_jit(ctx->jit.kernel5, ctx->F, S2, ctx->T, S2.x, S2.b, U_update, nullptr, ctx->stream, ctx->slots.TT);
+        launch_verify_jit(jk(ctx, S2.R).kernel5, ctx->F, S2, ctx->T, S2.x, S2.b, U_update, nullptr, ctx->stream, ctx->slots.TT);
         launch_verify(ctx->F, S2, S2.x, S2.b, U_update, nullptr, ctx->stream, ctx->F.generic_begin, ctx->F.generic_end);
         ctx->launches += 2;
     } else {
@@ -1078,10 +1113,10 @@ fsmt_status fsmt_verify_batch(fsmt_ctx* ctx, uint32_t R, const int8_t* x, const 
             if (dtt) {
                 DevSlots D2 = ctx->slots;
                 D2.TT = dtt;
-                launch_slot_truth(ctx->jit.ktruth, F, T, D2, dx, dy, ctx->stream);
+                launch_slot_truth(jk(ctx, R).ktruth, F, T, D2, dx, dy, ctx->stream);
                 ctx->launches += 1;
             }
-            launch_verify_jit(ctx->jit.kernel5, F, T, ctx->T_all, dx, dy, nullptr, dpc, ctx->stream, dtt);
+            launch_verify_jit(jk(ctx, R).kernel5, F, T, ctx->T_all, dx, dy, nullptr, dpc, ctx->stream, dtt);
             launch_verify(F, T, dx, dy, nullptr, dpc, ctx->stream, ctx->plan.jit_cons_end, F.n_cons);
             ctx->launches += 2;
         } else {

@@ -171,7 +171,8 @@ struct Plan {
 
 Plan make_plan(const Formula& f, const Built& b, bool enable_jit);
 // CUDA source of the specialised sweep kernel for the plan's JIT classes.
-std::string jit_source(const Formula& f, const Built& b, const Plan& p);
+// u_prefetch_default: how many constraints ahead the sweep loads U (FSMT_JIT_UPF overrides)
+std::string jit_source(const Formula& f, const Built& b, const Plan& p, int u_prefetch_default = 0);
 
 struct BuildError {
     std::string msg;

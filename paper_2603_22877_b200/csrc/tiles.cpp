@@ -615,6 +615,20 @@ bool jit_pair() {
     return !(e && e[0] == '0');
 }
 
+// FSMT_JIT_UPF=d: the sweep loads U[c][r] d constraints ahead (0: in the iteration, plain load).
+// Without the variable: g_upf (jit_source's argument; fsmt_prepare picks it from the size of U).
+int g_upf = 0;
+int u_prefetch() {
+    const char* e = getenv("FSMT_JIT_UPF");
+    return e ? std::max(0, std::min(12, atoi(e))) : g_upf;
+}
+
+// FSMT_JIT_UCS=1: the prefetched U loads carry the evict-first (streaming) hint.
+bool u_streaming() {
+    const char* e = getenv("FSMT_JIT_UCS");
+    return e && e[0] == '1';
+}
+
 // FSMT_JIT_ERFC_VOTE=1: warp-vote per atom, one erfc branch when the warp agrees (A/B,
 // DESIGN.md §9).
 bool erfc_vote() {
@@ -631,6 +645,14 @@ const char* kErfcPrelude =
     "  const float f2 = __uint_as_float((127u + ((u >> 7) << 6)) << 23);\n"
     "  return __fmul_rn(__fmul_rn(__fmul_rn(w, f1), f2), f2);\n"
     "}\n"
+    "// fsmt_prepare(R): the module compiled with FSMT_RC = R takes the restart count as a constant,\n"
+    "// so every [var][R] row offset (k * 4R bytes) folds into the load's immediate offset.  The\n"
+    "// launcher uses that module only for a state of exactly R restarts.\n"
+    "#ifdef FSMT_RC\n"
+    "#define FSMT_SPECIALISE_R R = FSMT_RC;\n"
+    "#else\n"
+    "#define FSMT_SPECIALISE_R\n"
+    "#endif\n"
     "#define FSMT_AT(base, off) (*(const float*)((const char*)(base) + (off)))\n"
     "__device__ __forceinline__ float fsmt_ex2(float x) { float r; asm(\"ex2.approx.ftz.f32 %0, %1;\" : \"=f\"(r) : \"f\"(x)); return r; }\n"
     "// 0.5*erfc(z) for z >= 0 and ez = exp(-z^2) (dd/db factor, P:1326-1327).  Coefficients from\n"
@@ -775,9 +797,25 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
         return "if (live) atomicAdd(" + dst + ", (double)acc" + std::to_string(i) + ");";
     };
     auto gm = [&](size_t h, size_t m) { return "gcur" + std::to_string(h) + " + (" + std::to_string(K.aff_dg[m]) + ")"; };
+    // ERWA counters: a streaming (evict-first) byte load per constraint, issued u_prefetch()
+    // constraints ahead so its DRAM latency overlaps the passes of the current constraints
+    const int upf = u_prefetch();
+    const char* uld = u_streaming() ? "__ldcs" : "__ldg";
+    if (upf > 0) {
+        o << "  const unsigned char* Up = U ? U + (u64)T.cons_begin * R + rr : nullptr;\n";
+        for (int k = 0; k < upf; ++k)
+            o << "  u32 un" << k << " = (U && " << k << "u < T.n_cons) ? (u32)" << uld << "(Up + (u64)" << k << "u * R) : 0u;\n";
+    }
     o << "  for (u32 c = 0; c < T.n_cons; ++c, rp += " << K.stride4 << ") {\n";
     for (uint32_t q = 0; q < K.stride4; ++q) o << "    const uint4 q" << q << " = __ldg(rp + " << q << ");\n";
-    o << "    const u32 uc = U ? (u32)U[(u64)(T.cons_begin + c) * R + rr] : 0u;\n";
+    if (upf > 0) {
+        o << "    const u32 uc = un0;\n";
+        for (int k = 0; k + 1 < upf; ++k) o << "    un" << k << " = un" << k + 1 << ";\n";
+        o << "    if (U) un" << upf - 1 << " = c + " << upf << "u < T.n_cons ? (u32)" << uld << "(Up + (u64)(c + " << upf
+          << "u) * R) : 0u;\n";
+    } else {
+        o << "    const u32 uc = U ? (u32)U[(u64)(T.cons_begin + c) * R + rr] : 0u;\n";
+    }
     o << "    float w = __uint_as_float(" << word(0) << ") * wscale;\n"
          "    if (U) w = fsmt_pow2_u8(w, uc);\n";
     for (size_t i = 0; i < nr; ++i) {
@@ -1208,7 +1246,8 @@ void emit_verify_class(std::ostringstream& o, uint32_t kid, const KClass& K, con
 
 }  // namespace
 
-std::string jit_source(const Formula& f, const Built& b, const Plan& p) {
+std::string jit_source(const Formula& f, const Built& b, const Plan& p, int u_prefetch_default) {
+    g_upf = u_prefetch_default;
     std::ostringstream o;
     o << "// generated by fsmt tiles.cpp: specialised K1 sweep for " << p.n_jit_kclasses << " kernel classes\n"
          "typedef unsigned int u32;\ntypedef unsigned long long u64;\n"
@@ -1226,6 +1265,7 @@ std::string jit_source(const Formula& f, const Built& b, const Plan& p) {
          "    double* __restrict__ obj, u32 R, u32 n_bool, float kappa, float wscale,\n"
          "    double* __restrict__ terms, u32 terms_r, const u32* __restrict__ orig,\n"
          "    const float* __restrict__ PT, const float* __restrict__ PF, double* __restrict__ gu) {\n"
+         "  FSMT_SPECIALISE_R\n"
          "  extern __shared__ float smem[];\n"
          "  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;\n"
          "  float* acc = smem + warp * (VMAX * 32);                  // stream-variable rows\n"
@@ -1280,6 +1320,7 @@ std::string jit_source(const Formula& f, const Built& b, const Plan& p) {
          "    unsigned char* __restrict__ per_con, const u32* __restrict__ orig, u32 R, u32 n_bool,\n"
          "    const u32* __restrict__ arow, const double* __restrict__ aval, const double* __restrict__ arhs,\n"
          "    const unsigned char* __restrict__ astrict, const unsigned char* __restrict__ TT) {\n"
+         "  FSMT_SPECIALISE_R\n"
          "  extern __shared__ float smem[];\n"
          "  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;\n"
          "  u32* vs = (u32*)smem + warp * VTOT;\n"

@@ -66,6 +66,11 @@ class Solver:
         self._check(N.lib.fsmt_get_dims(self._h, C.byref(d)))
         self.dims = d
 
+    def prepare(self, R: int):
+        """Compile the specialised kernels once more with R restarts as a constant (fsmt_prepare);
+        launches over exactly R restarts use that copy (bit-identical, fewer instructions)."""
+        self._check(N.lib.fsmt_prepare(self._h, int(R)))
+
     def get_dims(self) -> dict:
         d = N.Dims()
         self._check(N.lib.fsmt_get_dims(self._h, C.byref(d)))

@@ -45,6 +45,7 @@ def main():
     t0 = time.perf_counter()
     s.load_formula(inst.text)
     s.build_xbdd()
+    s.prepare(a.restarts)
     build_s = time.perf_counter() - t0
     kappas = [float(x) for x in a.kappas.split(",")] if a.kappas else None
     if a.schedule:

@@ -23,6 +23,8 @@ KNOBS = [
     {"FSMT_JIT_ERFC": "nr", "FSMT_JIT_ERFC_VOTE": "1"},
     {"FSMT_JIT_ERFC": "cuda"},
     {"FSMT_JIT_STREAM": "0"},
+    {"FSMT_JIT_PAIR": "0", "FSMT_JIT_UPF": "0"},
+    {"FSMT_JIT_UPF": "3"},
     {"FSMT_TILE_VMAX": "16", "FSMT_TILE_RMAX": "16", "FSMT_TILE_CMAX": "3"},
 ]
 
@@ -78,3 +80,47 @@ def test_knob_parity(name, knobs):
         check_gradient(ga[:, r], oga, what=f"{name} grad_a {knobs}")
         check_gradient(gb[:, r], ogb, what=f"{name} grad_b {knobs}")
         assert np.array_equal(pc[:, r].astype(int), want)
+
+
+@pytest.mark.parametrize("name", ["cfg3s", "cfg4s", "cfg2"])
+def test_prepared_r_bit_identical(name):
+    """fsmt_prepare(R) (restart count compiled in, DESIGN.md §7 item 10) changes no bit: sweep,
+    stage end (rounding, exact check, ERWA counters) and a second weighted sweep equal the
+    generic kernels'; another R still runs the generic module; and the values match the oracle."""
+    import paper_2603_22877_b200 as P
+    inst, f, a, b, x, w, vals = oracle_case(name)
+    R = 45
+    out = []
+    for prep in (0, R):
+        s = P.Solver(0)
+        s.load_formula(inst.text)
+        s.build_xbdd()
+        if prep:
+            s.prepare(prep)
+            s.prepare(prep)                  # idempotent
+        s.begin(R, 3)
+        s.set_state(a, b)
+        s.sweep(1.3, 1)
+        r1 = s.get_sweep()
+        unsat = s.stage_end(1)
+        s.sweep(0.7, 3)
+        r2 = s.get_sweep()
+        _, pc = s.verify_batch(x, b, per_con=True)
+        out.append((r1, np.array(unsat), r2, pc, s.get_counters()))
+        if prep:
+            s.begin(64, 3)                   # not the prepared R: generic module
+            s.sweep(1.0, 1)
+            assert np.all(np.isfinite(s.get_sweep()[0]))
+            s.prepare(0)                     # dropped
+    (g1, gu, g2, gpc, gU), (p1, pu, p2, ppc, pU) = out
+    # per-term arithmetic is identical; the fp64 atomic accumulation order is not fixed, so the
+    # sums agree to fp64 rounding
+    for A, B in zip(g1 + g2, p1 + p2):
+        np.testing.assert_allclose(A, B, rtol=1e-12, atol=1e-12)
+    assert np.array_equal(gu, pu) and np.array_equal(gpc, ppc) and np.array_equal(gU, pU)
+    for r in (0, 44):
+        C, oga, ogb, want = vals[r]
+        check_objective(p1[0][r], C, float(sum(w)), what=f"{name} prepared")
+        check_gradient(p1[1][:, r], oga, what=f"{name} prepared grad_a")
+        check_gradient(p1[2][:, r], ogb, what=f"{name} prepared grad_b")
+        assert np.array_equal(ppc[:, r].astype(int), want)
