@@ -705,17 +705,39 @@ fsmt_status fsmt_jit_info(const fsmt_ctx* ctx, uint32_t* n_jit_classes, uint32_t
     return FSMT_OK;
 }
 
+static std::string prepared_source(const fsmt_ctx* ctx, uint32_t R, bool& lane2);
+
 fsmt_status fsmt_jit_check(fsmt_ctx* ctx, size_t* cubin_bytes, char* log, size_t log_len) {
     if (!ctx) return FSMT_ERR_ARG;
     if (ctx->stage < 2) return fail(ctx, FSMT_ERR_STATE, "fsmt_jit_check: build first");
     if (ctx->jit_src.empty()) return fail(ctx, FSMT_ERR_STATE, "fsmt_jit_check: no JIT classes");
     std::vector<char> cubin;
     std::string lg, err;
-    bool ok = jit_cubin(ctx->jit_src, cubin, lg, err);
+    // FSMT_JIT_CHECK_RC=R: check the module fsmt_prepare(R) would build (register counts)
+    std::string src = ctx->jit_src;
+    if (const char* rc = getenv("FSMT_JIT_CHECK_RC")) {
+        bool lane2 = false;
+        src = prepared_source(ctx, (uint32_t)atoi(rc), lane2);
+    }
+    bool ok = jit_cubin(src, cubin, lg, err);
     if (log && log_len) snprintf(log, log_len, "%s", lg.c_str());
     if (!ok) return fail(ctx, FSMT_ERR_CUDA, err);
     if (cubin_bytes) *cubin_bytes = cubin.size();
     return FSMT_OK;
+}
+
+// The source fsmt_prepare(R) compiles: the restart count as a constant (FSMT_RC); U loaded 3
+// constraints ahead when U[c][r] (1 B per constraint and restart) exceeds ~1.5x the 126 MB L2
+// and so comes from HBM every sweep (cfg4 9.78 -> 8.85 ms; cfg3, whose 117 MB
+// of U stays in L2, is faster without); opt-in (FSMT_JIT_LANE2=1) two restarts per lane on the
+// f32x2 pipe when R is even (float2 loads of a lane's two restarts) and there are no symmetric
+// classes: 32 % fewer instructions per eval but 126 registers (16 warps/SM), slower on cfg3/cfg4.
+static std::string prepared_source(const fsmt_ctx* ctx, uint32_t R, bool& lane2) {
+    const int upf = (double)ctx->plan.jit_cons_end * R > 192e6 ? 3 : 0;
+    const char* l2e = getenv("FSMT_JIT_LANE2");
+    lane2 = R % 2 == 0 && !ctx->plan.has_sym && l2e && l2e[0] == '1';
+    const std::string src = (upf || lane2) ? jit_source(ctx->f, ctx->b, ctx->plan, upf, lane2) : ctx->jit_src;
+    return "#define FSMT_RC " + std::to_string(R) + "u\n" + src;
 }
 
 fsmt_status fsmt_prepare(fsmt_ctx* ctx, uint32_t R) {
@@ -731,22 +753,25 @@ fsmt_status fsmt_prepare(fsmt_ctx* ctx, uint32_t R) {
     cudaStreamSynchronize(ctx->stream);   // the previous copy may still be in flight
     jit_release(ctx->jit_r);
     ctx->jit_r_R = 0;
-    // U[c][r] (1 B per constraint and restart) larger than ~1.5x the 126 MB L2 comes from HBM
-    // every sweep: the sweep then loads it 3 constraints ahead (cfg4 9.78 ->
-    // 8.85 ms; cfg3, whose 117 MB of U stays in L2, is faster without)
-    const int upf = (double)ctx->plan.jit_cons_end * R > 192e6 ? 3 : 0;
-    const std::string src = upf ? jit_source(ctx->f, ctx->b, ctx->plan, upf) : ctx->jit_src;
+    bool lane2 = false;
+    const std::string src = prepared_source(ctx, R, lane2);
     std::string err;
-    if (!jit_compile("#define FSMT_RC " + std::to_string(R) + "u\n" + src, ctx->jit_r, err))
+    if (!jit_compile(src, ctx->jit_r, err))
         return fail(ctx, FSMT_ERR_CUDA, "fsmt_prepare: " + err);
+    ctx->jit_r.rpl = lane2 ? 2 : 1;
     ctx->jit_r_R = R;
     return FSMT_OK;
 }
 
 size_t fsmt_jit_source(const fsmt_ctx* ctx, char* buf, size_t len) {
     if (!ctx || ctx->stage < 2) return 0;
-    if (buf && len) snprintf(buf, len, "%s", ctx->jit_src.c_str());
-    return ctx->jit_src.size() + 1;
+    std::string src = ctx->jit_src;
+    if (const char* rc = getenv("FSMT_JIT_CHECK_RC")) {   // the source fsmt_prepare(R) would compile
+        bool lane2 = false;
+        if (!src.empty()) src = prepared_source(ctx, (uint32_t)atoi(rc), lane2);
+    }
+    if (buf && len) snprintf(buf, len, "%s", src.c_str());
+    return src.size() + 1;
 }
 
 // the JIT module for a launch over R restarts: the R-specialised copy when fsmt_prepare(R)
@@ -772,7 +797,7 @@ static fsmt_status sweep_impl(fsmt_ctx* ctx, float kappa, uint32_t stage_t, doub
             ctx->launches += 1;
         }
         if (ctx->T.n_tiles) {
-            launch_sweep_jit(jk(ctx, S.R).kernel, F, S, ctx->T, kappa, ws, terms, terms_r, ctx->stream, &ctx->slots);
+            launch_sweep_jit(jk(ctx, S.R).kernel, jk(ctx, S.R).rpl, F, S, ctx->T, kappa, ws, terms, terms_r, ctx->stream, &ctx->slots);
             ctx->launches += 1;
         }
         if (F.generic_begin < F.generic_end) {

@@ -14,6 +14,7 @@ struct JitKernel {
     cudaKernel_t kchain = nullptr;     // fsmt_kc_jit (slot-table gradients -> grad_a / grad_b)
     cudaKernel_t ktruth = nullptr;     // fsmt_kt_jit (slot truth table for the exact check)
     size_t cubin_bytes = 0;
+    uint32_t rpl = 1;                  // restarts per lane of fsmt_k1_jit (2: f32x2 module of fsmt_prepare)
     std::string log;
 };
 

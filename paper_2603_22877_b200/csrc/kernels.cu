@@ -400,14 +400,14 @@ void launch_scatter_rows_u8(uint8_t* dst, const uint8_t* src, const uint32_t* id
     k_gather_rows_u8<<<148 * 8, 256, 0, st>>>(dst, src, idx, rows, R, 1);
 }
 
-void launch_sweep_jit(cudaKernel_t k, const DevFormula& F, const DevState& S, const DevTiles& T, float kappa,
+void launch_sweep_jit(cudaKernel_t k, uint32_t rpl, const DevFormula& F, const DevState& S, const DevTiles& T, float kappa,
                       float wscale, double* terms, uint32_t terms_r, cudaStream_t st, const DevSlots* D) {
     if (T.n_tiles == 0 || S.R == 0) return;
     const int kJitWarps = (int)(T.warps ? T.warps : 1);
     const int kVmax = (int)T.vmax, kVtot = (int)(T.vmax + T.rmax);    // Plan::vmax, Plan::rmax
-    const uint64_t nw = (uint64_t)T.n_tiles * ((S.R + 31) / 32);
+    const uint64_t nw = (uint64_t)T.n_tiles * ((S.R + 32 * rpl - 1) / (32 * rpl));   // one warp per (tile, 32*rpl restarts)
     const unsigned blocks = (unsigned)((nw + kJitWarps - 1) / kJitWarps);
-    const size_t smem = (size_t)kJitWarps * ((size_t)kVmax * 32 * 4 + (size_t)kVtot * 4);
+    const size_t smem = (size_t)kJitWarps * ((size_t)kVmax * 32 * 4 * rpl + (size_t)kVtot * 4);
     if (smem > 48 * 1024) cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     uint32_t n_tiles = T.n_tiles, R = S.R, n_bool = F.n_bool;
     const uint8_t* U = S.U;

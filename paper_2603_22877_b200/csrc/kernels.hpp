@@ -109,7 +109,7 @@ void launch_slot_truth(cudaKernel_t k, const DevFormula& F, const DevState& S, c
 // K5 (JIT-specialised, tiles): exact check over the tiles of T (+ ERWA counters / per_con).
 void launch_verify_jit(cudaKernel_t k, const DevFormula& F, const DevState& S, const DevTiles& T, const int8_t* x,
                        const float* y, uint8_t* U_update, uint8_t* per_con, cudaStream_t st, const uint8_t* TT = nullptr);
-void launch_sweep_jit(cudaKernel_t k, const DevFormula& F, const DevState& S, const DevTiles& T, float kappa,
+void launch_sweep_jit(cudaKernel_t k, uint32_t rpl, const DevFormula& F, const DevState& S, const DevTiles& T, float kappa,
                       float wscale, double* terms, uint32_t terms_r, cudaStream_t st, const DevSlots* D = nullptr);
 // row gather for u8 matrices: dst[i][:] = src[idx[i]][:]  (U between original and internal order)
 void launch_gather_rows_u8(uint8_t* dst, const uint8_t* src, const uint32_t* idx, uint32_t rows, uint32_t R,

@@ -724,6 +724,35 @@ const char* kErfcPrelude =
     "  return z < 0.75f ? small : tail;\n"
     "}\n\n";
 
+// f32x2 arithmetic for the two-restarts-per-lane sweep: each operator is one packed FADD2 /
+// FMUL2 / FFMA2 whose components round exactly like the scalar op (a - b as a + (-b));
+// float operands broadcast.
+const char* kLane2Prelude =
+    "#define FSMT_Z2 make_float2(0.f, 0.f)\n"
+    "#define FSMT_AT2(base, off) (*(const float2*)((const char*)(base) + (off)))\n"
+    "__device__ __forceinline__ float2 fsmt_b2(float a) { return make_float2(a, a); }\n"
+    "__device__ __forceinline__ float2 fsmt_b2(float2 a) { return a; }\n"
+    "__device__ __forceinline__ float2 operator-(float2 a) { return make_float2(-a.x, -a.y); }\n"
+    "__device__ __forceinline__ float2 operator+(float2 a, float2 b) { return __fadd2_rn(a, b); }\n"
+    "__device__ __forceinline__ float2 operator-(float2 a, float2 b) { return __fadd2_rn(a, -b); }\n"
+    "__device__ __forceinline__ float2 operator*(float2 a, float2 b) { return __fmul2_rn(a, b); }\n"
+    "__device__ __forceinline__ float2 operator+(float a, float2 b) { return __fadd2_rn(fsmt_b2(a), b); }\n"
+    "__device__ __forceinline__ float2 operator+(float2 a, float b) { return __fadd2_rn(a, fsmt_b2(b)); }\n"
+    "__device__ __forceinline__ float2 operator-(float a, float2 b) { return __fadd2_rn(fsmt_b2(a), -b); }\n"
+    "__device__ __forceinline__ float2 operator-(float2 a, float b) { return __fadd2_rn(a, fsmt_b2(-b)); }\n"
+    "__device__ __forceinline__ float2 operator*(float a, float2 b) { return __fmul2_rn(fsmt_b2(a), b); }\n"
+    "__device__ __forceinline__ float2 operator*(float2 a, float b) { return __fmul2_rn(a, fsmt_b2(b)); }\n"
+    "__device__ __forceinline__ float2& operator+=(float2& a, float2 b) { a = a + b; return a; }\n"
+    "__device__ __forceinline__ float2& operator-=(float2& a, float2 b) { a = a - b; return a; }\n"
+    "#define FSMT_FMA2(A, B, C) __device__ __forceinline__ float2 fmaf(A a, B b, C c) { return __ffma2_rn(fsmt_b2(a), fsmt_b2(b), fsmt_b2(c)); }\n"
+    "FSMT_FMA2(float2, float2, float2) FSMT_FMA2(float, float2, float2) FSMT_FMA2(float2, float, float2)\n"
+    "FSMT_FMA2(float2, float2, float) FSMT_FMA2(float, float2, float) FSMT_FMA2(float2, float, float)\n"
+    "FSMT_FMA2(float, float, float2)\n"
+    "__device__ __forceinline__ float2 fsmt_abs2(float2 a) { return make_float2(fabsf(a.x), fabsf(a.y)); }\n"
+    "__device__ __forceinline__ float2 fsmt_sel_ge0(float2 u, float2 a, float2 b) {\n"
+    "  return make_float2(u.x >= 0.f ? a.x : b.x, u.y >= 0.f ? a.y : b.y);\n"
+    "}\n\n";
+
 const char* comp(uint32_t w) {
     static const char* c[] = {"x", "y", "z", "w"};
     return c[w % 4];
@@ -741,14 +770,21 @@ std::string word(uint32_t w) {
     return "q" + std::to_string(w / 4) + "." + comp(w);
 }
 
+// Two restarts per lane (fsmt_prepare with an even R, DESIGN.md §7 item 11): every per-restart
+// value is a float2 (restarts r, r + 1 of the lane), arithmetic on the packed f32x2 pipe through
+// the operator overloads of kLane2Prelude; per component the operations of the scalar sweep.
+bool g_v2 = false;
+
 void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Template& t) {
     g_wk = &K;
+    const std::string TY = g_v2 ? "float2" : "float", ZR = g_v2 ? "FSMT_Z2" : "0.f", AT = g_v2 ? "FSMT_AT2" : "FSMT_AT";
     const size_t ns = t.kinds.size();
     o << "__device__ __forceinline__ void kc" << kid
       << "(const TileDesc& T, const uint4* __restrict__ rp, const u32* __restrict__ vs, const u32* __restrict__ vr,\n"
-         "    float* __restrict__ accs, const float* __restrict__ ab, const float* __restrict__ bb,\n"
+         "    " << TY << "* __restrict__ accs, const float* __restrict__ ab, const float* __restrict__ bb,\n"
          "    double* __restrict__ ga, double* __restrict__ gb, const unsigned char* __restrict__ U,\n"
-         "    u32 R, u32 R4, u64 rr, u32 r, bool live, u32 n_bool, float kq, float dcoef, float wscale, double& objacc,\n"
+         "    u32 R, u32 R4, u64 rr, u32 r, bool live, u32 n_bool, float kq, float dcoef, float wscale, "
+      << (g_v2 ? "double2& objacc" : "double& objacc") << ",\n"
          "    double* __restrict__ terms, u32 terms_r, const u32* __restrict__ orig,\n"
          "    const float* __restrict__ PTl, const float* __restrict__ PFl, double* __restrict__ gu) {\n";
     // refs
@@ -778,7 +814,7 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
     for (size_t i = 0; i < nr; ++i) {
         if (is_stream(i) || alias_of(i) >= 0) continue;
         if (head_of(i) < 0) o << "  u32 cur" << i << " = 0xffffffffu, gcur" << i << " = 0u;";
-        o << " float val" << i << " = 0.f, acc" << i << " = 0.f"
+        o << " " << TY << " val" << i << " = " << ZR << ", acc" << i << " = " << ZR
           << (ref_kind[i] == 2 ? ", vaf" + std::to_string(i) + " = 0.f" : std::string()) << ";\n";
     }
     // value of reference i at byte offset `off` of its column base: Booleans in a (ab), reals
@@ -786,7 +822,7 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
     auto ld_at = [&](size_t i, const std::string& off) {
         const std::string is = std::to_string(i);
         if (ref_kind[i] == 2) return "val" + is + " = FSMT_AT(PTl, " + off + "); vaf" + is + " = FSMT_AT(PFl, " + off + ");";
-        return "val" + is + " = FSMT_AT(" + (ref_kind[i] == 0 ? "ab" : "bb") + ", " + off + ");";
+        return "val" + is + " = " + AT + "(" + (ref_kind[i] == 0 ? "ab" : "bb") + ", " + off + ");";
     };
     auto dgoff = [&](size_t m) { return "(u64)(" + std::to_string(K.aff_dg[m]) + " * (long long)R4)"; };
     // a run accumulator goes straight to the fp64 gradient (one atomic per run); g = the variable
@@ -794,6 +830,9 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
         const std::string dst = ref_kind[i] == 0 ? "ga + (u64)(" + g + ") * R + r"
                               : ref_kind[i] == 2 ? "gu + (u64)(" + g + ") * R + r"
                                                  : "gb + (u64)(" + g + " - n_bool) * R + r";
+        if (g_v2)
+            return "if (live) { atomicAdd(" + dst + ", (double)acc" + std::to_string(i) + ".x); atomicAdd(" + dst + " + 1, (double)acc" +
+                   std::to_string(i) + ".y); }";
         return "if (live) atomicAdd(" + dst + ", (double)acc" + std::to_string(i) + ");";
     };
     auto gm = [&](size_t h, size_t m) { return "gcur" + std::to_string(h) + " + (" + std::to_string(K.aff_dg[m]) + ")"; };
@@ -801,28 +840,36 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
     // constraints ahead so its DRAM latency overlaps the passes of the current constraints
     const int upf = u_prefetch();
     const char* uld = u_streaming() ? "__ldcs" : "__ldg";
+    const std::string ucast = g_v2 ? "(const unsigned short*)" : "";
     if (upf > 0) {
         o << "  const unsigned char* Up = U ? U + (u64)T.cons_begin * R + rr : nullptr;\n";
         for (int k = 0; k < upf; ++k)
-            o << "  u32 un" << k << " = (U && " << k << "u < T.n_cons) ? (u32)" << uld << "(Up + (u64)" << k << "u * R) : 0u;\n";
+            o << "  u32 un" << k << " = (U && " << k << "u < T.n_cons) ? (u32)" << uld << "(" << ucast << "(Up + (u64)" << k << "u * R)) : 0u;\n";
     }
     o << "  for (u32 c = 0; c < T.n_cons; ++c, rp += " << K.stride4 << ") {\n";
     for (uint32_t q = 0; q < K.stride4; ++q) o << "    const uint4 q" << q << " = __ldg(rp + " << q << ");\n";
     if (upf > 0) {
         o << "    const u32 uc = un0;\n";
         for (int k = 0; k + 1 < upf; ++k) o << "    un" << k << " = un" << k + 1 << ";\n";
-        o << "    if (U) un" << upf - 1 << " = c + " << upf << "u < T.n_cons ? (u32)" << uld << "(Up + (u64)(c + " << upf
-          << "u) * R) : 0u;\n";
+        o << "    if (U) un" << upf - 1 << " = c + " << upf << "u < T.n_cons ? (u32)" << uld << "(" << ucast << "(Up + (u64)(c + " << upf
+          << "u) * R)) : 0u;\n";
     } else {
-        o << "    const u32 uc = U ? (u32)U[(u64)(T.cons_begin + c) * R + rr] : 0u;\n";
+        if (g_v2)
+            o << "    const u32 uc = U ? (u32)*(const unsigned short*)(U + (u64)(T.cons_begin + c) * R + rr) : 0u;\n";
+        else
+            o << "    const u32 uc = U ? (u32)U[(u64)(T.cons_begin + c) * R + rr] : 0u;\n";
     }
-    o << "    float w = __uint_as_float(" << word(0) << ") * wscale;\n"
-         "    if (U) w = fsmt_pow2_u8(w, uc);\n";
+    if (g_v2)
+        o << "    const float w0 = __uint_as_float(" << word(0) << ") * wscale;\n"
+             "    const float2 w = U ? make_float2(fsmt_pow2_u8(w0, uc & 255u), fsmt_pow2_u8(w0, uc >> 8)) : make_float2(w0, w0);\n";
+    else
+        o << "    float w = __uint_as_float(" << word(0) << ") * wscale;\n"
+             "    if (U) w = fsmt_pow2_u8(w, uc);\n";
     for (size_t i = 0; i < nr; ++i) {
         uint32_t wd = 1 + (uint32_t)i / 2;
         const std::string ext = "(" + word(wd) + " >> " + std::to_string(16 * (i % 2)) + ") & 0xffffu";
         if (alias_of(i) >= 0) {
-            o << "    const float val" << i << " = val" << alias_of(i) << ";   // alias\n";
+            o << "    const " << TY << " val" << i << " = val" << alias_of(i) << ";   // alias\n";
             continue;
         }
         if (head_of(i) >= 0) continue;   // loaded with its group head
@@ -830,17 +877,17 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
             // stream reference: new variable (almost) every constraint; no run register
             o << "    const u32 sl" << i << " = " << ext << ";\n"
               << "    const u64 so" << i << " = (u64)vs[sl" << i << "] * R4;\n";
-            o << "    float val" << i << (ref_kind[i] == 2 ? ", vaf" + std::to_string(i) : std::string()) << "; " << ld_at(i, "so" + std::to_string(i)) << "\n";
+            o << "    " << TY << " val" << i << (ref_kind[i] == 2 ? ", vaf" + std::to_string(i) : std::string()) << "; " << ld_at(i, "so" + std::to_string(i)) << "\n";
             for (size_t m : members[i])
-                o << "    float val" << m << (ref_kind[m] == 2 ? ", vaf" + std::to_string(m) : std::string()) << "; "
+                o << "    " << TY << " val" << m << (ref_kind[m] == 2 ? ", vaf" + std::to_string(m) : std::string()) << "; "
                   << ld_at(m, "so" + std::to_string(i) + " + " + dgoff(m)) << "   // affine\n";
         } else {
             o << "    { const u32 l = " << ext << "; if (l != cur" << i << ") { if (cur" << i << " != 0xffffffffu) { "
               << flush_run(i, "gcur" + std::to_string(i));
             for (size_t m : members[i]) o << " " << flush_run(m, gm(i, m));
-            o << " } cur" << i << " = l; gcur" << i << " = vr[l]; acc" << i << " = 0.f; "
+            o << " } cur" << i << " = l; gcur" << i << " = vr[l]; acc" << i << " = " << ZR << "; "
               << ld_at(i, "(u64)gcur" + std::to_string(i) + " * R4");
-            for (size_t m : members[i]) o << " acc" << m << " = 0.f; " << ld_at(m, "(u64)gcur" + std::to_string(i) + " * R4 + " + dgoff(m));
+            for (size_t m : members[i]) o << " acc" << m << " = " << ZR << "; " << ld_at(m, "(u64)gcur" + std::to_string(i) + " * R4 + " + dgoff(m));
             o << " } }\n";
         }
     }
@@ -851,7 +898,7 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
     // atom pairs for the packed f32x2 pipe: consecutive atom slots with equal nnz and equal
     // class-constant status of 1/||q|| (their words are consecutive in the record)
     std::vector<int> pair_with(ns, -1), pair_second(ns, 0);
-    if (jit_pair() && fast_erfc() && !erfc_vote() && std::string(erfc_fn()) == "fsmt_half_erfc") {
+    if (!g_v2 && jit_pair() && fast_erfc() && !erfc_vote() && std::string(erfc_fn()) == "fsmt_half_erfc") {
         int pend = -1;
         uint32_t awp = 1 + ((uint32_t)nr + 1) / 2, pend_aw = 0;
         for (size_t s = 0, ai = 0; s < ns; ++s) {
@@ -906,7 +953,7 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
             continue;
         }
         if (t.kinds[s] == 0) {
-            o << "    const float pt" << s << " = 0.5f * (1.f - val" << slot_ref0[s] << "), pf" << s << " = 0.5f * (1.f + val"
+            o << "    const " << TY << " pt" << s << " = 0.5f * (1.f - val" << slot_ref0[s] << "), pf" << s << " = 0.5f * (1.f + val"
               << slot_ref0[s] << ");\n";
         } else if (t.kinds[s] == 2) {
             // negated literal: p_true and p_false of its row swap (Eq.4 / Eq.7 of the literal)
@@ -916,7 +963,8 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
               << " ? val" << ri << " : vaf" << ri << ";\n";
         } else {
             const uint32_t nnz = K.nnz[ai++];
-            o << "    float z" << s << " = -__uint_as_float(" << word(aw) << ");\n";
+            if (g_v2) o << "    float2 z" << s << " = FSMT_C2(-__uint_as_float(" << word(aw) << "));\n";
+            else o << "    float z" << s << " = -__uint_as_float(" << word(aw) << ");\n";
             o << "    const float inv" << s << " = __uint_as_float(" << word(aw + 1) << ");\n";
             for (uint32_t k = 0; k < nnz; ++k) {
                 coef_word[slot_ref0[s] + k] = aw + 2 + k;
@@ -926,9 +974,17 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
             // inv class-constant (folded): kappa/sqrt2 * inv and the dd factor are loop-invariant
             const bool inv_const = K.wpos[aw - 2 - nnz + 1] < 0;
             if (inv_const)
-                o << "    const float u" << s << " = z" << s << " * (kq * inv" << s << ");\n";
+                o << "    const " << TY << " u" << s << " = z" << s << " * (kq * inv" << s << ");\n";
             else
-                o << "    const float u" << s << " = kq * z" << s << " * inv" << s << ";\n";
+                o << "    const " << TY << " u" << s << " = kq * z" << s << " * inv" << s << ";\n";
+            if (g_v2) {
+                o << "    float2 ez" << s << ";\n    const float2 e" << s << " = fsmt_half_erfc2(fsmt_abs2(u" << s << "), ez" << s << ");\n"
+                  << "    const float2 om" << s << " = 1.f - e" << s << ";\n"
+                  << "    const float2 pt" << s << " = fsmt_sel_ge0(u" << s << ", e" << s << ", om" << s << ");\n"
+                  << "    const float2 pf" << s << " = fsmt_sel_ge0(u" << s << ", om" << s << ", e" << s << ");\n"
+                  << "    const float2 dd" << s << " = (dcoef * inv" << s << ") * ez" << s << ";\n";
+                continue;
+            }
             if (fast_erfc() && erfc_vote()) {
                 // warp vote: both erfc branches only when the warp's lanes straddle |u| = 0.75
                 o << "    const float za" << s << " = fabsf(u" << s << "), zb" << s << " = za" << s << " * za" << s << ";\n"
@@ -981,10 +1037,31 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
     }
     auto is_bool = [&](uint32_t lv) { return t.kinds[lv] == 0; };
     auto vref = [&](uint32_t lv) { return "val" + std::to_string(slot_ref0[lv]); };
+    // Boolean x Boolean diamonds' P_X / P_Y two at a time on the f32x2 pipe (FSMT_JIT_PAIR=0:
+    // one at a time inside the forward pass); per component the same operations
+    std::vector<char> dpre(nn, 0);
+    if (!g_v2 && jit_pair()) {
+        std::vector<size_t> bb;
+        for (size_t v = 0; v < nn; ++v)
+            if (dhead[v] && is_bool(t.nodes[v].level) && is_bool(t.nodes[t.nodes[v].hi].level)) bb.push_back(v);
+        for (size_t k = 0; k + 1 < bb.size(); k += 2) {
+            const size_t va = bb[k], vb = bb[k + 1];
+            const std::string a = std::to_string(va), b2 = std::to_string(vb);
+            const uint32_t a1 = t.nodes[va].level, a2 = t.nodes[t.nodes[va].hi].level;
+            const uint32_t b1 = t.nodes[vb].level, b22 = t.nodes[t.nodes[vb].hi].level;
+            o << "    const float2 vvp" << a << " = __fmul2_rn(make_float2(" << vref(a1) << ", " << vref(b1) << "), make_float2("
+              << vref(a2) << ", " << vref(b22) << "));\n"
+              << "    const float2 PXp" << a << " = __ffma2_rn(FSMT_C2(0.5f), vvp" << a << ", FSMT_C2(0.5f));\n"
+              << "    const float2 PYp" << a << " = __ffma2_rn(FSMT_C2(-0.5f), vvp" << a << ", FSMT_C2(0.5f));\n"
+              << "    const " << TY << " PX" << a << " = PXp" << a << ".x, PY" << a << " = PYp" << a << ".x, PX" << b2 << " = PXp" << a
+              << ".y, PY" << b2 << " = PYp" << a << ".y;\n";
+            dpre[va] = dpre[vb] = 1;
+        }
+    }
     // forward pass (Alg.F): m_td in registers
     for (size_t v = 0; v < nn; ++v)
-        if (!dskip[v]) o << "    float m" << v << " = " << ((int)v == t.root ? "1.f" : "0.f") << ";\n";
-    o << "    float pT = 0.f;\n";
+        if (!dskip[v]) o << "    " << TY << " m" << v << " = " << ((int)v == t.root ? (g_v2 ? "FSMT_C2(1.f)" : "1.f") : ZR) << ";\n";
+    o << "    " << TY << " pT = " << ZR << ";\n";
     for (size_t v = 0; v < nn; ++v) {
         if (dskip[v]) continue;
         const TNode& nd = t.nodes[v];
@@ -996,12 +1073,14 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
             const TNode& h = t.nodes[nd.hi];
             const uint32_t s1 = nd.level, s2 = h.level;
             const std::string P = "PX" + std::to_string(v), Q = "PY" + std::to_string(v);
-            if (is_bool(s1) && is_bool(s2)) {
-                o << "    const float vv" << v << " = " << vref(s1) << " * " << vref(s2) << ";\n"
-                  << "    const float " << P << " = fmaf(0.5f, vv" << v << ", 0.5f), " << Q << " = fmaf(-0.5f, vv" << v
+            if (dpre[v]) {
+                // P_X / P_Y computed in pairs above
+            } else if (is_bool(s1) && is_bool(s2)) {
+                o << "    const " << TY << " vv" << v << " = " << vref(s1) << " * " << vref(s2) << ";\n"
+                  << "    const " << TY << " " << P << " = fmaf(0.5f, vv" << v << ", 0.5f), " << Q << " = fmaf(-0.5f, vv" << v
                   << ", 0.5f);\n";
             } else {
-                o << "    const float " << P << " = fmaf(pt" << s1 << ", pt" << s2 << ", pf" << s1 << " * pf" << s2 << "), " << Q
+                o << "    const " << TY << " " << P << " = fmaf(pt" << s1 << ", pt" << s2 << ", pf" << s1 << " * pf" << s2 << "), " << Q
                   << " = fmaf(pt" << s1 << ", pf" << s2 << ", pf" << s1 << " * pt" << s2 << ");\n";
             }
             push(h.hi, P);   // X: s, s' equal
@@ -1011,11 +1090,39 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
         push(nd.hi, "pt" + std::to_string(nd.level));
         push(nd.lo, "pf" + std::to_string(nd.level));
     }
-    // backward pass (Alg.B, sign R1): m_bu in registers, dE/dv per slot
-    for (size_t s = 0; s < ns; ++s) o << "    float G" << s << " = 0.f;\n";
+    // backward pass (Alg.B, sign R1): m_bu in registers, dE/dv per slot.  Complement form
+    // (opt-in FSMT_JIT_CMP=1; fewer instructions but slower on cfg4): when more
+    // edges reach TRUE than FALSE, the pass carries
+    // c[v] = 1 - m_bu[v] (the same linear recurrence with the terminal values swapped,
+    // using p + (1 - p) = 1), so the OR-chains' "1 - m_bu" subtractions vanish; then
+    // G_s = -dCOP/dp_s and every use of G takes the sign back (gref).
+    size_t e_true = 0, e_false = 0;
+    for (size_t v = 0; v < nn; ++v) {
+        if (dskip[v]) continue;
+        for (int ch : {t.nodes[v].hi, t.nodes[v].lo}) {
+            e_true += ch == kTrue;
+            e_false += ch == kFalse;
+        }
+    }
+    const char* cmp_env = getenv("FSMT_JIT_CMP");
+    const bool cmp = cmp_env && cmp_env[0] == '1' && e_true > e_false;
+    for (size_t s = 0; s < ns; ++s) o << "    " << TY << " G" << s << " = " << ZR << ";\n";
+    // G_s += a * b; the first contribution is a plain product (G starts at 0: only the sign
+    // of a zero can differ)
+    std::vector<char> gz(ns, 1);
+    auto gfma = [&](size_t s, const std::string& a, const std::string& b) {
+        if (gz[s]) o << "    G" << s << " = " << a << " * " << b << ";\n";
+        else o << "    G" << s << " = fmaf(" << a << ", " << b << ", G" << s << ");\n";
+        gz[s] = 0;
+    };
+    auto gadd = [&](size_t s, const std::string& a, bool neg) {
+        if (gz[s]) o << "    G" << s << " = " << (neg ? "-" : "") << a << ";\n";
+        else o << "    G" << s << (neg ? " -= " : " += ") << a << ";\n";
+        gz[s] = 0;
+    };
     auto bu = [&](int child) -> std::string {
         if (child >= 0) return "bu" + std::to_string(child);
-        return child == kTrue ? "1.f" : "0.f";
+        return (child == kTrue) != cmp ? "1.f" : "0.f";
     };
     for (size_t vv = nn; vv-- > 0;) {
         if (dskip[vv]) continue;
@@ -1024,15 +1131,19 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
             const TNode& h = t.nodes[nd.hi];
             const uint32_t s1 = nd.level, s2 = h.level;
             const std::string X = bu(h.hi), Y = bu(h.lo), sv = std::to_string(vv);
-            o << "    const float d" << sv << " = " << X << " - " << Y << ";\n"
-              << "    const float bu" << sv << " = fmaf(PX" << sv << ", d" << sv << ", " << Y << ");\n"
-              << "    const float md" << sv << " = m" << sv << " * d" << sv << ";\n";
+            if (Y == "0.f")
+                o << "    const " << TY << " d" << sv << " = " << X << ";\n"
+                  << "    const " << TY << " bu" << sv << " = PX" << sv << " * d" << sv << ";\n";
+            else
+                o << "    const " << TY << " d" << sv << " = " << X << " - " << Y << ";\n"
+                  << "    const " << TY << " bu" << sv << " = fmaf(PX" << sv << ", d" << sv << ", " << Y << ");\n";
+            o << "    const " << TY << " md" << sv << " = m" << sv << " * d" << sv << ";\n";
             if (is_bool(s1) && is_bool(s2)) {
-                o << "    G" << s1 << " = fmaf(-md" << sv << ", " << vref(s2) << ", G" << s1 << ");\n"
-                  << "    G" << s2 << " = fmaf(-md" << sv << ", " << vref(s1) << ", G" << s2 << ");\n";
+                gfma(s1, "-md" + sv, vref(s2));
+                gfma(s2, "-md" + sv, vref(s1));
             } else {
-                o << "    G" << s1 << " = fmaf(md" << sv << ", pt" << s2 << " - pf" << s2 << ", G" << s1 << ");\n"
-                  << "    G" << s2 << " = fmaf(md" << sv << ", pt" << s1 << " - pf" << s1 << ", G" << s2 << ");\n";
+                gfma(s1, "md" + sv, "(pt" + std::to_string(s2) + " - pf" + std::to_string(s2) + ")");
+                gfma(s2, "md" + sv, "(pt" + std::to_string(s1) + " - pf" + std::to_string(s1) + ")");
             }
             continue;
         }
@@ -1049,23 +1160,28 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
         else {
             // both children internal: d = m_bu[hi] - m_bu[lo]; m_bu[v] = m_bu[lo] + p d (p + (1-p) = 1),
             // and d is reused by the gradient term below
-            o << "    const float d" << vv << " = " << bh << " - " << bl << ";\n";
-            o << "    const float bu" << vv << " = fmaf(pt" << lv << ", d" << vv << ", " << bl << ");\n";
-            o << "    G" << lv << " = fmaf(m" << vv << ", d" << vv << ", G" << lv << ");\n";
+            o << "    const " << TY << " d" << vv << " = " << bh << " - " << bl << ";\n";
+            o << "    const " << TY << " bu" << vv << " = fmaf(pt" << lv << ", d" << vv << ", " << bl << ");\n";
+            gfma(nd.level, "m" + std::to_string(vv), "d" + std::to_string(vv));
             continue;
         }
-        o << "    const float bu" << vv << " = " << val << ";\n";
-        std::string diff;
-        if (bh == "1.f" && bl == "0.f") diff = "";
-        else if (bh == "0.f" && bl == "1.f") diff = "-";
-        else diff = "(" + bh + " - " + bl + ")";
-        if (diff.empty()) o << "    G" << lv << " += m" << vv << ";\n";
-        else if (diff == "-") o << "    G" << lv << " -= m" << vv << ";\n";
-        else o << "    G" << lv << " = fmaf(m" << vv << ", " << diff << ", G" << lv << ");\n";
+        o << "    const " << TY << " bu" << vv << " = " << val << ";\n";
+        const std::string mv = "m" + std::to_string(vv);
+        if (bh == "1.f" && bl == "0.f") gadd(nd.level, mv, false);
+        else if (bh == "0.f" && bl == "1.f") gadd(nd.level, mv, true);
+        else if (bl == "0.f") gfma(nd.level, mv, bh);
+        else if (bh == "0.f") gfma(nd.level, mv, "(-" + bl + ")");
+        else gfma(nd.level, mv, "(" + bh + " - " + bl + ")");
     }
-    o << "    const float E = 1.f - 2.f * pT;\n"
-         "    objacc += (double)w * (double)E;\n"
-         "    if (terms != nullptr && live && r == terms_r) terms[orig[T.cons_begin + c]] = (double)E;\n";
+    auto gref = [&](size_t s) { return cmp ? "(-G" + std::to_string(s) + ")" : "G" + std::to_string(s); };
+    o << "    const " << TY << " E = 1.f - 2.f * pT;\n";
+    if (g_v2)
+        o << "    objacc.x += (double)w.x * (double)E.x;\n"
+             "    objacc.y += (double)w.y * (double)E.y;\n"
+             "    if (terms != nullptr && live && (r == terms_r || r + 1 == terms_r)) terms[orig[T.cons_begin + c]] = (double)(r == terms_r ? E.x : E.y);\n";
+    else
+        o << "    objacc += (double)w * (double)E;\n"
+             "    if (terms != nullptr && live && r == terms_r) terms[orig[T.cons_begin + c]] = (double)E;\n";
     // gradient terms per target reference (aliases fold into their target: one read-modify-write)
     std::vector<std::vector<std::pair<std::string, std::string>>> terms_of(nr);
     auto accum = [&](int ri, const std::string& a, const std::string& b) {
@@ -1074,18 +1190,18 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
     };
     for (size_t s = 0; s < ns; ++s) {
         if (t.kinds[s] == 0) {
-            accum(slot_ref0[s], "w", "G" + std::to_string(s));
+            accum(slot_ref0[s], "w", gref(s));
         } else if (t.kinds[s] == 2) {
             // dCOP/dp_true of the row = -dCOP/dp_true of a negated literal
-            accum(slot_ref0[s], "w", "(sg" + std::to_string(s) + " ? -G" + std::to_string(s) + " : G" + std::to_string(s) + ")");
+            accum(slot_ref0[s], "w", "(sg" + std::to_string(s) + " ? -" + gref(s) + " : " + gref(s) + ")");
         } else {
             if (pair_with[s] >= 0) {
                 const std::string sa = std::to_string(s), sb = std::to_string(pair_with[s]);
-                o << "    const float2 gdp" << sa << " = __fmul2_rn(__fmul2_rn(FSMT_C2(w), make_float2(G" << sa << ", G" << sb
+                o << "    const float2 gdp" << sa << " = __fmul2_rn(__fmul2_rn(FSMT_C2(w), make_float2(" << gref(s) << ", " << gref((size_t)pair_with[s])
                   << ")), ddp" << sa << ");\n"
                   << "    const float gd" << sa << " = gdp" << sa << ".x, gd" << sb << " = gdp" << sa << ".y;\n";
             } else if (!pair_second[s]) {
-                o << "    const float gd" << s << " = w * G" << s << " * dd" << s << ";\n";
+                o << "    const " << TY << " gd" << s << " = w * " << gref(s) << " * dd" << s << ";\n";
             }
             size_t ai = 0;
             for (size_t s2 = 0; s2 < s; ++s2) ai += t.kinds[s2] == 1;
@@ -1246,14 +1362,16 @@ void emit_verify_class(std::ostringstream& o, uint32_t kid, const KClass& K, con
 
 }  // namespace
 
-std::string jit_source(const Formula& f, const Built& b, const Plan& p, int u_prefetch_default) {
+std::string jit_source(const Formula& f, const Built& b, const Plan& p, int u_prefetch_default, bool lane2) {
     g_upf = u_prefetch_default;
+    g_v2 = lane2;
+    struct Reset { ~Reset() { g_v2 = false; } } reset_v2;
     std::ostringstream o;
     o << "// generated by fsmt tiles.cpp: specialised K1 sweep for " << p.n_jit_kclasses << " kernel classes\n"
          "typedef unsigned int u32;\ntypedef unsigned long long u64;\n"
          "struct TileDesc { u32 kclass, cons_begin, n_cons, var_off, n_vars, rec_off, pad0, pad1; };\n"
       << "#define VMAX " << p.kernel_vmax() << "\n#define VTOT " << p.kernel_vmax() + p.rmax << "\n#define WARPS " << p.jit_warps
-      << "\n\n" << kErfcPrelude;
+      << "\n#define RPL " << (lane2 ? 2 : 1) << "\n\n" << kErfcPrelude << (lane2 ? kLane2Prelude : "");
     auto tmpl_of = [&](const KClass& K) -> const Template& { return K.sym ? K.stmpl : b.tmpls[K.tmpl]; };
     for (uint32_t k = 0; k < p.n_jit_kclasses; ++k) emit_class(o, k, p.kclasses[k], tmpl_of(p.kclasses[k]));
     const char* minb = getenv("FSMT_JIT_MINB");      // optional min CTAs/SM (register cap), A/B tuning
@@ -1268,25 +1386,27 @@ std::string jit_source(const Formula& f, const Built& b, const Plan& p, int u_pr
          "  FSMT_SPECIALISE_R\n"
          "  extern __shared__ float smem[];\n"
          "  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;\n"
-         "  float* acc = smem + warp * (VMAX * 32);                  // stream-variable rows\n"
-         "  u32* vs = (u32*)(smem + WARPS * VMAX * 32) + warp * VTOT; // stream then run variable ids\n"
-         "  const u32 rtiles = (R + 31) / 32;\n"
+      << (lane2 ? "  float2* acc = (float2*)smem + warp * (VMAX * 32);       // stream-variable rows (2 restarts per lane)\n"
+                : "  float* acc = smem + warp * (VMAX * 32);                  // stream-variable rows\n")
+      << "  u32* vs = (u32*)(smem + WARPS * VMAX * 32 * RPL) + warp * VTOT; // stream then run variable ids\n"
+         "  const u32 rtiles = (R + 32 * RPL - 1) / (32 * RPL);\n"
          "  const u64 gw = (u64)blockIdx.x * WARPS + warp;\n"
          "  const u32 rt = (u32)(gw % rtiles);\n"
          "  const u64 ti = gw / rtiles;\n"
          "  if (ti >= n_tiles) return;\n"
          "  const TileDesc T = tiles[ti];\n"
          "  const u32 n_s = T.n_vars & 0xffffu, n_v = n_s + (T.n_vars >> 16);\n"
-         "  const u32 r = rt * 32 + lane;\n"
+         "  const u32 r = rt * 32 * RPL + lane * RPL;   // the lane's (first) restart\n"
          "  const bool live = r < R;\n"
          "  const u64 rr = live ? r : 0;\n"
          "  for (u32 l = lane; l < n_v; l += 32) vs[l] = tile_vars[T.var_off + l];\n"
-         "  for (u32 l = 0; l < n_s; ++l) acc[l * 32 + lane] = 0.f;\n"
+      << "  for (u32 l = 0; l < n_s; ++l) acc[l * 32 + lane] = " << (lane2 ? "FSMT_Z2" : "0.f") << ";\n"
          "  __syncwarp();\n"
          "  const u32* vr = vs + n_s;\n"
          "  const float kq = kappa * 0.70710678118654752f;\n"
          "  const float dcoef = kappa * 0.79788456080286536f;\n"
-         "  double objacc = 0.0;\n"
+      << (lane2 ? "  double2 objacc = make_double2(0.0, 0.0);\n" : "  double objacc = 0.0;\n")
+      << 
          "  const uint4* rp = recs + T.rec_off;\n"
          "  // the lane's column bases: element (v, restart rr) of a [var][R] array at base + v * 4R bytes\n"
          "  const u32 R4 = R * 4u;\n"
@@ -1302,15 +1422,26 @@ std::string jit_source(const Formula& f, const Built& b, const Plan& p, int u_pr
           << (p.kclasses[k].sym ? "symt = true; " : "") << "break;\n";
     o << "    default: break;\n  }\n"
          "  __syncwarp();\n"
-         "  if (!live) return;\n"
-         "  for (u32 l = 0; l < n_s; ++l) {\n"
-         "    const u32 g = vs[l];\n"
-         "    const double v = (double)acc[l * 32 + lane];\n"
-         "    if (symt) atomicAdd(gu + (u64)g * R + r, v);\n"
-         "    else if (g < n_bool) atomicAdd(ga + (u64)g * R + r, v); else atomicAdd(gb + (u64)(g - n_bool) * R + r, v);\n"
-         "  }\n"
-         "  atomicAdd(obj + r, objacc);\n"
-         "}\n\n";
+         "  if (!live) return;\n";
+    if (lane2)
+        o << "  (void)symt;\n"
+             "  for (u32 l = 0; l < n_s; ++l) {\n"
+             "    const u32 g = vs[l];\n"
+             "    const float2 v = acc[l * 32 + lane];\n"
+             "    double* dst = g < n_bool ? ga + (u64)g * R + r : gb + (u64)(g - n_bool) * R + r;\n"
+             "    atomicAdd(dst, (double)v.x); atomicAdd(dst + 1, (double)v.y);\n"
+             "  }\n"
+             "  atomicAdd(obj + r, objacc.x); atomicAdd(obj + r + 1, objacc.y);\n"
+             "}\n\n";
+    else
+        o << "  for (u32 l = 0; l < n_s; ++l) {\n"
+             "    const u32 g = vs[l];\n"
+             "    const double v = (double)acc[l * 32 + lane];\n"
+             "    if (symt) atomicAdd(gu + (u64)g * R + r, v);\n"
+             "    else if (g < n_bool) atomicAdd(ga + (u64)g * R + r, v); else atomicAdd(gb + (u64)(g - n_bool) * R + r, v);\n"
+             "  }\n"
+             "  atomicAdd(obj + r, objacc);\n"
+             "}\n\n";
     // K5: exact verification of the rounded models + ERWA counters over the same tiles
     for (uint32_t k = 0; k < p.n_jit_kclasses; ++k) emit_verify_class(o, k, p.kclasses[k], tmpl_of(p.kclasses[k]));
     o << "extern \"C\" __global__ void __launch_bounds__(WARPS * 32) fsmt_k5_jit(\n"

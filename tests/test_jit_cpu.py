@@ -1,4 +1,7 @@
-"""The JIT-specialised sweep compiles with NVRTC for sm_100a here (no GPU needed), without spills."""
+"""The JIT-specialised sweep compiles with NVRTC for sm_100a here (no GPU needed), without spills:
+the generic module of fsmt_build_xbdd and the modules fsmt_prepare(R) builds (restart count
+compiled in, U prefetch, and the opt-in two-restarts-per-lane f32x2 mode)."""
+import os
 import re
 
 import pytest
@@ -6,13 +9,30 @@ import pytest
 import fsmt_gen
 from paper_2603_22877_b200 import Solver
 
+VARIANTS = [{}, {"FSMT_JIT_CHECK_RC": "1024"}, {"FSMT_JIT_CHECK_RC": "1024", "FSMT_JIT_LANE2": "1"},
+            {"FSMT_JIT_CHECK_RC": "1000000", "FSMT_JIT_UPF": "3"}]
 
+
+@pytest.mark.parametrize("env", VARIANTS, ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()) or "generic")
 @pytest.mark.parametrize("name", ["cfg3s", "cfg4s"])
-def test_nvrtc_compiles_specialised_sweep(name):
+def test_nvrtc_compiles_specialised_sweep(name, env):
     s = Solver(-1)
     s.load_formula(fsmt_gen.config(name).text)
     s.build_xbdd()
-    nbytes, log = s.jit_check()
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        nbytes, log = s.jit_check()
+        src = s.jit_source()
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
     assert nbytes > 0
     m = re.findall(r"(\d+) bytes spill stores", log)
     assert m and all(int(x) == 0 for x in m), log[-2000:]
+    if "FSMT_JIT_CHECK_RC" in env:
+        assert src.startswith("#define FSMT_RC " + env["FSMT_JIT_CHECK_RC"] + "u")
+        assert ("#define RPL 2" in src) == ("FSMT_JIT_LANE2" in env)
