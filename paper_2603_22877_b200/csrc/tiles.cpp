@@ -846,8 +846,21 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
         for (int k = 0; k < upf; ++k)
             o << "  u32 un" << k << " = (U && " << k << "u < T.n_cons) ? (u32)" << uld << "(" << ucast << "(Up + (u64)" << k << "u * R)) : 0u;\n";
     }
+    // FSMT_JIT_RPF=1: the next constraint's record is loaded one iteration ahead (A/B)
+    const char* rpf_env = getenv("FSMT_JIT_RPF");
+    const bool rpf = rpf_env && rpf_env[0] == '1';
+    if (rpf)
+        for (uint32_t q = 0; q < K.stride4; ++q)
+            o << "  uint4 nq" << q << " = T.n_cons ? __ldg(rp + " << q << ") : make_uint4(0u, 0u, 0u, 0u);\n";
     o << "  for (u32 c = 0; c < T.n_cons; ++c, rp += " << K.stride4 << ") {\n";
-    for (uint32_t q = 0; q < K.stride4; ++q) o << "    const uint4 q" << q << " = __ldg(rp + " << q << ");\n";
+    if (rpf) {
+        for (uint32_t q = 0; q < K.stride4; ++q) o << "    const uint4 q" << q << " = nq" << q << ";\n";
+        o << "    if (c + 1 < T.n_cons) {";
+        for (uint32_t q = 0; q < K.stride4; ++q) o << " nq" << q << " = __ldg(rp + " << K.stride4 + q << ");";
+        o << " }\n";
+    } else {
+        for (uint32_t q = 0; q < K.stride4; ++q) o << "    const uint4 q" << q << " = __ldg(rp + " << q << ");\n";
+    }
     if (upf > 0) {
         o << "    const u32 uc = un0;\n";
         for (int k = 0; k + 1 < upf; ++k) o << "    un" << k << " = un" << k + 1 << ";\n";
