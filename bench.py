@@ -139,6 +139,14 @@ def time_oracle(f, a, b, kappa=KAPPA):
     return time.perf_counter() - t0
 
 
+def workload_config(args, n_vars: int, n_cons: int, world: int = 1) -> dict:
+    """The workload both arms name in `config` (same keys, so the driver compares like with like)."""
+    names = {"cfg4": "placement-10k", "cfg3": "scheduling-2k", "cfg2": "random-200"}
+    return {"workload": f"{args.config}: {names.get(args.config, args.config)}, {n_vars} vars / {n_cons} constraints",
+            "restarts_per_gpu": args.restarts, "global_restarts": args.restarts * world,
+            "pgd_steps_per_stage": args.pgd_steps, "kappa": KAPPA}
+
+
 def run_reference(args):
     """--impl reference: the fp64 oracle as it stands, on the host cores, same metric/config."""
     rank = int(os.environ.get("RANK", "0"))
@@ -157,8 +165,8 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(ts), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.config}: {inst.n_bool + inst.n_real} vars / {inst.n_cons} constraints",
-                   "restarts_per_gpu": 1, "pgd_steps_per_stage": 1},
+        "config": {**workload_config(args, inst.n_bool + inst.n_real, inst.n_cons),
+                   "oracle_sample": f"first {n} constraints, 1 restart, one objective+gradient evaluation per step"},
         "cpu_baseline": {"value": value, "unit": "evals/s", "cores": 1, "kind": "oracle",
                          "sample": f"first {n} constraints of {args.config}, 1 restart, objective+gradient per step"},
         "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -288,11 +296,9 @@ def main():
             "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"{args.config}: placement-10k, {dims['n_bool'] + dims['n_real']} vars / "
-                                   f"{dims['n_cons']} constraints" if args.config == "cfg4" else args.config,
-                       "restarts_per_gpu": R, "global_restarts": R * world,
-                       "kernels": "generic" if args.no_prepare else "specialised for R (fsmt_prepare)", "pgd_steps_per_stage": S,
-                       "kappa": KAPPA, "parallelism": f"restart-sharded x{world}",
+            "config": {**workload_config(args, dims["n_bool"] + dims["n_real"], dims["n_cons"], world),
+                       "kernels": "generic" if args.no_prepare else "specialised for R (fsmt_prepare)",
+                       "parallelism": f"restart-sharded x{world}",
                        "l2": "inputs exceed L2 (U counters %.0f MB + structure + state per step)" % (dims["n_cons"] * R / 1e6),
                        "accumulation": "fp64", "build_s": round(build_s, 2)},
             "roofline": {"bound": "alu", "achieved": alu_achieved, "peak": alu_peak, "unit": "TFLOP/s",
