@@ -705,7 +705,7 @@ fsmt_status fsmt_jit_info(const fsmt_ctx* ctx, uint32_t* n_jit_classes, uint32_t
     return FSMT_OK;
 }
 
-static std::string prepared_source(const fsmt_ctx* ctx, uint32_t R, bool& lane2);
+static std::string prepared_source_tuned(const fsmt_ctx* ctx, uint32_t R, bool& lane2);
 
 fsmt_status fsmt_jit_check(fsmt_ctx* ctx, size_t* cubin_bytes, char* log, size_t log_len) {
     if (!ctx) return FSMT_ERR_ARG;
@@ -717,7 +717,7 @@ fsmt_status fsmt_jit_check(fsmt_ctx* ctx, size_t* cubin_bytes, char* log, size_t
     std::string src = ctx->jit_src;
     if (const char* rc = getenv("FSMT_JIT_CHECK_RC")) {
         bool lane2 = false;
-        src = prepared_source(ctx, (uint32_t)atoi(rc), lane2);
+        src = prepared_source_tuned(ctx, (uint32_t)atoi(rc), lane2);
     }
     bool ok = jit_cubin(src, cubin, lg, err);
     if (log && log_len) snprintf(log, log_len, "%s", lg.c_str());
@@ -732,12 +732,37 @@ fsmt_status fsmt_jit_check(fsmt_ctx* ctx, size_t* cubin_bytes, char* log, size_t
 // of U stays in L2, is faster without); opt-in (FSMT_JIT_LANE2=1) two restarts per lane on the
 // f32x2 pipe when R is even (float2 loads of a lane's two restarts) and there are no symmetric
 // classes: 32 % fewer instructions per eval but 126 registers (16 warps/SM), slower on cfg3/cfg4.
-static std::string prepared_source(const fsmt_ctx* ctx, uint32_t R, bool& lane2) {
+static std::string prepared_source(const fsmt_ctx* ctx, uint32_t R, bool& lane2, int min_ctas) {
     const int upf = (double)ctx->plan.jit_cons_end * R > 192e6 ? 3 : 0;
     const char* l2e = getenv("FSMT_JIT_LANE2");
     lane2 = R % 2 == 0 && !ctx->plan.has_sym && l2e && l2e[0] == '1';
-    const std::string src = (upf || lane2) ? jit_source(ctx->f, ctx->b, ctx->plan, upf, lane2) : ctx->jit_src;
+    const std::string src = (upf || lane2 || min_ctas) ? jit_source(ctx->f, ctx->b, ctx->plan, upf, lane2, min_ctas) : ctx->jit_src;
     return "#define FSMT_RC " + std::to_string(R) + "u\n" + src;
+}
+
+// spill-store bytes ptxas reports for one kernel of an NVRTC log (-1 if not found)
+static long spill_stores(const std::string& log, const std::string& kernel) {
+    const std::string key = "Function properties for " + kernel + "\n";
+    const size_t at = log.find(key);
+    if (at == std::string::npos) return -1;
+    const size_t sp = log.find(" bytes spill stores", at + key.size());
+    if (sp == std::string::npos) return -1;
+    size_t b = sp;
+    while (b > 0 && isdigit((unsigned char)log[b - 1])) --b;
+    return atol(log.substr(b, sp - b).c_str());
+}
+
+// The prepared module's source with the hot kernel's register cap: the highest residency (32,
+// then 28 one-warp CTAs per SM: 64 / 72 registers) whose compile has no spills, else no cap
+// (cfg3 best at 64, cfg4 at 72, cfg2 uncapped)
+static std::string prepared_source_tuned(const fsmt_ctx* ctx, uint32_t R, bool& lane2) {
+    for (int mc : {32, 28}) {
+        const std::string src = prepared_source(ctx, R, lane2, mc);
+        std::vector<char> cubin;
+        std::string log, err;
+        if (jit_cubin(src, cubin, log, err) && spill_stores(log, "fsmt_k1_jit") == 0) return src;
+    }
+    return prepared_source(ctx, R, lane2, 0);
 }
 
 fsmt_status fsmt_prepare(fsmt_ctx* ctx, uint32_t R) {
@@ -754,7 +779,7 @@ fsmt_status fsmt_prepare(fsmt_ctx* ctx, uint32_t R) {
     jit_release(ctx->jit_r);
     ctx->jit_r_R = 0;
     bool lane2 = false;
-    const std::string src = prepared_source(ctx, R, lane2);
+    const std::string src = prepared_source_tuned(ctx, R, lane2);
     std::string err;
     if (!jit_compile(src, ctx->jit_r, err))
         return fail(ctx, FSMT_ERR_CUDA, "fsmt_prepare: " + err);
@@ -768,7 +793,7 @@ size_t fsmt_jit_source(const fsmt_ctx* ctx, char* buf, size_t len) {
     std::string src = ctx->jit_src;
     if (const char* rc = getenv("FSMT_JIT_CHECK_RC")) {   // the source fsmt_prepare(R) would compile
         bool lane2 = false;
-        if (!src.empty()) src = prepared_source(ctx, (uint32_t)atoi(rc), lane2);
+        if (!src.empty()) src = prepared_source_tuned(ctx, (uint32_t)atoi(rc), lane2);
     }
     if (buf && len) snprintf(buf, len, "%s", src.c_str());
     return src.size() + 1;
@@ -797,7 +822,8 @@ static fsmt_status sweep_impl(fsmt_ctx* ctx, float kappa, uint32_t stage_t, doub
             ctx->launches += 1;
         }
         if (ctx->T.n_tiles) {
-            launch_sweep_jit(jk(ctx, S.R).kernel, jk(ctx, S.R).rpl, F, S, ctx->T, kappa, ws, terms, terms_r, ctx->stream, &ctx->slots);
+            const JitKernel& J = jk(ctx, S.R);
+            launch_sweep_jit((S.U == nullptr || terms != nullptr) ? J.kernel_dbg : J.kernel, J.rpl, F, S, ctx->T, kappa, ws, terms, terms_r, ctx->stream, &ctx->slots);
             ctx->launches += 1;
         }
         if (F.generic_begin < F.generic_end) {

@@ -173,7 +173,9 @@ Plan make_plan(const Formula& f, const Built& b, bool enable_jit);
 // CUDA source of the specialised sweep kernel for the plan's JIT classes.
 // u_prefetch_default: how many constraints ahead the sweep loads U (FSMT_JIT_UPF overrides)
 // lane2: two restarts per lane on the f32x2 pipe (even R only; no symmetric classes)
-std::string jit_source(const Formula& f, const Built& b, const Plan& p, int u_prefetch_default = 0, bool lane2 = false);
+// k1_min_ctas > 0: __launch_bounds__(WARPS*32, k1_min_ctas) on the hot sweep kernel (register cap)
+std::string jit_source(const Formula& f, const Built& b, const Plan& p, int u_prefetch_default = 0, bool lane2 = false,
+                       int k1_min_ctas = 0);
 
 struct BuildError {
     std::string msg;

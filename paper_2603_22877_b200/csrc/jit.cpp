@@ -68,7 +68,7 @@ Nvrtc& nvrtc() {
 
 // process-wide cache: identical sources compile once
 std::mutex g_mu;
-std::unordered_map<std::string, std::vector<char>> g_cubins;
+std::unordered_map<std::string, std::pair<std::vector<char>, std::string>> g_cubins;   // source -> (cubin, log)
 
 }  // namespace
 
@@ -77,7 +77,8 @@ bool jit_cubin(const std::string& src, std::vector<char>& cubin, std::string& lo
         std::lock_guard<std::mutex> lk(g_mu);
         auto it = g_cubins.find(src);
         if (it != g_cubins.end()) {
-            cubin = it->second;
+            cubin = it->second.first;
+            log = it->second.second;
             return true;
         }
     }
@@ -109,7 +110,7 @@ bool jit_cubin(const std::string& src, std::vector<char>& cubin, std::string& lo
     n.cubin(prog, cubin.data());
     n.destroy(&prog);
     std::lock_guard<std::mutex> lk(g_mu);
-    g_cubins.emplace(src, cubin);
+    g_cubins.emplace(src, std::make_pair(cubin, log));
     return true;
 }
 
@@ -129,6 +130,13 @@ bool jit_compile(const std::string& src, JitKernel& out, std::string& err) {
         err = std::string("cudaLibraryGetKernel: ") + cudaGetErrorString(e);
         return false;
     }
+    cudaKernel_t kd = nullptr;
+    e = cudaLibraryGetKernel(&kd, lib, "fsmt_k1_jit_dbg");
+    if (e != cudaSuccess) {
+        cudaLibraryUnload(lib);
+        err = std::string("cudaLibraryGetKernel(k1 dbg): ") + cudaGetErrorString(e);
+        return false;
+    }
     cudaKernel_t k5 = nullptr;
     e = cudaLibraryGetKernel(&k5, lib, "fsmt_k5_jit");
     if (e != cudaSuccess) {
@@ -145,6 +153,7 @@ bool jit_compile(const std::string& src, JitKernel& out, std::string& err) {
     }
     out.lib = lib;
     out.kernel = k;
+    out.kernel_dbg = kd;
     out.kernel5 = k5;
     out.kprob = kp;
     out.kchain = kc;
@@ -157,6 +166,7 @@ void jit_release(JitKernel& k) {
     if (k.lib) cudaLibraryUnload((cudaLibrary_t)k.lib);
     k.lib = nullptr;
     k.kernel = nullptr;
+    k.kernel_dbg = nullptr;
     k.kernel5 = nullptr;
     k.kprob = k.kchain = k.ktruth = nullptr;
 }

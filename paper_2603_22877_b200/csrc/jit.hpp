@@ -9,6 +9,7 @@ namespace fsmt {
 struct JitKernel {
     void* lib = nullptr;          // cudaLibrary_t
     cudaKernel_t kernel = nullptr;     // fsmt_k1_jit (sweep)
+    cudaKernel_t kernel_dbg = nullptr; // fsmt_k1_jit_dbg (sweep with U == NULL allowed and the E_c debug output)
     cudaKernel_t kernel5 = nullptr;    // fsmt_k5_jit (exact check)
     cudaKernel_t kprob = nullptr;      // fsmt_kp_jit (shared slot probability tables; symmetric classes)
     cudaKernel_t kchain = nullptr;     // fsmt_kc_jit (slot-table gradients -> grad_a / grad_b)

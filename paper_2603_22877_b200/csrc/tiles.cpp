@@ -779,14 +779,17 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
     g_wk = &K;
     const std::string TY = g_v2 ? "float2" : "float", ZR = g_v2 ? "FSMT_Z2" : "0.f", AT = g_v2 ? "FSMT_AT2" : "FSMT_AT";
     const size_t ns = t.kinds.size();
-    o << "__device__ __forceinline__ void kc" << kid
+    // DBG = false (the hot instantiation): U present, no per-constraint E_c debug output, so
+    // neither test is in the loop
+    o << "template <bool DBG> __device__ __forceinline__ void kc" << kid
       << "(const TileDesc& T, const uint4* __restrict__ rp, const u32* __restrict__ vs, const u32* __restrict__ vr,\n"
          "    " << TY << "* __restrict__ accs, const float* __restrict__ ab, const float* __restrict__ bb,\n"
          "    double* __restrict__ ga, double* __restrict__ gb, const unsigned char* __restrict__ U,\n"
          "    u32 R, u32 R4, u64 rr, u32 r, bool live, u32 n_bool, float kq, float dcoef, float wscale, "
       << (g_v2 ? "double2& objacc" : "double& objacc") << ",\n"
          "    double* __restrict__ terms, u32 terms_r, const u32* __restrict__ orig,\n"
-         "    const float* __restrict__ PTl, const float* __restrict__ PFl, double* __restrict__ gu) {\n";
+         "    const float* __restrict__ PTl, const float* __restrict__ PFl, double* __restrict__ gu) {\n"
+         "  const bool hasU = !DBG || U != nullptr, hasT = DBG && terms != nullptr;\n";
     // refs
     std::vector<int> ref_kind;      // 0 Boolean, 1 real, 2 slot-table row (symmetric classes)
     std::vector<int> slot_ref0(ns);
@@ -842,9 +845,9 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
     const char* uld = u_streaming() ? "__ldcs" : "__ldg";
     const std::string ucast = g_v2 ? "(const unsigned short*)" : "";
     if (upf > 0) {
-        o << "  const unsigned char* Up = U ? U + (u64)T.cons_begin * R + rr : nullptr;\n";
+        o << "  const unsigned char* Up = hasU ? U + (u64)T.cons_begin * R + rr : nullptr;\n";
         for (int k = 0; k < upf; ++k)
-            o << "  u32 un" << k << " = (U && " << k << "u < T.n_cons) ? (u32)" << uld << "(" << ucast << "(Up + (u64)" << k << "u * R)) : 0u;\n";
+            o << "  u32 un" << k << " = (hasU && " << k << "u < T.n_cons) ? (u32)" << uld << "(" << ucast << "(Up + (u64)" << k << "u * R)) : 0u;\n";
     }
     // FSMT_JIT_RPF=1: the next constraint's record is loaded one iteration ahead (A/B)
     const char* rpf_env = getenv("FSMT_JIT_RPF");
@@ -864,20 +867,20 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
     if (upf > 0) {
         o << "    const u32 uc = un0;\n";
         for (int k = 0; k + 1 < upf; ++k) o << "    un" << k << " = un" << k + 1 << ";\n";
-        o << "    if (U) un" << upf - 1 << " = c + " << upf << "u < T.n_cons ? (u32)" << uld << "(" << ucast << "(Up + (u64)(c + " << upf
+        o << "    if (hasU) un" << upf - 1 << " = c + " << upf << "u < T.n_cons ? (u32)" << uld << "(" << ucast << "(Up + (u64)(c + " << upf
           << "u) * R)) : 0u;\n";
     } else {
         if (g_v2)
-            o << "    const u32 uc = U ? (u32)*(const unsigned short*)(U + (u64)(T.cons_begin + c) * R + rr) : 0u;\n";
+            o << "    const u32 uc = hasU ? (u32)*(const unsigned short*)(U + (u64)(T.cons_begin + c) * R + rr) : 0u;\n";
         else
-            o << "    const u32 uc = U ? (u32)U[(u64)(T.cons_begin + c) * R + rr] : 0u;\n";
+            o << "    const u32 uc = hasU ? (u32)U[(u64)(T.cons_begin + c) * R + rr] : 0u;\n";
     }
     if (g_v2)
         o << "    const float w0 = __uint_as_float(" << word(0) << ") * wscale;\n"
-             "    const float2 w = U ? make_float2(fsmt_pow2_u8(w0, uc & 255u), fsmt_pow2_u8(w0, uc >> 8)) : make_float2(w0, w0);\n";
+             "    const float2 w = hasU ? make_float2(fsmt_pow2_u8(w0, uc & 255u), fsmt_pow2_u8(w0, uc >> 8)) : make_float2(w0, w0);\n";
     else
         o << "    float w = __uint_as_float(" << word(0) << ") * wscale;\n"
-             "    if (U) w = fsmt_pow2_u8(w, uc);\n";
+             "    if (hasU) w = fsmt_pow2_u8(w, uc);\n";
     for (size_t i = 0; i < nr; ++i) {
         uint32_t wd = 1 + (uint32_t)i / 2;
         const std::string ext = "(" + word(wd) + " >> " + std::to_string(16 * (i % 2)) + ") & 0xffffu";
@@ -1191,10 +1194,10 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
     if (g_v2)
         o << "    objacc.x += (double)w.x * (double)E.x;\n"
              "    objacc.y += (double)w.y * (double)E.y;\n"
-             "    if (terms != nullptr && live && (r == terms_r || r + 1 == terms_r)) terms[orig[T.cons_begin + c]] = (double)(r == terms_r ? E.x : E.y);\n";
+             "    if (hasT && live && (r == terms_r || r + 1 == terms_r)) terms[orig[T.cons_begin + c]] = (double)(r == terms_r ? E.x : E.y);\n";
     else
         o << "    objacc += (double)w * (double)E;\n"
-             "    if (terms != nullptr && live && r == terms_r) terms[orig[T.cons_begin + c]] = (double)E;\n";
+             "    if (hasT && live && r == terms_r) terms[orig[T.cons_begin + c]] = (double)E;\n";
     // gradient terms per target reference (aliases fold into their target: one read-modify-write)
     std::vector<std::vector<std::pair<std::string, std::string>>> terms_of(nr);
     auto accum = [&](int ri, const std::string& a, const std::string& b) {
@@ -1375,7 +1378,7 @@ void emit_verify_class(std::ostringstream& o, uint32_t kid, const KClass& K, con
 
 }  // namespace
 
-std::string jit_source(const Formula& f, const Built& b, const Plan& p, int u_prefetch_default, bool lane2) {
+std::string jit_source(const Formula& f, const Built& b, const Plan& p, int u_prefetch_default, bool lane2, int k1_min_ctas) {
     g_upf = u_prefetch_default;
     g_v2 = lane2;
     struct Reset { ~Reset() { g_v2 = false; } } reset_v2;
@@ -1388,8 +1391,15 @@ std::string jit_source(const Formula& f, const Built& b, const Plan& p, int u_pr
     auto tmpl_of = [&](const KClass& K) -> const Template& { return K.sym ? K.stmpl : b.tmpls[K.tmpl]; };
     for (uint32_t k = 0; k < p.n_jit_kclasses; ++k) emit_class(o, k, p.kclasses[k], tmpl_of(p.kclasses[k]));
     const char* minb = getenv("FSMT_JIT_MINB");      // optional min CTAs/SM (register cap), A/B tuning
-    o << "extern \"C\" __global__ void __launch_bounds__(WARPS * 32" << (minb && atoi(minb) > 0 ? std::string(", ") + minb : std::string())
-      << ") fsmt_k1_jit(\n"
+    // fsmt_k1_jit: the hot kernel (U present, no E_c output); fsmt_k1_jit_dbg: U may be NULL and
+    // the per-constraint E_c debug hook is live.  Separate kernels, so the hot one keeps its own
+    // register allocation.
+    for (int dbgk = 0; dbgk < 2; ++dbgk) {
+    // hot kernel: k1_min_ctas resident one-warp CTAs per SM as a register cap (fsmt_prepare picks
+    // the largest of 32 / 28 that compiles without spills; 0 = none); FSMT_JIT_MINB overrides
+    const std::string mb = minb ? std::string(minb) : (dbgk || k1_min_ctas <= 0 ? std::string() : std::to_string(k1_min_ctas));
+    o << "extern \"C\" __global__ void __launch_bounds__(WARPS * 32" << (atoi(mb.c_str()) > 0 ? ", " + mb : std::string())
+      << ") fsmt_k1_jit" << (dbgk ? "_dbg" : "") << "(\n"
          "    const TileDesc* __restrict__ tiles, u32 n_tiles, const uint4* __restrict__ recs,\n"
          "    const u32* __restrict__ tile_vars, const float* __restrict__ a, const float* __restrict__ b,\n"
          "    double* __restrict__ ga, double* __restrict__ gb, const unsigned char* __restrict__ U,\n"
@@ -1428,11 +1438,14 @@ std::string jit_source(const Formula& f, const Built& b, const Plan& p, int u_pr
          "  const float* PTl = PT ? PT + rr : nullptr;\n"
          "  const float* PFl = PF ? PF + rr : nullptr;\n"
          "  bool symt = false;   // symmetric class: the tile's variables are slot-table rows\n"
+
          "  switch (T.kclass) {\n";
-    for (uint32_t k = 0; k < p.n_jit_kclasses; ++k)
-        o << "    case " << k << ": kc" << k
-          << "(T, rp, vs, vr, acc + lane, ab, bb, ga, gb, U, R, R4, rr, r, live, n_bool, kq, dcoef, wscale, objacc, terms, terms_r, orig, PTl, PFl, gu); "
+    for (uint32_t k = 0; k < p.n_jit_kclasses; ++k) {
+        const std::string args = "(T, rp, vs, vr, acc + lane, ab, bb, ga, gb, U, R, R4, rr, r, live, n_bool, kq, dcoef, wscale, objacc, "
+                                 "terms, terms_r, orig, PTl, PFl, gu); ";
+        o << "    case " << k << ": kc" << k << (dbgk ? "<true>" : "<false>") << args
           << (p.kclasses[k].sym ? "symt = true; " : "") << "break;\n";
+    }
     o << "    default: break;\n  }\n"
          "  __syncwarp();\n"
          "  if (!live) return;\n";
@@ -1455,6 +1468,7 @@ std::string jit_source(const Formula& f, const Built& b, const Plan& p, int u_pr
              "  }\n"
              "  atomicAdd(obj + r, objacc);\n"
              "}\n\n";
+    }
     // K5: exact verification of the rounded models + ERWA counters over the same tiles
     for (uint32_t k = 0; k < p.n_jit_kclasses; ++k) emit_verify_class(o, k, p.kclasses[k], tmpl_of(p.kclasses[k]));
     o << "extern \"C\" __global__ void __launch_bounds__(WARPS * 32) fsmt_k5_jit(\n"
