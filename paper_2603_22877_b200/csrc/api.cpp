@@ -38,6 +38,7 @@ struct fsmt_ctx {
     JitKernel jit;
     JitKernel jit_r;            // fsmt_prepare(R): the same module with R a compile-time constant
     uint32_t jit_r_R = 0;
+    int jit_r_cap = 0;          // the prepared hot sweep's register cap (min CTAs/SM; 0 = none)
     DevTiles T{};
     DevSlots slots{};                  // slot tables of the symmetric JIT classes (has_sym)
     cudaGraphExec_t gexec = nullptr;   // fsmt_run_stage's PGD steps as one CUDA graph (re-used, updated)
@@ -700,12 +701,15 @@ fsmt_status fsmt_jit_info(const fsmt_ctx* ctx, uint32_t* n_jit_classes, uint32_t
     if (jit_cons) *jit_cons = active ? ctx->plan.jit_cons_end : 0;
     if (msg && msg_len) {
         std::string m = ctx->host_only ? "host-only" : (active ? "active" : (ctx->plan.tiles.empty() ? "no JIT classes" : ctx->jit_error));
+        if (active && ctx->jit_r.kernel)
+            m += "; prepared R=" + std::to_string(ctx->jit_r_R) + " restarts/lane=" + std::to_string(ctx->jit_r.rpl) +
+                 " k1 cap=" + std::to_string(ctx->jit_r_cap);
         snprintf(msg, msg_len, "%s", m.c_str());
     }
     return FSMT_OK;
 }
 
-static std::string prepared_source_tuned(const fsmt_ctx* ctx, uint32_t R, bool& lane2);
+static std::string prepared_source_tuned(const fsmt_ctx* ctx, uint32_t R, bool& lane2, int* cap);
 
 fsmt_status fsmt_jit_check(fsmt_ctx* ctx, size_t* cubin_bytes, char* log, size_t log_len) {
     if (!ctx) return FSMT_ERR_ARG;
@@ -717,7 +721,7 @@ fsmt_status fsmt_jit_check(fsmt_ctx* ctx, size_t* cubin_bytes, char* log, size_t
     std::string src = ctx->jit_src;
     if (const char* rc = getenv("FSMT_JIT_CHECK_RC")) {
         bool lane2 = false;
-        src = prepared_source_tuned(ctx, (uint32_t)atoi(rc), lane2);
+        src = prepared_source_tuned(ctx, (uint32_t)atoi(rc), lane2, nullptr);
     }
     bool ok = jit_cubin(src, cubin, lg, err);
     if (log && log_len) snprintf(log, log_len, "%s", lg.c_str());
@@ -755,13 +759,17 @@ static long spill_stores(const std::string& log, const std::string& kernel) {
 // The prepared module's source with the hot kernel's register cap: the highest residency (32,
 // then 28 one-warp CTAs per SM: 64 / 72 registers) whose compile has no spills, else no cap
 // (cfg3 best at 64, cfg4 at 72, cfg2 uncapped)
-static std::string prepared_source_tuned(const fsmt_ctx* ctx, uint32_t R, bool& lane2) {
+static std::string prepared_source_tuned(const fsmt_ctx* ctx, uint32_t R, bool& lane2, int* cap = nullptr) {
     for (int mc : {32, 28}) {
         const std::string src = prepared_source(ctx, R, lane2, mc);
         std::vector<char> cubin;
         std::string log, err;
-        if (jit_cubin(src, cubin, log, err) && spill_stores(log, "fsmt_k1_jit") == 0) return src;
+        if (jit_cubin(src, cubin, log, err) && spill_stores(log, "fsmt_k1_jit") == 0) {
+            if (cap) *cap = mc;
+            return src;
+        }
     }
+    if (cap) *cap = 0;
     return prepared_source(ctx, R, lane2, 0);
 }
 
@@ -778,12 +786,30 @@ fsmt_status fsmt_prepare(fsmt_ctx* ctx, uint32_t R) {
     cudaStreamSynchronize(ctx->stream);   // the previous copy may still be in flight
     jit_release(ctx->jit_r);
     ctx->jit_r_R = 0;
+    // register cap of the hot sweep: the highest residency (32, then 28 one-warp CTAs per SM:
+    // 64 / 72 registers) whose kernel needs no local memory (no spills), else none (DESIGN.md
+    // §7 item 13).  Judged from the loaded kernel's attributes, not the compiler log.
     bool lane2 = false;
-    const std::string src = prepared_source_tuned(ctx, R, lane2);
+    int cap = 0;
     std::string err;
-    if (!jit_compile(src, ctx->jit_r, err))
-        return fail(ctx, FSMT_ERR_CUDA, "fsmt_prepare: " + err);
+    for (int mc : {32, 28, 0}) {
+        JitKernel cand;
+        if (!jit_compile(prepared_source(ctx, R, lane2, mc), cand, err)) {
+            if (mc == 0) return fail(ctx, FSMT_ERR_CUDA, "fsmt_prepare: " + err);
+            continue;
+        }
+        cudaFuncAttributes fa{};
+        const bool spills = cudaFuncGetAttributes(&fa, (const void*)cand.kernel) != cudaSuccess || fa.localSizeBytes > 0;
+        if (spills && mc != 0) {
+            jit_release(cand);
+            continue;
+        }
+        ctx->jit_r = cand;
+        cap = mc;
+        break;
+    }
     ctx->jit_r.rpl = lane2 ? 2 : 1;
+    ctx->jit_r_cap = cap;
     ctx->jit_r_R = R;
     return FSMT_OK;
 }
@@ -793,7 +819,7 @@ size_t fsmt_jit_source(const fsmt_ctx* ctx, char* buf, size_t len) {
     std::string src = ctx->jit_src;
     if (const char* rc = getenv("FSMT_JIT_CHECK_RC")) {   // the source fsmt_prepare(R) would compile
         bool lane2 = false;
-        if (!src.empty()) src = prepared_source_tuned(ctx, (uint32_t)atoi(rc), lane2);
+        if (!src.empty()) src = prepared_source_tuned(ctx, (uint32_t)atoi(rc), lane2, nullptr);
     }
     if (buf && len) snprintf(buf, len, "%s", src.c_str());
     return src.size() + 1;
