@@ -148,6 +148,8 @@ def test_k1_full_size_sampled(gpu_mod, name, R):
     constraints touching them), objective via sum of the kernel's own E_c terms."""
     inst = fsmt_gen.config(name)
     s = make(gpu_mod, inst.text)
+    s.prepare(R)                      # the kernels bench.py times (fsmt_prepare(R), DESIGN.md §7 item 11)
+    assert f"prepared R={R}" in s.jit_info()["status"]
     d = s.get_dims()
     a, b = random_points(d["n_bool"], d["n_real"], R, seed=4, b_lo=0.0, b_hi=1.0)
     s.begin(R, 4)
@@ -181,6 +183,7 @@ def test_k5_full_size_sampled(gpu_mod, name, R):
     (R22), and the unsat counts equal the per-constraint sums."""
     inst = fsmt_gen.config(name)
     s = make(gpu_mod, inst.text)
+    s.prepare(R)                      # the kernels bench.py times
     d = s.get_dims()
     rng = np.random.default_rng(11)
     x = np.where(rng.random((d["n_bool"], R)) < 0.5, -1, 1).astype(np.int8)
