@@ -1,3 +1,4 @@
+#include <cstdlib>
 // sm_100a kernels of the FourierSMT hot path.
 //
 //   K0 k0_init    Philox init of (a, b) + projection            (R20; Def.1)
@@ -409,6 +410,8 @@ void launch_sweep_jit(cudaKernel_t k, uint32_t rpl, const DevFormula& F, const D
     const unsigned blocks = (unsigned)((nw + kJitWarps - 1) / kJitWarps);
     const size_t smem = (size_t)kJitWarps * ((size_t)kVmax * 32 * 4 * rpl + (size_t)kVtot * 4);
     if (smem > 48 * 1024) cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (const char* co = getenv("FSMT_CARVEOUT"))   // A/B: preferred shared-memory carveout (% of max)
+        cudaFuncSetAttribute((const void*)k, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(co));
     uint32_t n_tiles = T.n_tiles, R = S.R, n_bool = F.n_bool;
     const uint8_t* U = S.U;
     const float* PT = D ? D->PT : nullptr;
