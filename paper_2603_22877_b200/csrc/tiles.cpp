@@ -1289,10 +1289,16 @@ void emit_verify_class(std::ostringstream& o, uint32_t kid, const KClass& K, con
     for (uint32_t i = 0; i < nref; ++i)
         if (!is_alias(i) && head_of(i) >= 0) members[(uint32_t)head_of(i)].push_back(i);
     auto ty = [&](uint32_t i) { return std::string(rk[i] == 1 ? "double" : "bool"); };
-    auto load = [&](uint32_t i, const std::string& g) {
-        if (rk[i] == 0) return "xb[(u64)(" + g + ") * R] == (signed char)-1";
-        if (rk[i] == 1) return "(double)FSMT_AT(yb, (u64)(" + g + ") * R4)";
-        return "TTl[(u64)(" + g + ") * R] != 0";
+    // reference i at element offset `e` (u64) of its column: a group member sits at its head's
+    // offset plus the constant dg * R, which folds into the load's immediate when R is a
+    // compile-time constant (fsmt_prepare)
+    auto load_e = [&](uint32_t i, const std::string& e) {
+        if (rk[i] == 0) return "xb[" + e + "] == (signed char)-1";
+        if (rk[i] == 1) return "(double)FSMT_AT(yb, (" + e + ") * 4u)";
+        return "TTl[" + e + "] != 0";
+    };
+    auto moff = [&](const std::string& base, uint32_t m) {
+        return base + " + (u64)((long long)(" + std::to_string(K.aff_dg[m]) + ") * R)";
     };
     // run groups keep their values while the head's variable does not change (one check per
     // group); stream groups load every constraint (one lookup per group)
@@ -1310,14 +1316,15 @@ void emit_verify_class(std::ostringstream& o, uint32_t kid, const KClass& K, con
         if (is_alias(i) || head_of(i) >= 0) continue;
         const std::string ext = "((" + word(1 + i / 2) + " >> " + std::to_string(16 * (i % 2)) + ") & 0xffffu)";
         if (is_stream(i)) {
-            o << "    const u32 gv" << i << " = vs[" << ext << "];\n";
-            o << "    const " << ty(i) << " kv" << i << " = " << load(i, "gv" + std::to_string(i)) << ";\n";
+            const std::string ob = "ob" + std::to_string(i);
+            o << "    const u64 " << ob << " = (u64)vs[" << ext << "] * R;\n";
+            o << "    const " << ty(i) << " kv" << i << " = " << load_e(i, ob) << ";\n";
             for (uint32_t m : members[i])
-                o << "    const " << ty(m) << " kv" << m << " = " << load(m, "gv" + std::to_string(i) + " + (" + std::to_string(K.aff_dg[m]) + ")") << ";\n";
+                o << "    const " << ty(m) << " kv" << m << " = " << load_e(m, moff(ob, m)) << ";\n";
         } else {
-            o << "    { const u32 l = " << ext << "; if (l != kc" << i << ") { kc" << i << " = l; const u32 g = vr[l]; kv" << i << " = "
-              << load(i, "g") << ";";
-            for (uint32_t m : members[i]) o << " kv" << m << " = " << load(m, "g + (" + std::to_string(K.aff_dg[m]) + ")") << ";";
+            o << "    { const u32 l = " << ext << "; if (l != kc" << i << ") { kc" << i << " = l; const u64 ob = (u64)vr[l] * R; kv" << i
+              << " = " << load_e(i, "ob") << ";";
+            for (uint32_t m : members[i]) o << " kv" << m << " = " << load_e(m, moff("ob", m)) << ";";
             o << " } }\n";
         }
     }
