@@ -406,8 +406,9 @@ void launch_sweep_jit(cudaKernel_t k, uint32_t rpl, const DevFormula& F, const D
     if (T.n_tiles == 0 || S.R == 0) return;
     const int kJitWarps = (int)(T.warps ? T.warps : 1);
     const int kVmax = (int)T.vmax, kVtot = (int)(T.vmax + T.rmax);    // Plan::vmax, Plan::rmax
-    const uint64_t nw = (uint64_t)T.n_tiles * ((S.R + 32 * rpl - 1) / (32 * rpl));   // one warp per (tile, 32*rpl restarts)
-    const unsigned blocks = (unsigned)((nw + kJitWarps - 1) / kJitWarps);
+    // one warp per (tile, 32*rpl restarts); a CTA's warps share one tile
+    const uint64_t rtiles = (S.R + 32 * rpl - 1) / (32 * rpl);
+    const unsigned blocks = (unsigned)((uint64_t)T.n_tiles * ((rtiles + kJitWarps - 1) / kJitWarps));
     const size_t smem = (size_t)kJitWarps * ((size_t)kVmax * 32 * 4 * rpl + (size_t)kVtot * 4);
     if (smem > 48 * 1024) cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (const char* co = getenv("FSMT_CARVEOUT"))   // A/B: preferred shared-memory carveout (% of max)

@@ -1408,9 +1408,10 @@ std::string jit_source(const Formula& f, const Built& b, const Plan& p, int u_pr
     // the per-constraint E_c debug hook is live.  Separate kernels, so the hot one keeps its own
     // register allocation.
     for (int dbgk = 0; dbgk < 2; ++dbgk) {
-    // hot kernel: k1_min_ctas resident one-warp CTAs per SM as a register cap (fsmt_prepare picks
+    // hot kernel: k1_min_ctas resident warps per SM as a register cap (fsmt_prepare picks
     // the largest of 32 / 28 that compiles without spills; 0 = none); FSMT_JIT_MINB overrides
-    const std::string mb = minb ? std::string(minb) : (dbgk || k1_min_ctas <= 0 ? std::string() : std::to_string(k1_min_ctas));
+    const std::string mb = minb ? std::string(minb)
+                                : (dbgk || k1_min_ctas <= 0 ? std::string() : std::to_string(std::max(1, k1_min_ctas / (int)p.jit_warps)));
     o << "extern \"C\" __global__ void __launch_bounds__(WARPS * 32" << (atoi(mb.c_str()) > 0 ? ", " + mb : std::string())
       << ") fsmt_k1_jit" << (dbgk ? "_dbg" : "") << "(\n"
          "    const TileDesc* __restrict__ tiles, u32 n_tiles, const uint4* __restrict__ recs,\n"
@@ -1426,10 +1427,11 @@ std::string jit_source(const Formula& f, const Built& b, const Plan& p, int u_pr
                 : "  float* acc = smem + warp * (VMAX * 32);                  // stream-variable rows\n")
       << "  u32* vs = (u32*)(smem + WARPS * VMAX * 32 * RPL) + warp * VTOT; // stream then run variable ids\n"
          "  const u32 rtiles = (R + 32 * RPL - 1) / (32 * RPL);\n"
-         "  const u64 gw = (u64)blockIdx.x * WARPS + warp;\n"
-         "  const u32 rt = (u32)(gw % rtiles);\n"
-         "  const u64 ti = gw / rtiles;\n"
-         "  if (ti >= n_tiles) return;\n"
+         "  // a CTA's warps are restart tiles of ONE constraint tile (CTA-uniform tile, shared records)\n"
+         "  const u32 rtw = (rtiles + WARPS - 1) / WARPS;\n"
+         "  const u64 ti = blockIdx.x / rtw;\n"
+         "  const u32 rt = (u32)(blockIdx.x % rtw) * WARPS + warp;\n"
+         "  if (ti >= n_tiles || rt >= rtiles) return;\n"
          "  const TileDesc T = tiles[ti];\n"
          "  const u32 n_s = T.n_vars & 0xffffu, n_v = n_s + (T.n_vars >> 16);\n"
          "  const u32 r = rt * 32 * RPL + lane * RPL;   // the lane's (first) restart\n"
