@@ -124,12 +124,15 @@ fsmt_status fsmt_load_formula(fsmt_ctx* ctx, const char* hsmt, size_t len);
 fsmt_status fsmt_build_xbdd(fsmt_ctx* ctx, uint64_t node_budget);
 
 /* Optional, after fsmt_build_xbdd: compile a second copy of the specialised sweep/check
- * kernels (K1, K5; DESIGN.md §7 item 10) with the restart count R as a compile-time
- * constant (NVRTC, about 1-3 s, host only).  Every later launch over a state of exactly R
- * restarts (fsmt_begin / fsmt_solve with restarts == R) uses it; other R keep the generic
- * kernels.  Results are bit-identical to the generic kernels.  R == 0 drops the copy.
- * FSMT_ERR_STATE before build; FSMT_ERR_CUDA if the compile fails (the generic kernels stay
- * in use); OK and no effect when the formula has no specialised kernel classes. */
+ * kernels (K1, K5; DESIGN.md §7 items 11 and 13) for exactly R restarts: R as a compile-time
+ * constant, U[c][r] loaded 3 constraints ahead when U exceeds the L2, and the hot sweep's
+ * register cap chosen among 64 / 72 / none as the first whose kernel does not spill (NVRTC +
+ * load, up to three candidate compiles, a few seconds).  Every later launch over a state of
+ * exactly R restarts (fsmt_begin / fsmt_solve with restarts == R) uses it; other R keep the
+ * generic kernels.  Per constraint and restart the arithmetic is the generic kernels'.  R == 0
+ * drops the copy.  FSMT_ERR_STATE before build; FSMT_ERR_CUDA if no candidate compiles (the
+ * generic kernels stay in use); OK and no effect for a host-only context or a formula
+ * without specialised kernel classes. */
 fsmt_status fsmt_prepare(fsmt_ctx* ctx, uint32_t R);
 
 fsmt_status fsmt_get_dims(const fsmt_ctx* ctx, fsmt_dims* out);
