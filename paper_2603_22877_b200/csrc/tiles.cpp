@@ -1113,8 +1113,8 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
         push(nd.lo, "pf" + std::to_string(nd.level));
     }
     // backward pass (Alg.B, sign R1): m_bu in registers, dE/dv per slot.  Complement form
-    // (opt-in FSMT_JIT_CMP=1; fewer instructions but slower on cfg4): when more
-    // edges reach TRUE than FALSE, the pass carries
+    // (FSMT_JIT_CMP=0 disables): when more edges reach TRUE than FALSE, the pass
+    // carries
     // c[v] = 1 - m_bu[v] (the same linear recurrence with the terminal values swapped,
     // using p + (1 - p) = 1), so the OR-chains' "1 - m_bu" subtractions vanish; then
     // G_s = -dCOP/dp_s and every use of G takes the sign back (gref).
@@ -1127,7 +1127,7 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
         }
     }
     const char* cmp_env = getenv("FSMT_JIT_CMP");
-    const bool cmp = cmp_env && cmp_env[0] == '1' && e_true > e_false;
+    const bool cmp = !(cmp_env && cmp_env[0] == '0') && e_true > e_false;
     for (size_t s = 0; s < ns; ++s) o << "    " << TY << " G" << s << " = " << ZR << ";\n";
     // G_s += a * b; the first contribution is a plain product (G starts at 0: only the sign
     // of a zero can differ)

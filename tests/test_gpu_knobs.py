@@ -25,7 +25,7 @@ KNOBS = [
     {"FSMT_JIT_STREAM": "0"},
     {"FSMT_JIT_PAIR": "0", "FSMT_JIT_UPF": "0"},
     {"FSMT_JIT_UPF": "3"},
-    {"FSMT_JIT_CMP": "1"},
+    {"FSMT_JIT_CMP": "0"},
     {"FSMT_TILE_VMAX": "16", "FSMT_TILE_RMAX": "16", "FSMT_TILE_CMAX": "3"},
 ]
 
