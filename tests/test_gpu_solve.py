@@ -75,22 +75,27 @@ def test_solve_rounding_modes_sound(rounding):
     assert sum(not v for v in sat) == res.stats["best_unsat"]
 
 
-def _init_nccl():
+@pytest.fixture(scope="module")
+def nccl_world1():
+    """A world-size-1 NCCL process group for the driver tests, destroyed afterwards."""
     import torch.distributed as dist
-    if not dist.is_initialized():
+    own = not dist.is_initialized()
+    if own:
         sock = socket.socket()
         sock.bind(("127.0.0.1", 0))
         port = sock.getsockname()[1]
         sock.close()
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK="0", WORLD_SIZE="1")
         dist.init_process_group("nccl", rank=0, world_size=1)
+    yield
+    if own:
+        dist.destroy_process_group()
 
 
 @pytest.mark.parametrize("mode", ["restart", "constraint"])
-def test_dist_drivers_world1_reproduce_solve(mode):
+def test_dist_drivers_world1_reproduce_solve(mode, nccl_world1):
     import torch
     from paper_2603_22877_b200 import dist as D
-    _init_nccl()
     torch.cuda.set_device(0)
     inst = fsmt_gen.config("cfg4s")
     kappas = [0.5, 1.0, 2.0, 4.0, 8.0]
