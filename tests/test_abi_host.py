@@ -139,7 +139,12 @@ def test_parse_errors_and_state_machine():
         s2.build_xbdd()
     assert e.value.status == N.ERR_STATE
     s2.load_formula(fsmt_gen.cfg1().text)
+    with pytest.raises(FsmtError) as e:       # fsmt_prepare needs a built formula
+        s2.prepare(64)
+    assert e.value.status == N.ERR_STATE
     s2.build_xbdd()
+    s2.prepare(64)                            # host-only: OK, no effect
+    assert "prepared" not in s2.jit_info()["status"]
     with pytest.raises(FsmtError) as e:
         s2.begin(4, 1)
     assert e.value.status == N.ERR_CUDA
