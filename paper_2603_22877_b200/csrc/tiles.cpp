@@ -617,7 +617,7 @@ bool jit_pair() {
 
 // FSMT_JIT_UPF=d: the sweep loads U[c][r] d constraints ahead (0: in the iteration, plain load).
 // Without the variable: g_upf (jit_source's argument; fsmt_prepare picks it from the size of U).
-int g_upf = 0;
+thread_local int g_upf = 0;   // per thread: contexts may build concurrently
 int u_prefetch() {
     const char* e = getenv("FSMT_JIT_UPF");
     return e ? std::max(0, std::min(12, atoi(e))) : g_upf;
@@ -760,7 +760,7 @@ const char* comp(uint32_t w) {
 
 // Record word w of the class being emitted (g_wk): a register of the loaded (compressed)
 // record, or a literal when the word is constant over the class (record compression).
-const KClass* g_wk = nullptr;
+thread_local const KClass* g_wk = nullptr;
 std::string word(uint32_t w) {
     if (g_wk && w < g_wk->wpos.size()) {
         const int32_t p = g_wk->wpos[w];
@@ -773,7 +773,7 @@ std::string word(uint32_t w) {
 // Two restarts per lane (fsmt_prepare with an even R, DESIGN.md §7 item 11): every per-restart
 // value is a float2 (restarts r, r + 1 of the lane), arithmetic on the packed f32x2 pipe through
 // the operator overloads of kLane2Prelude; per component the operations of the scalar sweep.
-bool g_v2 = false;
+thread_local bool g_v2 = false;
 
 void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Template& t) {
     g_wk = &K;
