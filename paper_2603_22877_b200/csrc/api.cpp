@@ -777,6 +777,8 @@ fsmt_status fsmt_prepare(fsmt_ctx* ctx, uint32_t R) {
     fsmt_status s = need(ctx, 2, "fsmt_prepare");
     if (s) return s;
     if (R == 0 || !ctx->jit.kernel || ctx->host_only) {
+        if (!ctx->host_only) cudaStreamSynchronize(ctx->stream);
+        if (ctx->gexec) { cudaGraphExecDestroy(ctx->gexec); ctx->gexec = nullptr; }
         jit_release(ctx->jit_r);
         ctx->jit_r_R = 0;
         return FSMT_OK;
@@ -784,6 +786,7 @@ fsmt_status fsmt_prepare(fsmt_ctx* ctx, uint32_t R) {
     if (ctx->jit_r.kernel && ctx->jit_r_R == R) return FSMT_OK;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);   // the previous copy may still be in flight
+    if (ctx->gexec) { cudaGraphExecDestroy(ctx->gexec); ctx->gexec = nullptr; }   // may hold its kernels
     jit_release(ctx->jit_r);
     ctx->jit_r_R = 0;
     // register cap of the hot sweep: the highest residency (32, then 28 one-warp CTAs per SM:
