@@ -200,3 +200,24 @@ def test_graph_captured_stages_reproduce_solve():
     assert out[0][0] == out[1][0] and out[0][1] == out[1][1]
     for k in (2, 3, 4, 5):
         assert np.array_equal(out[0][k], out[1][k])
+
+
+def test_graph_then_prepare_reproduces_solve():
+    """A stage graph captured with the generic kernels is dropped by fsmt_prepare, and the next
+    solve (prepared kernels, graph re-captured) reproduces the generic solve's verdict and
+    violation count."""
+    inst = fsmt_gen.config("cfg4s")
+    os.environ["FSMT_GRAPH"] = "1"
+    try:
+        s = make(inst.text)
+        s.set_params(eta=0.05, rounding=1, kappas=[0.5, 1.0, 2.0, 4.0])
+        r1 = s.solve(128, 12, 4)
+        s.prepare(128)
+        assert "prepared R=128" in s.jit_info()["status"]
+        r2 = s.solve(128, 12, 4)
+        s.prepare(0)
+        r3 = s.solve(128, 12, 4)
+    finally:
+        os.environ.pop("FSMT_GRAPH", None)
+    assert r1.verdict == r2.verdict == r3.verdict
+    assert r1.stats["best_unsat"] == r2.stats["best_unsat"] == r3.stats["best_unsat"]
