@@ -1223,8 +1223,8 @@ fsmt_status fsmt_solve(fsmt_ctx* ctx, uint32_t restarts, uint32_t steps, uint64_
     if ((s = fsmt_begin(ctx, restarts, seed, 0))) return s;
     const uint32_t nbool = ctx->F.n_bool, nreal = ctx->F.n_real;
     std::vector<uint32_t> unsat(restarts);
-    std::vector<int8_t> bx(nbool), cx(nbool);
-    std::vector<float> by(nreal), cy(nreal);
+    std::vector<int8_t> bx(nbool);
+    std::vector<float> by(nreal);
     uint32_t best_unsat = UINT32_MAX, best_stage = 0, best_r = 0;
     uint32_t stages = 0, steps_run = 0;
     bool sat = false, timeout = false;
@@ -1238,17 +1238,11 @@ fsmt_status fsmt_solve(fsmt_ctx* ctx, uint32_t restarts, uint32_t steps, uint64_
         uint32_t r_min = 0;
         for (uint32_t r = 1; r < restarts; ++r)
             if (unsat[r] < unsat[r_min]) r_min = r;
-        if (unsat[r_min] < best_unsat) {
-            if ((s = fsmt_get_model(ctx, r_min, cx.data(), cy.data()))) return s;
-            uint32_t host_unsat = verify_host(ctx->f, ctx->b, cx.data(), cy.data(), nullptr);
-            if (unsat[r_min] == 0 && host_unsat != 0)
-                return fail(ctx, FSMT_ERR_CUDA, "device verdict SAT contradicted by host re-verification");
+        if (unsat[r_min] < best_unsat) {   // keep the model; the host re-check runs once, on the returned one
+            if ((s = fsmt_get_model(ctx, r_min, bx.data(), by.data()))) return s;
             best_unsat = unsat[r_min];
             best_stage = t;
             best_r = r_min;
-            bx = cx;
-            by = cy;
-            st.host_verified = host_unsat == unsat[r_min];
         }
         if (best_unsat == 0) {
             sat = true;
@@ -1259,6 +1253,13 @@ fsmt_status fsmt_solve(fsmt_ctx* ctx, uint32_t restarts, uint32_t steps, uint64_
             timeout = true;
             break;
         }
+    }
+    // host fp64 re-verification of the returned model ("never SAT without verify")
+    if (best_unsat != UINT32_MAX) {
+        const uint32_t host_unsat = verify_host(ctx->f, ctx->b, bx.data(), by.data(), nullptr);
+        if (sat && host_unsat != 0)
+            return fail(ctx, FSMT_ERR_CUDA, "device verdict SAT contradicted by host re-verification");
+        st.host_verified = host_unsat == best_unsat;
     }
     *verdict = sat ? FSMT_SAT : FSMT_UNKNOWN;
     if (x_out) std::copy(bx.begin(), bx.end(), x_out);

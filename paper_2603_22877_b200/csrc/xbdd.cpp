@@ -12,6 +12,7 @@
 #include <cmath>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <unordered_map>
 
 #include "fsmt_internal.hpp"
@@ -361,9 +362,11 @@ Built build_xbdds(const Formula& f, uint64_t node_budget) {
     return b;
 }
 
-uint32_t verify_host(const Formula& f, const Built& b, const int8_t* x, const float* y, uint8_t* per_con) {
+// Exact check of one model (R22) over constraints [c0, c1): the number violated.
+static uint32_t verify_range(const Formula& f, const Built& b, const int8_t* x, const float* y, uint8_t* per_con,
+                             size_t c0, size_t c1) {
     uint32_t n = 0;
-    for (size_t ci = 0; ci < f.cons.size(); ++ci) {
+    for (size_t ci = c0; ci < c1; ++ci) {
         const Template& t = b.tmpls[b.cons_tmpl[ci]];
         const uint32_t* ids = b.slot_ids.data() + b.cons_slot_off[ci];
         int v = t.root;
@@ -376,6 +379,23 @@ uint32_t verify_host(const Formula& f, const Built& b, const int8_t* x, const fl
         n += u;
         if (per_con) per_con[ci] = u;
     }
+    return n;
+}
+
+// The host re-verification: constraint ranges on the host's cores (each constraint's
+// verdict is independent, so the count does not depend on the split).
+uint32_t verify_host(const Formula& f, const Built& b, const int8_t* x, const float* y, uint8_t* per_con) {
+    const size_t C = f.cons.size();
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const size_t nt = C < 20000 ? 1 : std::min<size_t>(hw, 16);
+    if (nt == 1) return verify_range(f, b, x, y, per_con, 0, C);
+    std::vector<uint32_t> part(nt, 0);
+    std::vector<std::thread> th;
+    for (size_t k = 0; k < nt; ++k)
+        th.emplace_back([&, k] { part[k] = verify_range(f, b, x, y, per_con, C * k / nt, C * (k + 1) / nt); });
+    for (auto& t : th) t.join();
+    uint32_t n = 0;
+    for (uint32_t v : part) n += v;
     return n;
 }
 

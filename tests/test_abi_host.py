@@ -174,3 +174,24 @@ def test_jit_source_compiles_for_sm100a(tmp_path, name):
                          capture_output=True, text=True)
     assert out.returncode == 0, out.stderr[-3000:]
     assert "0 bytes spill stores" in out.stderr, out.stderr[-2000:]
+
+
+def test_host_verify_threaded_large_matches_oracle():
+    """fsmt_verify on cfg3 (114,688 constraints: the multi-threaded host re-check) agrees with
+    the oracle's exact semantics on a sample of constraints, and its count with its per-constraint
+    verdicts."""
+    from tests.helpers import subformula
+    inst = fsmt_gen.config("cfg3")
+    s = _host(inst.text)
+    rng = np.random.default_rng(5)
+    x = inst.x_star.copy()
+    flip = rng.random(len(x)) < 0.05
+    x[flip] = -x[flip]
+    y = (inst.y_star + rng.normal(0, 0.02, len(inst.y_star))).astype(np.float32)
+    n, pc = s.verify(x, y, per_con=True)
+    assert n == int(pc.sum()) and 0 < n < len(pc)
+    csel = np.sort(rng.choice(len(pc), 1500, replace=False))
+    sub, keep = subformula(inst.text, extra_constraints=csel)
+    fs = hsmt.parse(sub)
+    want = np.array([0 if semantics.constraint_sat(fs, c, x, y) else 1 for c in fs.constraints])
+    assert np.array_equal(pc[keep].astype(int), want)
