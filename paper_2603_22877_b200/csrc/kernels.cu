@@ -348,9 +348,9 @@ __global__ void __launch_bounds__(256) k5_verify(DevFormula F, DevState S, const
         }
         const uint32_t u = (v == kFalseT) ? 1u : 0u;            // u_c = f_c/2 + 1/2 (Alg.2 line 7)
         cnt += u;
-        if (Uupd) {
+        if (Uupd && u) {                                      // U += u: only violated constraints touch memory
             uint8_t& cell = Uupd[(size_t)c * R + r];
-            cell = (uint8_t)min(255u, (uint32_t)cell + u);
+            cell = (uint8_t)min(255u, (uint32_t)cell + 1u);
         }
         if (per_con) per_con[(size_t)F.orig[c] * R + r] = (uint8_t)u;
     }

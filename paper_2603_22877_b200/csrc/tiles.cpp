@@ -1383,7 +1383,7 @@ void emit_verify_class(std::ostringstream& o, uint32_t kid, const KClass& K, con
     o << "    const u32 u = " << (t.root >= 0 ? "s" + std::to_string(t.root) : std::string(t.root == kTrue ? "true" : "false"))
       << " ? 0u : 1u;\n"
          "    if (live) {\n"
-         "      if (U) { unsigned char* cell = U + (u64)(T.cons_begin + c) * R + rr; const u32 nv = (u32)*cell + u; *cell = (unsigned char)(nv > 255u ? 255u : nv); }\n"
+         "      if (U && u) { unsigned char* cell = U + (u64)(T.cons_begin + c) * R + rr; const u32 nv = (u32)*cell + 1u; *cell = (unsigned char)(nv > 255u ? 255u : nv); }   // U += u: only violated constraints touch memory\n"
          "      if (per_con) per_con[(u64)orig[T.cons_begin + c] * R + rr] = (unsigned char)u;\n"
          "    }\n"
          "    cnt += u;\n  }\n  return cnt;\n}\n\n";
