@@ -592,7 +592,7 @@ fsmt_status fsmt_begin(fsmt_ctx* ctx, uint32_t R, uint64_t seed, uint32_t restar
         return FSMT_OK;
     };
     const size_t nb = (size_t)F.n_bool * R, nr = (size_t)F.n_real * R, nc = (size_t)F.n_cons * R;
-    const size_t parts = (size_t)update_parts(F);
+    const size_t parts = (size_t)update_parts(F, R);
     if ((s = alloc((void**)&S.a, nb * 4)) || (s = alloc((void**)&S.b, nr * 4)) || (s = alloc((void**)&S.ga, nb * 8)) ||
         (s = alloc((void**)&S.gb, nr * 8)) || (s = alloc((void**)&S.U, nc)) || (s = alloc((void**)&S.obj, (size_t)R * 8)) ||
         (s = alloc((void**)&S.x, nb)) || (s = alloc((void**)&S.unsat, (size_t)R * 4)) ||

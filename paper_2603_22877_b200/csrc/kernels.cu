@@ -244,12 +244,12 @@ __global__ void __launch_bounds__(128) k_dykstra(DevFormula F, DevState S, float
     for (uint32_t v = threadIdx.x; v < nv; v += blockDim.x) X[(size_t)F.hvars[v] * R + r] = xs[v];
 }
 
-__global__ void k3_norm(DevFormula F, DevState S, float eta, float eta_b) {
+__global__ void k3_norm(DevFormula F, DevState S, float eta, float eta_b, uint32_t vpp) {
     const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= S.R) return;
     const uint32_t part = blockIdx.y;
     const uint32_t nv = F.n_bool + F.n_real;
-    const uint32_t v0 = part * kVarsPerPart, v1 = min(v0 + kVarsPerPart, nv);
+    const uint32_t v0 = part * vpp, v1 = min(v0 + vpp, nv);
     double acc = 0.0;
     for (uint32_t v = v0; v < v1; ++v) {
         float x, xn;
@@ -265,6 +265,23 @@ __global__ void k3_norm(DevFormula F, DevState S, float eta, float eta_b) {
         acc += d * d;
     }
     S.gm2_part[(size_t)part * S.R + r] = acc;
+}
+
+// few restarts (R < 512): many short parts, summed per restart by one block (fixed order)
+__global__ void k3_final_block(DevState S, uint32_t n_parts, float eps) {
+    __shared__ double red[8];
+    const uint32_t r = blockIdx.x;
+    double acc = 0.0;
+    for (uint32_t p = threadIdx.x; p < n_parts; p += blockDim.x) acc += S.gm2_part[(size_t)p * S.R + r];
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (uint32_t w = 0; w < blockDim.x / 32; ++w) t += red[w];
+        S.gm2[r] = t;
+        if (!S.frozen[r] && t <= (double)eps * (double)eps) S.frozen[r] = 1;   // Eq.14
+    }
 }
 
 __global__ void k3_final(DevState S, uint32_t n_parts, float eps) {
@@ -481,11 +498,17 @@ void launch_sweep(const DevFormula& F, const DevState& S, float kappa, float wsc
                                                          std::max<int>(1, F.max_slots), std::max<int>(1, F.max_nodes));
 }
 
-int update_parts(const DevFormula& F) { return (int)((F.n_bool + F.n_real + kVarsPerPart - 1) / kVarsPerPart); }
+// variables per part of the gradient-mapping norm: 64 for many restarts (one thread per restart
+// and part is enough parallelism), fewer for small R so the grid still fills the GPU
+static uint32_t vars_per_part(uint32_t R) { return R >= 512 ? (uint32_t)kVarsPerPart : (R >= 128 ? 16u : 4u); }
+int update_parts(const DevFormula& F, uint32_t R) {
+    const uint32_t vpp = vars_per_part(R);
+    return (int)((F.n_bool + F.n_real + vpp - 1) / vpp);
+}
 
 void launch_update(const DevFormula& F, const DevState& S, float eta, float eps, cudaStream_t st, float eta_b) {
     if (!(eta_b > 0.f)) eta_b = eta;
-    const uint32_t parts = (uint32_t)update_parts(F);
+    const uint32_t parts = (uint32_t)update_parts(F, S.R);
     if (parts == 0 || S.R == 0) return;
     DevState Sp = S;
     if (F.proj_iters && F.n_half && S.bn) {       // Prop.1 with halfspaces (R33): candidate + Dykstra
@@ -495,9 +518,11 @@ void launch_update(const DevFormula& F, const DevState& S, float eta, float eps,
     } else {
         Sp.bn = nullptr;
     }
-    dim3 g1((S.R + 127) / 128, parts);
-    k3_norm<<<g1, 128, 0, st>>>(F, Sp, eta, eta_b);
-    k3_final<<<(S.R + 127) / 128, 128, 0, st>>>(S, parts, eps);
+    const uint32_t tpb = S.R >= 128 ? 128u : 32u * ((S.R + 31) / 32);
+    dim3 g1((S.R + tpb - 1) / tpb, parts);
+    k3_norm<<<g1, tpb, 0, st>>>(F, Sp, eta, eta_b, vars_per_part(S.R));
+    if (S.R >= 512) k3_final<<<(S.R + 127) / 128, 128, 0, st>>>(S, parts, eps);
+    else k3_final_block<<<S.R, 256, 0, st>>>(S, parts, eps);
     const uint64_t n = (uint64_t)(F.n_bool + F.n_real) * S.R;
     const uint64_t blocks = std::min<uint64_t>((n + 255) / 256, 148ull * 16);
     k3_apply<<<(unsigned)blocks, 256, 0, st>>>(F, Sp, eta, eta_b);

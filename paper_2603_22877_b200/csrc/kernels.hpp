@@ -117,7 +117,7 @@ void launch_gather_rows_u8(uint8_t* dst, const uint8_t* src, const uint32_t* idx
 void launch_scatter_rows_u8(uint8_t* dst, const uint8_t* src, const uint32_t* idx, uint32_t rows, uint32_t R,
                             cudaStream_t st);
 // K3: projected step (three launches: partial norms, finalize, apply).
-int update_parts(const DevFormula& F);
+int update_parts(const DevFormula& F, uint32_t R);   // parts of the K3 norm (size of gm2_part / R)
 // eta: step for a (Booleans); eta_b: step for b (reals), <= 0 -> eta (Eq.11 uses one eta; R13).
 void launch_update(const DevFormula& F, const DevState& S, float eta, float eps, cudaStream_t st, float eta_b = 0.f);
 // Dykstra projection (R33) of X [n_real][R] in place: F.proj_iters sweeps over the halfspaces then
