@@ -3,7 +3,11 @@
 return, excluding load/build (reported separately), median over seeds (paper protocol:
 8 replicas, median; 1000 s cap).
 
-  python scripts/time_to_sat.py --config cfg4 --restarts 1024 --steps 50 --seeds 0 1 2 3 4 5 6 7
+  python scripts/time_to_sat.py --config cfg4 --seeds 0 1 2 3 4 5 6 7
+
+Defaults are the cfg4 recipe of DESIGN.md §9 (R = 32, 2 PGD steps per stage, eta = 0.4 with
+eta_mode 3, reset-to-0 ERWA, kappa 1 -> 300 over 20 stages then held 200 more); the paper's
+own example schedule is `--schedule "" --kappas ""` with `--eta-mode 0 --erwa 0`.
 """
 from __future__ import annotations
 
@@ -21,18 +25,18 @@ sys.path.insert(0, ROOT)
 def main():
     p = argparse.ArgumentParser()
     p.add_argument("--config", default="cfg4")
-    p.add_argument("--restarts", type=int, default=1024)
-    p.add_argument("--steps", type=int, default=50)
+    p.add_argument("--restarts", type=int, default=32)
+    p.add_argument("--steps", type=int, default=2)
     p.add_argument("--seeds", type=int, nargs="+", default=list(range(8)))
-    p.add_argument("--eta", type=float, default=0.05)
+    p.add_argument("--eta", type=float, default=0.4)
     p.add_argument("--kappas", type=str, default="")
-    p.add_argument("--schedule", type=str, default="",
+    p.add_argument("--schedule", type=str, default="geo1-300-hold10",
                    help="geo<kmin>-<kmax>[-hold<m>]: <stages> geometric kappas kmin..kmax, then kmax m*<stages> more times")
     p.add_argument("--stages", type=int, default=20)
-    p.add_argument("--eta-mode", type=int, default=0)
+    p.add_argument("--eta-mode", type=int, default=3)
     p.add_argument("--proj-iters", type=int, default=0)
     p.add_argument("--n-roundings", type=int, default=1)
-    p.add_argument("--erwa", type=int, default=0)
+    p.add_argument("--erwa", type=int, default=1)
     p.add_argument("--rounding", type=int, default=0)
     p.add_argument("--time-limit", type=float, default=1000.0)
     p.add_argument("--warmup", type=int, default=1, help="untimed solves (seeds 10000+) before the timed seeds")
