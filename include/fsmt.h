@@ -174,6 +174,14 @@ fsmt_status fsmt_sweep(fsmt_ctx* ctx, float kappa, uint32_t stage_t);
 /* Read the last sweep's outputs: grad_a[n_bool][R], grad_b[n_real][R] (f64), obj[R] (f64).
  * Any pointer may be NULL. */
 fsmt_status fsmt_get_sweep(fsmt_ctx* ctx, double* grad_a, double* grad_b, double* obj, int where);
+/* One call for the parity / bench hook of SURVEY §8(b): objective and gradient of R restarts at
+ * the given point.  Allocates (fsmt_begin, seed 0) when no state of R restarts exists, then
+ * overwrites a[n_bool][R], b[n_real][R] (not projected) and the ERWA counters (U[n_cons][R];
+ * NULL = all 0), runs K1 (= fsmt_sweep(kappa, stage_t)) and writes obj[R], grad_a[n_bool][R],
+ * grad_b[n_real][R] (f64; any output may be NULL).  All pointers are host (FSMT_HOST) or device
+ * (FSMT_DEVICE) per `where`.  Replaces the context's current state. */
+fsmt_status fsmt_eval(fsmt_ctx* ctx, uint32_t R, const float* a, const float* b, float kappa, const uint8_t* U,
+                      uint32_t stage_t, double* obj, double* grad_a, double* grad_b, int where);
 /* Per-constraint E_c for restart r from the last sweep's kernels (debug/parity hook, host E[n_cons]). */
 fsmt_status fsmt_constraint_terms(fsmt_ctx* ctx, float kappa, uint32_t restart, double* E);
 

@@ -943,6 +943,22 @@ fsmt_status fsmt_get_sweep(fsmt_ctx* ctx, double* ga, double* gb, double* obj, i
     return copy_out(ctx, obj, ctx->S.obj, (size_t)ctx->S.R, where);
 }
 
+fsmt_status fsmt_eval(fsmt_ctx* ctx, uint32_t R, const float* a, const float* b, float kappa, const uint8_t* U,
+                      uint32_t stage_t, double* obj, double* grad_a, double* grad_b, int where) {
+    fsmt_status s = need(ctx, 2, "fsmt_eval");
+    if (s) return s;
+    if (R == 0 || !a || !b) return fail(ctx, FSMT_ERR_ARG, "fsmt_eval: R > 0 and the point a, b are required");
+    if (ctx->stage < 3 || ctx->S.R != R) {
+        if ((s = fsmt_begin(ctx, R, 0, 0))) return s;
+    } else if (!U) {
+        CK(cudaMemsetAsync(ctx->S.U, 0, (size_t)ctx->F.n_cons * R, ctx->stream));
+    }
+    if ((s = fsmt_set_state(ctx, a, b, where))) return s;
+    if (U && (s = fsmt_set_counters(ctx, U, where))) return s;
+    if ((s = fsmt_sweep(ctx, kappa, stage_t))) return s;
+    return fsmt_get_sweep(ctx, grad_a, grad_b, obj, where);
+}
+
 fsmt_status fsmt_constraint_terms(fsmt_ctx* ctx, float kappa, uint32_t restart, double* E) {
     fsmt_status s = need(ctx, 3, "fsmt_constraint_terms");
     if (s) return s;

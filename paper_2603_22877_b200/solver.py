@@ -66,6 +66,21 @@ class Solver:
         self._check(N.lib.fsmt_get_dims(self._h, C.byref(d)))
         self.dims = d
 
+    def eval(self, a, b, kappa: float, U=None, stage_t: int = 1):
+        """fsmt_eval: (obj[R], grad_a[n_bool][R], grad_b[n_real][R]) at host point a, b (float32)."""
+        a = np.ascontiguousarray(a, dtype=np.float32)
+        b = np.ascontiguousarray(b, dtype=np.float32)
+        R = a.shape[1] if a.ndim == 2 and a.shape[0] else b.shape[1]
+        u = None if U is None else np.ascontiguousarray(U, dtype=np.uint8)
+        obj = np.empty(R, dtype=np.float64)
+        ga = np.empty((self.dims.n_bool, R), dtype=np.float64)
+        gb = np.empty((self.dims.n_real, R), dtype=np.float64)
+        self._check(N.lib.fsmt_eval(self._h, R, a.ctypes.data, b.ctypes.data, kappa,
+                                    None if u is None else u.ctypes.data, stage_t,
+                                    obj.ctypes.data, ga.ctypes.data, gb.ctypes.data, N.HOST))
+        self.R = R                        # fsmt_eval leaves its R-restart state in the context
+        return obj, ga, gb
+
     def prepare(self, R: int):
         """Compile the specialised kernels once more with R restarts as a constant (fsmt_prepare);
         launches over exactly R restarts use that copy (bit-identical, fewer instructions)."""

@@ -392,3 +392,35 @@ def test_jit_active_and_matches_generic(gpu_mod, name, monkeypatch):
     for gj, gg in ((gaj, gag), (gbj, gbg)):
         assert np.max(np.abs(gj - gg)) <= 1e-5 * max(1.0, float(np.max(np.abs(gg))))
     assert np.max(np.abs(Ej - Eg)) <= 1e-6
+
+
+@pytest.mark.parametrize("name", ["cfg3s", "cfg4s"])
+def test_fsmt_eval_one_call(gpu_mod, name):
+    """fsmt_eval (SURVEY §8(b)'s one-call hook) equals set_state + set_counters + sweep + get_sweep
+    on the same context and matches the oracle, with and without ERWA counters."""
+    inst, f = parsed(name)
+    s = make(gpu_mod, inst.text)
+    R = 40
+    a, b = random_points(f.n_bool, f.n_real, R, seed=31, b_lo=0.0, b_hi=1.0)
+    obj, ga, gb = s.eval(a, b, 1.1)
+    for r in (0, R - 1):
+        C, oga, ogb = objective.objective_and_gradient(f, a[:, r], b[:, r], 1.1)
+        check_objective(obj[r], C, float(sum(c.weight for c in f.constraints)), what=f"{name} eval")
+        check_gradient(ga[:, r], oga, what=f"{name} eval grad_a")
+        check_gradient(gb[:, r], ogb, what=f"{name} eval grad_b")
+    rng = np.random.default_rng(2)
+    U = rng.integers(0, 4, size=(len(f.constraints), R), dtype=np.uint8)
+    obj2, ga2, gb2 = s.eval(a, b, 0.9, U=U, stage_t=5)
+    s.set_state(a, b)
+    s.set_counters(U)
+    s.sweep(0.9, 5)
+    o3, g3a, g3b = s.get_sweep()
+    np.testing.assert_allclose(obj2, o3, rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(ga2, g3a, rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(gb2, g3b, rtol=1e-12, atol=1e-12)
+    for r in (0, R - 1):
+        w = weights_of(f, U, r, 5)
+        C, oga, ogb = objective.objective_and_gradient(f, a[:, r], b[:, r], 0.9, w)
+        check_objective(obj2[r], C, float(w.sum()), what=f"{name} eval weighted")
+        check_gradient(np.concatenate([ga2[:, r], gb2[:, r]]), np.concatenate([oga, ogb]), scale_relative=True,
+                       what=f"{name} eval weighted")
