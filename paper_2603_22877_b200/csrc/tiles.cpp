@@ -206,6 +206,27 @@ Plan make_plan(const Formula& f, const Built& b, bool enable_jit) {
         }
     };
     std::vector<uint32_t> vars;
+    // stream-row budget from the typical constraint: 3x its distinct variables, in [40, 56]
+    // (cfg4, 18 variables, best at 54; cfg3, 10 variables, best at 40), unless
+    // FSMT_TILE_VMAX / FSMT_TILE_GROUP set it
+    if (!getenv("FSMT_TILE_VMAX")) {
+        std::map<size_t, uint32_t> nvars;
+        for (uint32_t c = 0; c < C; ++c) {
+            const KClass& K = p.kclasses[kcl[c]];
+            if (!K.jit || K.sym) continue;
+            cons_vars(c, vars);
+            std::sort(vars.begin(), vars.end());
+            ++nvars[(size_t)(std::unique(vars.begin(), vars.end()) - vars.begin())];
+        }
+        size_t mode = 0;
+        uint32_t best = 0;
+        for (const auto& kv : nvars)
+            if (kv.second > best) { best = kv.second; mode = kv.first; }
+        if (best) {
+            p.vmax = (uint32_t)std::max<size_t>(40, std::min<size_t>(56, 3 * mode));
+            if (!getenv("FSMT_TILE_GROUP")) p.group = p.vmax;
+        }
+    }
     for (uint32_t c = 0; c < C; ++c) {
         cons_vars(c, vars);
         batch.clear();
