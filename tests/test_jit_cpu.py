@@ -36,3 +36,15 @@ def test_nvrtc_compiles_specialised_sweep(name, env):
     if "FSMT_JIT_CHECK_RC" in env:
         assert src.startswith("#define FSMT_RC " + env["FSMT_JIT_CHECK_RC"] + "u")
         assert ("#define RPL 2" in src) == ("FSMT_JIT_LANE2" in env)
+
+
+@pytest.mark.parametrize("name,vmax", [("cfg4", 54), ("cfg3", 40)])
+def test_stream_row_budget_from_typical_constraint(name, vmax):
+    """The planner's stream-row budget is 3x the typical constraint's variables in [40, 56]
+    (DESIGN.md §7 / §9: the measured optima of cfg4 and cfg3)."""
+    if os.environ.get("FSMT_TILE_VMAX"):
+        pytest.skip("FSMT_TILE_VMAX overrides the rule")
+    s = Solver(-1)
+    s.load_formula(fsmt_gen.config(name).text)
+    s.build_xbdd()
+    assert f"#define VMAX {vmax}\n" in s.jit_source()
