@@ -47,6 +47,7 @@ def parse_args():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-prepare", action="store_true", help="generic kernels (no fsmt_prepare(R))")
+    p.add_argument("--no-tts", action="store_true", help="skip the time-to-SAT field (cfg4, N=1)")
     return p.parse_args()
 
 
@@ -137,6 +138,29 @@ def time_oracle(f, a, b, kappa=KAPPA):
     t0 = time.perf_counter()
     objective.objective_and_gradient_grouped(f, a, b, kappa)
     return time.perf_counter() - t0
+
+
+def time_to_sat(P, inst, device: int, seeds=range(8), R: int = 32) -> dict:
+    """BASELINE metric, second half: fsmt_solve wall time from call to verified return on this
+    instance (load/build/prepare excluded), median over 8 seeds, with the DESIGN.md §9
+    recipe; one untimed warm-up solve first (module loading)."""
+    s = P.Solver(device)
+    s.load_formula(inst.text)
+    s.build_xbdd()
+    s.prepare(R)
+    kappas = [300.0 ** (i / 19) for i in range(20)] + [300.0] * 200
+    s.set_params(kappas=kappas, eta=0.4, eta_mode=3, erwa_mode=1, time_limit_s=1000.0)
+    s.solve(R, 2, 10_000)
+    times, solved = [], 0
+    for seed in seeds:
+        res = s.solve(R, 2, seed)
+        ok = res.verdict == P.SAT and s.verify(res.x, res.y) == 0
+        solved += ok
+        times.append(res.stats["solve_ms"] / 1e3 if ok else float("inf"))
+    med = statistics.median(times)
+    return {"median_s": med if math.isfinite(med) else None, "max_s": max(times) if solved == len(times) else None,
+            "solved": solved, "seeds": len(times), "restarts": R, "steps_per_stage": 2,
+            "recipe": "eta 0.4 (eta_mode 3), ERWA reset-to-0, kappa 1->300 over 20 stages then held 200"}
 
 
 def workload_config(args, n_vars: int, n_cons: int, world: int = 1) -> dict:
@@ -332,6 +356,11 @@ def main():
             except Exception as e:  # the baseline must never kill the bench line
                 line["cpu_baseline"] = {"value": None, "unit": "evals/s", "cores": 1, "kind": "oracle",
                                         "sample": f"failed: {e}"}
+        if not args.no_tts and world == 1 and args.config == "cfg4":
+            try:
+                line["time_to_sat"] = time_to_sat(P, inst, local)
+            except Exception as e:  # never kill the bench line
+                line["time_to_sat"] = {"median_s": None, "note": f"failed: {e}"}
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
