@@ -29,8 +29,8 @@ def smoothed_atoms(f, b, kappa, needed=None):
 def objective_and_gradient(f, a, b, kappa, weights=None, subset=None, want_terms=False):
     """Returns (C, grad_a, grad_b[, E per constraint]) at one restart point.
 
-    weights: per-constraint w_c (default 1).  subset: optional iterable of
-    constraint indices to restrict the sums to (sampled parity at full size).
+    weights: per-constraint w_c (default: the formula's weights, Eq.3).  subset: optional
+    iterable of constraint indices to restrict the sums to (sampled parity at full size).
     """
     a = np.asarray(a, dtype=np.float64)
     b = np.asarray(b, dtype=np.float64)
@@ -48,7 +48,7 @@ def objective_and_gradient(f, a, b, kappa, weights=None, subset=None, want_terms
     terms = {}
     for ci in cons:
         c = f.constraints[ci]
-        w = 1.0 if weights is None else float(weights[ci])
+        w = float(c.weight) if weights is None else float(weights[ci])
         sl = cslots[ci]
         v = [a[i] if k == "b" else d[i] for k, i in sl]
         E, dE = constraint_expectation_and_gradient(c, v)
@@ -103,7 +103,7 @@ def objective_and_gradient_grouped(f, a, b, kappa, weights=None, subset=None, wa
     ga = np.zeros(f.n_bool)
     gb = np.zeros(f.n_real)
     for ci in cons:                      # accumulate in constraint order
-        w = 1.0 if weights is None else float(weights[ci])
+        w = float(f.constraints[ci].weight) if weights is None else float(weights[ci])
         E, dE = Eall[ci], dEall[ci]
         C += w * E
         for s_, (k, i) in enumerate(cslots[ci]):

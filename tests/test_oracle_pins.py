@@ -601,3 +601,79 @@ def test_multiple_roundings_reading_r34():
     base.kappas = [0.5]
     res = solve.solve_restart(f, 7, 3, base, lo, hi)
     assert res.history[0][2] == min(draws)
+
+
+# ----------------------------------------------------------------------------- Alg.2 loop / Eq.13 pins
+
+
+@pytest.mark.parametrize("erwa_mode", [0, 1])
+def test_solve_restart_loop_weights_match_r18_closed_form(erwa_mode, monkeypatch):
+    """solve_restart runs Alg.2 literally: h <- rho h + u; w <- w gamma^h; h <- 1
+    (verbatim) or 0 (reset reading).  With an injected violation sequence u_t, the weights it
+    hands to each stage's PGD steps must equal R18's closed form, derived independently:
+    w(t) = 2^(U_{t-1} + max(t-2, 0)/2) (verbatim) and 2^(U_{t-1}) (reset-to-0), U_{t-1} = the
+    violations of stages 1..t-1."""
+    f = hsmt.parse("p hsmt 3 0\nc or 1 +b0 +b1\nc xor 1 +b1 +b2\nc or 2 -b0\nc nae 1 +b0 +b1 +b2\n")
+    T, C = 9, len(f.constraints)
+    rng = np.random.default_rng(7)
+    useq = (rng.random((T, C)) < 0.6).astype(np.int64)
+    useq[:, 0] = 1                                   # never SAT: every stage reaches the weight update
+    seen = []
+    stage = {"t": 0}
+
+    def fake_violations(ff, x, y):
+        stage["t"] += 1
+        return useq[stage["t"] - 1].copy()
+
+    def fake_pgd(ff, a, b, kappa, w, eta, lo, hi, eta_b=None, H=None, proj_iters=0):
+        seen.append(np.array(w, dtype=np.float64).copy())
+        return np.asarray(a), np.asarray(b), 1.0, 0.0            # gm2 > eps^2: one step, no move
+
+    monkeypatch.setattr(solve, "violations", fake_violations)
+    monkeypatch.setattr(solve, "pgd_step", fake_pgd)
+    p = solve.Params(kappas=[1.0] * T, steps=1, eps=1e-3, erwa_mode=erwa_mode)
+    res = solve.solve_restart(f, 3, 0, p)
+    assert res.sat_stage == 0 and len(seen) == T
+    base = np.array([c.weight for c in f.constraints])
+    U = np.zeros(C)
+    for t in range(1, T + 1):
+        e = 0.0 if erwa_mode == 1 else max(t - 2, 0) / 2.0
+        want = base * 2.0 ** (U + e)
+        np.testing.assert_allclose(seen[t - 1], want, rtol=1e-13, atol=0)
+        U += useq[t - 1]
+
+
+def test_pgd_step_eq13_blockwise_norm_hand_case():
+    """Eq.11-13 with the block step reading (eta for a, eta_b for b): one step on
+    {b0 or a0} (a0: y0 <= 0.5) at a = -0.99, b = 0.3, kappa = 1, eta = 0.1, eta_b = 0.05.
+    By hand (Eq.8: E = -1 + 2 (1 + v)/2 (1 + d)/2 with v = a, d = erf((y0 - 0.5)/sqrt 2)):
+    dE/da = (1 + d)/2, dE/db = (1 + a)/2 sqrt(2/pi) exp(-(y0 - 0.5)^2 / 2);
+    a' = clip(a - eta dE/da, -1, 1) = -1 (the step crosses -1), b' = b - eta_b dE/db (no bound);
+    ||gm||^2 = ((a - a')/eta)^2 + ((b - b')/eta_b)^2 = 0.1^2 + (dE/db)^2."""
+    f = hsmt.parse("p hsmt 1 1\na 0 <= 0.5 0:1\nc or 1 +b0 +a0\n")
+    lo, hi = solve.bounds(f)
+    a, b, eta, eta_b = -0.99, 0.3, 0.1, 0.05
+    d = math.erf((b - 0.5) / math.sqrt(2.0))
+    ga = (1.0 + d) / 2.0
+    gb = (1.0 + a) / 2.0 * math.sqrt(2.0 / math.pi) * math.exp(-((b - 0.5) ** 2) / 2.0)
+    a2, b2, gm2, C = solve.pgd_step(f, np.array([a]), np.array([b]), 1.0, None, eta, lo, hi, eta_b=eta_b)
+    assert a - eta * ga < -1.0
+    assert a2[0] == -1.0
+    assert abs(b2[0] - (b - eta_b * gb)) <= 1e-15
+    assert abs(gm2 - (((a + 1.0) / eta) ** 2 + gb ** 2)) <= 1e-12
+    assert abs(C - (-1.0 + (1.0 + a) * (1.0 + d) / 2.0)) <= 1e-15
+
+
+def test_objective_default_weights_are_the_formula_weights():
+    """Eq.3 / Eq.10 weight every constraint by its w_c: omitting `weights` must use the
+    formula's weights, not 1."""
+    f = hsmt.parse("p hsmt 2 0\nc or 3 +b0 +b1\nc xor 0.5 +b0 +b1\n")
+    a, b = np.array([0.3, -0.6]), np.zeros(0)
+    C, ga, gb = objective.objective_and_gradient(f, a, b, 1.0)
+    # E_or = -1 + 2 (1+a0)/2 (1+a1)/2, E_xor = a0 a1 (SURVEY §8(c) O4 closed forms)
+    e_or = -1.0 + (1 + a[0]) * (1 + a[1]) / 2.0
+    e_xor = a[0] * a[1]
+    assert abs(C - (3 * e_or + 0.5 * e_xor)) <= 1e-15
+    np.testing.assert_allclose(ga, [3 * (1 + a[1]) / 2 + 0.5 * a[1], 3 * (1 + a[0]) / 2 + 0.5 * a[0]], atol=1e-15)
+    Cg, gag, _ = objective.objective_and_gradient_grouped(f, a, b, 1.0)
+    assert abs(Cg - C) <= 1e-15 and np.allclose(gag, ga, atol=1e-15)
