@@ -5,14 +5,21 @@ A bench *step* is one pass of the whole hot path over the synthetic workload: on
 annealing stage of Alg.2 for all restarts = S PGD steps (each: K1 sweep
 = slot probabilities + smoothing + forward/backward xBDD pass + gradient accumulation,
 then K3 projected update with the eps test) followed by K4 rounding and K5 exact
-verification + ERWA counter update, ending in the 4-byte found-flag exchange (C1).
+verification + ERWA counter update, ending in the per-stage exchange of the multi-GPU
+driver (restart-sharded: C1/C2 best-(unsat, restart) all-reduce + C3 model broadcast,
+paper_2603_22877_b200.dist.RestartShardedStage; constraint-sharded: C4 one flat gradient
+all-reduce per PGD step + C5 per stage).
 value = constraints x restarts x S x K / time, whole job (all ranks).
 
 Workload (N=1): cfg4 "placement-10k" = 10,656 vars / 705,072 constraints, R = 1,024
-restarts per GPU (weak scaling: restart-sharded, global restart ids rank*R + r).
+restarts per GPU (restart mode: weak scaling, global restart ids rank*R + r; constraint mode,
+BASELINE config 5: R restarts in total, constraints split over the ranks, strong scaling).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg4] [--restarts R]
-                  [--pgd-steps S] [--impl reference]
+                  [--pgd-steps S] [--mode restart|constraint] [--impl reference]
+
+--gpus N > 1 without torchrun re-launches itself under torch.distributed.run with N ranks
+(one per GPU, NCCL, 127.0.0.1); under torchrun WORLD_SIZE must equal N.
 """
 from __future__ import annotations
 
@@ -20,6 +27,8 @@ import argparse
 import json
 import math
 import os
+import platform
+import socket
 import statistics
 import subprocess
 import sys
@@ -33,6 +42,7 @@ SURVEY_BYTES_PER_EVAL = {"cfg4": 193.0, "cfg3": 97.9, "cfg2": 193.0}    # SURVEY
 FMA_PER_EVAL = {"cfg4": 264.0, "cfg3": 142.0, "cfg2": 480.0}            # SURVEY §8(d) model
 KAPPA = 1.0                                                              # fixed kappa, t = 1
 METRIC = "xBDD COP+grad evals/s (constraints x restarts)"
+TTS_KAPPAS = [300.0 ** (i / 19) for i in range(20)] + [300.0] * 200     # DESIGN.md §9 recipe
 
 
 def parse_args():
@@ -43,12 +53,39 @@ def parse_args():
     p.add_argument("--config", default="cfg4")
     p.add_argument("--restarts", type=int, default=1024)
     p.add_argument("--pgd-steps", type=int, default=8)
+    p.add_argument("--mode", default="restart", choices=["restart", "constraint"])
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-prepare", action="store_true", help="generic kernels (no fsmt_prepare(R))")
-    p.add_argument("--no-tts", action="store_true", help="skip the time-to-SAT field (cfg4, N=1)")
+    p.add_argument("--no-tts", action="store_true", help="skip the time-to-SAT fields (cfg4, N=1)")
     return p.parse_args()
+
+
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def maybe_relaunch(args) -> bool:
+    """--gpus N > 1 outside torchrun: re-exec under torch.distributed.run (N ranks).  Returns True
+    when this process only launched the ranks (their rank 0 printed the line)."""
+    world = os.environ.get("WORLD_SIZE")
+    if world is not None:
+        if int(world) != args.gpus:
+            sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+        return False
+    if args.gpus <= 1:
+        return False
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    rc = subprocess.call(cmd)
+    if rc:
+        sys.exit(rc)
+    return True
 
 
 def peaks():
@@ -115,32 +152,84 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------------- CPU oracle
 
-
-def oracle_sample(inst, n_cons_sample: int, seed: int = 0):
-    """Bounded sample of the workload for the oracle: the first n constraints, one restart."""
-    import numpy as np
-    from tests.helpers import subformula
-    from oracle import hsmt
-    text = inst.text
-    lines = text.splitlines()
-    n_atoms_lines = sum(1 for ln in lines if ln.startswith("a "))
-    # constraints are after the atoms; take the first n_cons_sample constraints
-    sub, keep = subformula(text, extra_constraints=range(n_cons_sample))
-    f = hsmt.parse(sub)
-    rng = np.random.default_rng(seed)
-    a = rng.uniform(-1, 1, f.n_bool)
-    b = rng.uniform(0, 1, f.n_real)
-    return f, a, b, len(keep)
+_OS = {}      # the oracle sample, inherited by forked workers
 
 
-def time_oracle(f, a, b, kappa=KAPPA):
+def _oracle_chunk(args):
     from oracle import objective
-    t0 = time.perf_counter()
-    objective.objective_and_gradient_grouped(f, a, b, kappa)
-    return time.perf_counter() - t0
+    lo, hi = args
+    f, pts, kappa = _OS["f"], _OS["pts"], _OS["kappa"]
+    for a, b in pts:
+        objective.objective_and_gradient_grouped(f, a, b, kappa, subset=range(lo, hi))
+    return (hi - lo) * len(pts)
 
 
-def time_to_sat(P, inst, device: int, seeds=range(8), R: int = 32) -> dict:
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return platform.processor() or "unknown"
+
+
+class OracleSample:
+    """A bounded sample of the workload for the fp64 CPU oracle (test infrastructure; the
+    bench's cpu_baseline and --impl reference legs only): the first n constraints of the config,
+    SURVEY §8(d)'s 4 sampled restarts (seeded points), objective + gradient per restart with the
+    oracle's grouped sparse-WFE path, split into constraint chunks over all host cores."""
+
+    def __init__(self, inst, n_cons: int, restarts: int = 4, kappa: float = KAPPA):
+        import numpy as np
+        from tests.helpers import subformula
+        from oracle import hsmt
+        sub, keep = subformula(inst.text, extra_constraints=range(min(n_cons, inst.n_cons)))
+        f = hsmt.parse(sub)
+        rng = np.random.default_rng(0)
+        lo = 0.0 if inst.name.startswith("cfg4") else -1.0
+        pts = [(rng.uniform(-1, 1, f.n_bool), rng.uniform(lo, 1, f.n_real)) for _ in range(restarts)]
+        _OS.update(f=f, pts=pts, kappa=kappa)
+        self.n = len(keep)
+        self.restarts = restarts
+        self.cores = os.cpu_count() or 1
+
+    def run(self, cores: int | None = None) -> tuple[float, int]:
+        """(wall seconds, evals) of one pass over the sample on `cores` processes (fork)."""
+        import multiprocessing as mp
+        cores = cores or self.cores
+        edges = [self.n * k // (cores * 4) for k in range(cores * 4 + 1)]
+        chunks = [(lo, hi) for lo, hi in zip(edges[:-1], edges[1:]) if hi > lo]
+        t0 = time.perf_counter()
+        if cores == 1:
+            evals = sum(_oracle_chunk(c) for c in chunks)
+        else:
+            with mp.get_context("fork").Pool(cores) as pool:
+                evals = sum(pool.map(_oracle_chunk, chunks))
+        return time.perf_counter() - t0, evals
+
+
+def oracle_sample_size(cores: int) -> int:
+    """~6,000 constraints x 4 restarts per core: about 15 s of oracle work per pass."""
+    return 6000 * max(1, cores)
+
+
+def cpu_baseline(inst, config: str) -> dict:
+    cores = os.cpu_count() or 1
+    smp = OracleSample(inst, oracle_sample_size(cores))
+    smp.run()                                               # warm (page-in, imports)
+    wall, evals = smp.run()
+    one = OracleSample(inst, 1500, restarts=1)
+    w1, e1 = one.run(cores=1)
+    return {"value": evals / wall, "unit": "evals/s", "cores": cores, "kind": "oracle",
+            "cpu_model": cpu_model(), "one_thread_value": e1 / w1,
+            "sample": f"first {smp.n} constraints of {config} x {smp.restarts} seeded restarts, fp64 oracle "
+                      f"(grouped sparse xWFE) objective+gradient, constraint chunks over {cores} processes "
+                      f"({wall:.1f} s); one_thread_value: first {one.n} constraints x 1 restart on 1 process"}
+
+
+def time_to_sat(P, inst, device: int, R: int, seeds=range(8)) -> dict:
     """BASELINE metric, second half: fsmt_solve wall time from call to verified return on this
     instance (load/build/prepare excluded), median over 8 seeds, with the DESIGN.md §9
     recipe; one untimed warm-up solve first (module loading)."""
@@ -148,8 +237,7 @@ def time_to_sat(P, inst, device: int, seeds=range(8), R: int = 32) -> dict:
     s.load_formula(inst.text)
     s.build_xbdd()
     s.prepare(R)
-    kappas = [300.0 ** (i / 19) for i in range(20)] + [300.0] * 200
-    s.set_params(kappas=kappas, eta=0.4, eta_mode=3, erwa_mode=1, time_limit_s=1000.0)
+    s.set_params(kappas=TTS_KAPPAS, eta=0.4, eta_mode=3, erwa_mode=1, time_limit_s=1000.0)
     s.solve(R, 2, 10_000)
     times, solved = [], 0
     for seed in seeds:
@@ -166,36 +254,42 @@ def time_to_sat(P, inst, device: int, seeds=range(8), R: int = 32) -> dict:
 def workload_config(args, n_vars: int, n_cons: int, world: int = 1) -> dict:
     """The workload both arms name in `config` (same keys, so the driver compares like with like)."""
     names = {"cfg4": "placement-10k", "cfg3": "scheduling-2k", "cfg2": "random-200"}
+    g = args.restarts * world if args.mode == "restart" else args.restarts
     return {"workload": f"{args.config}: {names.get(args.config, args.config)}, {n_vars} vars / {n_cons} constraints",
-            "restarts_per_gpu": args.restarts, "global_restarts": args.restarts * world,
-            "pgd_steps_per_stage": args.pgd_steps, "kappa": KAPPA}
+            "restarts_per_gpu": args.restarts if args.mode == "restart" else None, "global_restarts": g,
+            "pgd_steps_per_stage": args.pgd_steps, "kappa": KAPPA, "mode": args.mode}
 
 
 def run_reference(args):
-    """--impl reference: the fp64 oracle as it stands, on the host cores, same metric/config."""
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
+    """--impl reference: the fp64 oracle as it stands, on all host cores, same metric/config."""
+    if int(os.environ.get("RANK", "0")) != 0:
         return
     import fsmt_gen
     inst = fsmt_gen.config(args.config)
-    n_sample = 1500 if args.config in ("cfg4", "cfg3") else min(inst.n_cons, 500)
-    f, a, b, n = oracle_sample(inst, n_sample)
+    cores = os.cpu_count() or 1
+    smp = OracleSample(inst, oracle_sample_size(cores) // 3)
     for _ in range(args.warmup):
-        time_oracle(f, a, b)
-    ts = [time_oracle(f, a, b) for _ in range(args.steps)]
+        smp.run()
+    ts, ev = [], 0
+    for _ in range(args.steps):
+        w, e = smp.run()
+        ts.append(w)
+        ev += e
     total = sum(ts)
-    value = n * len(ts) / total
+    value = ev / total
+    sample = (f"first {smp.n} constraints of {args.config} x {smp.restarts} seeded restarts per step, fp64 oracle "
+              f"objective+gradient over {cores} processes")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(ts), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {**workload_config(args, inst.n_bool + inst.n_real, inst.n_cons),
-                   "oracle_sample": f"first {n} constraints, 1 restart, one objective+gradient evaluation per step"},
-        "cpu_baseline": {"value": value, "unit": "evals/s", "cores": 1, "kind": "oracle",
-                         "sample": f"first {n} constraints of {args.config}, 1 restart, objective+gradient per step"},
+        "scaling": "weak" if args.mode == "restart" else "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {**workload_config(args, inst.n_bool + inst.n_real, inst.n_cons, args.gpus), "oracle_sample": sample},
+        "cpu_baseline": {"value": value, "unit": "evals/s", "cores": cores, "kind": "oracle", "cpu_model": cpu_model(),
+                         "sample": sample},
         "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line))
+    print(json.dumps(line), flush=True)
 
 
 # ----------------------------------------------------------------------------------- GPU arm
@@ -205,6 +299,8 @@ def main():
     args = parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if maybe_relaunch(args):
+        return
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -213,9 +309,15 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
+        # communicator init lines (NCCL INFO) on stderr, so the driver can check comm_nranks
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+        torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     import paper_2603_22877_b200 as P
+    from paper_2603_22877_b200 import dist as D
     import fsmt_gen
 
     inst = fsmt_gen.config(args.config)
@@ -232,15 +334,28 @@ def main():
     s.set_params(eta=0.01, eps=1e-2)
     stream = torch.cuda.current_stream()
     s.bind_stream(stream.cuda_stream)
-    s.begin(R, seed=12345, restart_offset=rank * R)
-    found = torch.zeros(1, dtype=torch.int32, device="cuda")
+    constraint_mode = args.mode == "constraint" and world > 1
+    if constraint_mode:
+        s.shard(rank, world, 1)
+        s.begin(R, seed=12345, restart_offset=0)
+        bufs = D.ConstraintShardedBuffers(s, dims["n_bool"], dims["n_real"], R)
+        eta_a, eta_b = s.step_sizes(KAPPA)
 
-    def step(t):
-        _, mn = s.run_stage(t, KAPPA, S, want_unsat=False)
-        if world > 1:                                   # C1: early-exit flag, 4 bytes
-            found.fill_(1 if mn == 0 else 0)
-            dist.all_reduce(found, op=dist.ReduceOp.MAX)
-        return mn
+        def step(t):
+            for _ in range(S):                              # K1 (shard) + C4 + K3
+                s.sweep(KAPPA, t)
+                bufs.reduce_grads()
+                s.update(eta_a, 1e-2, eta_b=eta_b)
+            s.stage_end(t, copy=False)                      # K4 + K5 (shard) + C5
+            bufs.reduce_stage()
+    else:
+        s.begin(R, seed=12345, restart_offset=rank * R)
+        ex = D.RestartShardedStage(s, dims["n_bool"], dims["n_real"], R) if world > 1 else None
+
+        def step(t):
+            unsat, mn = s.run_stage(t, KAPPA, S)           # S x (K1 + K3), K4 + K5; unsat[R] to host
+            if ex is not None:
+                ex.exchange(t, unsat)                       # C1/C2 (+ C3 when the best model improves)
 
     for w in range(args.warmup):
         step(1)
@@ -268,12 +383,12 @@ def main():
     if world > 1:
         dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
     ms_max = float(t_max.item())
-    evals_per_rank = dims["n_cons"] * R * S * args.steps
-    value = evals_per_rank * world / (ms_max / 1e3)
+    units = dims["n_cons"] * R * S * args.steps * (1 if constraint_mode else world)   # whole job
+    value = units / (ms_max / 1e3)
 
     # e2e: through the C ABI with HOST buffers: H2D of the step's state, stage, D2H of the result
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not constraint_mode:
         a_h = torch.empty((dims["n_bool"], R), dtype=torch.float32).pin_memory()
         b_h = torch.empty((dims["n_real"], R), dtype=torch.float32).pin_memory()
         a_np, b_np = a_h.numpy(), b_h.numpy()
@@ -281,7 +396,6 @@ def main():
         st_a, st_b = s.get_state()
         a_np[...] = st_a
         b_np[...] = st_b
-        unsat = np.empty(R, dtype=np.uint32)
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
@@ -294,19 +408,19 @@ def main():
         if world > 1:
             dist.all_reduce(te_t, op=dist.ReduceOp.MAX)
         h2d = (dims["n_bool"] + dims["n_real"]) * R * 4
-        e2e = {"value": evals_per_rank * world / float(te_t.item()), "unit": "evals/s",
+        e2e = {"value": units / float(te_t.item()), "unit": "evals/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": R * 4}
 
     # roofline for the dominant kernel (K1) from live per-launch CUDA-event timing
     k1_ms, k1_n = timing["k1_sweep"]
     hbm, peak_src, sm_max = peaks()
     k1_avg_s = (k1_ms / max(k1_n, 1)) / 1e3
-    evals_per_launch = dims["n_cons"] * R
+    evals_per_launch = dims["n_cons"] * R / (world if constraint_mode else 1)
     bpe = SURVEY_BYTES_PER_EVAL.get(args.config, 193.0)
     achieved = bpe * evals_per_launch / k1_avg_s / 1e9
     traffic = None
     prof = os.path.join(ROOT, "profiles", f"k1_traffic_{args.config}.json")
-    if os.path.exists(prof):
+    if os.path.exists(prof) and not constraint_mode and R == 1024:
         try:
             traffic = json.load(open(prof)).get("dram_bytes_per_launch")
         except Exception:
@@ -318,17 +432,19 @@ def main():
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "strong" if constraint_mode else "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {**workload_config(args, dims["n_bool"] + dims["n_real"], dims["n_cons"], world),
                        "kernels": "generic" if args.no_prepare else "specialised for R (fsmt_prepare)",
-                       "parallelism": f"restart-sharded x{world}",
+                       "parallelism": (f"constraint-sharded x{world} (one flat all-reduce per PGD step)" if constraint_mode
+                                       else f"restart-sharded x{world}"),
                        "l2": "inputs exceed L2 (U counters %.0f MB + structure + state per step)" % (dims["n_cons"] * R / 1e6),
-                       "accumulation": "fp64", "build_s": round(build_s, 2)},
+                       "accumulation": "fp64, exact on-grid sums (deterministic)", "build_s": round(build_s, 2)},
             "roofline": {"bound": "alu", "achieved": alu_achieved, "peak": alu_peak, "unit": "TFLOP/s",
                          "frac": alu_achieved / alu_peak, "traffic": traffic, "kernel": "fsmt_k1_jit",
                          "basis": f"SURVEY 8(d) model {fma_pe:.0f} FMA-eq (x2 flop) per (constraint,restart) eval x "
-                                  f"{evals_per_launch} evals per launch / live CUDA-event launch time; peak = 148 SMs x "
+                                  f"{evals_per_launch:.0f} evals per launch / live CUDA-event launch time; peak = 148 SMs x "
                                   f"128 FP32 lanes x 2 x {sm_max:.0f} MHz (DESIGN.md §7)",
                          "k1_ms_per_launch": k1_ms / max(k1_n, 1),
                          "k1_share_of_step": k1_ms / ms if ms > 0 else None,
@@ -343,25 +459,17 @@ def main():
         }
         if not args.no_cpu_baseline and world == 1:
             try:
-                n_sample = 1500 if args.config in ("cfg4", "cfg3") else min(inst.n_cons, 500)
-                f, a, b, n = oracle_sample(inst, n_sample)
-                time_oracle(f, a, b)
-                reps, tot = 0, 0.0
-                while tot < 10.0 and reps < 50:
-                    tot += time_oracle(f, a, b)
-                    reps += 1
-                line["cpu_baseline"] = {"value": n * reps / tot, "unit": "evals/s", "cores": 1, "kind": "oracle",
-                                        "sample": f"first {n} constraints of {args.config}, 1 restart, "
-                                                  f"objective+gradient x{reps} ({tot:.1f} s)"}
+                line["cpu_baseline"] = cpu_baseline(inst, args.config)
             except Exception as e:  # the baseline must never kill the bench line
-                line["cpu_baseline"] = {"value": None, "unit": "evals/s", "cores": 1, "kind": "oracle",
+                line["cpu_baseline"] = {"value": None, "unit": "evals/s", "cores": os.cpu_count(), "kind": "oracle",
                                         "sample": f"failed: {e}"}
         if not args.no_tts and world == 1 and args.config == "cfg4":
-            try:
-                line["time_to_sat"] = time_to_sat(P, inst, local)
-            except Exception as e:  # never kill the bench line
-                line["time_to_sat"] = {"median_s": None, "note": f"failed: {e}"}
-        print(json.dumps(line))
+            for key, Rt in (("time_to_sat", 32), ("time_to_sat_r1024", 1024)):
+                try:
+                    line[key] = time_to_sat(P, inst, local, Rt)
+                except Exception as e:  # never kill the bench line
+                    line[key] = {"median_s": None, "note": f"failed: {e}"}
+        print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
 

@@ -317,6 +317,8 @@ CONFIGS = {
     # small versions of the structured families (parity at oracle-friendly sizes)
     "cfg3s": lambda: scheduling(n_w=4, n_j=24, seed=13),
     "cfg4s": lambda: placement(n_m=2, n_l=2, counts=(4, 12, 4, 6), seed=14),
+    # mid-size placement with cfg4's real class (n_m = 32, n_l = 4: 7 bit pairs, 25 nodes, 18 slots)
+    "cfg4m": lambda: placement(n_m=32, n_l=4, counts=(8, 32, 8, 12), seed=44),
     "cfg2s": lambda: random_hybrid(n_bool=20, n_real=20, n_atoms=20, n_card=30, n_nae=30, n_xor=6,
                                    l_card=8, l_nae=8, l_xor=12, seed=12),
 }

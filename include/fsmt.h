@@ -19,7 +19,7 @@
  *
  * Layouts: per-restart state is restart-minor, row = variable:
  *     a[n_bool][R] f32, b[n_real][R] f32, grad_a[n_bool][R] f64, grad_b[n_real][R] f64,
- *     U[n_cons][R] u8, x[n_bool][R] i8, obj[R] f64, unsat[R] u32.
+ *     U[n_cons][R] u8, x[n_bool][R] i8, obj[R] f64, unsat[R] u32, umax[R] u32.
  * Truth encoding: -1 = True, +1 = False.
  */
 #ifndef FSMT_H
@@ -43,7 +43,9 @@ typedef enum {
     FSMT_ERR_NODE_BUDGET = 5,  /* a constraint's xBDD exceeds the node budget / encoding limits */
     FSMT_ERR_OOM = 6,          /* device or host allocation failed */
     FSMT_ERR_CUDA = 7,         /* CUDA runtime error (no device, launch failure, ...) */
-    FSMT_ERR_TIMEOUT = 8       /* time limit hit inside fsmt_solve (verdict is still set) */
+    FSMT_ERR_TIMEOUT = 8,      /* time limit hit inside fsmt_solve (verdict is still set) */
+    FSMT_ERR_RANGE = 9         /* an ERWA counter U[c][r] (u8, R18) passed 255 violations, or the stage
+                                  exponent e_t = (t-2)/2 of Alg.2 verbatim passed 600 (weights beyond fp64) */
 } fsmt_status;
 
 typedef enum { FSMT_UNKNOWN = 0, FSMT_SAT = 10 } fsmt_verdict;   /* S:514 exit codes */
@@ -61,6 +63,7 @@ typedef struct {
     uint64_t n_nodes;          /* sum over constraints of |V_c| */
     uint64_t n_slot_refs;      /* sum over constraints of slot count */
     uint32_t n_halfspaces;     /* multi-variable unit atom literals (projection halfspaces, R33) */
+    uint32_t n_slot_rows;      /* rows of the symmetric classes' slot-table gradient gu[rows][R] (0: none) */
 } fsmt_dims;
 
 typedef struct {
@@ -107,7 +110,9 @@ fsmt_status fsmt_create(int cuda_device, fsmt_ctx** out);
 void fsmt_destroy(fsmt_ctx* ctx);
 /* Last error message of ctx (never NULL; "" when none). */
 const char* fsmt_last_error(const fsmt_ctx* ctx);
-/* Bind a cudaStream_t (as void*) for all subsequent launches; NULL = the ctx's own stream. */
+/* Bind a cudaStream_t (as void*) for all subsequent launches; NULL = the ctx's own (non-blocking)
+ * stream.  The legacy default stream is cudaStreamLegacy ((void*)1): a framework whose current
+ * stream handle is 0 (e.g. torch's default stream) must pass 1, not NULL, to be ordered with it. */
 fsmt_status fsmt_bind_stream(fsmt_ctx* ctx, void* cuda_stream);
 
 /* ---- a0: formula -> xBDDs (Alg.1 lines 1-2) ---------------------------------- */
@@ -169,7 +174,12 @@ fsmt_status fsmt_get_counters(fsmt_ctx* ctx, uint8_t* U, int where);
 
 /* K1: objective and gradient at the current point for all restarts (a1-a4 of SURVEY §8(a)):
  * obj[r] = sum_c w_cr E_c (Eq.10), grad = dC/d(a,b) (Alg.B with the sign of R1, chain rule
- * P:1326-1327), w_cr = w_c * 2^(U[c][r] + e_t), e_t = max(t-2,0)/2 (VERBATIM) or 0 (RESET0). */
+ * P:1326-1327), w_cr = w_c * 2^(U[c][r] + e_t), e_t = max(t-2,0)/2 (VERBATIM) or 0 (RESET0).
+ * Per-term arithmetic is fp32; every fp64 partial sum is rounded to a per-restart power-of-two
+ * grid before it is added, so obj and the gradients are exact sums of those values: bitwise
+ * reproducible and independent of restart or constraint sharding (DESIGN.md §7 item 14; the
+ * grid is <= 2^-48 of an a-priori bound of the restart's gradient).  FSMT_ERR_RANGE when
+ * e_t > 600 (weights beyond fp64). */
 fsmt_status fsmt_sweep(fsmt_ctx* ctx, float kappa, uint32_t stage_t);
 /* Read the last sweep's outputs: grad_a[n_bool][R], grad_b[n_real][R] (f64), obj[R] (f64).
  * Any pointer may be NULL. */
@@ -186,19 +196,27 @@ fsmt_status fsmt_eval(fsmt_ctx* ctx, uint32_t R, const float* a, const float* b,
 fsmt_status fsmt_constraint_terms(fsmt_ctx* ctx, float kappa, uint32_t restart, double* E);
 
 /* K3: projected gradient step (Eq.11-14): for every non-frozen restart,
- * (a',b') = proj((a,b) - eta*grad); gm2[r] = ||((a,b)-(a',b'))/eta||^2; if gm2 <= eps^2 the
- * restart is frozen for the rest of the stage (no update), else (a,b) <- (a',b').
+ * (a',b') = proj(a - eta*grad_a, b - eta_b*grad_b); gm2[r] = ||(a-a')/eta||^2 + ||(b-b')/eta_b||^2
+ * (Eq.13 blockwise); if gm2 <= eps^2 the restart is frozen for the rest of the stage (no update),
+ * else (a,b) <- (a',b').  eta_b <= 0 means eta_b = eta (Eq.11's single step).  fsmt_step_sizes
+ * gives the (eta, eta_b) of a stage under the ctx's eta_mode (what fsmt_run_stage uses).
  * gm2_out[R] (host, may be NULL) receives the squared gradient-mapping norms. */
-fsmt_status fsmt_update(fsmt_ctx* ctx, float eta, float eps, double* gm2_out);
+fsmt_status fsmt_update(fsmt_ctx* ctx, float eta, float eta_b, float eps, double* gm2_out);
+/* The step sizes of a stage at kappa under the ctx params (eta, eta_mode; R13): eta_a for the
+ * Boolean block, eta_b for the real block. */
+fsmt_status fsmt_step_sizes(const fsmt_ctx* ctx, float kappa, float* eta_a, float* eta_b);
 
 /* K4+K5 (a6-a9): round x = sgn(a) or R(a) (R17), y = b; exact check of every constraint
- * (R22); U[c][r] += u_c; unsat[r] = #violated; clears the per-stage frozen flags.
- * unsat_out[R] (host, may be NULL). */
+ * (R22); U[c][r] += u_c; umax[r] = max_c U[c][r]; unsat[r] = #violated; clears the per-stage
+ * frozen flags.  unsat_out[R] (host, may be NULL).  FSMT_ERR_RANGE when a counter would pass
+ * 255 (it is then held at 255; the u8 counter is never silently saturated). */
 fsmt_status fsmt_stage_end(fsmt_ctx* ctx, uint32_t stage_t, uint32_t* unsat_out);
 /* One whole annealing stage for all restarts, as fsmt_solve runs it (Alg.2 loop body,
- * P:513-528): `steps` x {K1 sweep at kappa, K3 update(eta, eps)} then K4+K5 stage_end.
- * The frozen flags are cleared first.  unsat_out[R] (host, may be NULL); *min_unsat (may be
- * NULL) receives min_r unsat[r].  Uses the ctx params (eta, eps, rounding, erwa_mode). */
+ * P:513-528): `steps` x {K1 sweep at kappa, K3 update(fsmt_step_sizes(kappa), eps)} then K4+K5
+ * stage_end.  The frozen flags are cleared first.  unsat_out[R] (host, may be NULL); *min_unsat
+ * (may be NULL) receives min_r unsat[r].  Uses the ctx params (eta, eta_mode, eps, rounding,
+ * erwa_mode).  FSMT_ERR_STATE on a constraint-sharded context with world > 1 (its steps need the
+ * caller's all-reduces); FSMT_ERR_RANGE as fsmt_stage_end / fsmt_sweep. */
 fsmt_status fsmt_run_stage(fsmt_ctx* ctx, uint32_t stage_t, float kappa, uint32_t steps, uint32_t* unsat_out,
                            uint32_t* min_unsat);
 
@@ -209,11 +227,23 @@ fsmt_status fsmt_run_stage(fsmt_ctx* ctx, uint32_t stage_t, float kappa, uint32_
  * the caller must all-reduce (SUM) across ranks before fsmt_update / before reading unsat;
  * every rank then holds and updates all R restarts identically. Call after fsmt_build_xbdd. */
 fsmt_status fsmt_shard(fsmt_ctx* ctx, uint32_t rank, uint32_t world, uint32_t mode);
-/* Replace the ctx's grad_a[n_bool][R] f64, grad_b[n_real][R] f64, obj[R] f64 and unsat[R] u32
+/* Constraint-sharded mode with symmetric classes (n_slot_rows > 0): fsmt_sweep leaves the
+ * slot-table gradient rows gu[n_slot_rows][R] f64 (grid units, partial) and does NOT chain them into
+ * grad_a / grad_b; the caller all-reduces gu with the gradients, then calls fsmt_sweep_finish, which
+ * chains the summed rows identically on every rank (the chain's rounding is not linear, so it must
+ * see the full rows).  Unsharded / restart-sharded: fsmt_sweep chains them itself and
+ * fsmt_sweep_finish is a no-op.  fsmt_bind_slot_grads binds caller device memory for gu. */
+fsmt_status fsmt_sweep_finish(fsmt_ctx* ctx);
+fsmt_status fsmt_bind_slot_grads(fsmt_ctx* ctx, void* gu);
+/* Replace the ctx's grad_a[n_bool][R] f64, grad_b[n_real][R] f64, obj[R] f64, unsat[R] u32 and
+ * umax[R] u32 (max_c U[c][r], the weight shift of the sweep; its current values are copied in)
  * device buffers with caller-owned device memory of the same shapes (NULL keeps the ctx's own),
- * e.g. torch tensors that torch.distributed all-reduces. Valid until the next fsmt_begin; the
- * caller keeps ownership and must keep them alive. */
-fsmt_status fsmt_bind_buffers(fsmt_ctx* ctx, void* grad_a, void* grad_b, void* obj, void* unsat);
+ * e.g. torch tensors that torch.distributed all-reduces.  In constraint-sharded mode the caller
+ * all-reduces grad/obj (SUM, after fsmt_sweep), unsat (SUM) and umax (MAX, after fsmt_stage_end);
+ * the sums are exact (fsmt_sweep), so every rank holds the single-GPU values bit for bit.
+ * FSMT_ERR_ARG for host memory.  Valid until the next fsmt_begin; the caller keeps ownership and
+ * must keep them alive; the ctx's kernels run on its bound stream (fsmt_bind_stream). */
+fsmt_status fsmt_bind_buffers(fsmt_ctx* ctx, void* grad_a, void* grad_b, void* obj, void* unsat, void* umax);
 
 /* Rounded model of one restart from the last stage_end: x[n_bool] (-1/+1), y[n_real] (host). */
 fsmt_status fsmt_get_model(fsmt_ctx* ctx, uint32_t restart, int8_t* x_out, float* y_out);

@@ -1,7 +1,7 @@
 """Builds paper_2603_22877_b200/libfsmt.so (the C-ABI library of include/fsmt.h) for sm_100a.
 
-nvcc cross-compiles here without a GPU.  Rebuilds only when a source is newer
-than the library (or when force=True).
+nvcc cross-compiles here without a GPU.  Rebuilds unless the library was built from exactly the
+current sources (content hash in libfsmt.so.sha256), or when force=True.
 """
 from __future__ import annotations
 
@@ -27,11 +27,24 @@ def deps():
         [os.path.join(ROOT, "include", "fsmt.h"), os.path.abspath(__file__)]
 
 
+def source_hash() -> str:
+    import hashlib
+    h = hashlib.sha256()
+    for d in sorted(deps()):
+        h.update(os.path.relpath(d, ROOT).encode())
+        with open(d, "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()
+
+
 def up_to_date() -> bool:
-    if not os.path.exists(LIB):
+    """The library exists AND was built from exactly the current sources (content hash recorded at
+    build time next to it; a copied-in or stale .so never counts)."""
+    stamp = LIB + ".sha256"
+    if not (os.path.exists(LIB) and os.path.exists(stamp)):
         return False
-    t = os.path.getmtime(LIB)
-    return all(os.path.getmtime(d) <= t for d in deps())
+    with open(stamp) as fh:
+        return fh.read().strip() == source_hash()
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
@@ -54,6 +67,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     subprocess.run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs, "-lpthread", "-ldl", "-lrt"],
                    check=True)
     os.replace(tmp, LIB)
+    with open(LIB + ".sha256", "w") as fh:
+        fh.write(source_hash() + "\n")
     return LIB
 
 

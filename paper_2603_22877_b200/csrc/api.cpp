@@ -31,6 +31,7 @@ struct fsmt_ctx {
     DevState S{};
     std::vector<void*> sallocs;
     double* terms = nullptr;    // [C] debug hook buffer
+    double* scratch = nullptr;  // [max(n_bool, n_real)][R] gradients scaled out of grid units (fsmt_get_sweep)
     // device work plan (tiles.cpp) + JIT-specialised sweep (jit.cpp)
     bool jit_enabled = true;
     Plan plan;
@@ -59,6 +60,7 @@ struct fsmt_ctx {
     uint32_t restart_offset = 0;
     bool rounded = false;
     uint64_t launches = 0;
+    uint32_t* hflags = nullptr;        // pinned host copy of S.flags[0] (read at every stage end)
     // per-kernel-class device timing (fsmt_set_timing)
     bool timing = false;
     std::vector<cudaEvent_t> ev_pool;
@@ -155,6 +157,7 @@ void drop_state(fsmt_ctx* ctx) {
     ctx->slots.PT = ctx->slots.PF = ctx->slots.DD = nullptr;
     ctx->slots.GU = nullptr;
     ctx->slots.TT = nullptr;
+    ctx->scratch = nullptr;     // freed with the state allocations
     ctx->rounded = false;
     if (ctx->terms) { cudaFree(ctx->terms); ctx->terms = nullptr; }
 }
@@ -183,10 +186,27 @@ fsmt_status upload_bytes(fsmt_ctx* ctx, const void* src, size_t bytes, const voi
     return FSMT_OK;
 }
 
-float wscale_of(uint32_t stage_t, uint32_t mode) {
-    // R18: weight during stage t = w_c * 2^(U + e_t), e_t = max(t-2,0)/2 (Alg.2 verbatim) or 0
-    if (mode == FSMT_ERWA_RESET0 || stage_t <= 2) return 1.0f;
-    return (float)std::pow(2.0, (double)(stage_t - 2) / 2.0);
+// R18: weight during stage t = w_c * 2^(U + e_t), e_t = max(t-2,0)/2 (Alg.2 verbatim) or 0
+// (reset-to-0): the integer part of e_t is applied exactly in the fp64 flush (FxScale), the
+// fractional part 2^(1/2) in the fp32 weight.
+int et_int_of(uint32_t stage_t, uint32_t mode) {
+    if (mode == FSMT_ERWA_RESET0 || stage_t <= 2) return 0;
+    return (int)((stage_t - 2) / 2);
+}
+float wfrac_of(uint32_t stage_t, uint32_t mode) {
+    if (mode == FSMT_ERWA_RESET0 || stage_t <= 2 || (stage_t - 2) % 2 == 0) return 1.0f;
+    return 1.41421356237309505f;
+}
+// stage exponents past this would take 2^(U + e_t) beyond the fp64 range of the flush scales
+constexpr uint32_t kMaxStageExp = 600;
+
+// after a stage end and a sync: the K5 overflow flag (an ERWA counter passed 255; R18 needs the
+// exact count, so the u8 counter is never silently saturated)
+fsmt_status check_flags(fsmt_ctx* ctx) {
+    if (ctx->hflags && (*ctx->hflags & 1u))
+        return fail(ctx, FSMT_ERR_RANGE, "ERWA counter overflow: a constraint was violated more than 255 times in one restart "
+                                         "(u8 U[c][r], R18)");
+    return FSMT_OK;
 }
 
 fsmt_status need(fsmt_ctx* ctx, int stage, const char* what) {
@@ -247,6 +267,12 @@ fsmt_status fsmt_create(int cuda_device, fsmt_ctx** out) {
         return FSMT_ERR_CUDA;
     }
     ctx->stream = ctx->own_stream;
+    if (cudaMallocHost((void**)&ctx->hflags, 16) != cudaSuccess) {
+        cudaStreamDestroy(ctx->own_stream);
+        delete ctx;
+        return FSMT_ERR_OOM;
+    }
+    *ctx->hflags = 0;
     default_kappas(ctx->kappas);
     *out = ctx;
     return FSMT_OK;
@@ -263,6 +289,7 @@ void fsmt_destroy(fsmt_ctx* ctx) {
     timing_collect(ctx);
     for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+    if (ctx->hflags) cudaFreeHost(ctx->hflags);
     delete ctx;
 }
 
@@ -333,7 +360,7 @@ fsmt_status fsmt_build_xbdd(fsmt_ctx* ctx, uint64_t node_budget) {
     for (size_t i = 0; i < C; ++i) {
         const uint32_t o = P.order[i];
         c_tmpl[i] = b.cons_tmpl[o];
-        c_w[i] = b.cons_w[o];
+        c_w[i] = std::ldexp(b.cons_w[o], -P.wexp);   // normalised base weight (FxScale; exact)
         c_ids.insert(c_ids.end(), b.slot_ids.begin() + b.cons_slot_off[o], b.slot_ids.begin() + b.cons_slot_off[o + 1]);
         c_off[i + 1] = (uint32_t)c_ids.size();
     }
@@ -364,6 +391,37 @@ fsmt_status fsmt_build_xbdd(fsmt_ctx* ctx, uint64_t node_budget) {
     F.n_atoms = f.n_atoms();
     F.max_slots = b.max_slots;
     F.max_nodes = b.max_nodes;
+    {   // a-priori bounds of the on-grid fp64 accumulation (kernels.hpp FxScale, DevFormula::fx_*)
+        std::vector<double> fbool(f.n_bool, 0.0), fatom(f.n_atoms(), 0.0), freal(f.n_real, 0.0), inv(f.n_atoms(), 0.0);
+        for (uint32_t i = 0; i < f.n_atoms(); ++i) {
+            double n2 = 0.0;
+            for (uint32_t t = f.atom_rowptr[i]; t < f.atom_rowptr[i + 1]; ++t) n2 += f.atom_val[t] * f.atom_val[t];
+            inv[i] = n2 > 0 ? 1.0 / std::sqrt(n2) : 0.0;
+        }
+        double sw = 0.0;
+        for (size_t c = 0; c < C; ++c) {
+            const double w = std::ldexp((double)b.cons_w[c], -P.wexp);
+            sw += w;
+            const Template& t = b.tmpls[b.cons_tmpl[c]];
+            for (size_t sl = 0; sl < t.kinds.size(); ++sl) {
+                const uint32_t id = b.slot_ids[b.cons_slot_off[c] + sl];
+                if (t.kinds[sl] == 0) {
+                    fbool[id] += w;
+                } else {
+                    fatom[id] += w;
+                    for (uint32_t k = f.atom_rowptr[id]; k < f.atom_rowptr[id + 1]; ++k)
+                        freal[f.atom_col[k]] += w * std::fabs(f.atom_val[k]) * inv[id] * 0.7978845608028654;
+                }
+            }
+        }
+        F.fx_fb = 0.0;
+        for (double v : fbool) F.fx_fb = std::max(F.fx_fb, v);
+        for (double v : fatom) F.fx_fb = std::max(F.fx_fb, v);
+        F.fx_fa = 0.0;
+        for (double v : freal) F.fx_fa = std::max(F.fx_fa, v);
+        F.fx_sw = sw;
+        F.wexp = P.wexp;
+    }
 #define UP(vec, field) do { s = upload(ctx, vec, F.field, ctx->fallocs); if (s) return s; } while (0)
     UP(c_tmpl, cons_tmpl);
     UP(c_off, cons_slot_off);
@@ -458,7 +516,6 @@ fsmt_status fsmt_build_xbdd(fsmt_ctx* ctx, uint64_t node_budget) {
             ctx->T.n_tiles = (uint32_t)P.tiles.size();
             ctx->T.recs = rp;
             ctx->T.tile_vars = vp;
-            ctx->T.warps = P.jit_warps;
             ctx->T.vmax = P.kernel_vmax();
             ctx->T.rmax = P.rmax;
             const uint32_t* vr = nullptr;
@@ -507,6 +564,7 @@ fsmt_status fsmt_get_dims(const fsmt_ctx* ctx, fsmt_dims* out) {
         d.n_nodes = ctx->b.n_nodes;
         d.n_slot_refs = ctx->b.slot_ids.size();
         d.n_halfspaces = (uint32_t)(ctx->b.h_rowptr.size() - 1);
+        d.n_slot_rows = ctx->has_sym ? ctx->slots.nv + ctx->slots.n_sa : 0;
     }
     *out = d;
     return FSMT_OK;
@@ -612,7 +670,10 @@ fsmt_status fsmt_begin(fsmt_ctx* ctx, uint32_t R, uint64_t seed, uint32_t restar
         }
     }
     if ((s = alloc((void**)&S.x_best, nb)) || (s = alloc((void**)&S.unsat_m, (size_t)R * 4)) ||
-        (s = alloc((void**)&S.unsat_best, (size_t)R * 4)) || (s = alloc((void**)&S.better, R))) {
+        (s = alloc((void**)&S.unsat_best, (size_t)R * 4)) || (s = alloc((void**)&S.better, R)) ||
+        (s = alloc((void**)&S.umax, (size_t)R * 4)) || (s = alloc((void**)&S.fx, (size_t)R * sizeof(FxScale))) ||
+        (s = alloc((void**)&S.gsc, (size_t)R * 8)) || (s = alloc((void**)&S.flags, 16)) ||
+        (s = alloc((void**)&ctx->scratch, (size_t)std::max(F.n_bool, F.n_real) * R * 8))) {
         drop_state(ctx);
         return s;
     }
@@ -624,6 +685,8 @@ fsmt_status fsmt_begin(fsmt_ctx* ctx, uint32_t R, uint64_t seed, uint32_t restar
         }
     }
     CK(cudaMemsetAsync(S.U, 0, nc, ctx->stream));
+    CK(cudaMemsetAsync(S.umax, 0, (size_t)R * 4, ctx->stream));
+    CK(cudaMemsetAsync(S.flags, 0, 16, ctx->stream));
     CK(cudaMemsetAsync(S.frozen, 0, R, ctx->stream));
     CK(cudaMemsetAsync(S.ga, 0, nb * 8, ctx->stream));
     CK(cudaMemsetAsync(S.gb, 0, nr * 8, ctx->stream));
@@ -666,7 +729,8 @@ fsmt_status fsmt_set_counters(fsmt_ctx* ctx, const uint8_t* U, int where) {
                                     ctx->stream);
     if (e == cudaSuccess) {
         launch_gather_rows_u8(ctx->S.U, tmp, ctx->F.orig, ctx->F.n_cons, ctx->S.R, ctx->stream);
-        ctx->launches += 1;
+        launch_umax(ctx->F, ctx->S, ctx->stream);      // the weight shift follows the new counters
+        ctx->launches += 2;
         e = cudaStreamSynchronize(ctx->stream);
     }
     cudaFree(tmp);
@@ -702,14 +766,13 @@ fsmt_status fsmt_jit_info(const fsmt_ctx* ctx, uint32_t* n_jit_classes, uint32_t
     if (msg && msg_len) {
         std::string m = ctx->host_only ? "host-only" : (active ? "active" : (ctx->plan.tiles.empty() ? "no JIT classes" : ctx->jit_error));
         if (active && ctx->jit_r.kernel)
-            m += "; prepared R=" + std::to_string(ctx->jit_r_R) + " restarts/lane=" + std::to_string(ctx->jit_r.rpl) +
-                 " k1 cap=" + std::to_string(ctx->jit_r_cap);
+            m += "; prepared R=" + std::to_string(ctx->jit_r_R) + " k1 cap=" + std::to_string(ctx->jit_r_cap);
         snprintf(msg, msg_len, "%s", m.c_str());
     }
     return FSMT_OK;
 }
 
-static std::string prepared_source_tuned(const fsmt_ctx* ctx, uint32_t R, bool& lane2, int* cap);
+static std::string prepared_source_tuned(const fsmt_ctx* ctx, uint32_t R, int* cap);
 
 fsmt_status fsmt_jit_check(fsmt_ctx* ctx, size_t* cubin_bytes, char* log, size_t log_len) {
     if (!ctx) return FSMT_ERR_ARG;
@@ -719,10 +782,7 @@ fsmt_status fsmt_jit_check(fsmt_ctx* ctx, size_t* cubin_bytes, char* log, size_t
     std::string lg, err;
     // FSMT_JIT_CHECK_RC=R: check the module fsmt_prepare(R) would build (register counts)
     std::string src = ctx->jit_src;
-    if (const char* rc = getenv("FSMT_JIT_CHECK_RC")) {
-        bool lane2 = false;
-        src = prepared_source_tuned(ctx, (uint32_t)atoi(rc), lane2, nullptr);
-    }
+    if (const char* rc = getenv("FSMT_JIT_CHECK_RC")) src = prepared_source_tuned(ctx, (uint32_t)atoi(rc), nullptr);
     bool ok = jit_cubin(src, cubin, lg, err);
     if (log && log_len) snprintf(log, log_len, "%s", lg.c_str());
     if (!ok) return fail(ctx, FSMT_ERR_CUDA, err);
@@ -733,14 +793,10 @@ fsmt_status fsmt_jit_check(fsmt_ctx* ctx, size_t* cubin_bytes, char* log, size_t
 // The source fsmt_prepare(R) compiles: the restart count as a constant (FSMT_RC); U loaded 3
 // constraints ahead when U[c][r] (1 B per constraint and restart) exceeds ~1.5x the 126 MB L2
 // and so comes from HBM every sweep (cfg4 9.78 -> 8.85 ms; cfg3, whose 117 MB
-// of U stays in L2, is faster without); opt-in (FSMT_JIT_LANE2=1) two restarts per lane on the
-// f32x2 pipe when R is even (float2 loads of a lane's two restarts) and there are no symmetric
-// classes: 32 % fewer instructions per eval but 126 registers (16 warps/SM), slower on cfg3/cfg4.
-static std::string prepared_source(const fsmt_ctx* ctx, uint32_t R, bool& lane2, int min_ctas) {
+// of U stays in L2, is faster without).
+static std::string prepared_source(const fsmt_ctx* ctx, uint32_t R, int min_ctas) {
     const int upf = (double)ctx->plan.jit_cons_end * R > 192e6 ? 3 : 0;
-    const char* l2e = getenv("FSMT_JIT_LANE2");
-    lane2 = R % 2 == 0 && !ctx->plan.has_sym && l2e && l2e[0] == '1';
-    const std::string src = (upf || lane2 || min_ctas) ? jit_source(ctx->f, ctx->b, ctx->plan, upf, lane2, min_ctas) : ctx->jit_src;
+    const std::string src = (upf || min_ctas) ? jit_source(ctx->f, ctx->b, ctx->plan, upf, min_ctas) : ctx->jit_src;
     return "#define FSMT_RC " + std::to_string(R) + "u\n" + src;
 }
 
@@ -759,9 +815,9 @@ static long spill_stores(const std::string& log, const std::string& kernel) {
 // The prepared module's source with the hot kernel's register cap: the highest residency (32,
 // then 28 one-warp CTAs per SM: 64 / 72 registers) whose compile has no spills, else no cap
 // (cfg3 best at 64, cfg4 at 72, cfg2 uncapped)
-static std::string prepared_source_tuned(const fsmt_ctx* ctx, uint32_t R, bool& lane2, int* cap = nullptr) {
+static std::string prepared_source_tuned(const fsmt_ctx* ctx, uint32_t R, int* cap) {
     for (int mc : {32, 28}) {
-        const std::string src = prepared_source(ctx, R, lane2, mc);
+        const std::string src = prepared_source(ctx, R, mc);
         std::vector<char> cubin;
         std::string log, err;
         if (jit_cubin(src, cubin, log, err) && spill_stores(log, "fsmt_k1_jit") == 0) {
@@ -770,7 +826,7 @@ static std::string prepared_source_tuned(const fsmt_ctx* ctx, uint32_t R, bool& 
         }
     }
     if (cap) *cap = 0;
-    return prepared_source(ctx, R, lane2, 0);
+    return prepared_source(ctx, R, 0);
 }
 
 fsmt_status fsmt_prepare(fsmt_ctx* ctx, uint32_t R) {
@@ -792,12 +848,11 @@ fsmt_status fsmt_prepare(fsmt_ctx* ctx, uint32_t R) {
     // register cap of the hot sweep: the highest residency (32, then 28 one-warp CTAs per SM:
     // 64 / 72 registers) whose kernel needs no local memory (no spills), else none (DESIGN.md
     // §7 item 13).  Judged from the loaded kernel's attributes, not the compiler log.
-    bool lane2 = false;
     int cap = 0;
     std::string err;
     for (int mc : {32, 28, 0}) {
         JitKernel cand;
-        if (!jit_compile(prepared_source(ctx, R, lane2, mc), cand, err)) {
+        if (!jit_compile(prepared_source(ctx, R, mc), cand, err)) {
             if (mc == 0) return fail(ctx, FSMT_ERR_CUDA, "fsmt_prepare: " + err);
             continue;
         }
@@ -811,7 +866,6 @@ fsmt_status fsmt_prepare(fsmt_ctx* ctx, uint32_t R) {
         cap = mc;
         break;
     }
-    ctx->jit_r.rpl = lane2 ? 2 : 1;
     ctx->jit_r_cap = cap;
     ctx->jit_r_R = R;
     return FSMT_OK;
@@ -820,10 +874,8 @@ fsmt_status fsmt_prepare(fsmt_ctx* ctx, uint32_t R) {
 size_t fsmt_jit_source(const fsmt_ctx* ctx, char* buf, size_t len) {
     if (!ctx || ctx->stage < 2) return 0;
     std::string src = ctx->jit_src;
-    if (const char* rc = getenv("FSMT_JIT_CHECK_RC")) {   // the source fsmt_prepare(R) would compile
-        bool lane2 = false;
-        if (!src.empty()) src = prepared_source_tuned(ctx, (uint32_t)atoi(rc), lane2, nullptr);
-    }
+    if (const char* rc = getenv("FSMT_JIT_CHECK_RC"))   // the source fsmt_prepare(R) would compile
+        if (!src.empty()) src = prepared_source_tuned(ctx, (uint32_t)atoi(rc), nullptr);
     if (buf && len) snprintf(buf, len, "%s", src.c_str());
     return src.size() + 1;
 }
@@ -837,29 +889,33 @@ static const JitKernel& jk(const fsmt_ctx* ctx, uint32_t R) {
 static fsmt_status sweep_impl(fsmt_ctx* ctx, float kappa, uint32_t stage_t, double* terms, uint32_t terms_r) {
     const DevFormula& F = ctx->F;
     const DevState& S = ctx->S;
-    CK(cudaMemsetAsync(S.ga, 0, (size_t)F.n_bool * S.R * 8, ctx->stream));
-    CK(cudaMemsetAsync(S.gb, 0, (size_t)F.n_real * S.R * 8, ctx->stream));
-    CK(cudaMemsetAsync(S.obj, 0, (size_t)S.R * 8, ctx->stream));
+    const int et = et_int_of(stage_t, ctx->erwa_mode);
+    if ((uint32_t)et > kMaxStageExp)
+        return fail(ctx, FSMT_ERR_RANGE, "stage exponent e_t = (t - 2)/2 beyond the fp64 range of the ERWA weights (R18)");
     {
         Timed tm(ctx, 0);
-        const float ws = wscale_of(stage_t, ctx->erwa_mode);
+        const float ws = wfrac_of(stage_t, ctx->erwa_mode);
         const bool sym = ctx->has_sym && ctx->T.n_tiles;
+        // zero grad_a / grad_b / obj (+ the slot-table gradients) and write the per-restart scales
+        launch_prologue(F, S, kappa, et, ws, ctx->has_sym ? ctx->slots.GU : nullptr,
+                        ctx->has_sym ? (uint64_t)ctx->slots.nv + ctx->slots.n_sa : 0, ctx->stream);
+        ctx->launches += 1;
         if (sym) {   // shared slot probabilities for the symmetric classes
-            const DevSlots& D = ctx->slots;
-            CK(cudaMemsetAsync(D.GU, 0, ((size_t)D.nv + D.n_sa) * S.R * 8, ctx->stream));
-            launch_slot_prob(jk(ctx, S.R).kprob, F, S, D, kappa, ctx->stream);
+            launch_slot_prob(jk(ctx, S.R).kprob, F, S, ctx->slots, kappa, ctx->stream);
             ctx->launches += 1;
         }
         if (ctx->T.n_tiles) {
             const JitKernel& J = jk(ctx, S.R);
-            launch_sweep_jit((S.U == nullptr || terms != nullptr) ? J.kernel_dbg : J.kernel, J.rpl, F, S, ctx->T, kappa, ws, terms, terms_r, ctx->stream, &ctx->slots);
+            launch_sweep_jit((S.U == nullptr || terms != nullptr) ? J.kernel_dbg : J.kernel, F, S, ctx->T, kappa, terms, terms_r,
+                             ctx->stream, &ctx->slots);
             ctx->launches += 1;
         }
         if (F.generic_begin < F.generic_end) {
-            launch_sweep(F, S, kappa, ws, terms, terms_r, ctx->stream);
+            launch_sweep(F, S, kappa, terms, terms_r, ctx->stream);
             ctx->launches += 1;
         }
-        if (sym) {
+        // constraint-sharded: the rows are partial; the chain waits for their all-reduce
+        if (ctx->has_sym && !(ctx->shard_mode == 1 && ctx->shard_world > 1)) {
             launch_slot_chain(jk(ctx, S.R).kchain, F, S, ctx->slots, ctx->stream);
             ctx->launches += 1;
         }
@@ -919,6 +975,7 @@ static fsmt_status stage_end_impl(fsmt_ctx* ctx, uint32_t stage_t) {
         }
         CK(cudaMemsetAsync(S.unsat, 0, (size_t)S.R * 4, ctx->stream));
         verify_rounded(ctx, S, S.U);
+        CK(cudaMemcpyAsync(ctx->hflags, S.flags, 4, cudaMemcpyDeviceToHost, ctx->stream));   // read after the sync
     }
     CK(cudaMemsetAsync(S.frozen, 0, S.R, ctx->stream));
     fsmt_status s = check_launch(ctx);
@@ -935,12 +992,49 @@ fsmt_status fsmt_sweep(fsmt_ctx* ctx, float kappa, uint32_t stage_t) {
     return sweep_impl(ctx, kappa, stage_t, nullptr, 0);
 }
 
+fsmt_status fsmt_sweep_finish(fsmt_ctx* ctx) {
+    fsmt_status s = need(ctx, 3, "fsmt_sweep_finish");
+    if (s) return s;
+    if (ctx->has_sym && ctx->shard_mode == 1 && ctx->shard_world > 1) {
+        launch_slot_chain(jk(ctx, ctx->S.R).kchain, ctx->F, ctx->S, ctx->slots, ctx->stream);
+        ctx->launches += 1;
+    }
+    return check_launch(ctx);
+}
+
+fsmt_status fsmt_bind_slot_grads(fsmt_ctx* ctx, void* gu) {
+    fsmt_status s = need(ctx, 3, "fsmt_bind_slot_grads");
+    if (s) return s;
+    if (!ctx->has_sym) return gu ? fail(ctx, FSMT_ERR_ARG, "fsmt_bind_slot_grads: no slot-table rows") : FSMT_OK;
+    cudaPointerAttributes at{};
+    if (gu && (cudaPointerGetAttributes(&at, gu) != cudaSuccess || at.type != cudaMemoryTypeDevice)) {
+        cudaGetLastError();
+        return fail(ctx, FSMT_ERR_ARG, "fsmt_bind_slot_grads: device memory only");
+    }
+    if (gu) ctx->slots.GU = (double*)gu;
+    return FSMT_OK;
+}
+
 fsmt_status fsmt_get_sweep(fsmt_ctx* ctx, double* ga, double* gb, double* obj, int where) {
     fsmt_status s = need(ctx, 3, "fsmt_get_sweep");
     if (s) return s;
-    if ((s = copy_out(ctx, ga, ctx->S.ga, (size_t)ctx->F.n_bool * ctx->S.R, where))) return s;
-    if ((s = copy_out(ctx, gb, ctx->S.gb, (size_t)ctx->F.n_real * ctx->S.R, where))) return s;
-    return copy_out(ctx, obj, ctx->S.obj, (size_t)ctx->S.R, where);
+    const DevState& S = ctx->S;
+    // the sweep leaves the gradients in grid units (kernels.hpp FxScale): scale them by gsc[r]
+    auto grad_out = [&](double* dst, const double* src, uint32_t rows) -> fsmt_status {
+        if (!dst || rows == 0) return FSMT_OK;
+        double* to = where == FSMT_DEVICE ? dst : ctx->scratch;
+        launch_scale_rows(to, src, S.gsc, rows, S.R, ctx->stream);
+        ctx->launches += 1;
+        if (where == FSMT_DEVICE) {
+            CK(cudaGetLastError());
+            CK(cudaStreamSynchronize(ctx->stream));
+            return FSMT_OK;
+        }
+        return copy_out(ctx, dst, (const double*)ctx->scratch, (size_t)rows * S.R, FSMT_HOST);
+    };
+    if ((s = grad_out(ga, S.ga, ctx->F.n_bool))) return s;
+    if ((s = grad_out(gb, S.gb, ctx->F.n_real))) return s;
+    return copy_out(ctx, obj, S.obj, (size_t)S.R, where);
 }
 
 fsmt_status fsmt_eval(fsmt_ctx* ctx, uint32_t R, const float* a, const float* b, float kappa, const uint8_t* U,
@@ -952,6 +1046,7 @@ fsmt_status fsmt_eval(fsmt_ctx* ctx, uint32_t R, const float* a, const float* b,
         if ((s = fsmt_begin(ctx, R, 0, 0))) return s;
     } else if (!U) {
         CK(cudaMemsetAsync(ctx->S.U, 0, (size_t)ctx->F.n_cons * R, ctx->stream));
+        CK(cudaMemsetAsync(ctx->S.umax, 0, (size_t)R * 4, ctx->stream));
     }
     if ((s = fsmt_set_state(ctx, a, b, where))) return s;
     if (U && (s = fsmt_set_counters(ctx, U, where))) return s;
@@ -968,11 +1063,11 @@ fsmt_status fsmt_constraint_terms(fsmt_ctx* ctx, float kappa, uint32_t restart, 
     return copy_out(ctx, E, ctx->terms, ctx->F.n_cons, FSMT_HOST);
 }
 
-fsmt_status fsmt_update(fsmt_ctx* ctx, float eta, float eps, double* gm2_out) {
+fsmt_status fsmt_update(fsmt_ctx* ctx, float eta, float eta_b, float eps, double* gm2_out) {
     fsmt_status s = need(ctx, 3, "fsmt_update");
     if (s) return s;
     if (!(eta > 0.f) || !(eps >= 0.f)) return fail(ctx, FSMT_ERR_ARG, "eta must be > 0 and eps >= 0");
-    if ((s = update_impl(ctx, eta, eps))) return s;
+    if ((s = update_impl(ctx, eta, eps, eta_b > 0.f ? eta_b : eta))) return s;
     if (gm2_out) return copy_out(ctx, gm2_out, ctx->S.gm2, ctx->S.R, FSMT_HOST);
     return FSMT_OK;
 }
@@ -982,9 +1077,12 @@ fsmt_status fsmt_stage_end(fsmt_ctx* ctx, uint32_t stage_t, uint32_t* unsat_out)
     if (s) return s;
     if (stage_t == 0) stage_t = 1;
     if ((s = stage_end_impl(ctx, stage_t))) return s;
-    if (unsat_out) return copy_out(ctx, unsat_out, ctx->S.unsat, ctx->S.R, FSMT_HOST);
-    CK(cudaStreamSynchronize(ctx->stream));
-    return FSMT_OK;
+    if (unsat_out) {
+        if ((s = copy_out(ctx, unsat_out, ctx->S.unsat, ctx->S.R, FSMT_HOST))) return s;
+    } else {
+        CK(cudaStreamSynchronize(ctx->stream));
+    }
+    return check_flags(ctx);
 }
 
 fsmt_status fsmt_shard(fsmt_ctx* ctx, uint32_t rank, uint32_t world, uint32_t mode) {
@@ -1031,8 +1129,11 @@ fsmt_status fsmt_shard(fsmt_ctx* ctx, uint32_t rank, uint32_t world, uint32_t mo
     ctx->T.tiles = (const char*)ctx->T_all.tiles + (size_t)t0 * sizeof(TileDesc);
     ctx->T.n_tiles = t1 - t0;
     const uint32_t gn = C - jit_end;
-    F.generic_begin = jit_end + (uint32_t)((uint64_t)gn * rank / world);
-    F.generic_end = jit_end + (uint32_t)((uint64_t)gn * (rank + 1) / world);
+    // split on the generic sweep's 16-constraint chunk boundaries (kernels.cu kChunk): each chunk's
+    // objective partial is then the unsharded one, so the shards' sums are bit-identical
+    auto cut = [&](uint32_t k) { return std::min<uint32_t>(gn, (uint32_t)(((uint64_t)gn * k / world + 15) / 16 * 16)); };
+    F.generic_begin = jit_end + cut(rank);
+    F.generic_end = jit_end + cut(rank + 1);
     if (t1 > t0) {
         ctx->vrange[0][0] = P.tiles[t0].cons_begin;
         ctx->vrange[0][1] = P.tiles[t1 - 1].cons_begin + P.tiles[t1 - 1].n_cons;
@@ -1044,13 +1145,23 @@ fsmt_status fsmt_shard(fsmt_ctx* ctx, uint32_t rank, uint32_t world, uint32_t mo
     return FSMT_OK;
 }
 
-fsmt_status fsmt_bind_buffers(fsmt_ctx* ctx, void* grad_a, void* grad_b, void* obj, void* unsat) {
+fsmt_status fsmt_bind_buffers(fsmt_ctx* ctx, void* grad_a, void* grad_b, void* obj, void* unsat, void* umax) {
     fsmt_status s = need(ctx, 3, "fsmt_bind_buffers");
     if (s) return s;
+    for (void* p : {grad_a, grad_b, obj, unsat, umax}) {   // device memory only (the kernels write them)
+        cudaPointerAttributes at{};
+        if (p && (cudaPointerGetAttributes(&at, p) != cudaSuccess || at.type != cudaMemoryTypeDevice)) {
+            cudaGetLastError();
+            return fail(ctx, FSMT_ERR_ARG, "fsmt_bind_buffers: buffers must be device memory");
+        }
+    }
+    if (umax && ctx->S.umax) CK(cudaMemcpyAsync(umax, ctx->S.umax, (size_t)ctx->S.R * 4, cudaMemcpyDeviceToDevice, ctx->stream));
     if (grad_a) ctx->S.ga = (double*)grad_a;
     if (grad_b) ctx->S.gb = (double*)grad_b;
     if (obj) ctx->S.obj = (double*)obj;
     if (unsat) ctx->S.unsat = (uint32_t*)unsat;
+    if (umax) ctx->S.umax = (uint32_t*)umax;
+    CK(cudaStreamSynchronize(ctx->stream));
     return FSMT_OK;
 }
 
@@ -1060,12 +1171,12 @@ fsmt_status fsmt_run_stage(fsmt_ctx* ctx, uint32_t stage_t, float kappa, uint32_
     if (s) return s;
     if (!(kappa >= 0.f) || !std::isfinite(kappa)) return fail(ctx, FSMT_ERR_ARG, "kappa must be finite and >= 0");
     if (stage_t == 0) stage_t = 1;
+    if (ctx->shard_mode == 1 && ctx->shard_world > 1)
+        return fail(ctx, FSMT_ERR_STATE, "fsmt_run_stage: constraint-sharded contexts need the caller's all-reduce per step "
+                                         "(use fsmt_sweep / fsmt_update / fsmt_stage_end)");
     CK(cudaMemsetAsync(ctx->S.frozen, 0, ctx->S.R, ctx->stream));
-    const float kk = std::max(kappa, 1.0f);
-    float eta_t = ctx->eta, eta_b = ctx->eta;      // eta_mode 0
-    if (ctx->eta_mode == 1) eta_t = eta_b = ctx->eta / kk;
-    if (ctx->eta_mode == 2) eta_t = eta_b = ctx->eta / (kk * kk);
-    if (ctx->eta_mode == 3) eta_b = ctx->eta / (kk * kk);   // block steps: a keeps eta, b gets eta/kappa^2
+    float eta_t = 0.f, eta_b = 0.f;
+    fsmt_step_sizes(ctx, kappa, &eta_t, &eta_b);
     // FSMT_GRAPH=1: the S PGD steps are captured into one CUDA graph (one graph launch instead of
     // ~5 S kernel launches); the executable graph is kept and updated in place with the next
     // stage's parameters.  Opt-in: capture + update cost about what the launches cost on the
@@ -1118,6 +1229,18 @@ fsmt_status fsmt_run_stage(fsmt_ctx* ctx, uint32_t stage_t, float kappa, uint32_
     } else {
         CK(cudaStreamSynchronize(ctx->stream));
     }
+    return check_flags(ctx);
+}
+
+fsmt_status fsmt_step_sizes(const fsmt_ctx* ctx, float kappa, float* eta_a, float* eta_b) {
+    if (!ctx || !eta_a || !eta_b) return FSMT_ERR_ARG;
+    const float kk = std::max(kappa, 1.0f);
+    float ea = ctx->eta, eb = ctx->eta;                    // eta_mode 0
+    if (ctx->eta_mode == 1) ea = eb = ctx->eta / kk;
+    if (ctx->eta_mode == 2) ea = eb = ctx->eta / (kk * kk);
+    if (ctx->eta_mode == 3) eb = ctx->eta / (kk * kk);     // block steps: a keeps eta, b gets eta/kappa^2
+    *eta_a = ea;
+    *eta_b = eb;
     return FSMT_OK;
 }
 
@@ -1235,6 +1358,8 @@ fsmt_status fsmt_solve(fsmt_ctx* ctx, uint32_t restarts, uint32_t steps, uint64_
     if (s) return s;
     if (ctx->host_only) return fail(ctx, FSMT_ERR_CUDA, "fsmt_solve: host-only context has no device");
     if (!verdict || restarts == 0) return fail(ctx, FSMT_ERR_ARG, "bad arguments");
+    if (ctx->shard_mode == 1 && ctx->shard_world > 1)
+        return fail(ctx, FSMT_ERR_STATE, "fsmt_solve: constraint-sharded context (use the step API with all-reduces)");
     auto t0 = std::chrono::steady_clock::now();
     if ((s = fsmt_begin(ctx, restarts, seed, 0))) return s;
     const uint32_t nbool = ctx->F.n_bool, nreal = ctx->F.n_real;

@@ -155,7 +155,8 @@ struct Plan {
     std::vector<uint32_t> vrecs;      // K5 JIT records (atom ids, vstride4*4 per constraint); tile.pad1 = offset
     uint32_t jit_cons_end = 0;        // internal [0, jit_cons_end) are JIT constraints
     uint32_t n_jit_kclasses = 0;
-    uint32_t jit_warps = 1;           // warps per CTA of the JIT sweep (A/B: profiles/README.md)
+    int wexp = 0;                     // base weights enter the records as w_c 2^-wexp (max <= 1, exact;
+                                      // k1_prologue multiplies 2^wexp back in the fp64 flush)
     uint32_t vmax = kTileVmaxDefault; // stream variables per tile = shared-memory accumulator rows
     uint32_t rmax = kTileRmaxDefault; // run variables per tile (register accumulators, flushed to HBM)
     uint32_t group = kTileVmaxDefault;  // footprint group size in variables (FSMT_TILE_GROUP)
@@ -172,10 +173,11 @@ struct Plan {
 Plan make_plan(const Formula& f, const Built& b, bool enable_jit);
 // CUDA source of the specialised sweep kernel for the plan's JIT classes.
 // u_prefetch_default: how many constraints ahead the sweep loads U (FSMT_JIT_UPF overrides)
-// lane2: two restarts per lane on the f32x2 pipe (even R only; no symmetric classes)
-// k1_min_ctas > 0: __launch_bounds__(WARPS*32, k1_min_ctas) on the hot sweep kernel (register cap)
-std::string jit_source(const Formula& f, const Built& b, const Plan& p, int u_prefetch_default = 0, bool lane2 = false,
-                       int k1_min_ctas = 0);
+// k1_min_ctas > 0: __launch_bounds__(32, k1_min_ctas) on the hot sweep kernel (register cap)
+std::string jit_source(const Formula& f, const Built& b, const Plan& p, int u_prefetch_default = 0, int k1_min_ctas = 0);
+// Exponent k with max_c w_c 2^-k in (1/2, 1] (0 for no constraints): the weight normalisation of
+// the sweep (DESIGN.md §7 item 14).
+int weight_exponent(const Built& b);
 
 struct BuildError {
     std::string msg;

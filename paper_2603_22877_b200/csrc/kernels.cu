@@ -43,11 +43,21 @@ __device__ __forceinline__ uint32_t draw24(uint64_t seed, uint32_t r, uint32_t v
 
 // ---------------------------------------------------------------------------------------- K0
 
-// w * 2^u, u in [0, 255]: exactly ldexpf(w, u) (powers of two <= 2^127, an overflow stays inf)
-__device__ __forceinline__ float pow2_u8(float w, uint32_t u) {
-    const float f1 = __uint_as_float((127u + (u & 127u)) << 23);
-    const float f2 = __uint_as_float((127u + ((u >> 7) << 6)) << 23);
-    return __fmul_rn(__fmul_rn(__fmul_rn(w, f1), f2), f2);
+// w0 * 2^(u + ebias - 127): the fp32 ERWA weight with the restart's shift (FxScale; exact, 0 below
+// 2^-126, never inf since u + ebias <= 127 + kWeightWindow)
+__device__ __forceinline__ float weight_of(float w0, uint32_t u, int ebias) {
+    return w0 * __uint_as_float((uint32_t)max((int)u + ebias, 0) << 23);
+}
+
+// v on the restart's grid, in grid units (FxScale): rintf(v 2^-G), exact scaling; fp32 values of
+// magnitude >= 2^23 are integers already
+__device__ __forceinline__ double grid_units(float v, float gif) { return (double)rintf(v * gif); }
+
+__device__ __forceinline__ int ceil_log2(double x) {
+    if (!(x > 0.0)) return 0;
+    int e = 0;
+    const double f = frexp(x, &e);    // x = f 2^e, f in [1/2, 1)
+    return f == 0.5 ? e - 1 : e;
 }
 
 __global__ void k0_init(DevFormula F, DevState S, uint64_t seed, uint32_t off) {
@@ -77,7 +87,7 @@ __global__ void k0_init(DevFormula F, DevState S, uint64_t seed, uint32_t off) {
 
 // ---------------------------------------------------------------------------------------- K1
 
-__global__ void __launch_bounds__(256) k1_sweep(DevFormula F, DevState S, float kappa, float wscale,
+__global__ void __launch_bounds__(256) k1_sweep(DevFormula F, DevState S, float kappa,
                                                 double* __restrict__ terms, uint32_t terms_r, int smax, int nmax) {
     extern __shared__ float smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -99,6 +109,7 @@ __global__ void __launch_bounds__(256) k1_sweep(DevFormula F, DevState S, float 
     const float kq = kappa * 0.70710678118654752f;               // kappa / sqrt(2)
     const float dcoef = kappa * 0.79788456080286536f;            // kappa * sqrt(2/pi)
     double objacc = 0.0;
+    const FxScale fx = S.fx[rr];
     for (uint64_t c = c0; c < c1; ++c) {
         const uint32_t tid = F.cons_tmpl[c];
         const uint32_t so = F.cons_slot_off[c];
@@ -107,8 +118,8 @@ __global__ void __launch_bounds__(256) k1_sweep(DevFormula F, DevState S, float 
         const uint32_t no = F.tmpl_node_off[tid];
         const uint32_t nn = F.tmpl_node_off[tid + 1] - no;
         const int root = F.tmpl_root[tid];
-        float w = F.cons_w[c] * wscale;                               // w_cr = w_c 2^(U + e_t)  (R18)
-        if (S.U) w = pow2_u8(w, S.U[(size_t)c * R + rr]);
+        // w_cr = w_c 2^(U + e_t) (R18) in the restart's reduced units (FxScale)
+        const float w = weight_of(F.cons_w[c], S.U ? S.U[(size_t)c * R + rr] : 0u, fx.ebias);   // 2^frac(e_t): fx.gif
         // a1: slot probabilities (Eq.4 for Booleans, Eq.7 for atoms; erfc form, R28b)
         for (uint32_t s = 0; s < ns; ++s) {
             const uint32_t gid = F.slot_ids[so + s];
@@ -155,24 +166,75 @@ __global__ void __launch_bounds__(256) k1_sweep(DevFormula F, DevState S, float 
             G[nd.level * 32 + lane] += mt * (bh - bl);
             M[v * 32 + lane] = PT[nd.level * 32 + lane] * bh + PF[nd.level * 32 + lane] * bl;
         }
-        // a4: chain rule + accumulate (fp64, R28)
+        // a4: chain rule + accumulate (fp64, R28; every term on the restart's grid: exact sums)
         if (live) {
             for (uint32_t s = 0; s < ns; ++s) {
                 const uint32_t gid = F.slot_ids[so + s];
                 const float g = w * G[s * 32 + lane];
                 if (F.kinds[ko + s] == 0) {
-                    atomicAdd(&S.ga[(size_t)gid * R + r], (double)g);
+                    atomicAdd(&S.ga[(size_t)gid * R + r], grid_units(g, fx.gif));
                 } else {
                     const float gd = g * DD[s * 32 + lane];
                     for (uint32_t k = F.atom_rowptr[gid]; k < F.atom_rowptr[gid + 1]; ++k)
-                        atomicAdd(&S.gb[(size_t)F.atom_col[k] * R + r], (double)(gd * F.atom_val[k]));
+                        atomicAdd(&S.gb[(size_t)F.atom_col[k] * R + r], grid_units(gd * F.atom_val[k], fx.gif));
                 }
             }
             objacc += (double)w * (double)E;
             if (terms != nullptr && r == terms_r) terms[F.orig[c]] = (double)E;
         }
     }
-    if (live) atomicAdd(&S.obj[r], objacc);
+    if (live) atomicAdd(&S.obj[r], rint(objacc * fx.oi) * fx.os);
+}
+
+// Before every sweep (DESIGN.md §7 item 14): zero the fp64 outputs and write the restart's FxScale.
+// With m = umax[r], s_r = max(0, m - W), wm = min(m, W): fp32 weights are <= 2^wm (normalised
+// w_c <= 1, times 2^frac(e_t) <= sqrt 2), so every partial gradient sum in reduced units is
+// bounded by B_g = 2^wm max(fx_fb, kappa fx_fa) times 2 (sqrt 2) times 2 (margin); the grid 2^G,
+// G = ceil(log2 B_g) - 48, keeps every sum below 2^50 grid units (exact integers in fp64).
+__global__ void k1_prologue(DevFormula F, DevState S, float kappa, int et_int, float wfrac, double* __restrict__ gu,
+                            uint64_t gu_rows) {
+    const uint64_t R = S.R;
+    const uint64_t nb = (uint64_t)F.n_bool * R, nr = (uint64_t)F.n_real * R, ng = gu ? gu_rows * R : 0;
+    const uint64_t n = nb + nr + R + ng;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        if (i < nb) S.ga[i] = 0.0;
+        else if (i < nb + nr) S.gb[i - nb] = 0.0;
+        else if (i < nb + nr + R) {
+            const uint32_t r = (uint32_t)(i - nb - nr);
+            S.obj[r] = 0.0;
+            const int m = (int)S.umax[r];
+            const int sh = max(0, m - kWeightWindow), wm = min(m, kWeightWindow);
+            // G in [-100, 120]: 2^-G is a normal fp32 (bounds >= 2^-52 for any non-empty formula)
+            const int G = min(120, max(-100, ceil_log2(ldexp(fmax(F.fx_fb, (double)kappa * F.fx_fa), wm)) - 48));
+            const int O = ceil_log2(ldexp(F.fx_sw, wm)) - 48;
+            const int tail = sh + F.wexp + et_int;
+            FxScale fx;
+            fx.gs = ldexp(1.0, G + tail);
+            fx.ti = ldexp(1.0, -(G + tail));
+            fx.oi = (double)wfrac * ldexp(1.0, -O);   // 2^frac(e_t) applied at the flush (x wfrac: one fp64 rounding)
+            fx.os = ldexp(1.0, O + tail);
+            fx.gif = wfrac * ldexpf(1.f, -G);         // 2^frac(e_t) times 2^-G (exact scaling by 2^-G)
+            fx.ebias = 127 - sh;
+            S.fx[r] = fx;
+            S.gsc[r] = fx.gs;
+        } else {
+            gu[i - nb - nr - R] = 0.0;
+        }
+    }
+}
+
+__global__ void k_scale_rows(double* __restrict__ dst, const double* __restrict__ src, const double* __restrict__ gsc,
+                             uint64_t n, uint32_t R) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        dst[i] = src[i] * gsc[i % R];
+}
+
+__global__ void k_umax(const uint8_t* __restrict__ U, uint32_t C, uint32_t R, uint32_t* __restrict__ umax) {
+    const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= R) return;
+    uint32_t m = 0;
+    for (uint32_t c = 0; c < C; ++c) m = max(m, (uint32_t)U[(size_t)c * R + r]);
+    umax[r] = m;
 }
 
 // ---------------------------------------------------------------------------------------- K3
@@ -192,7 +254,7 @@ __global__ void k3_cand(DevFormula F, DevState S, float eta_b) {
     for (uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t j = (uint32_t)(idx / S.R);
         const bool h = F.in_h[j];
-        S.bn[idx] = step_value(S.b[idx], S.gb[idx], eta_b, h ? -INFINITY : F.lo[j], h ? INFINITY : F.hi[j]);
+        S.bn[idx] = step_value(S.b[idx], S.gb[idx] * S.gsc[idx % S.R], eta_b, h ? -INFINITY : F.lo[j], h ? INFINITY : F.hi[j]);
     }
 }
 
@@ -250,16 +312,17 @@ __global__ void k3_norm(DevFormula F, DevState S, float eta, float eta_b, uint32
     const uint32_t part = blockIdx.y;
     const uint32_t nv = F.n_bool + F.n_real;
     const uint32_t v0 = part * vpp, v1 = min(v0 + vpp, nv);
+    const double gs = S.gsc[r];                 // grid units -> gradient (FxScale)
     double acc = 0.0;
     for (uint32_t v = v0; v < v1; ++v) {
         float x, xn;
         if (v < F.n_bool) {
             x = S.a[(size_t)v * S.R + r];
-            xn = step_value(x, S.ga[(size_t)v * S.R + r], eta, -1.f, 1.f);
+            xn = step_value(x, S.ga[(size_t)v * S.R + r] * gs, eta, -1.f, 1.f);
         } else {
             const uint32_t j = v - F.n_bool;
             x = S.b[(size_t)j * S.R + r];
-            xn = S.bn ? S.bn[(size_t)j * S.R + r] : step_value(x, S.gb[(size_t)j * S.R + r], eta_b, F.lo[j], F.hi[j]);
+            xn = S.bn ? S.bn[(size_t)j * S.R + r] : step_value(x, S.gb[(size_t)j * S.R + r] * gs, eta_b, F.lo[j], F.hi[j]);
         }
         const double d = ((double)x - (double)xn) / (double)(v < F.n_bool ? eta : eta_b);
         acc += d * d;
@@ -298,13 +361,14 @@ __global__ void k3_apply(DevFormula F, DevState S, float eta, float eta_b) {
     for (uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t v = (uint32_t)(idx / S.R), r = (uint32_t)(idx % S.R);
         if (S.frozen[r]) continue;
+        const double gs = S.gsc[r];
         if (v < F.n_bool) {
             float& x = S.a[(size_t)v * S.R + r];
-            x = step_value(x, S.ga[(size_t)v * S.R + r], eta, -1.f, 1.f);
+            x = step_value(x, S.ga[(size_t)v * S.R + r] * gs, eta, -1.f, 1.f);
         } else {
             const uint32_t j = v - F.n_bool;
             float& x = S.b[(size_t)j * S.R + r];
-            x = S.bn ? S.bn[(size_t)j * S.R + r] : step_value(x, S.gb[(size_t)j * S.R + r], eta_b, F.lo[j], F.hi[j]);
+            x = S.bn ? S.bn[(size_t)j * S.R + r] : step_value(x, S.gb[(size_t)j * S.R + r] * gs, eta_b, F.lo[j], F.hi[j]);
         }
     }
 }
@@ -342,7 +406,7 @@ __global__ void __launch_bounds__(256) k5_verify(DevFormula F, DevState S, const
     const uint64_t c1 = min(c0 + (uint64_t)kChunk, (uint64_t)ce);
     const uint32_t r = rt * 32 + lane;
     if (r >= R) return;
-    uint32_t cnt = 0;
+    uint32_t cnt = 0, umx = 0, ovf = 0;
     for (uint64_t c = c0; c < c1; ++c) {
         const uint32_t tid = F.cons_tmpl[c];
         const uint32_t so = F.cons_slot_off[c];
@@ -367,11 +431,17 @@ __global__ void __launch_bounds__(256) k5_verify(DevFormula F, DevState S, const
         cnt += u;
         if (Uupd && u) {                                      // U += u: only violated constraints touch memory
             uint8_t& cell = Uupd[(size_t)c * R + r];
-            cell = (uint8_t)min(255u, (uint32_t)cell + 1u);
+            const uint32_t nv = (uint32_t)cell + 1u;
+            ovf |= nv > 255u;                                 // reported (FSMT_ERR_RANGE), never silent
+            const uint32_t nc = min(255u, nv);
+            cell = (uint8_t)nc;
+            umx = max(umx, nc);
         }
         if (per_con) per_con[(size_t)F.orig[c] * R + r] = (uint8_t)u;
     }
     atomicAdd(&S.unsat[r], cnt);
+    if (umx) atomicMax(&S.umax[r], umx);
+    if (ovf) atomicOr(S.flags, 1u);
 }
 
 
@@ -418,27 +488,24 @@ void launch_scatter_rows_u8(uint8_t* dst, const uint8_t* src, const uint32_t* id
     k_gather_rows_u8<<<148 * 8, 256, 0, st>>>(dst, src, idx, rows, R, 1);
 }
 
-void launch_sweep_jit(cudaKernel_t k, uint32_t rpl, const DevFormula& F, const DevState& S, const DevTiles& T, float kappa,
-                      float wscale, double* terms, uint32_t terms_r, cudaStream_t st, const DevSlots* D) {
+void launch_sweep_jit(cudaKernel_t k, const DevFormula& F, const DevState& S, const DevTiles& T, float kappa,
+                      double* terms, uint32_t terms_r, cudaStream_t st, const DevSlots* D) {
     if (T.n_tiles == 0 || S.R == 0) return;
-    const int kJitWarps = (int)(T.warps ? T.warps : 1);
     const int kVmax = (int)T.vmax, kVtot = (int)(T.vmax + T.rmax);    // Plan::vmax, Plan::rmax
-    // one warp per (tile, 32*rpl restarts); a CTA's warps share one tile
-    const uint64_t rtiles = (S.R + 32 * rpl - 1) / (32 * rpl);
-    const unsigned blocks = (unsigned)((uint64_t)T.n_tiles * ((rtiles + kJitWarps - 1) / kJitWarps));
-    const size_t smem = (size_t)kJitWarps * ((size_t)kVmax * 32 * 4 * rpl + (size_t)kVtot * 4);
+    // one one-warp CTA per (tile, 32 restarts)
+    const uint64_t rtiles = (S.R + 31) / 32;
+    const unsigned blocks = (unsigned)((uint64_t)T.n_tiles * rtiles);
+    const size_t smem = (size_t)kVmax * 32 * 4 + (size_t)kVtot * 4;
     if (smem > 48 * 1024) cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (const char* co = getenv("FSMT_CARVEOUT"))   // A/B: preferred shared-memory carveout (% of max)
-        cudaFuncSetAttribute((const void*)k, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(co));
     uint32_t n_tiles = T.n_tiles, R = S.R, n_bool = F.n_bool;
     const uint8_t* U = S.U;
     const float* PT = D ? D->PT : nullptr;
     const float* PF = D ? D->PF : nullptr;
     double* GU = D ? D->GU : nullptr;
     void* args[] = {(void*)&T.tiles, &n_tiles, (void*)&T.recs, (void*)&T.tile_vars, (void*)&S.a, (void*)&S.b,
-                    (void*)&S.ga, (void*)&S.gb, (void*)&U, (void*)&S.obj, &R, &n_bool, &kappa, &wscale,
-                    &terms, &terms_r, (void*)&F.orig, (void*)&PT, (void*)&PF, (void*)&GU};
-    cudaLaunchKernel((const void*)k, dim3(blocks), dim3(kJitWarps * 32), args, smem, st);
+                    (void*)&S.ga, (void*)&S.gb, (void*)&U, (void*)&S.obj, &R, &n_bool, &kappa,
+                    &terms, &terms_r, (void*)&F.orig, (void*)&PT, (void*)&PF, (void*)&GU, (void*)&S.fx};
+    cudaLaunchKernel((const void*)k, dim3(blocks), dim3(32), args, smem, st);
 }
 
 void launch_slot_prob(cudaKernel_t k, const DevFormula& F, const DevState& S, const DevSlots& D, float kappa, cudaStream_t st) {
@@ -472,21 +539,38 @@ void launch_slot_truth(cudaKernel_t k, const DevFormula& F, const DevState& S, c
 void launch_verify_jit(cudaKernel_t k, const DevFormula& F, const DevState& S, const DevTiles& T, const int8_t* x,
                        const float* y, uint8_t* U_update, uint8_t* per_con, cudaStream_t st, const uint8_t* TT) {
     if (T.n_tiles == 0 || S.R == 0) return;
-    const int warps = (int)(T.warps ? T.warps : 1);
     const int vtot = (int)(T.vmax + T.rmax);
-    const uint64_t nw = (uint64_t)T.n_tiles * ((S.R + 31) / 32);
-    const unsigned blocks = (unsigned)((nw + warps - 1) / warps);
-    const size_t smem = (size_t)warps * vtot * 4;
+    const unsigned blocks = (unsigned)((uint64_t)T.n_tiles * ((S.R + 31) / 32));   // one warp per (tile, 32 restarts)
+    const size_t smem = (size_t)vtot * 4;
     uint32_t n_tiles = T.n_tiles, R = S.R, n_bool = F.n_bool;
     uint32_t* unsat = S.unsat;
     void* args[] = {(void*)&T.tiles, &n_tiles, (void*)&T.recs, (void*)&T.vrecs, (void*)&T.tile_vars, (void*)&x,
                     (void*)&y, (void*)&U_update, (void*)&unsat, (void*)&per_con, (void*)&F.orig, &R, &n_bool,
-                    (void*)&F.atom_rowptr, (void*)&F.atom_val64, (void*)&F.atom_rhs64, (void*)&F.atom_strict, (void*)&TT};
-    cudaLaunchKernel((const void*)k, dim3(blocks), dim3(warps * 32), args, smem, st);
+                    (void*)&F.atom_rowptr, (void*)&F.atom_val64, (void*)&F.atom_rhs64, (void*)&F.atom_strict, (void*)&TT,
+                    (void*)&S.umax, (void*)&S.flags};
+    cudaLaunchKernel((const void*)k, dim3(blocks), dim3(32), args, smem, st);
 }
 
-void launch_sweep(const DevFormula& F, const DevState& S, float kappa, float wscale, double* terms, uint32_t terms_r,
-                  cudaStream_t st) {
+void launch_prologue(const DevFormula& F, const DevState& S, float kappa, int et_int, float wfrac, double* gu, uint64_t gu_rows,
+                     cudaStream_t st) {
+    if (S.R == 0) return;
+    const uint64_t n = ((uint64_t)F.n_bool + F.n_real + 1 + (gu ? gu_rows : 0)) * S.R;
+    const unsigned blocks = (unsigned)std::min<uint64_t>((n + 255) / 256, 148ull * 16);
+    k1_prologue<<<blocks, 256, 0, st>>>(F, S, kappa, et_int, wfrac, gu, gu_rows);
+}
+
+void launch_scale_rows(double* dst, const double* src, const double* gsc, uint64_t rows, uint32_t R, cudaStream_t st) {
+    const uint64_t n = rows * R;
+    if (!n) return;
+    k_scale_rows<<<(unsigned)std::min<uint64_t>((n + 255) / 256, 148ull * 16), 256, 0, st>>>(dst, src, gsc, n, R);
+}
+
+void launch_umax(const DevFormula& F, const DevState& S, cudaStream_t st) {
+    if (S.R == 0) return;
+    k_umax<<<(S.R + 127) / 128, 128, 0, st>>>(S.U, F.n_cons, S.R, S.umax);
+}
+
+void launch_sweep(const DevFormula& F, const DevState& S, float kappa, double* terms, uint32_t terms_r, cudaStream_t st) {
     if (F.generic_end <= F.generic_begin || S.R == 0) return;
     const int warps = sweep_warps(F);
     const int smem = sweep_smem_bytes(F, warps);
@@ -494,7 +578,7 @@ void launch_sweep(const DevFormula& F, const DevState& S, float kappa, float wsc
     const uint64_t chunks = (F.generic_end - F.generic_begin + kChunk - 1) / kChunk;
     const uint64_t nw = chunks * ((S.R + 31) / 32);
     const uint64_t blocks = (nw + warps - 1) / warps;
-    k1_sweep<<<(unsigned)blocks, warps * 32, smem, st>>>(F, S, kappa, wscale, terms, terms_r,
+    k1_sweep<<<(unsigned)blocks, warps * 32, smem, st>>>(F, S, kappa, terms, terms_r,
                                                          std::max<int>(1, F.max_slots), std::max<int>(1, F.max_nodes));
 }
 

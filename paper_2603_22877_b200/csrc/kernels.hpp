@@ -6,6 +6,23 @@
 
 namespace fsmt {
 
+// Per-restart scales of one sweep (k1_prologue; mirrored in the JIT source, DESIGN.md §7 item 14).
+// The ERWA weight w_c 2^(U + e_t) (R18) enters the fp32 arithmetic as w_c 2^-wexp 2^(U - s_r)
+// 2^frac(e_t) with s_r = max(0, max_c U[c][r] - kWeightWindow) (no fp32 weight overflows).  Every
+// fp32 partial gradient sum v (reduced units) is flushed as the integer rint(v 2^-G_r) (fp32:
+// exact scaling, values >= 2^23 are integers already) into grad_a / grad_b, which therefore hold
+// integers in GRID UNITS whose sums stay below 2^51 (G_r from an a-priori bound): the fp64 sums
+// are exact, whatever the order of the atomics or the sharding.  The true gradient is the
+// stored value times gs = 2^(G_r + s_r + wexp + floor(e_t)) (K3 and fsmt_get_sweep apply it);
+// ti = 1/gs.  The objective is flushed on its own grid in true units: rint(v oi) os.
+struct FxScale {
+    double gs, ti;
+    double oi, os;
+    float gif;                   // 2^frac(e_t) 2^-G_r (the flush scale into grid units)
+    int32_t ebias;               // 127 - s_r (exponent bias of the fp32 weight 2^(U - s_r))
+};
+constexpr int kWeightWindow = 24;   // fp32 weights stay <= 2^24 w_c 2^-wexp
+
 struct DevNode {          // = TNode (8 bytes): level, hi, lo (-1 FALSE, -2 TRUE), pad
     uint16_t level;
     int16_t hi;
@@ -50,6 +67,13 @@ struct DevFormula {
     const uint32_t* h_level_off = nullptr;  // [n_hlevels+1] halfspace range of each level
     uint32_t generic_begin;         // internal [generic_begin, generic_end) run through the generic K1
     uint32_t generic_end;           //   (generic_end < n_cons only in constraint-sharded mode)
+    // a-priori bounds of the on-grid accumulation (FxScale), over the whole formula with the
+    // normalised weights w_c 2^-wexp: fx_fb = max over Booleans / slot-table rows of the summed
+    // weights of their slots (|dE/dv| <= 1), fx_fa = max over reals j of sum w |q_ij| / ||q_i||
+    // sqrt(2/pi) (times kappa: |dd/db_j| <= kappa sqrt(2/pi) |q_j| / ||q||),
+    // fx_sw = sum of the weights (|E_c| <= 1)
+    double fx_fb = 0.0, fx_fa = 0.0, fx_sw = 0.0;
+    int32_t wexp = 0;
 };
 
 // Per-restart state, restart-minor (row = variable / constraint).
@@ -57,8 +81,8 @@ struct DevState {
     uint32_t R;
     float* a;          // [n_bool][R]
     float* b;          // [n_real][R]
-    double* ga;        // [n_bool][R]
-    double* gb;        // [n_real][R]
+    double* ga;        // [n_bool][R] gradient in grid units (times gsc[r]: FxScale)
+    double* gb;        // [n_real][R] gradient in grid units
     uint8_t* U;        // [C][R]
     double* obj;       // [R]
     int8_t* x;         // [n_bool][R]
@@ -71,6 +95,10 @@ struct DevState {
     uint32_t* unsat_m; // [R]
     uint32_t* unsat_best;  // [R]
     uint8_t* better;   // [R]
+    uint32_t* umax;    // [R] max_c U[c][r] (K5 keeps it; the sweep's weight shift)
+    FxScale* fx;       // [R] per-restart scales of the current sweep (k1_prologue)
+    double* gsc;       // [R] fx[r].gs (grid scale of the gradients, read by K3 / the output copy)
+    uint32_t* flags;   // [4] bit 0 of flags[0]: an ERWA counter passed 255
 };
 
 int sweep_smem_bytes(const DevFormula& F, int warps);
@@ -79,15 +107,22 @@ int sweep_smem_bytes(const DevFormula& F, int warps);
 void launch_init(const DevFormula& F, const DevState& S, uint64_t seed, uint32_t restart_offset, cudaStream_t st);
 // K1 (generic interpreter): forward/backward xBDD sweep over internal constraints
 // [F.generic_begin, n_cons), objective + gradient (fp64 accumulation).
-void launch_sweep(const DevFormula& F, const DevState& S, float kappa, float wscale, double* terms, uint32_t terms_r,
-                  cudaStream_t st);
+void launch_sweep(const DevFormula& F, const DevState& S, float kappa, double* terms, uint32_t terms_r, cudaStream_t st);
+// Before every sweep: zero grad_a, grad_b, obj (and the slot-table gradients gu[gu_rows][R] when
+// non-null) and write S.fx / S.gsc for the stage exponent e_t = et_int + log2(wfrac) (wfrac = 1 or
+// sqrt 2, applied in the flush).
+void launch_prologue(const DevFormula& F, const DevState& S, float kappa, int et_int, float wfrac, double* gu,
+                     uint64_t gu_rows, cudaStream_t st);
+// umax[r] = max_c U[c][r] (after fsmt_set_counters).
+void launch_umax(const DevFormula& F, const DevState& S, cudaStream_t st);
+// dst[i][r] = src[i][r] * gsc[r] (grid units -> gradient), rows x R doubles.
+void launch_scale_rows(double* dst, const double* src, const double* gsc, uint64_t rows, uint32_t R, cudaStream_t st);
 // K1 (JIT-specialised, tiles): see tiles.cpp / jit.cpp.
 struct DevTiles {
     const void* tiles;           // TileDesc[n_tiles]
     uint32_t n_tiles;
     const void* recs;            // uint4 records
     const uint32_t* tile_vars;
-    uint32_t warps;              // warps per CTA (Plan::jit_warps)
     uint32_t vmax;               // stream variables (shared-memory accumulator rows) per tile (Plan::vmax)
     uint32_t rmax;               // run variables per tile (Plan::rmax)
     const void* vrecs;           // K5 records (atom ids), tile.pad1 = offset in uint4
@@ -109,8 +144,8 @@ void launch_slot_truth(cudaKernel_t k, const DevFormula& F, const DevState& S, c
 // K5 (JIT-specialised, tiles): exact check over the tiles of T (+ ERWA counters / per_con).
 void launch_verify_jit(cudaKernel_t k, const DevFormula& F, const DevState& S, const DevTiles& T, const int8_t* x,
                        const float* y, uint8_t* U_update, uint8_t* per_con, cudaStream_t st, const uint8_t* TT = nullptr);
-void launch_sweep_jit(cudaKernel_t k, uint32_t rpl, const DevFormula& F, const DevState& S, const DevTiles& T, float kappa,
-                      float wscale, double* terms, uint32_t terms_r, cudaStream_t st, const DevSlots* D = nullptr);
+void launch_sweep_jit(cudaKernel_t k, const DevFormula& F, const DevState& S, const DevTiles& T, float kappa,
+                      double* terms, uint32_t terms_r, cudaStream_t st, const DevSlots* D = nullptr);
 // row gather for u8 matrices: dst[i][:] = src[idx[i]][:]  (U between original and internal order)
 void launch_gather_rows_u8(uint8_t* dst, const uint8_t* src, const uint32_t* idx, uint32_t rows, uint32_t R,
                            cudaStream_t st);

@@ -34,9 +34,18 @@ constexpr uint32_t kJitMaxNodesSym = 160; // symmetric classes (messages only, n
 constexpr uint32_t kSymMark = 0xFFFFFFF0u;
 }  // namespace
 
+int weight_exponent(const Built& b) {
+    float m = 0.f;
+    for (float w : b.cons_w) m = std::max(m, w);
+    if (!(m > 0.f)) return 0;
+    int e = 0;
+    const float fr = std::frexp(m, &e);   // m = fr 2^e, fr in [1/2, 1)
+    return fr == 0.5f ? e - 1 : e;
+}
+
 Plan make_plan(const Formula& f, const Built& b, bool enable_jit) {
     Plan p;
-    if (const char* w = getenv("FSMT_JIT_WARPS")) p.jit_warps = std::max(1, std::min(8, atoi(w)));
+    p.wexp = weight_exponent(b);
     if (const char* v = getenv("FSMT_TILE_VMAX")) p.vmax = (uint32_t)std::max(16, std::min(256, atoi(v)));
     if (const char* v = getenv("FSMT_TILE_CMAX")) p.cmax = (uint32_t)std::max(1, std::min(1024, atoi(v)));
     if (const char* v = getenv("FSMT_TILE_RMAX")) p.rmax = (uint32_t)std::max(16, std::min(1024, atoi(v)));
@@ -301,8 +310,7 @@ Plan make_plan(const Formula& f, const Built& b, bool enable_jit) {
             for (uint32_t r = 1; r < nr; ++r)
                 for (uint32_t q = 0; q < r; ++q) sm[(size_t)r * nr + q] &= (uint8_t)(rv[r] == rv[q]);
         }
-        const char* ms_env = getenv("FSMT_JIT_STREAM");   // "0": every reference in run mode (A/B)
-        const bool use_stream = !(ms_env && ms_env[0] == '0');
+        const bool use_stream = true;   // stream-off (every reference in run mode) lost 32.8 vs 22.6 ms
         const char* ae = getenv("FSMT_JIT_ALIAS");
         const bool use_alias = !(ae && ae[0] == '0');
         for (uint32_t k = 0; k < p.n_jit_kclasses; ++k) {
@@ -395,7 +403,7 @@ Plan make_plan(const Formula& f, const Built& b, bool enable_jit) {
             if (K.sym) {
                 // weight, one table-row ref per slot, then the slots' literal signs (1 = negated)
                 std::vector<uint32_t> rec(K.stride4 * 4, 0);
-                float w = b.cons_w[c];
+                float w = std::ldexp(b.cons_w[c], -p.wexp);
                 memcpy(&rec[0], &w, 4);
                 const uint32_t L = K.n_refs, so = b.cons_slot_off[c];
                 for (uint32_t r = 0; r < L; ++r) {
@@ -412,7 +420,7 @@ Plan make_plan(const Formula& f, const Built& b, bool enable_jit) {
             const Template& t = b.tmpls[K.tmpl];
             const uint32_t* ids = b.slot_ids.data() + b.cons_slot_off[c];
             std::vector<uint32_t> rec(K.stride4 * 4, 0);
-            float w = b.cons_w[c];
+            float w = std::ldexp(b.cons_w[c], -p.wexp);
             memcpy(&rec[0], &w, 4);
             uint32_t ref = 0;
             auto put_ref = [&](uint32_t u) {
@@ -540,21 +548,6 @@ Plan make_plan(const Formula& f, const Built& b, bool enable_jit) {
         }
     }
 
-    // 5d. alias and affine-member references need no record field (K1 and K5 derive them from
-    //     their target / head).  FSMT_JIT_DROPREF=1 zeroes the fields so words holding only such
-    //     fields fold away (cfg4: 4 -> 2 uint4 per record); measured slower for K1 (10.58 vs
-    //     10.36 ms) though faster for K5, and slower overall, so the fields stay by default
-    const char* dre = getenv("FSMT_JIT_DROPREF");
-    if (dre && dre[0] == '1')
-        for (const TileDesc& T : p.tiles) {
-            const KClass& K = p.kclasses[T.kclass];
-            for (uint32_t c = 0; c < T.n_cons; ++c) {
-                uint32_t* rec = p.recs.data() + ((size_t)T.rec_off + (size_t)c * K.stride4) * 4;
-                for (uint32_t r = 0; r < K.n_refs; ++r)
-                    if (K.alias[r] >= 0 || K.aff_head[r] >= 0) rec[1 + r / 2] &= ~(0xFFFFu << (16 * (r % 2)));
-            }
-        }
-
     // 6. record compression: words equal across a whole class become literals in the code
     // (FSMT_JIT_FOLD=0 disables; cfg4: 7 -> 4 uint4 per record, 13.7 vs 14.0 ms at vmax 48)
     const char* cz = getenv("FSMT_JIT_FOLD");
@@ -618,17 +611,6 @@ std::string fnum(float v) {
     return buf;
 }
 
-// Default: the short erfc below (max abs error ~8e-8 on 0.5*erfc);
-// FSMT_JIT_ERFC=cuda selects CUDA's erfcf + expf (A/B).
-bool fast_erfc() {
-    const char* e = getenv("FSMT_JIT_ERFC");
-    return !(e && std::string(e) == "cuda");
-}
-const char* erfc_fn() {
-    const char* e = getenv("FSMT_JIT_ERFC");
-    return (e && std::string(e) == "nr") ? "fsmt_half_erfc_nr" : "fsmt_half_erfc";
-}
-
 // FSMT_JIT_PAIR=0: atoms one at a time on the scalar FP32 pipe instead of in pairs on the
 // packed f32x2 pipe (A/B; both bit-identical).
 bool jit_pair() {
@@ -644,27 +626,19 @@ int u_prefetch() {
     return e ? std::max(0, std::min(12, atoi(e))) : g_upf;
 }
 
-// FSMT_JIT_UCS=1: the prefetched U loads carry the evict-first (streaming) hint.
-bool u_streaming() {
-    const char* e = getenv("FSMT_JIT_UCS");
-    return e && e[0] == '1';
-}
-
-// FSMT_JIT_ERFC_VOTE=1: warp-vote per atom, one erfc branch when the warp agrees (A/B,
-// DESIGN.md §9).
-bool erfc_vote() {
-    const char* e = getenv("FSMT_JIT_ERFC_VOTE");
-    return e && e[0] == '1';
-}
-
 const char* kErfcPrelude =
-    "// w * 2^u for u in [0, 255], exactly ldexpf(w, u): every factor is a power of two <= 2^127,\n"
-    "// so each product is exact until it overflows, and an overflow stays inf (the exact value\n"
-    "// overflows too, all factors being >= 1)\n"
-    "__device__ __forceinline__ float fsmt_pow2_u8(float w, u32 u) {\n"
-    "  const float f1 = __uint_as_float((127u + (u & 127u)) << 23);\n"
-    "  const float f2 = __uint_as_float((127u + ((u >> 7) << 6)) << 23);\n"
-    "  return __fmul_rn(__fmul_rn(__fmul_rn(w, f1), f2), f2);\n"
+    "// Per-restart scales of the sweep (kernels.hpp FxScale, written by k1_prologue; DESIGN.md §7\n"
+    "// item 14): the ERWA weight w_c 2^(U + e_t) (R18) is applied as fp32 w_c' 2^(U - s_r) (s_r =\n"
+    "// max(0, max_c U - 24), so no fp32 weight overflows), and every fp32 partial sum is flushed as\n"
+    "// the integer rint(v 2^frac(e_t) 2^-G_r) into the fp64 gradient: integer sums below 2^53 are exact, so the\n"
+    "// atomics' order does not matter (deterministic, sharding-invariant); the consumers multiply by\n"
+    "// the restart's grid scale 2^(G_r + s_r + weight and stage exponents).\n"
+    "struct FxScale { double gs, ti, oi, os; float gif; int ebias; };\n"
+    "// v on the grid, in grid units: rintf(v gif), gif = 2^frac(e_t) 2^-G (fp32 values >= 2^23 are integers)\n"
+    "__device__ __forceinline__ double fsmt_q(float v, float gif) { return (double)rintf(v * gif); }\n"
+    "// w0 * 2^(u + ebias - 127) exactly (a power of two times w0; 0 below 2^-126, never inf: u + ebias <= 151)\n"
+    "__device__ __forceinline__ float fsmt_w(float w0, u32 u, int ebias) {\n"
+    "  return w0 * __uint_as_float((u32)max((int)u + ebias, 0) << 23);\n"
     "}\n"
     "// fsmt_prepare(R): the module compiled with FSMT_RC = R takes the restart count as a constant,\n"
     "// so every [var][R] row offset (k * 4R bytes) folds into the load's immediate offset.  The\n"
@@ -679,8 +653,7 @@ const char* kErfcPrelude =
     "// 0.5*erfc(z) for z >= 0 and ez = exp(-z^2) (dd/db factor, P:1326-1327).  Coefficients from\n"
     "// scripts/fit_erfc.py: z < 0.75: 0.5 (1 - z P(z^2)), P ~ erf(z)/z (degree 5);\n"
     "// z >= 0.75: t Q(t) ez, t = 1/(1 + z/2), Q ~ 0.5 erfcx(z)/t (degree 7), reusing ez.\n"
-    "// Max abs error 5.3e-8 in fp32 (with exact exp).  FSMT_JIT_ERFC=nr: the previous\n"
-    "// Maclaurin + Numerical Recipes erfcc pair; =cuda: erfcf + expf (A/B).\n"
+    "// Max abs error 5.3e-8 in fp32 (with exact exp).\n"
     "__device__ __forceinline__ float fsmt_half_erfc(float z, float& ez) {\n"
     "  const float z2 = z * z;\n"
     "  ez = fsmt_ex2(-1.44269504088896341f * z2);\n"
@@ -696,22 +669,6 @@ const char* kErfcPrelude =
     "  q = fmaf(q, t, 1.410473883e-01f);\n"
     "  const float tail = t * q * ez;\n"
     "  return z < 0.75f ? small : tail;\n"
-    "}\n"
-    "__device__ __forceinline__ float fsmt_erfc_small(float z, float z2) {\n"
-    "  float q = -1.4503291e-7f;\n"
-    "  q = fmaf(q, z2, 1.4589169e-6f); q = fmaf(q, z2, -1.3227513e-5f); q = fmaf(q, z2, 1.0683761e-4f);\n"
-    "  q = fmaf(q, z2, -7.5757576e-4f); q = fmaf(q, z2, 4.6296296e-3f); q = fmaf(q, z2, -2.3809524e-2f);\n"
-    "  q = fmaf(q, z2, 0.1f); q = fmaf(q, z2, -0.33333333f); q = fmaf(q, z2, 1.f);\n"
-    "  return 0.5f * fmaf(-1.12837916709551257f * z, q, 1.f);\n"
-    "}\n"
-    "__device__ __forceinline__ float fsmt_erfc_tail(float z, float z2) {\n"
-    "  float t;\n"
-    "  asm(\"rcp.approx.ftz.f32 %0, %1;\" : \"=f\"(t) : \"f\"(fmaf(0.5f, z, 1.f)));\n"
-    "  float p = 0.17087277f;\n"
-    "  p = fmaf(p, t, -0.82215223f); p = fmaf(p, t, 1.48851587f); p = fmaf(p, t, -1.13520398f);\n"
-    "  p = fmaf(p, t, 0.27886807f); p = fmaf(p, t, -0.18628806f); p = fmaf(p, t, 0.09678418f);\n"
-    "  p = fmaf(p, t, 0.37409196f); p = fmaf(p, t, 1.00002368f); p = fmaf(p, t, -1.26551223f);\n"
-    "  return 0.5f * t * fsmt_ex2((p - z2) * 1.44269504088896341f);\n"
     "}\n"
     "// Two atoms at once on the packed fp32x2 pipe (FFMA2/FMUL2, sm_100): per component exactly\n"
     "// the operations of fsmt_half_erfc (each f32x2 lane rounds like the scalar op), so the\n"
@@ -737,41 +694,6 @@ const char* kErfcPrelude =
     "  q = __ffma2_rn(q, t, FSMT_C2(1.410473883e-01f));\n"
     "  const float2 tail = __fmul2_rn(__fmul2_rn(t, q), ez);\n"
     "  return make_float2(z.x < 0.75f ? small.x : tail.x, z.y < 0.75f ? small.y : tail.y);\n"
-    "}\n"
-    "__device__ __forceinline__ float fsmt_half_erfc_nr(float z, float& ez) {\n"
-    "  const float z2 = z * z;\n"
-    "  ez = fsmt_ex2(-1.44269504088896341f * z2);\n"
-    "  const float small = fsmt_erfc_small(z, z2), tail = fsmt_erfc_tail(z, z2);\n"
-    "  return z < 0.75f ? small : tail;\n"
-    "}\n\n";
-
-// f32x2 arithmetic for the two-restarts-per-lane sweep: each operator is one packed FADD2 /
-// FMUL2 / FFMA2 whose components round exactly like the scalar op (a - b as a + (-b));
-// float operands broadcast.
-const char* kLane2Prelude =
-    "#define FSMT_Z2 make_float2(0.f, 0.f)\n"
-    "#define FSMT_AT2(base, off) (*(const float2*)((const char*)(base) + (off)))\n"
-    "__device__ __forceinline__ float2 fsmt_b2(float a) { return make_float2(a, a); }\n"
-    "__device__ __forceinline__ float2 fsmt_b2(float2 a) { return a; }\n"
-    "__device__ __forceinline__ float2 operator-(float2 a) { return make_float2(-a.x, -a.y); }\n"
-    "__device__ __forceinline__ float2 operator+(float2 a, float2 b) { return __fadd2_rn(a, b); }\n"
-    "__device__ __forceinline__ float2 operator-(float2 a, float2 b) { return __fadd2_rn(a, -b); }\n"
-    "__device__ __forceinline__ float2 operator*(float2 a, float2 b) { return __fmul2_rn(a, b); }\n"
-    "__device__ __forceinline__ float2 operator+(float a, float2 b) { return __fadd2_rn(fsmt_b2(a), b); }\n"
-    "__device__ __forceinline__ float2 operator+(float2 a, float b) { return __fadd2_rn(a, fsmt_b2(b)); }\n"
-    "__device__ __forceinline__ float2 operator-(float a, float2 b) { return __fadd2_rn(fsmt_b2(a), -b); }\n"
-    "__device__ __forceinline__ float2 operator-(float2 a, float b) { return __fadd2_rn(a, fsmt_b2(-b)); }\n"
-    "__device__ __forceinline__ float2 operator*(float a, float2 b) { return __fmul2_rn(fsmt_b2(a), b); }\n"
-    "__device__ __forceinline__ float2 operator*(float2 a, float b) { return __fmul2_rn(a, fsmt_b2(b)); }\n"
-    "__device__ __forceinline__ float2& operator+=(float2& a, float2 b) { a = a + b; return a; }\n"
-    "__device__ __forceinline__ float2& operator-=(float2& a, float2 b) { a = a - b; return a; }\n"
-    "#define FSMT_FMA2(A, B, C) __device__ __forceinline__ float2 fmaf(A a, B b, C c) { return __ffma2_rn(fsmt_b2(a), fsmt_b2(b), fsmt_b2(c)); }\n"
-    "FSMT_FMA2(float2, float2, float2) FSMT_FMA2(float, float2, float2) FSMT_FMA2(float2, float, float2)\n"
-    "FSMT_FMA2(float2, float2, float) FSMT_FMA2(float, float2, float) FSMT_FMA2(float2, float, float)\n"
-    "FSMT_FMA2(float, float, float2)\n"
-    "__device__ __forceinline__ float2 fsmt_abs2(float2 a) { return make_float2(fabsf(a.x), fabsf(a.y)); }\n"
-    "__device__ __forceinline__ float2 fsmt_sel_ge0(float2 u, float2 a, float2 b) {\n"
-    "  return make_float2(u.x >= 0.f ? a.x : b.x, u.y >= 0.f ? a.y : b.y);\n"
     "}\n\n";
 
 const char* comp(uint32_t w) {
@@ -791,14 +713,9 @@ std::string word(uint32_t w) {
     return "q" + std::to_string(w / 4) + "." + comp(w);
 }
 
-// Two restarts per lane (fsmt_prepare with an even R, DESIGN.md §7 item 11): every per-restart
-// value is a float2 (restarts r, r + 1 of the lane), arithmetic on the packed f32x2 pipe through
-// the operator overloads of kLane2Prelude; per component the operations of the scalar sweep.
-thread_local bool g_v2 = false;
-
 void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Template& t) {
     g_wk = &K;
-    const std::string TY = g_v2 ? "float2" : "float", ZR = g_v2 ? "FSMT_Z2" : "0.f", AT = g_v2 ? "FSMT_AT2" : "FSMT_AT";
+    const std::string TY = "float", ZR = "0.f", AT = "FSMT_AT";
     const size_t ns = t.kinds.size();
     // DBG = false (the hot instantiation): U present, no per-constraint E_c debug output, so
     // neither test is in the loop
@@ -806,8 +723,8 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
       << "(const TileDesc& T, const uint4* __restrict__ rp, const u32* __restrict__ vs, const u32* __restrict__ vr,\n"
          "    " << TY << "* __restrict__ accs, const float* __restrict__ ab, const float* __restrict__ bb,\n"
          "    double* __restrict__ ga, double* __restrict__ gb, const unsigned char* __restrict__ U,\n"
-         "    u32 R, u32 R4, u64 rr, u32 r, bool live, u32 n_bool, float kq, float dcoef, float wscale, "
-      << (g_v2 ? "double2& objacc" : "double& objacc") << ",\n"
+         "    u32 R, u32 R4, u64 rr, u32 r, bool live, u32 n_bool, float kq, float dcoef, int ebias,\n"
+         "    float gif, double& objacc,\n"
          "    double* __restrict__ terms, u32 terms_r, const u32* __restrict__ orig,\n"
          "    const float* __restrict__ PTl, const float* __restrict__ PFl, double* __restrict__ gu) {\n"
          "  const bool hasU = !DBG || U != nullptr, hasT = DBG && terms != nullptr;\n";
@@ -854,28 +771,19 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
         const std::string dst = ref_kind[i] == 0 ? "ga + (u64)(" + g + ") * R + r"
                               : ref_kind[i] == 2 ? "gu + (u64)(" + g + ") * R + r"
                                                  : "gb + (u64)(" + g + " - n_bool) * R + r";
-        if (g_v2)
-            return "if (live) { atomicAdd(" + dst + ", (double)acc" + std::to_string(i) + ".x); atomicAdd(" + dst + " + 1, (double)acc" +
-                   std::to_string(i) + ".y); }";
-        return "if (live) atomicAdd(" + dst + ", (double)acc" + std::to_string(i) + ");";
+        return "if (live) atomicAdd(" + dst + ", fsmt_q(acc" + std::to_string(i) + ", gif));";
     };
     auto gm = [&](size_t h, size_t m) { return "gcur" + std::to_string(h) + " + (" + std::to_string(K.aff_dg[m]) + ")"; };
-    // ERWA counters: a streaming (evict-first) byte load per constraint, issued u_prefetch()
-    // constraints ahead so its DRAM latency overlaps the passes of the current constraints
+    // ERWA counters: a byte load per constraint, issued u_prefetch() constraints ahead so its
+    // DRAM latency overlaps the passes of the current constraints
     const int upf = u_prefetch();
-    const char* uld = u_streaming() ? "__ldcs" : "__ldg";
-    const std::string ucast = g_v2 ? "(const unsigned short*)" : "";
+    const char* uld = "__ldg";
+    const std::string ucast = "";
     if (upf > 0) {
         o << "  const unsigned char* Up = hasU ? U + (u64)T.cons_begin * R + rr : nullptr;\n";
         for (int k = 0; k < upf; ++k)
             o << "  u32 un" << k << " = (hasU && " << k << "u < T.n_cons) ? (u32)" << uld << "(" << ucast << "(Up + (u64)" << k << "u * R)) : 0u;\n";
     }
-    // FSMT_JIT_RPF=1: the next constraint's record is loaded one iteration ahead (A/B)
-    const char* rpf_env = getenv("FSMT_JIT_RPF");
-    const bool rpf = rpf_env && rpf_env[0] == '1';
-    if (rpf)
-        for (uint32_t q = 0; q < K.stride4; ++q)
-            o << "  uint4 nq" << q << " = T.n_cons ? __ldg(rp + " << q << ") : make_uint4(0u, 0u, 0u, 0u);\n";
     // the constraint loop unrolled twice (FSMT_JIT_UNROLL overrides; cfg3 0.884 ->
     // 0.849 ms, cfg4 8.36 -> 8.33 ms; 4 is slower on cfg4)
     {
@@ -883,31 +791,17 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
         o << "#pragma unroll " << (ur ? std::max(1, atoi(ur)) : 2) << "\n";
     }
     o << "  for (u32 c = 0; c < T.n_cons; ++c, rp += " << K.stride4 << ") {\n";
-    if (rpf) {
-        for (uint32_t q = 0; q < K.stride4; ++q) o << "    const uint4 q" << q << " = nq" << q << ";\n";
-        o << "    if (c + 1 < T.n_cons) {";
-        for (uint32_t q = 0; q < K.stride4; ++q) o << " nq" << q << " = __ldg(rp + " << K.stride4 + q << ");";
-        o << " }\n";
-    } else {
-        for (uint32_t q = 0; q < K.stride4; ++q) o << "    const uint4 q" << q << " = __ldg(rp + " << q << ");\n";
-    }
+    for (uint32_t q = 0; q < K.stride4; ++q) o << "    const uint4 q" << q << " = __ldg(rp + " << q << ");\n";
     if (upf > 0) {
         o << "    const u32 uc = un0;\n";
         for (int k = 0; k + 1 < upf; ++k) o << "    un" << k << " = un" << k + 1 << ";\n";
         o << "    if (hasU) un" << upf - 1 << " = c + " << upf << "u < T.n_cons ? (u32)" << uld << "(" << ucast << "(Up + (u64)(c + " << upf
           << "u) * R)) : 0u;\n";
     } else {
-        if (g_v2)
-            o << "    const u32 uc = hasU ? (u32)*(const unsigned short*)(U + (u64)(T.cons_begin + c) * R + rr) : 0u;\n";
-        else
-            o << "    const u32 uc = hasU ? (u32)U[(u64)(T.cons_begin + c) * R + rr] : 0u;\n";
+        o << "    const u32 uc = hasU ? (u32)U[(u64)(T.cons_begin + c) * R + rr] : 0u;\n";
     }
-    if (g_v2)
-        o << "    const float w0 = __uint_as_float(" << word(0) << ") * wscale;\n"
-             "    const float2 w = hasU ? make_float2(fsmt_pow2_u8(w0, uc & 255u), fsmt_pow2_u8(w0, uc >> 8)) : make_float2(w0, w0);\n";
-    else
-        o << "    float w = __uint_as_float(" << word(0) << ") * wscale;\n"
-             "    if (hasU) w = fsmt_pow2_u8(w, uc);\n";
+    // w_c' 2^(U - s_r) (R18 with the restart's shift; 2^frac(e_t) is applied in the flush: FxScale)
+    o << "    const float w = fsmt_w(__uint_as_float(" << word(0) << "), uc, ebias);\n";
     for (size_t i = 0; i < nr; ++i) {
         uint32_t wd = 1 + (uint32_t)i / 2;
         const std::string ext = "(" + word(wd) + " >> " + std::to_string(16 * (i % 2)) + ") & 0xffffu";
@@ -941,7 +835,7 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
     // atom pairs for the packed f32x2 pipe: consecutive atom slots with equal nnz and equal
     // class-constant status of 1/||q|| (their words are consecutive in the record)
     std::vector<int> pair_with(ns, -1), pair_second(ns, 0);
-    if (!g_v2 && jit_pair() && fast_erfc() && !erfc_vote() && std::string(erfc_fn()) == "fsmt_half_erfc") {
+    if (jit_pair()) {
         int pend = -1;
         uint32_t awp = 1 + ((uint32_t)nr + 1) / 2, pend_aw = 0;
         for (size_t s = 0, ai = 0; s < ns; ++s) {
@@ -1006,8 +900,7 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
               << " ? val" << ri << " : vaf" << ri << ";\n";
         } else {
             const uint32_t nnz = K.nnz[ai++];
-            if (g_v2) o << "    float2 z" << s << " = FSMT_C2(-__uint_as_float(" << word(aw) << "));\n";
-            else o << "    float z" << s << " = -__uint_as_float(" << word(aw) << ");\n";
+            o << "    float z" << s << " = -__uint_as_float(" << word(aw) << ");\n";
             o << "    const float inv" << s << " = __uint_as_float(" << word(aw + 1) << ");\n";
             for (uint32_t k = 0; k < nnz; ++k) {
                 coef_word[slot_ref0[s] + k] = aw + 2 + k;
@@ -1020,29 +913,7 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
                 o << "    const " << TY << " u" << s << " = z" << s << " * (kq * inv" << s << ");\n";
             else
                 o << "    const " << TY << " u" << s << " = kq * z" << s << " * inv" << s << ";\n";
-            if (g_v2) {
-                o << "    float2 ez" << s << ";\n    const float2 e" << s << " = fsmt_half_erfc2(fsmt_abs2(u" << s << "), ez" << s << ");\n"
-                  << "    const float2 om" << s << " = 1.f - e" << s << ";\n"
-                  << "    const float2 pt" << s << " = fsmt_sel_ge0(u" << s << ", e" << s << ", om" << s << ");\n"
-                  << "    const float2 pf" << s << " = fsmt_sel_ge0(u" << s << ", om" << s << ", e" << s << ");\n"
-                  << "    const float2 dd" << s << " = (dcoef * inv" << s << ") * ez" << s << ";\n";
-                continue;
-            }
-            if (fast_erfc() && erfc_vote()) {
-                // warp vote: both erfc branches only when the warp's lanes straddle |u| = 0.75
-                o << "    const float za" << s << " = fabsf(u" << s << "), zb" << s << " = za" << s << " * za" << s << ";\n"
-                  << "    const float ez" << s << " = fsmt_ex2(-1.44269504088896341f * zb" << s << ");\n"
-                  << "    float e" << s << ";\n"
-                  << "    { const unsigned bal = __ballot_sync(0xffffffffu, za" << s << " < 0.75f);\n"
-                  << "      if (bal == 0xffffffffu) e" << s << " = fsmt_erfc_small(za" << s << ", zb" << s << ");\n"
-                  << "      else if (bal == 0u) e" << s << " = fsmt_erfc_tail(za" << s << ", zb" << s << ");\n"
-                  << "      else e" << s << " = za" << s << " < 0.75f ? fsmt_erfc_small(za" << s << ", zb" << s
-                  << ") : fsmt_erfc_tail(za" << s << ", zb" << s << "); }\n";
-            } else if (fast_erfc())
-                o << "    float ez" << s << ";\n    const float e" << s << " = " << erfc_fn() << "(fabsf(u" << s << "), ez" << s << ");\n";
-            else
-                o << "    const float e" << s << " = 0.5f * erfcf(fabsf(u" << s << "));\n"
-                  << "    const float ez" << s << " = expf(-u" << s << " * u" << s << ");\n";
+            o << "    float ez" << s << ";\n    const float e" << s << " = fsmt_half_erfc(fabsf(u" << s << "), ez" << s << ");\n";
             o << "    const float pt" << s << " = u" << s << " >= 0.f ? e" << s << " : 1.f - e" << s << ";\n"
               << "    const float pf" << s << " = u" << s << " >= 0.f ? 1.f - e" << s << " : e" << s << ";\n"
               << "    const float dd" << s << " = (dcoef * inv" << s << ") * ez" << s << ";\n";
@@ -1083,7 +954,7 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
     // Boolean x Boolean diamonds' P_X / P_Y two at a time on the f32x2 pipe (FSMT_JIT_PAIR=0:
     // one at a time inside the forward pass); per component the same operations
     std::vector<char> dpre(nn, 0);
-    if (!g_v2 && jit_pair()) {
+    if (jit_pair()) {
         std::vector<size_t> bb;
         for (size_t v = 0; v < nn; ++v)
             if (dhead[v] && is_bool(t.nodes[v].level) && is_bool(t.nodes[t.nodes[v].hi].level)) bb.push_back(v);
@@ -1103,7 +974,7 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
     }
     // forward pass (Alg.F): m_td in registers
     for (size_t v = 0; v < nn; ++v)
-        if (!dskip[v]) o << "    " << TY << " m" << v << " = " << ((int)v == t.root ? (g_v2 ? "FSMT_C2(1.f)" : "1.f") : ZR) << ";\n";
+        if (!dskip[v]) o << "    " << TY << " m" << v << " = " << ((int)v == t.root ? "1.f" : ZR) << ";\n";
     o << "    " << TY << " pT = " << ZR << ";\n";
     for (size_t v = 0; v < nn; ++v) {
         if (dskip[v]) continue;
@@ -1218,13 +1089,8 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
     }
     auto gref = [&](size_t s) { return cmp ? "(-G" + std::to_string(s) + ")" : "G" + std::to_string(s); };
     o << "    const " << TY << " E = 1.f - 2.f * pT;\n";
-    if (g_v2)
-        o << "    objacc.x += (double)w.x * (double)E.x;\n"
-             "    objacc.y += (double)w.y * (double)E.y;\n"
-             "    if (hasT && live && (r == terms_r || r + 1 == terms_r)) terms[orig[T.cons_begin + c]] = (double)(r == terms_r ? E.x : E.y);\n";
-    else
-        o << "    objacc += (double)w * (double)E;\n"
-             "    if (hasT && live && r == terms_r) terms[orig[T.cons_begin + c]] = (double)E;\n";
+    o << "    objacc += (double)w * (double)E;\n"
+         "    if (hasT && live && r == terms_r) terms[orig[T.cons_begin + c]] = (double)E;\n";
     // gradient terms per target reference (aliases fold into their target: one read-modify-write)
     std::vector<std::vector<std::pair<std::string, std::string>>> terms_of(nr);
     auto accum = [&](int ri, const std::string& a, const std::string& b) {
@@ -1287,7 +1153,7 @@ void emit_verify_class(std::ostringstream& o, uint32_t kid, const KClass& K, con
          "    unsigned char* __restrict__ per_con, const u32* __restrict__ orig, u32 R, u64 rr, u32 r, bool live,\n"
          "    u32 n_bool, const u32* __restrict__ arow, const double* __restrict__ aval,\n"
          "    const double* __restrict__ arhs, const unsigned char* __restrict__ astrict,\n"
-         "    const unsigned char* __restrict__ TT) {\n"
+         "    const unsigned char* __restrict__ TT, u32& umx, u32& ovf) {\n"
          "  u32 cnt = 0u;\n"
          "  const u32 R4 = R * 4u;\n"
          "  const signed char* xb = x + rr;                          // the lane's column bases\n"
@@ -1404,7 +1270,14 @@ void emit_verify_class(std::ostringstream& o, uint32_t kid, const KClass& K, con
     o << "    const u32 u = " << (t.root >= 0 ? "s" + std::to_string(t.root) : std::string(t.root == kTrue ? "true" : "false"))
       << " ? 0u : 1u;\n"
          "    if (live) {\n"
-         "      if (U && u) { unsigned char* cell = U + (u64)(T.cons_begin + c) * R + rr; const u32 nv = (u32)*cell + 1u; *cell = (unsigned char)(nv > 255u ? 255u : nv); }   // U += u: only violated constraints touch memory\n"
+         "      if (U && u) {   // U += u (R18): only violated constraints touch memory; > 255 is reported\n"
+         "        unsigned char* cell = U + (u64)(T.cons_begin + c) * R + rr;\n"
+         "        const u32 nv = (u32)*cell + 1u;\n"
+         "        ovf |= nv > 255u;\n"
+         "        const u32 nc = nv > 255u ? 255u : nv;\n"
+         "        *cell = (unsigned char)nc;\n"
+         "        umx = umx > nc ? umx : nc;\n"
+         "      }\n"
          "      if (per_con) per_con[(u64)orig[T.cons_begin + c] * R + rr] = (unsigned char)u;\n"
          "    }\n"
          "    cnt += u;\n  }\n  return cnt;\n}\n\n";
@@ -1412,60 +1285,55 @@ void emit_verify_class(std::ostringstream& o, uint32_t kid, const KClass& K, con
 
 }  // namespace
 
-std::string jit_source(const Formula& f, const Built& b, const Plan& p, int u_prefetch_default, bool lane2, int k1_min_ctas) {
+std::string jit_source(const Formula& f, const Built& b, const Plan& p, int u_prefetch_default, int k1_min_ctas) {
     g_upf = u_prefetch_default;
-    g_v2 = lane2;
-    struct Reset { ~Reset() { g_v2 = false; } } reset_v2;
     std::ostringstream o;
     o << "// generated by fsmt tiles.cpp: specialised K1 sweep for " << p.n_jit_kclasses << " kernel classes\n"
          "typedef unsigned int u32;\ntypedef unsigned long long u64;\n"
          "struct TileDesc { u32 kclass, cons_begin, n_cons, var_off, n_vars, rec_off, pad0, pad1; };\n"
-      << "#define VMAX " << p.kernel_vmax() << "\n#define VTOT " << p.kernel_vmax() + p.rmax << "\n#define WARPS " << p.jit_warps
-      << "\n#define RPL " << (lane2 ? 2 : 1) << "\n\n" << kErfcPrelude << (lane2 ? kLane2Prelude : "");
+      << "#define VMAX " << p.kernel_vmax() << "\n#define VTOT " << p.kernel_vmax() + p.rmax << "\n\n" << kErfcPrelude;
     auto tmpl_of = [&](const KClass& K) -> const Template& { return K.sym ? K.stmpl : b.tmpls[K.tmpl]; };
     for (uint32_t k = 0; k < p.n_jit_kclasses; ++k) emit_class(o, k, p.kclasses[k], tmpl_of(p.kclasses[k]));
     const char* minb = getenv("FSMT_JIT_MINB");      // optional min CTAs/SM (register cap), A/B tuning
     // fsmt_k1_jit: the hot kernel (U present, no E_c output); fsmt_k1_jit_dbg: U may be NULL and
     // the per-constraint E_c debug hook is live.  Separate kernels, so the hot one keeps its own
-    // register allocation.
+    // register allocation.  One warp per CTA (CTA-uniform control flow, DESIGN.md §7 item 5).
     for (int dbgk = 0; dbgk < 2; ++dbgk) {
     // hot kernel: k1_min_ctas resident warps per SM as a register cap (fsmt_prepare picks
     // the largest of 32 / 28 that compiles without spills; 0 = none); FSMT_JIT_MINB overrides
-    const std::string mb = minb ? std::string(minb)
-                                : (dbgk || k1_min_ctas <= 0 ? std::string() : std::to_string(std::max(1, k1_min_ctas / (int)p.jit_warps)));
-    o << "extern \"C\" __global__ void __launch_bounds__(WARPS * 32" << (atoi(mb.c_str()) > 0 ? ", " + mb : std::string())
+    const std::string mb = minb ? std::string(minb) : (dbgk || k1_min_ctas <= 0 ? std::string() : std::to_string(k1_min_ctas));
+    o << "extern \"C\" __global__ void __launch_bounds__(32" << (atoi(mb.c_str()) > 0 ? ", " + mb : std::string())
       << ") fsmt_k1_jit" << (dbgk ? "_dbg" : "") << "(\n"
          "    const TileDesc* __restrict__ tiles, u32 n_tiles, const uint4* __restrict__ recs,\n"
          "    const u32* __restrict__ tile_vars, const float* __restrict__ a, const float* __restrict__ b,\n"
          "    double* __restrict__ ga, double* __restrict__ gb, const unsigned char* __restrict__ U,\n"
-         "    double* __restrict__ obj, u32 R, u32 n_bool, float kappa, float wscale,\n"
+         "    double* __restrict__ obj, u32 R, u32 n_bool, float kappa,\n"
          "    double* __restrict__ terms, u32 terms_r, const u32* __restrict__ orig,\n"
-         "    const float* __restrict__ PT, const float* __restrict__ PF, double* __restrict__ gu) {\n"
+         "    const float* __restrict__ PT, const float* __restrict__ PF, double* __restrict__ gu,\n"
+         "    const FxScale* __restrict__ fxs) {\n"
          "  FSMT_SPECIALISE_R\n"
          "  extern __shared__ float smem[];\n"
-         "  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;\n"
-      << (lane2 ? "  float2* acc = (float2*)smem + warp * (VMAX * 32);       // stream-variable rows (2 restarts per lane)\n"
-                : "  float* acc = smem + warp * (VMAX * 32);                  // stream-variable rows\n")
-      << "  u32* vs = (u32*)(smem + WARPS * VMAX * 32 * RPL) + warp * VTOT; // stream then run variable ids\n"
-         "  const u32 rtiles = (R + 32 * RPL - 1) / (32 * RPL);\n"
-         "  // a CTA's warps are restart tiles of ONE constraint tile (CTA-uniform tile, shared records)\n"
-         "  const u32 rtw = (rtiles + WARPS - 1) / WARPS;\n"
-         "  const u64 ti = blockIdx.x / rtw;\n"
-         "  const u32 rt = (u32)(blockIdx.x % rtw) * WARPS + warp;\n"
-         "  if (ti >= n_tiles || rt >= rtiles) return;\n"
+         "  const int lane = threadIdx.x & 31;\n"
+         "  float* acc = smem;                                    // stream-variable rows\n"
+         "  u32* vs = (u32*)(smem + VMAX * 32);                   // stream then run variable ids\n"
+         "  const u32 rtiles = (R + 31) / 32;\n"
+         "  const u64 ti = blockIdx.x / rtiles;\n"
+         "  const u32 rt = (u32)(blockIdx.x % rtiles);\n"
+         "  if (ti >= n_tiles) return;\n"
          "  const TileDesc T = tiles[ti];\n"
          "  const u32 n_s = T.n_vars & 0xffffu, n_v = n_s + (T.n_vars >> 16);\n"
-         "  const u32 r = rt * 32 * RPL + lane * RPL;   // the lane's (first) restart\n"
+         "  const u32 r = rt * 32 + lane;\n"
          "  const bool live = r < R;\n"
          "  const u64 rr = live ? r : 0;\n"
          "  for (u32 l = lane; l < n_v; l += 32) vs[l] = tile_vars[T.var_off + l];\n"
-      << "  for (u32 l = 0; l < n_s; ++l) acc[l * 32 + lane] = " << (lane2 ? "FSMT_Z2" : "0.f") << ";\n"
+         "  for (u32 l = 0; l < n_s; ++l) acc[l * 32 + lane] = 0.f;\n"
          "  __syncwarp();\n"
          "  const u32* vr = vs + n_s;\n"
          "  const float kq = kappa * 0.70710678118654752f;\n"
          "  const float dcoef = kappa * 0.79788456080286536f;\n"
-      << (lane2 ? "  double2 objacc = make_double2(0.0, 0.0);\n" : "  double objacc = 0.0;\n")
-      << 
+         "  const float gif = fxs[rr].gif;\n"
+         "  const int ebias = fxs[rr].ebias;\n"
+         "  double objacc = 0.0;\n"
          "  const uint4* rp = recs + T.rec_off;\n"
          "  // the lane's column bases: element (v, restart rr) of a [var][R] array at base + v * 4R bytes\n"
          "  const u32 R4 = R * 4u;\n"
@@ -1474,52 +1342,41 @@ std::string jit_source(const Formula& f, const Built& b, const Plan& p, int u_pr
          "  const float* PTl = PT ? PT + rr : nullptr;\n"
          "  const float* PFl = PF ? PF + rr : nullptr;\n"
          "  bool symt = false;   // symmetric class: the tile's variables are slot-table rows\n"
-
          "  switch (T.kclass) {\n";
     for (uint32_t k = 0; k < p.n_jit_kclasses; ++k) {
-        const std::string args = "(T, rp, vs, vr, acc + lane, ab, bb, ga, gb, U, R, R4, rr, r, live, n_bool, kq, dcoef, wscale, objacc, "
-                                 "terms, terms_r, orig, PTl, PFl, gu); ";
+        const std::string args = "(T, rp, vs, vr, acc + lane, ab, bb, ga, gb, U, R, R4, rr, r, live, n_bool, kq, dcoef, ebias, "
+                                 "gif, objacc, terms, terms_r, orig, PTl, PFl, gu); ";
         o << "    case " << k << ": kc" << k << (dbgk ? "<true>" : "<false>") << args
           << (p.kclasses[k].sym ? "symt = true; " : "") << "break;\n";
     }
     o << "    default: break;\n  }\n"
          "  __syncwarp();\n"
-         "  if (!live) return;\n";
-    if (lane2)
-        o << "  (void)symt;\n"
-             "  for (u32 l = 0; l < n_s; ++l) {\n"
-             "    const u32 g = vs[l];\n"
-             "    const float2 v = acc[l * 32 + lane];\n"
-             "    double* dst = g < n_bool ? ga + (u64)g * R + r : gb + (u64)(g - n_bool) * R + r;\n"
-             "    atomicAdd(dst, (double)v.x); atomicAdd(dst + 1, (double)v.y);\n"
-             "  }\n"
-             "  atomicAdd(obj + r, objacc.x); atomicAdd(obj + r + 1, objacc.y);\n"
-             "}\n\n";
-    else
-        o << "  for (u32 l = 0; l < n_s; ++l) {\n"
-             "    const u32 g = vs[l];\n"
-             "    const double v = (double)acc[l * 32 + lane];\n"
-             "    if (symt) atomicAdd(gu + (u64)g * R + r, v);\n"
-             "    else if (g < n_bool) atomicAdd(ga + (u64)g * R + r, v); else atomicAdd(gb + (u64)(g - n_bool) * R + r, v);\n"
-             "  }\n"
-             "  atomicAdd(obj + r, objacc);\n"
-             "}\n\n";
+         "  if (!live) return;\n"
+         "  for (u32 l = 0; l < n_s; ++l) {   // stream rows: one on-grid fp64 add per row and tile\n"
+         "    const u32 g = vs[l];\n"
+         "    const double v = fsmt_q(acc[l * 32 + lane], gif);\n"
+         "    if (symt) atomicAdd(gu + (u64)g * R + r, v);\n"
+         "    else if (g < n_bool) atomicAdd(ga + (u64)g * R + r, v); else atomicAdd(gb + (u64)(g - n_bool) * R + r, v);\n"
+         "  }\n"
+         "  atomicAdd(obj + r, rint(objacc * fxs[r].oi) * fxs[r].os);   // on the objective's grid, true units\n"
+         "}\n\n";
     }
     // K5: exact verification of the rounded models + ERWA counters over the same tiles
     for (uint32_t k = 0; k < p.n_jit_kclasses; ++k) emit_verify_class(o, k, p.kclasses[k], tmpl_of(p.kclasses[k]));
-    o << "extern \"C\" __global__ void __launch_bounds__(WARPS * 32) fsmt_k5_jit(\n"
+    o << "extern \"C\" __global__ void __launch_bounds__(32) fsmt_k5_jit(\n"
          "    const TileDesc* __restrict__ tiles, u32 n_tiles, const uint4* __restrict__ recs,\n"
          "    const uint4* __restrict__ vrecs, const u32* __restrict__ tile_vars, const signed char* __restrict__ x,\n"
          "    const float* __restrict__ y, unsigned char* __restrict__ U, u32* __restrict__ unsat,\n"
          "    unsigned char* __restrict__ per_con, const u32* __restrict__ orig, u32 R, u32 n_bool,\n"
          "    const u32* __restrict__ arow, const double* __restrict__ aval, const double* __restrict__ arhs,\n"
-         "    const unsigned char* __restrict__ astrict, const unsigned char* __restrict__ TT) {\n"
+         "    const unsigned char* __restrict__ astrict, const unsigned char* __restrict__ TT,\n"
+         "    u32* __restrict__ umax, u32* __restrict__ flags) {\n"
          "  FSMT_SPECIALISE_R\n"
          "  extern __shared__ float smem[];\n"
-         "  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;\n"
-         "  u32* vs = (u32*)smem + warp * VTOT;\n"
+         "  const int lane = threadIdx.x & 31;\n"
+         "  u32* vs = (u32*)smem;\n"
          "  const u32 rtiles = (R + 31) / 32;\n"
-         "  const u64 gw = (u64)blockIdx.x * WARPS + warp;\n"
+         "  const u64 gw = (u64)blockIdx.x;\n"
          "  const u32 rt = (u32)(gw % rtiles);\n"
          "  const u64 ti = gw / rtiles;\n"
          "  if (ti >= n_tiles) return;\n"
@@ -1533,13 +1390,15 @@ std::string jit_source(const Formula& f, const Built& b, const Plan& p, int u_pr
          "  const u32* vr = vs + n_s;\n"
          "  const uint4* rp = recs + T.rec_off;\n"
          "  const uint4* vp = vrecs + T.pad1;\n"
-         "  u32 cnt = 0u;\n"
+         "  u32 cnt = 0u, umx = 0u, ovf = 0u;\n"
          "  switch (T.kclass) {\n";
     for (uint32_t k = 0; k < p.n_jit_kclasses; ++k)
         o << "    case " << k << ": cnt = kv" << k
-          << "(T, rp, vp, vs, vr, x, y, U, per_con, orig, R, rr, r, live, n_bool, arow, aval, arhs, astrict, TT); break;\n";
+          << "(T, rp, vp, vs, vr, x, y, U, per_con, orig, R, rr, r, live, n_bool, arow, aval, arhs, astrict, TT, umx, ovf); break;\n";
     o << "    default: break;\n  }\n"
          "  if (live && cnt) atomicAdd(unsat + r, cnt);\n"
+         "  if (live && umx) atomicMax(umax + r, umx);   // the restart's largest counter (k1_prologue's shift)\n"
+         "  if (ovf) atomicOr(flags, 1u);                 // a counter passed 255: fsmt_stage_end fails (FSMT_ERR_RANGE)\n"
          "}\n";
     // slot tables for the symmetric classes: probabilities of every Boolean and
     // table atom once per sweep, the row gradients chained back to grad_a / grad_b, and the rows'
@@ -1562,7 +1421,7 @@ std::string jit_source(const Formula& f, const Built& b, const Plan& p, int u_pr
          "      for (u32 k = arow[at]; k < arow[at + 1]; ++k) z = fmaf(aval[k], b[(u64)acol[k] * R + r], z);\n"
          "      const float inv = ainv[at], u = kq * z * inv;\n"
          "      float ez;\n"
-         "      const float e = " << erfc_fn() << "(fabsf(u), ez);\n"
+         "      const float e = fsmt_half_erfc(fabsf(u), ez);\n"
          "      const u64 o = (u64)(nv + t) * R + r;\n"
          "      PT[o] = u >= 0.f ? e : 1.f - e; PF[o] = u >= 0.f ? 1.f - e : e;\n"
          "      DD[(u64)t * R + r] = dcoef * inv * ez;\n"
@@ -1574,11 +1433,13 @@ std::string jit_source(const Formula& f, const Built& b, const Plan& p, int u_pr
          "    const double* __restrict__ gu, const float* __restrict__ DD, double* __restrict__ ga, double* __restrict__ gb) {\n"
          "  const u32 r = blockIdx.x * blockDim.x + threadIdx.x;\n"
          "  if (r >= R) return;\n"
+         "  // grid units throughout (the rows are exact integer sums; the b terms are rounded to the grid),\n"
+         "  // so these sums are exact like the sweep's atomics\n"
          "  for (u32 i = 0; i < n_bool; ++i) ga[(u64)i * R + r] += gu[(u64)i * R + r];\n"
          "  for (u32 t = 0; t < n_sa; ++t) {               // dE/db_j = sum over rows of G dd q_j (P:1326-1327)\n"
          "    const double g = gu[(u64)(nv + t) * R + r] * (double)DD[(u64)t * R + r];\n"
          "    const u32 at = satoms[t];\n"
-         "    for (u32 k = arow[at]; k < arow[at + 1]; ++k) gb[(u64)acol[k] * R + r] += g * (double)aval[k];\n"
+         "    for (u32 k = arow[at]; k < arow[at + 1]; ++k) gb[(u64)acol[k] * R + r] += rint(g * (double)aval[k]);\n"
          "  }\n"
          "}\n\n"
          "extern \"C\" __global__ void fsmt_kt_jit(u32 n_bool, u32 nv, u32 n_sa, const u32* __restrict__ satoms,\n"

@@ -14,9 +14,9 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libfsmt.so")
 
-OK, ERR_ARG, ERR_PARSE, ERR_UNSUPPORTED, ERR_STATE, ERR_NODE_BUDGET, ERR_OOM, ERR_CUDA, ERR_TIMEOUT = range(9)
+OK, ERR_ARG, ERR_PARSE, ERR_UNSUPPORTED, ERR_STATE, ERR_NODE_BUDGET, ERR_OOM, ERR_CUDA, ERR_TIMEOUT, ERR_RANGE = range(10)
 STATUS_NAMES = ["OK", "ERR_ARG", "ERR_PARSE", "ERR_UNSUPPORTED", "ERR_STATE", "ERR_NODE_BUDGET", "ERR_OOM",
-                "ERR_CUDA", "ERR_TIMEOUT"]
+                "ERR_CUDA", "ERR_TIMEOUT", "ERR_RANGE"]
 UNKNOWN, SAT = 0, 10
 HOST, DEVICE = 0, 1
 ROUND_SIGN, ROUND_PHILOX = 0, 1
@@ -27,7 +27,7 @@ class Dims(C.Structure):
     _fields_ = [("n_bool", C.c_uint32), ("n_real", C.c_uint32), ("n_atoms", C.c_uint32), ("n_cons", C.c_uint32),
                 ("n_templates", C.c_uint32), ("max_slots", C.c_uint32), ("max_nodes", C.c_uint32),
                 ("n_bounded", C.c_uint32), ("n_nodes", C.c_uint64), ("n_slot_refs", C.c_uint64),
-                ("n_halfspaces", C.c_uint32)]
+                ("n_halfspaces", C.c_uint32), ("n_slot_rows", C.c_uint32)]
 
 
 class Params(C.Structure):
@@ -80,7 +80,8 @@ _SIGS = {
     "fsmt_sweep": (_i32, [_vp, _f32, _u32]),
     "fsmt_get_sweep": (_i32, [_vp, _vp, _vp, _vp, _i32]),
     "fsmt_constraint_terms": (_i32, [_vp, _f32, _u32, _vp]),
-    "fsmt_update": (_i32, [_vp, _f32, _f32, _vp]),
+    "fsmt_update": (_i32, [_vp, _f32, _f32, _f32, _vp]),
+    "fsmt_step_sizes": (_i32, [_vp, _f32, C.POINTER(_f32), C.POINTER(_f32)]),
     "fsmt_stage_end": (_i32, [_vp, _u32, _vp]),
     "fsmt_get_model": (_i32, [_vp, _u32, _vp, _vp]),
     "fsmt_get_rounded": (_i32, [_vp, _vp, _i32]),
@@ -99,7 +100,9 @@ _SIGS = {
     "fsmt_eval": (_i32, [_vp, _u32, _vp, _vp, _f32, _vp, _u32, _vp, _vp, _vp, _i32]),
     "fsmt_jit_check": (_i32, [_vp, C.POINTER(C.c_size_t), C.c_char_p, C.c_size_t]),
     "fsmt_shard": (_i32, [_vp, _u32, _u32, _u32]),
-    "fsmt_bind_buffers": (_i32, [_vp, _vp, _vp, _vp, _vp]),
+    "fsmt_bind_buffers": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp]),
+    "fsmt_bind_slot_grads": (_i32, [_vp, _vp]),
+    "fsmt_sweep_finish": (_i32, [_vp]),
 }
 for _name, (_res, _args) in _SIGS.items():
     _fn = getattr(lib, _name)

@@ -52,6 +52,10 @@ class Solver:
         self.close()
 
     def bind_stream(self, stream_ptr: int | None):
+        """Launch on this cudaStream_t handle (int); 0 (torch's default stream) means the legacy
+        default stream (cudaStreamLegacy); None = the context's own non-blocking stream."""
+        if stream_ptr is not None and int(stream_ptr) == 0:
+            stream_ptr = 1                                   # cudaStreamLegacy
         self._check(N.lib.fsmt_bind_stream(self._h, stream_ptr))
 
     # ---------------------------------------------------------------- a0
@@ -157,6 +161,15 @@ class Solver:
     def sweep(self, kappa: float, stage_t: int = 1):
         self._check(N.lib.fsmt_sweep(self._h, kappa, stage_t))
 
+    def sweep_finish(self):
+        """fsmt_sweep_finish: constraint-sharded mode chains the all-reduced slot-table rows into the
+        gradients (no-op otherwise)."""
+        self._check(N.lib.fsmt_sweep_finish(self._h))
+
+    def bind_slot_grads(self, gu):
+        """Bind a device float64 [n_slot_rows][R] tensor as the slot-table gradient rows."""
+        self._check(N.lib.fsmt_bind_slot_grads(self._h, None if gu is None else gu.data_ptr()))
+
     def get_sweep(self):
         ga = np.empty((self.dims.n_bool, self.R), dtype=np.float64)
         gb = np.empty((self.dims.n_real, self.R), dtype=np.float64)
@@ -169,10 +182,17 @@ class Solver:
         self._check(N.lib.fsmt_constraint_terms(self._h, kappa, restart, E.ctypes.data))
         return E
 
-    def update(self, eta: float, eps: float, want_gm2: bool = False):
+    def update(self, eta: float, eps: float, want_gm2: bool = False, eta_b: float = 0.0):
+        """K3 with step eta for the Booleans and eta_b (<= 0: eta) for the reals (fsmt_update)."""
         gm2 = np.empty(self.R, dtype=np.float64) if want_gm2 else None
-        self._check(N.lib.fsmt_update(self._h, eta, eps, gm2.ctypes.data if want_gm2 else None))
+        self._check(N.lib.fsmt_update(self._h, eta, eta_b, eps, gm2.ctypes.data if want_gm2 else None))
         return gm2
+
+    def step_sizes(self, kappa: float):
+        """(eta_a, eta_b) of a stage at kappa under the params' eta / eta_mode (fsmt_step_sizes)."""
+        ea, eb = C.c_float(), C.c_float()
+        self._check(N.lib.fsmt_step_sizes(self._h, kappa, C.byref(ea), C.byref(eb)))
+        return ea.value, eb.value
 
     def stage_end(self, stage_t: int, copy: bool = True):
         """K4 + K5; returns unsat[R] (host) or None when copy=False (the result stays in the
@@ -251,10 +271,11 @@ class Solver:
         """mode 0: restart-sharded (all constraints); 1: constraint-sharded (partial sums)."""
         self._check(N.lib.fsmt_shard(self._h, rank, world, mode))
 
-    def bind_buffers(self, grad_a=None, grad_b=None, obj=None, unsat=None):
-        """Bind caller-owned device tensors (float64 [n_bool][R], [n_real][R], [R]; uint32/int32 [R])."""
+    def bind_buffers(self, grad_a=None, grad_b=None, obj=None, unsat=None, umax=None):
+        """Bind caller-owned device tensors (float64 [n_bool][R], [n_real][R], [R]; int32 [R] unsat and
+        umax); host tensors are rejected (FSMT_ERR_ARG)."""
         ptr = lambda t: None if t is None else t.data_ptr()
-        self._check(N.lib.fsmt_bind_buffers(self._h, ptr(grad_a), ptr(grad_b), ptr(obj), ptr(unsat)))
+        self._check(N.lib.fsmt_bind_buffers(self._h, ptr(grad_a), ptr(grad_b), ptr(obj), ptr(unsat), ptr(umax)))
 
     def jit_check(self):
         """NVRTC-compile the specialised sweep (no device needed): (cubin bytes, compiler log)."""

@@ -24,8 +24,11 @@ class FakeConstraintEngine:
         self.a = torch.randint(-8, 8, (NB, R), generator=g).double()
         self.b = torch.randint(-8, 8, (NR, R), generator=g).double()
 
-    def bind_buffers(self, ga, gb, obj, unsat):
-        self.ga, self.gb, self.obj, self.unsat = ga, gb, obj, unsat
+    def bind_buffers(self, ga, gb, obj, unsat, umax):
+        self.ga, self.gb, self.obj, self.unsat, self.umax = ga, gb, obj, unsat, umax
+
+    def step_sizes(self, kappa):
+        return 0.5, 0.25
 
     def sweep(self, kappa, t):
         self.ga.zero_()
@@ -36,15 +39,16 @@ class FakeConstraintEngine:
             self.gb[c % NR] += (c % 3) - 1.0
             self.obj += torch.floor(self.a[c % NB] / 4)
 
-    def update(self, eta, eps):
-        self.a -= 0.5 * self.ga
-        self.b -= 0.5 * self.gb
+    def update(self, eta, eps, eta_b=0.0):
+        self.a -= eta * self.ga
+        self.b -= eta_b * self.gb
 
     def stage_end(self, t, copy=False):
         self.unsat.zero_()
         for c in range(self.c0, self.c1):
             v = (c + t + torch.arange(self.R) + torch.floor(self.a[c % NB]).long()) % 5 != 0
             self.unsat += v.int()
+            self.umax.copy_(torch.maximum(self.umax, self.unsat))     # a local max the driver all-reduces
 
     def get_model(self, r):
         return np.sign(self.a[:, r].numpy() + 0.5).astype(np.int8), self.b[:, r].numpy().astype(np.float32)
@@ -54,7 +58,7 @@ def _worker(rank, world, port, out):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2603_22877_b200.dist import solve_constraint_sharded
-    res = solve_constraint_sharded(FakeConstraintEngine(), NB, NR, 16, 2, 5, [1.0, 2.0, 3.0, 4.0], 0.5, 0.0)
+    res = solve_constraint_sharded(FakeConstraintEngine(), NB, NR, 16, 2, 5, [1.0, 2.0, 3.0, 4.0], 0.0)
     out[(world, rank)] = (res.verdict, res.winner_restart, res.winner_stage, res.best_unsat, res.x.tolist(),
                           res.y.tolist())
     dist.destroy_process_group()

@@ -109,7 +109,7 @@ def test_dist_drivers_world1_reproduce_solve(mode, nccl_world1):
     if mode == "restart":
         out = D.solve_restart_sharded(s, d["n_bool"], d["n_real"], 256, 20, 11, kappas)
     else:
-        out = D.solve_constraint_sharded(s, d["n_bool"], d["n_real"], 256, 20, 11, kappas, 0.05, 1e-2)
+        out = D.solve_constraint_sharded(s, d["n_bool"], d["n_real"], 256, 20, 11, kappas, 1e-2)
     assert out.verdict == res.verdict
     assert (out.best_unsat, out.winner_stage, out.winner_restart) == (
         res.stats["best_unsat"], res.stats["winner_stage"], res.stats["winner_restart"])

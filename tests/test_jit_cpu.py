@@ -1,6 +1,6 @@
 """The JIT-specialised sweep compiles with NVRTC for sm_100a here (no GPU needed), without spills:
 the generic module of fsmt_build_xbdd and the modules fsmt_prepare(R) builds (restart count
-compiled in, U prefetch, and the opt-in two-restarts-per-lane f32x2 mode)."""
+compiled in, U prefetch)."""
 import os
 import re
 
@@ -9,8 +9,7 @@ import pytest
 import fsmt_gen
 from paper_2603_22877_b200 import Solver
 
-VARIANTS = [{}, {"FSMT_JIT_CHECK_RC": "1024"}, {"FSMT_JIT_CHECK_RC": "1024", "FSMT_JIT_LANE2": "1"},
-            {"FSMT_JIT_CHECK_RC": "1000000", "FSMT_JIT_UPF": "3"}]
+VARIANTS = [{}, {"FSMT_JIT_CHECK_RC": "1024"}, {"FSMT_JIT_CHECK_RC": "1000000", "FSMT_JIT_UPF": "3"}]
 
 
 @pytest.mark.parametrize("env", VARIANTS, ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()) or "generic")
@@ -35,7 +34,7 @@ def test_nvrtc_compiles_specialised_sweep(name, env):
     assert m and all(int(x) == 0 for x in m), log[-2000:]
     if "FSMT_JIT_CHECK_RC" in env:
         assert src.startswith("#define FSMT_RC " + env["FSMT_JIT_CHECK_RC"] + "u")
-        assert ("#define RPL 2" in src) == ("FSMT_JIT_LANE2" in env)
+    assert "fsmt_q(" in src and "fsmt_w(" in src          # on-grid flushes and shifted ERWA weights
 
 
 @pytest.mark.parametrize("name,vmax", [("cfg4", 54), ("cfg3", 40)])
