@@ -10,8 +10,9 @@ Configs (DESIGN.md §5 input recipe):
   cfg2  random hybrid 100 Booleans / 100 reals / 100 atoms / 2,000 card/nae/xor constraints
   cfg3  scheduling n_w = 16, n_j = 448: 2,240 vars / ~114,688 constraints (reading R23)
   cfg4  placement n_m = 32, n_l = 4, 1,184 modules: 10,656 vars / 705,072 constraints (R24-R26)
+  randN the paper's random hybrid family at n = 100..1000 (reading R36)
 """
 from .instances import (  # noqa: F401
-    Instance, cfg1, random_hybrid, scheduling, placement, config, CONFIGS,
+    Instance, cfg1, random_hybrid, paper_random, scheduling, placement, config, CONFIGS,
 )
 from .points import random_points  # noqa: F401

@@ -121,6 +121,22 @@ def random_hybrid(n_bool=100, n_real=100, n_atoms=100, n_card=952, n_nae=952, n_
                     {"seed": seed})
 
 
+def paper_random(n: int, seed: int = 0) -> Instance:
+    """The paper's random hybrid family (Results "random benchmark"): n
+    Booleans, n reals, n LRA atoms; m_card = m_nae = n/5 and m_xor = n/50 constraints of lengths
+    l_card = l_nae = min(50, n/5) and l_xor = 50, n in {100, ..., 1000}.  Readings (DESIGN.md §3
+    R36): the card threshold is k = l/2 ("sum l_i <= k", k unstated); atoms and literals
+    as cfg2 (3-real atoms; literals drawn from the 2n-slot pool with random polarity,
+    planted-SAT repair)."""
+    assert n % 50 == 0 and n >= 100
+    l = min(50, n // 5)
+    inst = random_hybrid(n_bool=n, n_real=n, n_atoms=n, n_card=n // 5, n_nae=n // 5, n_xor=n // 50,
+                         l_card=l, l_nae=l, l_xor=50, k_card=l // 2, seed=1000 + n + 7919 * seed)
+    inst.name = f"rand{n}"
+    inst.meta.update({"n": n, "l": l, "k_card": l // 2, "family_seed": seed})
+    return inst
+
+
 # ----------------------------------------------------------------------------- cfg3 scheduling
 
 
@@ -322,3 +338,5 @@ CONFIGS = {
     "cfg2s": lambda: random_hybrid(n_bool=20, n_real=20, n_atoms=20, n_card=30, n_nae=30, n_xor=6,
                                    l_card=8, l_nae=8, l_xor=12, seed=12),
 }
+# the paper's random family at every n: "rand100" ... "rand1000"
+CONFIGS.update({f"rand{n}": (lambda n=n: paper_random(n)) for n in range(100, 1001, 100)})

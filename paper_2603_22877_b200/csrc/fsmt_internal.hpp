@@ -130,6 +130,9 @@ struct KClass {
     bool sym = false;
     uint32_t sym_kind = 0, sym_L = 0, sym_k = 0;
     Template stmpl;
+    // count class (CARD only): the sweep evaluates the constraint by its count distribution
+    // (O(L^2)) instead of the xBDD's messages, and K5 counts true literals
+    bool count = false;
     // K5 record folding: every constraint of the class has the same coefficients and strictness
     // at each atom slot (kept here, emitted as exact fp64 literals); the K5 record then holds only
     // the atoms' fp64 right-hand sides

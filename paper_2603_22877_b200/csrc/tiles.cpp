@@ -30,6 +30,8 @@ constexpr uint32_t kJitMaxNodes = 96;
 constexpr uint32_t kJitMaxRefs = 64;
 constexpr uint32_t kJitMaxClasses = 32;
 constexpr uint64_t kJitMinCons = 32;      // specialise only classes with enough constraints
+constexpr uint64_t kJitMinConsSym = 1;    // symmetric classes: few (kind, L, k) classes, each worth specialising
+constexpr uint32_t kCountMaxL = 64;       // count classes: q[0..L] in registers
 constexpr uint32_t kJitMaxNodesSym = 160; // symmetric classes (messages only, no inline atom math)
 constexpr uint32_t kSymMark = 0xFFFFFFF0u;
 }  // namespace
@@ -94,7 +96,13 @@ Plan make_plan(const Formula& f, const Built& b, bool enable_jit) {
                 kc.words = 1 + (Ls + 1) / 2 + (Ls + 31) / 32;   // weight, slot refs, sign bits
                 kc.stride4 = (kc.words + 3) / 4;
                 kc.vstride4 = 1;
-                kc.jit = enable_jit && kc.stmpl.nodes.size() <= kJitMaxNodesSym && Ls <= kJitMaxRefs && kc.stmpl.root >= 0;
+                // CARD over many literals (CARD(50, 25): 650 nodes) cannot keep its messages in registers:
+                // its count distribution q[0..L] can (FSMT_JIT_COUNT=1: every CARD class, =0: none)
+                const char* ce = getenv("FSMT_JIT_COUNT");
+                const bool big = kc.stmpl.nodes.size() > kJitMaxNodesSym;
+                kc.count = kind == K_CARD && Ls <= kCountMaxL && kc.stmpl.root >= 0 && kk < Ls &&
+                           (ce ? ce[0] == '1' : big);
+                kc.jit = enable_jit && (!big || kc.count) && Ls <= kJitMaxRefs && kc.stmpl.root >= 0;
                 kc.n_cons = 0;
                 p.kclasses.push_back(kc);
             } else {
@@ -156,7 +164,8 @@ Plan make_plan(const Formula& f, const Built& b, bool enable_jit) {
     });
     uint32_t njit = 0;
     for (uint32_t k : idx)
-        if (p.kclasses[k].jit && p.kclasses[k].n_cons < kJitMinCons) p.kclasses[k].jit = false;
+        if (p.kclasses[k].jit && p.kclasses[k].n_cons < (p.kclasses[k].sym ? kJitMinConsSym : kJitMinCons))
+            p.kclasses[k].jit = false;
     for (uint32_t k : idx)
         if (p.kclasses[k].jit) {
             if (njit < kJitMaxClasses) ++njit;
@@ -928,13 +937,14 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
     //            dCOP/dpt_s += m[n] d (pt_s' - pf_s'), dCOP/dpt_s' += m[n] d (pt_s - pf_s)
     // which is Alg.F/Alg.B over n, h, l regrouped (P_X + P_Y = 1).  For two Boolean slots
     // P_X = (1 + v_s v_s')/2 and pt - pf = -v.
-    const size_t nn = t.nodes.size();
+    // (A count class has no node passes: nn = 0 and the count DP below sets pT and G.)
+    const size_t nn = K.count ? 0 : t.nodes.size();
     std::vector<int> indeg(nn, 0);
     for (size_t v = 0; v < nn; ++v) {
         if (t.nodes[v].hi >= 0) ++indeg[t.nodes[v].hi];
         if (t.nodes[v].lo >= 0) ++indeg[t.nodes[v].lo];
     }
-    if (t.root >= 0) ++indeg[t.root];
+    if (t.root >= 0 && nn) ++indeg[t.root];
     std::vector<char> dhead(nn, 0), dskip(nn, 0);
     const char* dm_env = getenv("FSMT_JIT_DIAMOND");
     if (!(dm_env && dm_env[0] == '0')) {
@@ -1086,6 +1096,37 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
         else if (bl == "0.f") gfma(nd.level, mv, bh);
         else if (bh == "0.f") gfma(nd.level, mv, "(-" + bl + ")");
         else gfma(nd.level, mv, "(" + bh + " - " + bl + ")");
+    }
+    if (K.count) {
+        // CARD(L, k) by its count distribution ("O((n+k)^2)" for symmetric literals): with
+        // pt_s = P(literal s true), q_c = P(c of the literals true) by the DP q'_c = q_c pf + q_{c-1} pt
+        // (full q_0..q_L, in registers); COP = q_0 + ... + q_k.  dCOP/dpt_s = -r_k with r the
+        // distribution of the OTHER literals (moving mass from count k to k+1), taken out of q by the
+        // recursion q_c = r_c pf_s + r_{c-1} pt_s: upward (r_c = (q_c - pt_s r_{c-1}) / pf_s) when
+        // pt_s <= 1/2, downward from r_{L-1} = q_L / pt_s when pt_s > 1/2 -- the direction whose
+        // ratio pt/pf (pf/pt) is <= 1, so rounding errors do not grow.
+        const uint32_t L = (uint32_t)ns, kk = K.sym_k;
+        auto cq = [](uint32_t c) { return "cq" + std::to_string(c); };
+        o << "    float cq0 = pf0, cq1 = pt0;\n";
+        for (uint32_t i = 1; i < L; ++i) {
+            const std::string is = std::to_string(i);
+            o << "    float " << cq(i + 1) << " = " << cq(i) << " * pt" << is << ";\n";
+            for (uint32_t c = i; c >= 1; --c)
+                o << "    " << cq(c) << " = fmaf(" << cq(c - 1) << ", pt" << is << ", " << cq(c) << " * pf" << is << ");\n";
+            o << "    cq0 = cq0 * pf" << is << ";\n";
+        }
+        o << "    pT = cq0;";
+        for (uint32_t c = 1; c <= kk; ++c) o << " pT += " << cq(c) << ";";
+        o << "\n";
+        for (uint32_t s2 = 0; s2 < L; ++s2) {
+            const std::string ss = std::to_string(s2);
+            o << "    { const float rf = __frcp_rn(pf" << ss << "), rb = __frcp_rn(pt" << ss << ");\n"
+              << "      float cf = cq0 * rf;";
+            for (uint32_t c = 1; c <= kk; ++c) o << " cf = fmaf(-pt" << ss << ", cf, " << cq(c) << ") * rf;";
+            o << "\n      float cb = " << cq(L) << " * rb;";
+            for (uint32_t c = L - 1; c >= kk + 1; --c) o << " cb = fmaf(-pf" << ss << ", cb, " << cq(c) << ") * rb;";
+            o << "\n      G" << ss << " = pt" << ss << " <= 0.5f ? -cf : -cb; }\n";
+        }
     }
     auto gref = [&](size_t s) { return cmp ? "(-G" + std::to_string(s) + ")" : "G" + std::to_string(s); };
     o << "    const " << TY << " E = 1.f - 2.f * pT;\n";
@@ -1263,12 +1304,19 @@ void emit_verify_class(std::ostringstream& o, uint32_t kid, const KClass& K, con
         if (child >= 0) return "s" + std::to_string(child);
         return child == kTrue ? "true" : "false";
     };
-    for (size_t vv = t.nodes.size(); vv-- > 0;) {
-        const TNode& nd = t.nodes[vv];
-        o << "    const bool s" << vv << " = t" << nd.level << " ? " << sat(nd.hi) << " : " << sat(nd.lo) << ";\n";
+    if (K.count) {   // CARD(L, k): satisfied iff at most k literals are true
+        o << "    u32 nt = 0u;";
+        for (size_t s = 0; s < ns; ++s) o << " nt += (u32)t" << s << ";";
+        o << "\n    const u32 u = nt <= " << K.sym_k << "u ? 0u : 1u;\n";
+    } else {
+        for (size_t vv = t.nodes.size(); vv-- > 0;) {
+            const TNode& nd = t.nodes[vv];
+            o << "    const bool s" << vv << " = t" << nd.level << " ? " << sat(nd.hi) << " : " << sat(nd.lo) << ";\n";
+        }
+        o << "    const u32 u = " << (t.root >= 0 ? "s" + std::to_string(t.root) : std::string(t.root == kTrue ? "true" : "false"))
+          << " ? 0u : 1u;\n";
     }
-    o << "    const u32 u = " << (t.root >= 0 ? "s" + std::to_string(t.root) : std::string(t.root == kTrue ? "true" : "false"))
-      << " ? 0u : 1u;\n"
+    o << ""
          "    if (live) {\n"
          "      if (U && u) {   // U += u (R18): only violated constraints touch memory; > 255 is reported\n"
          "        unsigned char* cell = U + (u64)(T.cons_begin + c) * R + rr;\n"

@@ -294,9 +294,12 @@ Built build_xbdds(const Formula& f, uint64_t node_budget) {
         if (hit != shape_to_tid.end()) {
             tid = hit->second;
         } else {
-            Mgr m(node_budget);
+            // the manager also holds the intermediate diagrams of the construction (a CARD count DP
+            // builds far more than it keeps): its cap is a memory guard; the budget binds the result
+            Mgr m(std::max<uint64_t>(node_budget, 1u << 21));
             int root = c.kind == K_EXPR ? compile_expr(f, c.expr_root, sm, m) : compile_symmetric(f, c, sm, m);
             Template t = canonicalise(m, root, sm.kinds);
+            if (t.nodes.size() > node_budget) throw BuildError{"node budget exceeded", true};
             std::string key = template_key(t);
             auto kh = key_to_tid.find(key);
             if (kh != key_to_tid.end()) {
