@@ -975,7 +975,7 @@ static fsmt_status stage_end_impl(fsmt_ctx* ctx, uint32_t stage_t) {
         }
         CK(cudaMemsetAsync(S.unsat, 0, (size_t)S.R * 4, ctx->stream));
         verify_rounded(ctx, S, S.U);
-        CK(cudaMemcpyAsync(ctx->hflags, S.flags, 4, cudaMemcpyDeviceToHost, ctx->stream));   // read after the sync
+        if (!S.ds) CK(cudaMemcpyAsync(ctx->hflags, S.flags, 4, cudaMemcpyDeviceToHost, ctx->stream));   // read after the sync
     }
     CK(cudaMemsetAsync(S.frozen, 0, S.R, ctx->stream));
     fsmt_status s = check_launch(ctx);
@@ -1352,6 +1352,137 @@ fsmt_status fsmt_verify_batch(fsmt_ctx* ctx, uint32_t R, const int8_t* x, const 
     return FSMT_OK;
 }
 
+// The device-side solve loop (DESIGN.md §7 item 16): the whole Alg.2 loop as ONE
+// CUDA graph whose WHILE node runs a stage per iteration -- k_stage_begin (the stage's kappa, steps,
+// e_t from the schedule), S x {sweep, update}, stage end (K4, K5), k_stage_best (best model kept on
+// the device; continue while nothing is SAT and stages remain) -- so there is no host round trip per
+// stage.  The host relaunches the same executable graph every `chunk` stages only to honour the
+// time limit.  Same kernels and arithmetic as the host loop: identical results (tests).
+static fsmt_status solve_graph(fsmt_ctx* ctx, uint32_t steps, std::chrono::steady_clock::time_point t0, uint32_t& stages,
+                               uint32_t& best_unsat, uint32_t& best_stage, uint32_t& best_r, std::vector<int8_t>& bx,
+                               std::vector<float>& by, bool& timeout) {
+    const uint32_t T = (uint32_t)ctx->kappas.size();
+    const uint32_t nbool = ctx->F.n_bool, nreal = ctx->F.n_real;
+    std::vector<DevStage> sched(T);
+    for (uint32_t t = 1; t <= T; ++t) {
+        DevStage& d = sched[t - 1];
+        d = DevStage{};
+        d.kappa = ctx->kappas[t - 1];
+        fsmt_step_sizes(ctx, d.kappa, &d.eta_a, &d.eta_b);
+        d.t = t;
+        d.et_int = et_int_of(t, ctx->erwa_mode);
+        d.wfrac = wfrac_of(t, ctx->erwa_mode);
+        if ((uint32_t)d.et_int > kMaxStageExp)
+            return fail(ctx, FSMT_ERR_RANGE, "stage exponent e_t = (t - 2)/2 beyond the fp64 range of the ERWA weights (R18)");
+    }
+    const uint32_t chunk = ctx->time_limit > 0 ? 16u : T;
+    DevStage* d_sched = nullptr;
+    DevStage* d_ds = nullptr;
+    DevSolve* d_sv = nullptr;
+    int8_t* d_xk = nullptr;
+    float* d_yk = nullptr;
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t ex = nullptr;
+    fsmt_status st = FSMT_OK;
+    auto cleanup = [&]() {
+        if (ex) cudaGraphExecDestroy(ex);
+        if (g) cudaGraphDestroy(g);
+        for (void* p : {(void*)d_sched, (void*)d_ds, (void*)d_sv, (void*)d_xk, (void*)d_yk})
+            if (p) cudaFree(p);
+        ctx->S.ds = nullptr;
+    };
+#define CKG(call)                                                                                            \
+    do {                                                                                                     \
+        cudaError_t e_ = (call);                                                                             \
+        if (e_ != cudaSuccess) {                                                                             \
+            cudaStreamCaptureStatus cs_;                                                                     \
+            if (cudaStreamIsCapturing(ctx->stream, &cs_) == cudaSuccess && cs_ != cudaStreamCaptureStatusNone) { \
+                cudaGraph_t junk_ = nullptr;                                                                 \
+                cudaStreamEndCapture(ctx->stream, &junk_);                                                   \
+                if (junk_) cudaGraphDestroy(junk_);                                                          \
+            }                                                                                                \
+            cudaGetLastError();                                                                              \
+            cleanup();                                                                                       \
+            return fail(ctx, FSMT_ERR_CUDA, std::string(#call ": ") + cudaGetErrorString(e_));                \
+        }                                                                                                    \
+    } while (0)
+    CKG(cudaMalloc((void**)&d_sched, sizeof(DevStage) * std::max<uint32_t>(T, 1)));
+    CKG(cudaMalloc((void**)&d_ds, sizeof(DevStage)));
+    CKG(cudaMalloc((void**)&d_sv, sizeof(DevSolve)));
+    CKG(cudaMalloc((void**)&d_xk, std::max<uint32_t>(nbool, 1)));
+    CKG(cudaMalloc((void**)&d_yk, 4 * std::max<uint32_t>(nreal, 1)));
+    CKG(cudaMemcpyAsync(d_sched, sched.data(), sizeof(DevStage) * T, cudaMemcpyHostToDevice, ctx->stream));
+    DevSolve sv{};
+    sv.t = 1;
+    sv.t_end = std::min(T, chunk);
+    sv.best_unsat = UINT32_MAX;
+    CKG(cudaMemcpyAsync(d_sv, &sv, sizeof(sv), cudaMemcpyHostToDevice, ctx->stream));
+    CKG(cudaStreamSynchronize(ctx->stream));
+    // the graph: one WHILE node whose body is one stage
+    CKG(cudaGraphCreate(&g, 0));
+    cudaGraphConditionalHandle h;
+    CKG(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams cp{};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t node;
+    CKG(cudaGraphAddNode(&node, g, nullptr, 0, &cp));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    ctx->S.ds = d_ds;
+    const uint64_t l0 = ctx->launches;
+    CKG(cudaStreamBeginCaptureToGraph(ctx->stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    launch_stage_begin(d_sv, d_sched, d_ds, ctx->stream);
+    CKG(cudaMemsetAsync(ctx->S.frozen, 0, ctx->S.R, ctx->stream));
+    for (uint32_t k = 0; k < steps && !st; ++k) {
+        st = sweep_impl(ctx, 0.f, 1, nullptr, 0);              // kappa / e_t from the DevStage
+        if (!st) st = update_impl(ctx, 1.f, ctx->eps, 1.f);   // eta / eta_b from the DevStage
+    }
+    if (!st) st = stage_end_impl(ctx, 0);                      // Philox stage word from the DevStage
+    launch_stage_best(d_sv, ctx->S, nbool, nreal, d_xk, d_yk, h, ctx->stream);
+    cudaGraph_t cap = nullptr;
+    const cudaError_t ec = cudaStreamEndCapture(ctx->stream, &cap);
+    ctx->S.ds = nullptr;
+    const uint64_t per_stage = ctx->launches - l0 + 2;
+    ctx->launches = l0;
+    if (st) {
+        cleanup();
+        return st;
+    }
+    CKG(ec);
+    CKG(cudaGraphInstantiate(&ex, g, 0));
+    for (;;) {
+        CKG(cudaGraphLaunch(ex, ctx->stream));
+        CKG(cudaMemcpyAsync(&sv, d_sv, sizeof(sv), cudaMemcpyDeviceToHost, ctx->stream));
+        CKG(cudaMemcpyAsync(ctx->hflags, ctx->S.flags, 4, cudaMemcpyDeviceToHost, ctx->stream));
+        CKG(cudaStreamSynchronize(ctx->stream));
+        if ((st = check_flags(ctx))) break;
+        if (sv.best_unsat == 0 || sv.t > T) break;
+        const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if (ctx->time_limit > 0 && el > ctx->time_limit) {
+            timeout = true;
+            break;
+        }
+        const uint32_t t_end = std::min(T, sv.t + chunk - 1);
+        CKG(cudaMemcpyAsync(&d_sv->t_end, &t_end, 4, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    stages = sv.t - 1;
+    ctx->launches += per_stage * stages;
+    best_unsat = sv.best_unsat;
+    best_stage = sv.best_stage;
+    best_r = sv.best_r;
+    if (!st && best_unsat != UINT32_MAX) {
+        if (nbool) CKG(cudaMemcpyAsync(bx.data(), d_xk, nbool, cudaMemcpyDeviceToHost, ctx->stream));
+        if (nreal) CKG(cudaMemcpyAsync(by.data(), d_yk, 4 * (size_t)nreal, cudaMemcpyDeviceToHost, ctx->stream));
+        CKG(cudaStreamSynchronize(ctx->stream));
+        ctx->rounded = true;
+    }
+#undef CKG
+    cleanup();
+    return st;
+}
+
 fsmt_status fsmt_solve(fsmt_ctx* ctx, uint32_t restarts, uint32_t steps, uint64_t seed, fsmt_verdict* verdict,
                        int8_t* x_out, float* y_out, fsmt_stats* stats) {
     fsmt_status s = need(ctx, 2, "fsmt_solve");
@@ -1370,7 +1501,17 @@ fsmt_status fsmt_solve(fsmt_ctx* ctx, uint32_t restarts, uint32_t steps, uint64_
     uint32_t stages = 0, steps_run = 0;
     bool sat = false, timeout = false;
     fsmt_stats st{};
-    for (uint32_t t = 1; t <= ctx->kappas.size(); ++t) {
+    // the device-side loop (one CUDA graph, no per-stage host round trip) unless FSMT_SOLVE_GRAPH=0,
+    // per-kernel timing is on (events) or the stage graph of FSMT_GRAPH is requested
+    const char* sg = getenv("FSMT_SOLVE_GRAPH");
+    const char* og = getenv("FSMT_GRAPH");
+    const bool graph = !(sg && sg[0] == '0') && !ctx->timing && !(og && og[0] == '1');
+    if (graph) {
+        if ((s = solve_graph(ctx, steps, t0, stages, best_unsat, best_stage, best_r, bx, by, timeout))) return s;
+        steps_run = stages * steps;
+        sat = best_unsat == 0;
+    }
+    for (uint32_t t = 1; !graph && t <= ctx->kappas.size(); ++t) {
         const float kappa = ctx->kappas[t - 1];
         if ((s = fsmt_run_stage(ctx, t, kappa, steps, unsat.data(), nullptr))) return s;
         steps_run += steps;

@@ -90,6 +90,7 @@ __global__ void k0_init(DevFormula F, DevState S, uint64_t seed, uint32_t off) {
 __global__ void __launch_bounds__(256) k1_sweep(DevFormula F, DevState S, float kappa,
                                                 double* __restrict__ terms, uint32_t terms_r, int smax, int nmax) {
     extern __shared__ float smem[];
+    if (S.ds) kappa = S.ds->kappa;                               // device-side solve loop (DevStage)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t R = S.R;
     const uint32_t rtiles = (R + 31) / 32;
@@ -193,6 +194,11 @@ __global__ void __launch_bounds__(256) k1_sweep(DevFormula F, DevState S, float 
 // G = ceil(log2 B_g) - 48, keeps every sum below 2^50 grid units (exact integers in fp64).
 __global__ void k1_prologue(DevFormula F, DevState S, float kappa, int et_int, float wfrac, double* __restrict__ gu,
                             uint64_t gu_rows) {
+    if (S.ds) {                                                   // device-side solve loop (DevStage)
+        kappa = S.ds->kappa;
+        et_int = S.ds->et_int;
+        wfrac = S.ds->wfrac;
+    }
     const uint64_t R = S.R;
     const uint64_t nb = (uint64_t)F.n_bool * R, nr = (uint64_t)F.n_real * R, ng = gu ? gu_rows * R : 0;
     const uint64_t n = nb + nr + R + ng;
@@ -250,6 +256,7 @@ __device__ __forceinline__ float step_value(float x, double g, float eta, float 
 // candidate b' of the projected step (R33): halfspace variables unclamped (Dykstra projects
 // them), the others clamped to their interval (their exact projection)
 __global__ void k3_cand(DevFormula F, DevState S, float eta_b) {
+    if (S.ds) eta_b = S.ds->eta_b;
     const uint64_t n = (uint64_t)F.n_real * S.R;
     for (uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t j = (uint32_t)(idx / S.R);
@@ -307,6 +314,7 @@ __global__ void __launch_bounds__(128) k_dykstra(DevFormula F, DevState S, float
 }
 
 __global__ void k3_norm(DevFormula F, DevState S, float eta, float eta_b, uint32_t vpp) {
+    if (S.ds) { eta = S.ds->eta_a; eta_b = S.ds->eta_b; }
     const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= S.R) return;
     const uint32_t part = blockIdx.y;
@@ -357,6 +365,7 @@ __global__ void k3_final(DevState S, uint32_t n_parts, float eps) {
 }
 
 __global__ void k3_apply(DevFormula F, DevState S, float eta, float eta_b) {
+    if (S.ds) { eta = S.ds->eta_a; eta_b = S.ds->eta_b; }
     const uint64_t n = (uint64_t)(F.n_bool + F.n_real) * S.R;
     for (uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t v = (uint32_t)(idx / S.R), r = (uint32_t)(idx % S.R);
@@ -376,6 +385,7 @@ __global__ void k3_apply(DevFormula F, DevState S, float eta, float eta_b) {
 // ---------------------------------------------------------------------------------------- K4
 
 __global__ void k4_round(DevFormula F, DevState S, uint32_t rounding, uint64_t seed, uint32_t off, uint32_t stage) {
+    if (S.ds) stage += S.ds->t;            // device-side solve loop: the launch passes only the R34 draw (m << 16)
     const uint64_t n = (uint64_t)F.n_bool * S.R;
     for (uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t i = (uint32_t)(idx / S.R), r = (uint32_t)(idx % S.R);
@@ -498,13 +508,14 @@ void launch_sweep_jit(cudaKernel_t k, const DevFormula& F, const DevState& S, co
     const size_t smem = (size_t)kVmax * 32 * 4 + (size_t)kVtot * 4;
     if (smem > 48 * 1024) cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     uint32_t n_tiles = T.n_tiles, R = S.R, n_bool = F.n_bool;
+    const float* kdev = S.ds ? &S.ds->kappa : nullptr;
     const uint8_t* U = S.U;
     const float* PT = D ? D->PT : nullptr;
     const float* PF = D ? D->PF : nullptr;
     double* GU = D ? D->GU : nullptr;
     void* args[] = {(void*)&T.tiles, &n_tiles, (void*)&T.recs, (void*)&T.tile_vars, (void*)&S.a, (void*)&S.b,
                     (void*)&S.ga, (void*)&S.gb, (void*)&U, (void*)&S.obj, &R, &n_bool, &kappa,
-                    &terms, &terms_r, (void*)&F.orig, (void*)&PT, (void*)&PF, (void*)&GU, (void*)&S.fx};
+                    &terms, &terms_r, (void*)&F.orig, (void*)&PT, (void*)&PF, (void*)&GU, (void*)&S.fx, (void*)&kdev};
     cudaLaunchKernel((const void*)k, dim3(blocks), dim3(32), args, smem, st);
 }
 
@@ -512,9 +523,10 @@ void launch_slot_prob(cudaKernel_t k, const DevFormula& F, const DevState& S, co
     uint32_t n_bool = F.n_bool, nv = D.nv, n_sa = D.n_sa, R = S.R;
     const uint64_t n = (uint64_t)(n_bool + n_sa) * R;
     if (!n) return;
+    const float* kdev = S.ds ? &S.ds->kappa : nullptr;
     void* args[] = {&n_bool, &nv, &n_sa, (void*)&D.atoms, (void*)&S.a, (void*)&S.b, (void*)&F.atom_rowptr,
                     (void*)&F.atom_col, (void*)&F.atom_val, (void*)&F.atom_rhs, (void*)&F.atom_invnorm, &R, &kappa,
-                    (void*)&D.PT, (void*)&D.PF, (void*)&D.DD};
+                    (void*)&D.PT, (void*)&D.PF, (void*)&D.DD, (void*)&kdev};
     cudaLaunchKernel((const void*)k, dim3((unsigned)std::min<uint64_t>((n + 255) / 256, 148ull * 16)), dim3(256), args, 0, st);
 }
 
@@ -634,6 +646,67 @@ __global__ void k_copy_cols(uint64_t n, uint32_t R, const int8_t* __restrict__ x
                             const uint8_t* __restrict__ flag) {
     for (uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += (uint64_t)gridDim.x * blockDim.x)
         if (flag[idx % R]) xb[idx] = x[idx];
+}
+
+// ---------------------------------------------------------------- device-side solve loop (Alg.2)
+
+// Top of a stage: its parameters from the schedule (entry t - 1).
+__global__ void k_stage_begin(const DevSolve* __restrict__ sv, const DevStage* __restrict__ sched, DevStage* __restrict__ ds) {
+    if (threadIdx.x == 0) *ds = sched[sv->t - 1];
+}
+
+// End of a stage (Alg.2 P:526-528 and the lock-step winner rule of fsmt_solve): the restart with the
+// fewest violated constraints (the lowest index among equals); when it beats the best so far its
+// rounded model (x[:, r], y = b[:, r]) is kept; the loop continues while no restart is SAT and
+// stages remain in this launch.  One block.
+__global__ void __launch_bounds__(1024) k_stage_best(DevSolve* __restrict__ sv, DevState S, uint32_t n_bool, uint32_t n_real,
+                                                     int8_t* __restrict__ xk, float* __restrict__ yk,
+                                                     cudaGraphConditionalHandle h) {
+    __shared__ unsigned long long red[32];
+    __shared__ int improved;
+    unsigned long long key = ~0ull;
+    for (uint32_t r = threadIdx.x; r < S.R; r += blockDim.x) {
+        const unsigned long long k = ((unsigned long long)S.unsat[r] << 32) | r;
+        key = k < key ? k : key;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long v = __shfl_down_sync(0xffffffffu, key, o);
+        key = v < key ? v : key;
+    }
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = key;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (uint32_t w = 1; w < (blockDim.x + 31) / 32; ++w) key = red[w] < key ? red[w] : key;
+        red[0] = key;
+        const uint32_t u = (uint32_t)(key >> 32);
+        improved = u < sv->best_unsat;
+        if (improved) {
+            sv->best_unsat = u;
+            sv->best_stage = sv->t;
+            sv->best_r = (uint32_t)(key & 0xffffffffu);
+        }
+    }
+    __syncthreads();
+    if (improved) {
+        const uint32_t r = (uint32_t)(red[0] & 0xffffffffu);
+        for (uint32_t i = threadIdx.x; i < n_bool; i += blockDim.x) xk[i] = S.x[(size_t)i * S.R + r];
+        for (uint32_t j = threadIdx.x; j < n_real; j += blockDim.x) yk[j] = S.b[(size_t)j * S.R + r];
+    }
+    if (threadIdx.x == 0) {
+        const uint32_t t = sv->t + 1;
+        sv->t = t;
+        sv->done = sv->best_unsat == 0 || t > sv->t_end;
+        cudaGraphSetConditional(h, sv->done ? 0u : 1u);
+    }
+}
+
+void launch_stage_begin(const DevSolve* sv, const DevStage* sched, DevStage* ds, cudaStream_t st) {
+    k_stage_begin<<<1, 32, 0, st>>>(sv, sched, ds);
+}
+
+void launch_stage_best(DevSolve* sv, const DevState& S, uint32_t n_bool, uint32_t n_real, int8_t* xk, float* yk,
+                       cudaGraphConditionalHandle h, cudaStream_t st) {
+    k_stage_best<<<1, 1024, 0, st>>>(sv, S, n_bool, n_real, xk, yk, h);
 }
 
 void launch_keep_best(const DevFormula& F, const DevState& S, const uint32_t* unsat_m, uint32_t* unsat_best,

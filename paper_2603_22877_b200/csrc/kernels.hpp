@@ -23,6 +23,26 @@ struct FxScale {
 };
 constexpr int kWeightWindow = 24;   // fp32 weights stay <= 2^24 w_c 2^-wexp
 
+// The parameters of one annealing stage on the device (the device-side solve loop, DESIGN.md §7
+// item 16): k_stage_begin copies entry t-1 of the schedule here at the top of every stage, and the
+// stage's kernels read kappa / step sizes / stage number from it instead of their launch arguments
+// when DevState::ds is set.
+struct DevStage {
+    float kappa, eta_a, eta_b;
+    uint32_t t;                  // stage number (1-based): Philox rounding counter, ERWA e_t
+    int32_t et_int;              // floor(e_t) (R18)
+    float wfrac;                 // 2^frac(e_t)
+    uint32_t pad[2];
+};
+// Progress of the device-side solve loop (one per solve).
+struct DevSolve {
+    uint32_t t;                  // the stage the next loop iteration runs (1-based)
+    uint32_t t_end;              // last stage of this graph launch
+    uint32_t best_unsat, best_stage, best_r;
+    uint32_t done;               // 1: a restart is SAT, or t passed t_end
+    uint32_t pad[2];
+};
+
 struct DevNode {          // = TNode (8 bytes): level, hi, lo (-1 FALSE, -2 TRUE), pad
     uint16_t level;
     int16_t hi;
@@ -97,6 +117,7 @@ struct DevState {
     uint8_t* better;   // [R]
     uint32_t* umax;    // [R] max_c U[c][r] (K5 keeps it; the sweep's weight shift)
     FxScale* fx;       // [R] per-restart scales of the current sweep (k1_prologue)
+    const DevStage* ds = nullptr;   // device-side stage parameters (graph solve loop), or null
     double* gsc;       // [R] fx[r].gs (grid scale of the gradients, read by K3 / the output copy)
     uint32_t* flags;   // [4] bit 0 of flags[0]: an ERWA counter passed 255
 };
@@ -163,6 +184,11 @@ size_t project_smem_bytes(const DevFormula& F, uint32_t nnz);   // k_dykstra sha
 // unsat_best (or m == 0) copy x into x_best.
 void launch_keep_best(const DevFormula& F, const DevState& S, const uint32_t* unsat_m, uint32_t* unsat_best,
                       int8_t* x_best, uint8_t* flag, uint32_t m, cudaStream_t st);
+// Device-side solve loop (DESIGN.md §7 item 16): stage parameters from the schedule, and the
+// per-stage best-model / continue decision that drives the graph's WHILE node.
+void launch_stage_begin(const DevSolve* sv, const DevStage* sched, DevStage* ds, cudaStream_t st);
+void launch_stage_best(DevSolve* sv, const DevState& S, uint32_t n_bool, uint32_t n_real, int8_t* xk, float* yk,
+                       cudaGraphConditionalHandle h, cudaStream_t st);
 // K4: rounding (R17).
 void launch_round(const DevFormula& F, const DevState& S, uint32_t rounding, uint64_t seed, uint32_t restart_offset,
                   uint32_t stage, cudaStream_t st);

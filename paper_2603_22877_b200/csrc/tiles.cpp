@@ -627,6 +627,14 @@ bool jit_pair() {
     return !(e && e[0] == '0');
 }
 
+// FSMT_JIT_ORDER=1: the sweep's CTAs run restart-tile-major (all tiles of restarts 0..31, then
+// 32..63, ...) instead of tile-major (A/B: the concurrently touched gradient / state lines of one
+// restart tile fit the L2)
+bool k1_order() {
+    const char* e = getenv("FSMT_JIT_ORDER");
+    return e && e[0] == '1';
+}
+
 // FSMT_JIT_UPF=d: the sweep loads U[c][r] d constraints ahead (0: in the iteration, plain load).
 // Without the variable: g_upf (jit_source's argument; fsmt_prepare picks it from the size of U).
 thread_local int g_upf = 0;   // per thread: contexts may build concurrently
@@ -733,7 +741,7 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
          "    " << TY << "* __restrict__ accs, const float* __restrict__ ab, const float* __restrict__ bb,\n"
          "    double* __restrict__ ga, double* __restrict__ gb, const unsigned char* __restrict__ U,\n"
          "    u32 R, u32 R4, u64 rr, u32 r, bool live, u32 n_bool, float kq, float dcoef, int ebias,\n"
-         "    float gif, double& objacc,\n"
+         "    float gif, float& objacc,\n"
          "    double* __restrict__ terms, u32 terms_r, const u32* __restrict__ orig,\n"
          "    const float* __restrict__ PTl, const float* __restrict__ PFl, double* __restrict__ gu) {\n"
          "  const bool hasU = !DBG || U != nullptr, hasT = DBG && terms != nullptr;\n";
@@ -1130,7 +1138,10 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
     }
     auto gref = [&](size_t s) { return cmp ? "(-G" + std::to_string(s) + ")" : "G" + std::to_string(s); };
     o << "    const " << TY << " E = 1.f - 2.f * pT;\n";
-    o << "    objacc += (double)w * (double)E;\n"
+    // the objective's first level in fp32 over the tile's <= 64 constraints, flushed once per tile into
+    // the fp64 objective (two-level accumulation, R28: the per-tile fp32 sum of <= 64 terms adds
+    // <= 64 x 2^-24 relative; across tiles the sum is exact on the objective's grid)
+    o << "    objacc = fmaf(w, E, objacc);\n"
          "    if (hasT && live && r == terms_r) terms[orig[T.cons_begin + c]] = (double)E;\n";
     // gradient terms per target reference (aliases fold into their target: one read-modify-write)
     std::vector<std::vector<std::pair<std::string, std::string>>> terms_of(nr);
@@ -1358,16 +1369,19 @@ std::string jit_source(const Formula& f, const Built& b, const Plan& p, int u_pr
          "    double* __restrict__ obj, u32 R, u32 n_bool, float kappa,\n"
          "    double* __restrict__ terms, u32 terms_r, const u32* __restrict__ orig,\n"
          "    const float* __restrict__ PT, const float* __restrict__ PF, double* __restrict__ gu,\n"
-         "    const FxScale* __restrict__ fxs) {\n"
+         "    const FxScale* __restrict__ fxs, const float* __restrict__ kdev) {\n"
          "  FSMT_SPECIALISE_R\n"
+         "  if (kdev) kappa = *kdev;   // the device-side solve loop's stage kappa (DevStage)\n"
          "  extern __shared__ float smem[];\n"
          "  const int lane = threadIdx.x & 31;\n"
          "  float* acc = smem;                                    // stream-variable rows\n"
          "  u32* vs = (u32*)(smem + VMAX * 32);                   // stream then run variable ids\n"
          "  const u32 rtiles = (R + 31) / 32;\n"
-         "  const u64 ti = blockIdx.x / rtiles;\n"
-         "  const u32 rt = (u32)(blockIdx.x % rtiles);\n"
-         "  if (ti >= n_tiles) return;\n"
+      << (k1_order() ? "  const u64 ti = blockIdx.x % n_tiles;                 // restart-tile-major (FSMT_JIT_ORDER=1)\n"
+                       "  const u32 rt = (u32)(blockIdx.x / n_tiles);\n"
+                     : "  const u64 ti = blockIdx.x / rtiles;                  // tile-major: a tile's restart tiles together\n"
+                       "  const u32 rt = (u32)(blockIdx.x % rtiles);\n")
+      << "  if (ti >= n_tiles) return;\n"
          "  const TileDesc T = tiles[ti];\n"
          "  const u32 n_s = T.n_vars & 0xffffu, n_v = n_s + (T.n_vars >> 16);\n"
          "  const u32 r = rt * 32 + lane;\n"
@@ -1381,7 +1395,7 @@ std::string jit_source(const Formula& f, const Built& b, const Plan& p, int u_pr
          "  const float dcoef = kappa * 0.79788456080286536f;\n"
          "  const float gif = fxs[rr].gif;\n"
          "  const int ebias = fxs[rr].ebias;\n"
-         "  double objacc = 0.0;\n"
+         "  float objacc = 0.f;\n"
          "  const uint4* rp = recs + T.rec_off;\n"
          "  // the lane's column bases: element (v, restart rr) of a [var][R] array at base + v * 4R bytes\n"
          "  const u32 R4 = R * 4u;\n"
@@ -1406,7 +1420,7 @@ std::string jit_source(const Formula& f, const Built& b, const Plan& p, int u_pr
          "    if (symt) atomicAdd(gu + (u64)g * R + r, v);\n"
          "    else if (g < n_bool) atomicAdd(ga + (u64)g * R + r, v); else atomicAdd(gb + (u64)(g - n_bool) * R + r, v);\n"
          "  }\n"
-         "  atomicAdd(obj + r, rint(objacc * fxs[r].oi) * fxs[r].os);   // on the objective's grid, true units\n"
+         "  atomicAdd(obj + r, rint((double)objacc * fxs[r].oi) * fxs[r].os);   // on the objective's grid, true units\n"
          "}\n\n";
     }
     // K5: exact verification of the rounded models + ERWA counters over the same tiles
@@ -1455,7 +1469,8 @@ std::string jit_source(const Formula& f, const Built& b, const Plan& p, int u_pr
          "    const float* __restrict__ a, const float* __restrict__ b, const u32* __restrict__ arow,\n"
          "    const u32* __restrict__ acol, const float* __restrict__ aval, const float* __restrict__ arhs,\n"
          "    const float* __restrict__ ainv, u32 R, float kappa, float* __restrict__ PT, float* __restrict__ PF,\n"
-         "    float* __restrict__ DD) {\n"
+         "    float* __restrict__ DD, const float* __restrict__ kdev) {\n"
+         "  if (kdev) kappa = *kdev;\n"
          "  const u64 n = (u64)(n_bool + n_sa) * R;\n"
          "  const float kq = kappa * 0.70710678118654752f, dcoef = kappa * 0.79788456080286536f;\n"
          "  for (u64 idx = (u64)blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += (u64)gridDim.x * blockDim.x) {\n"

@@ -14,7 +14,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def main():
     variants = sys.argv[1:] or [""]
-    extra = os.environ.get("AB_ARGS", "--steps 5 --warmup 3 --no-e2e --no-cpu-baseline").split()
+    extra = os.environ.get("AB_ARGS", "--steps 5 --warmup 3 --no-e2e --no-cpu-baseline --no-tts").split()
     for v in variants:
         env = dict(os.environ)
         for kv in v.split():

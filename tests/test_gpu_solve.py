@@ -221,3 +221,44 @@ def test_graph_then_prepare_reproduces_solve():
         os.environ.pop("FSMT_GRAPH", None)
     assert r1.verdict == r2.verdict == r3.verdict
     assert r1.stats["best_unsat"] == r2.stats["best_unsat"] == r3.stats["best_unsat"]
+
+
+@pytest.mark.parametrize("name,params", [
+    ("cfg1", dict(eta=0.1)),
+    ("cfg4s", dict(eta=0.05, rounding=1, kappas=[0.5, 1.0, 2.0, 4.0, 8.0])),
+    ("cfg4s", dict(eta=0.05, rounding=1, n_roundings=4, kappas=[0.5, 1.0, 2.0, 4.0])),
+    ("cfg3s", dict(eta=0.02, erwa_mode=1, eta_mode=3, kappas=[1.0, 3.0, 9.0, 27.0, 81.0] * 3)),
+    ("cfg2s", dict(eta=0.05, kappas=[0.5, 1.0, 2.0] * 4)),
+])
+def test_device_side_solve_loop_matches_host_loop(name, params):
+    """fsmt_solve's device-side loop (one CUDA graph with a WHILE node per stage, DESIGN.md §7 item 16)
+    runs the host loop's kernels with the same arithmetic: verdict, winner, stages, model bit-identical."""
+    inst = fsmt_gen.config(name)
+    out = []
+    for g in ("0", "1"):
+        os.environ["FSMT_SOLVE_GRAPH"] = g
+        try:
+            s = make(inst.text)
+            s.set_params(**params)
+            res = s.solve(96, 6, 5)
+            out.append(res)
+        finally:
+            os.environ.pop("FSMT_SOLVE_GRAPH", None)
+    h, d = out
+    for k in ("best_unsat", "winner_stage", "winner_restart", "stages_run", "steps_run", "host_verified"):
+        assert h.stats[k] == d.stats[k], (k, h.stats[k], d.stats[k])
+    assert h.verdict == d.verdict
+    assert np.array_equal(h.x, d.x) and np.array_equal(h.y, d.y)
+
+
+def test_device_side_solve_loop_time_limit():
+    """With a time limit the device-side loop returns to the host every 16 stages; an exhausted
+    limit gives FSMT_ERR_TIMEOUT with the best model so far (soundness unchanged)."""
+    inst = fsmt_gen.config("cfg3s")
+    f = hsmt.parse(inst.text)
+    s = make(inst.text)
+    s.set_params(eta=0.001, kappas=[0.01] * 400, time_limit_s=1e-6)
+    res = s.solve(64, 2, 1)
+    assert res.stats["timeout"] and res.stats["stages_run"] == 16
+    _, sat = semantics.eval_formula(f, res.x, res.y)
+    assert sum(not v for v in sat) == res.stats["best_unsat"]
