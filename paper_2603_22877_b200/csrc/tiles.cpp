@@ -627,14 +627,6 @@ bool jit_pair() {
     return !(e && e[0] == '0');
 }
 
-// FSMT_JIT_ORDER=1: the sweep's CTAs run restart-tile-major (all tiles of restarts 0..31, then
-// 32..63, ...) instead of tile-major (A/B: the concurrently touched gradient / state lines of one
-// restart tile fit the L2)
-bool k1_order() {
-    const char* e = getenv("FSMT_JIT_ORDER");
-    return e && e[0] == '1';
-}
-
 // FSMT_JIT_UPF=d: the sweep loads U[c][r] d constraints ahead (0: in the iteration, plain load).
 // Without the variable: g_upf (jit_source's argument; fsmt_prepare picks it from the size of U).
 thread_local int g_upf = 0;   // per thread: contexts may build concurrently
@@ -801,11 +793,13 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
         for (int k = 0; k < upf; ++k)
             o << "  u32 un" << k << " = (hasU && " << k << "u < T.n_cons) ? (u32)" << uld << "(" << ucast << "(Up + (u64)" << k << "u * R)) : 0u;\n";
     }
-    // the constraint loop unrolled twice (FSMT_JIT_UNROLL overrides; cfg3 0.884 ->
-    // 0.849 ms, cfg4 8.36 -> 8.33 ms; 4 is slower on cfg4)
+    // the constraint loop unrolled twice for small classes (FSMT_JIT_UNROLL overrides; DESIGN.md §9:
+    // round 1 cfg3 0.884 -> 0.849 ms, cfg4 8.36 -> 8.33 ms; 4 is slower on cfg4)
     {
+        // round 2: with the exact flush, the 22-reference placement class is faster not unrolled (cfg4
+        // 8.08 vs 8.42 ms) while the 12-reference scheduling class keeps unroll 2 (cfg3 0.774 vs 0.864 ms)
         const char* ur = getenv("FSMT_JIT_UNROLL");
-        o << "#pragma unroll " << (ur ? std::max(1, atoi(ur)) : 2) << "\n";
+        o << "#pragma unroll " << (ur ? std::max(1, atoi(ur)) : (K.n_refs <= 16 ? 2 : 1)) << "\n";
     }
     o << "  for (u32 c = 0; c < T.n_cons; ++c, rp += " << K.stride4 << ") {\n";
     for (uint32_t q = 0; q < K.stride4; ++q) o << "    const uint4 q" << q << " = __ldg(rp + " << q << ");\n";
@@ -1377,11 +1371,9 @@ std::string jit_source(const Formula& f, const Built& b, const Plan& p, int u_pr
          "  float* acc = smem;                                    // stream-variable rows\n"
          "  u32* vs = (u32*)(smem + VMAX * 32);                   // stream then run variable ids\n"
          "  const u32 rtiles = (R + 31) / 32;\n"
-      << (k1_order() ? "  const u64 ti = blockIdx.x % n_tiles;                 // restart-tile-major (FSMT_JIT_ORDER=1)\n"
-                       "  const u32 rt = (u32)(blockIdx.x / n_tiles);\n"
-                     : "  const u64 ti = blockIdx.x / rtiles;                  // tile-major: a tile's restart tiles together\n"
-                       "  const u32 rt = (u32)(blockIdx.x % rtiles);\n")
-      << "  if (ti >= n_tiles) return;\n"
+      << "  const u64 ti = blockIdx.x / rtiles;                  // tile-major: a tile's restart tiles together\n"
+         "  const u32 rt = (u32)(blockIdx.x % rtiles);\n"
+         "  if (ti >= n_tiles) return;\n"
          "  const TileDesc T = tiles[ti];\n"
          "  const u32 n_s = T.n_vars & 0xffffu, n_v = n_s + (T.n_vars >> 16);\n"
          "  const u32 r = rt * 32 + lane;\n"
