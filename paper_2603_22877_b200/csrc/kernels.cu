@@ -535,7 +535,9 @@ void launch_slot_chain(cudaKernel_t k, const DevFormula& F, const DevState& S, c
     if (!R) return;
     void* args[] = {&n_bool, &nv, &n_sa, (void*)&D.atoms, (void*)&F.atom_rowptr, (void*)&F.atom_col, (void*)&F.atom_val,
                     &R, (void*)&D.GU, (void*)&D.DD, (void*)&S.ga, (void*)&S.gb};
-    cudaLaunchKernel((const void*)k, dim3((R + 63) / 64), dim3(64), args, 0, st);
+    const uint64_t n = ((uint64_t)n_bool + n_sa) * R;
+    cudaLaunchKernel((const void*)k, dim3((unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, 148ull * 16))), dim3(256),
+                     args, 0, st);
 }
 
 void launch_slot_truth(cudaKernel_t k, const DevFormula& F, const DevState& S, const DevSlots& D, const int8_t* x,
@@ -594,11 +596,16 @@ void launch_sweep(const DevFormula& F, const DevState& S, float kappa, double* t
                                                          std::max<int>(1, F.max_slots), std::max<int>(1, F.max_nodes));
 }
 
-// variables per part of the gradient-mapping norm: 64 for many restarts (one thread per restart
-// and part is enough parallelism), fewer for small R so the grid still fills the GPU
-static uint32_t vars_per_part(uint32_t R) { return R >= 512 ? (uint32_t)kVarsPerPart : (R >= 128 ? 16u : 4u); }
+// variables per part of the gradient-mapping norm: at most 64, and few enough that the grid of
+// (restart blocks x parts) has >= 8 blocks per SM (cfg4 at R = 1,024: 72 -> 64; cfg2: 2)
+static uint32_t vars_per_part(const DevFormula& F, uint32_t R) {
+    const uint32_t nv = F.n_bool + F.n_real;
+    const uint32_t rblocks = R >= 128 ? (R + 127) / 128 : 1;
+    const uint32_t want_parts = std::max<uint32_t>(1, (148u * 8u + rblocks - 1) / rblocks);
+    return std::max<uint32_t>(1, std::min<uint32_t>((uint32_t)kVarsPerPart, (nv + want_parts - 1) / want_parts));
+}
 int update_parts(const DevFormula& F, uint32_t R) {
-    const uint32_t vpp = vars_per_part(R);
+    const uint32_t vpp = vars_per_part(F, R);
     return (int)((F.n_bool + F.n_real + vpp - 1) / vpp);
 }
 
@@ -616,9 +623,9 @@ void launch_update(const DevFormula& F, const DevState& S, float eta, float eps,
     }
     const uint32_t tpb = S.R >= 128 ? 128u : 32u * ((S.R + 31) / 32);
     dim3 g1((S.R + tpb - 1) / tpb, parts);
-    k3_norm<<<g1, tpb, 0, st>>>(F, Sp, eta, eta_b, vars_per_part(S.R));
-    if (S.R >= 512) k3_final<<<(S.R + 127) / 128, 128, 0, st>>>(S, parts, eps);
-    else k3_final_block<<<S.R, 256, 0, st>>>(S, parts, eps);
+    k3_norm<<<g1, tpb, 0, st>>>(F, Sp, eta, eta_b, vars_per_part(F, S.R));
+    if (S.R >= 512 && parts <= 256) k3_final<<<(S.R + 127) / 128, 128, 0, st>>>(S, parts, eps);
+    else k3_final_block<<<S.R, 256, 0, st>>>(S, parts, eps);   // few restarts or many parts: a block per restart
     const uint64_t n = (uint64_t)(F.n_bool + F.n_real) * S.R;
     const uint64_t blocks = std::min<uint64_t>((n + 255) / 256, 148ull * 16);
     k3_apply<<<(unsigned)blocks, 256, 0, st>>>(F, Sp, eta, eta_b);

@@ -1486,15 +1486,15 @@ std::string jit_source(const Formula& f, const Built& b, const Plan& p, int u_pr
          "extern \"C\" __global__ void fsmt_kc_jit(u32 n_bool, u32 nv, u32 n_sa, const u32* __restrict__ satoms,\n"
          "    const u32* __restrict__ arow, const u32* __restrict__ acol, const float* __restrict__ aval, u32 R,\n"
          "    const double* __restrict__ gu, const float* __restrict__ DD, double* __restrict__ ga, double* __restrict__ gb) {\n"
-         "  const u32 r = blockIdx.x * blockDim.x + threadIdx.x;\n"
-         "  if (r >= R) return;\n"
-         "  // grid units throughout (the rows are exact integer sums; the b terms are rounded to the grid),\n"
-         "  // so these sums are exact like the sweep's atomics\n"
-         "  for (u32 i = 0; i < n_bool; ++i) ga[(u64)i * R + r] += gu[(u64)i * R + r];\n"
-         "  for (u32 t = 0; t < n_sa; ++t) {               // dE/db_j = sum over rows of G dd q_j (P:1326-1327)\n"
-         "    const double g = gu[(u64)(nv + t) * R + r] * (double)DD[(u64)t * R + r];\n"
+         "  // one thread per (row, restart); grid units throughout (the rows are exact integer sums, the b\n"
+         "  // terms are rounded to the grid), so the atomics' sums are exact and their order is immaterial\n"
+         "  const u64 nb = (u64)n_bool * R, n = nb + (u64)n_sa * R;\n"
+         "  for (u64 idx = (u64)blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += (u64)gridDim.x * blockDim.x) {\n"
+         "    if (idx < nb) { ga[idx] += gu[idx]; continue; }          // Boolean rows: dE/da_i\n"
+         "    const u32 t = (u32)((idx - nb) / R), r = (u32)((idx - nb) % R);\n"
+         "    const double g = gu[(u64)(nv + t) * R + r] * (double)DD[(u64)t * R + r];   // dE/db_j = sum G dd q_j (P:1326-1327)\n"
          "    const u32 at = satoms[t];\n"
-         "    for (u32 k = arow[at]; k < arow[at + 1]; ++k) gb[(u64)acol[k] * R + r] += rint(g * (double)aval[k]);\n"
+         "    for (u32 k = arow[at]; k < arow[at + 1]; ++k) atomicAdd(gb + (u64)acol[k] * R + r, rint(g * (double)aval[k]));\n"
          "  }\n"
          "}\n\n"
          "extern \"C\" __global__ void fsmt_kt_jit(u32 n_bool, u32 nv, u32 n_sa, const u32* __restrict__ satoms,\n"

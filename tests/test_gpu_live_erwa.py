@@ -277,3 +277,39 @@ def test_erwa_counter_overflow_is_reported():
         s.stage_end(2)                                # 255 -> 256: reported
     assert ei.value.status == N.ERR_RANGE
     assert s.get_counters().max() == 255
+
+
+def test_cfg4_large_r_sampled():
+    """SURVEY §8(d) config 5 scale: cfg4 at R = 16,384 restarts (U 11.6 GB, state 0.7 GB: beyond the
+    L2, so the stream values come from HBM) with the kernels fsmt_prepare(16384) builds; the K0 init
+    point of sampled restarts in three different warps and restart blocks, sampled variables'
+    gradients and E_c against the oracle."""
+    import paper_2603_22877_b200 as P
+    inst = fsmt_gen.config("cfg4")
+    Rl, kappa = 16384, 1.0
+    s = _solver(P, inst.text, prepare=Rl)
+    assert s.jit_info()["status"].startswith("active; prepared R=16384")
+    d = s.get_dims()
+    s.begin(Rl, 11)
+    s.sweep(kappa, 1)
+    obj, ga, gb = s.get_sweep()
+    a, b = s.get_state()
+    assert np.all(np.isfinite(obj)) and np.all(np.isfinite(ga)) and np.all(np.isfinite(gb))
+    f = _FULL.setdefault("f", hsmt.parse(inst.text))
+    from oracle import semantics
+    rng = np.random.default_rng(91)
+    bsel = np.sort(rng.choice(d["n_bool"], 8, replace=False))
+    rsel = np.sort(rng.choice(d["n_real"], 8, replace=False))
+    bs, rs = set(bsel.tolist()), set(rsel.tolist())
+    touch = [ci for ci, c in enumerate(f.constraints)
+             if any((k == "b" and i in bs) or (k == "a" and any(j in rs for j, _ in f.atoms[i].coeffs))
+                    for k, i in semantics.slots(c))]
+    csel = np.sort(rng.choice(d["n_cons"], 4000, replace=False))
+    for r in (5, 8191, Rl - 1):
+        _, oga, ogb = objective.objective_and_gradient_grouped(f, a[:, r], b[:, r], kappa, subset=touch)
+        check_gradient(ga[bsel, r], oga[bsel], what=f"R=16384 grad_a r={r}")
+        check_gradient(gb[rsel, r], ogb[rsel], what=f"R=16384 grad_b r={r}")
+        E = s.constraint_terms(kappa, r)
+        _, _, _, terms = objective.objective_and_gradient_grouped(f, a[:, r], b[:, r], kappa, subset=csel,
+                                                                  want_terms=True)
+        assert np.max(np.abs(E[csel] - np.array([terms[ci] for ci in csel]))) <= 1e-6
