@@ -61,6 +61,10 @@ struct fsmt_ctx {
     bool rounded = false;
     uint64_t launches = 0;
     uint32_t* hflags = nullptr;        // pinned host copy of S.flags[0] (read at every stage end)
+    // auxiliary streams for the concurrent per-class sweep launches (fork / join by events)
+    static constexpr size_t kAux = 4;
+    cudaStream_t aux[kAux] = {nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t ev_fork = nullptr, ev_join[kAux] = {nullptr, nullptr, nullptr, nullptr};
     // per-kernel-class device timing (fsmt_set_timing)
     bool timing = false;
     std::vector<cudaEvent_t> ev_pool;
@@ -273,6 +277,16 @@ fsmt_status fsmt_create(int cuda_device, fsmt_ctx** out) {
         return FSMT_ERR_OOM;
     }
     *ctx->hflags = 0;
+    for (size_t i = 0; i < fsmt_ctx::kAux; ++i)
+        if (cudaStreamCreateWithFlags(&ctx->aux[i], cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&ctx->ev_join[i], cudaEventDisableTiming) != cudaSuccess) {
+            fsmt_destroy(ctx);
+            return FSMT_ERR_CUDA;
+        }
+    if (cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess) {
+        fsmt_destroy(ctx);
+        return FSMT_ERR_CUDA;
+    }
     default_kappas(ctx->kappas);
     *out = ctx;
     return FSMT_OK;
@@ -290,6 +304,11 @@ void fsmt_destroy(fsmt_ctx* ctx) {
     for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     if (ctx->hflags) cudaFreeHost(ctx->hflags);
+    for (size_t i = 0; i < fsmt_ctx::kAux; ++i) {
+        if (ctx->aux[i]) cudaStreamDestroy(ctx->aux[i]);
+        if (ctx->ev_join[i]) cudaEventDestroy(ctx->ev_join[i]);
+    }
+    if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
     delete ctx;
 }
 
@@ -794,9 +813,11 @@ fsmt_status fsmt_jit_check(fsmt_ctx* ctx, size_t* cubin_bytes, char* log, size_t
 // constraints ahead when U[c][r] (1 B per constraint and restart) exceeds ~1.5x the 126 MB L2
 // and so comes from HBM every sweep (cfg4 9.78 -> 8.85 ms; cfg3, whose 117 MB
 // of U stays in L2, is faster without).
-static std::string prepared_source(const fsmt_ctx* ctx, uint32_t R, int min_ctas) {
+static std::string prepared_source(const fsmt_ctx* ctx, uint32_t R, int min_ctas, const std::vector<int>* caps = nullptr) {
     const int upf = (double)ctx->plan.jit_cons_end * R > 192e6 ? 3 : 0;
-    const std::string src = (upf || min_ctas) ? jit_source(ctx->f, ctx->b, ctx->plan, upf, min_ctas) : ctx->jit_src;
+    std::vector<int> all(ctx->plan.n_jit_kclasses, min_ctas);
+    const std::string src = (upf || min_ctas || caps) ? jit_source(ctx->f, ctx->b, ctx->plan, upf, min_ctas, caps ? caps : &all)
+                                                       : ctx->jit_src;
     return "#define FSMT_RC " + std::to_string(R) + "u\n" + src;
 }
 
@@ -847,25 +868,33 @@ fsmt_status fsmt_prepare(fsmt_ctx* ctx, uint32_t R) {
     ctx->jit_r_R = 0;
     // register cap of the hot sweep: the highest residency (32, then 28 one-warp CTAs per SM:
     // 64 / 72 registers) whose kernel needs no local memory (no spills), else none (DESIGN.md
-    // §7 item 13).  Judged from the loaded kernel's attributes, not the compiler log.
+    // §7 item 13) -- chosen for the all-class kernel and for each per-class kernel fsmt_k1_c<k>
+    // separately (§7 item 17).  Judged from the loaded kernels' attributes, not the compiler log.
+    const uint32_t nk = ctx->plan.n_jit_kclasses;
     int cap = 0;
+    bool cap_found = false;
+    std::vector<int> caps(nk, 0);
+    std::vector<char> found(nk, 0);
     std::string err;
-    for (int mc : {32, 28, 0}) {
-        JitKernel cand;
-        if (!jit_compile(prepared_source(ctx, R, mc), cand, err)) {
-            if (mc == 0) return fail(ctx, FSMT_ERR_CUDA, "fsmt_prepare: " + err);
-            continue;
-        }
+    auto spills = [](cudaKernel_t k) {
         cudaFuncAttributes fa{};
-        const bool spills = cudaFuncGetAttributes(&fa, (const void*)cand.kernel) != cudaSuccess || fa.localSizeBytes > 0;
-        if (spills && mc != 0) {
-            jit_release(cand);
-            continue;
+        return cudaFuncGetAttributes(&fa, (const void*)k) != cudaSuccess || fa.localSizeBytes > 0;
+    };
+    for (int mc : {32, 28}) {
+        JitKernel cand;
+        if (!jit_compile(prepared_source(ctx, R, mc), cand, err)) continue;
+        if (!cap_found && !spills(cand.kernel)) {
+            cap = mc;
+            cap_found = true;
         }
-        ctx->jit_r = cand;
-        cap = mc;
-        break;
+        for (uint32_t k = 0; k < nk && k < cand.kclass.size(); ++k)
+            if (!found[k] && !spills(cand.kclass[k])) {
+                caps[k] = mc;
+                found[k] = 1;
+            }
+        jit_release(cand);
     }
+    if (!jit_compile(prepared_source(ctx, R, cap, &caps), ctx->jit_r, err)) return fail(ctx, FSMT_ERR_CUDA, "fsmt_prepare: " + err);
     ctx->jit_r_cap = cap;
     ctx->jit_r_R = R;
     return FSMT_OK;
@@ -906,9 +935,46 @@ static fsmt_status sweep_impl(fsmt_ctx* ctx, float kappa, uint32_t stage_t, doub
         }
         if (ctx->T.n_tiles) {
             const JitKernel& J = jk(ctx, S.R);
-            launch_sweep_jit((S.U == nullptr || terms != nullptr) ? J.kernel_dbg : J.kernel, F, S, ctx->T, kappa, terms, terms_r,
-                             ctx->stream, &ctx->slots);
-            ctx->launches += 1;
+            const bool dbg = S.U == nullptr || terms != nullptr;
+            const char* pc = getenv("FSMT_JIT_PERCLASS");
+            const std::vector<uint32_t>& cb = ctx->plan.class_tile_begin;
+            if (!dbg && !(pc && pc[0] == '0') && J.kclass.size() == ctx->plan.n_jit_kclasses && cb.size() == J.kclass.size() + 1) {
+                // classes that gain from their own register allocation launch their own kernel; runs of
+                // the others share one all-class launch (DESIGN.md §7 item 17); the launches run
+                // concurrently on the auxiliary streams (their atomics add exact grid units)
+                const uint32_t lo = ctx->T.first, hi = ctx->T.first + ctx->T.n_tiles;
+                std::vector<std::pair<cudaKernel_t, std::pair<uint32_t, uint32_t>>> L;
+                for (size_t k = 0; k < J.kclass.size(); ++k) {
+                    const uint32_t b0 = std::max(lo, cb[k]), b1 = std::min(hi, cb[k + 1]);
+                    if (b1 <= b0) continue;
+                    const cudaKernel_t kk = J.kclass_sep[k] ? J.kclass[k] : J.kernel;
+                    if (!L.empty() && kk == J.kernel && L.back().first == J.kernel && L.back().second.second == b0)
+                        L.back().second.second = b1;
+                    else
+                        L.push_back({kk, {b0, b1}});
+                }
+                const bool fork = L.size() > 1;
+                if (fork) CK(cudaEventRecord(ctx->ev_fork, ctx->stream));
+                for (size_t i = 0; i < L.size(); ++i) {
+                    const uint32_t b0 = L[i].second.first, b1 = L[i].second.second;
+                    DevTiles Tk = ctx->T;
+                    Tk.tiles = (const char*)ctx->T.tiles + (size_t)(b0 - lo) * sizeof(TileDesc);
+                    Tk.n_tiles = b1 - b0;
+                    Tk.first = b0;
+                    cudaStream_t st = fork ? ctx->aux[i % fsmt_ctx::kAux] : ctx->stream;
+                    if (fork && i < fsmt_ctx::kAux) CK(cudaStreamWaitEvent(st, ctx->ev_fork, 0));
+                    launch_sweep_jit(L[i].first, F, S, Tk, kappa, terms, terms_r, st, &ctx->slots);
+                    ctx->launches += 1;
+                }
+                if (fork)
+                    for (size_t i = 0; i < std::min(L.size(), (size_t)fsmt_ctx::kAux); ++i) {
+                        CK(cudaEventRecord(ctx->ev_join[i], ctx->aux[i]));
+                        CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_join[i], 0));
+                    }
+            } else {
+                launch_sweep_jit(dbg ? J.kernel_dbg : J.kernel, F, S, ctx->T, kappa, terms, terms_r, ctx->stream, &ctx->slots);
+                ctx->launches += 1;
+            }
         }
         if (F.generic_begin < F.generic_end) {
             launch_sweep(F, S, kappa, terms, terms_r, ctx->stream);
@@ -1127,6 +1193,7 @@ fsmt_status fsmt_shard(fsmt_ctx* ctx, uint32_t rank, uint32_t world, uint32_t mo
     }
     ctx->T = ctx->T_all;
     ctx->T.tiles = (const char*)ctx->T_all.tiles + (size_t)t0 * sizeof(TileDesc);
+    ctx->T.first = t0;
     ctx->T.n_tiles = t1 - t0;
     const uint32_t gn = C - jit_end;
     // split on the generic sweep's 16-constraint chunk boundaries (kernels.cu kChunk): each chunk's

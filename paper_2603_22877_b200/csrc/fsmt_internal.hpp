@@ -171,13 +171,16 @@ struct Plan {
     uint32_t vmax_sym = 128;          // stream rows of symmetric-class tiles (FSMT_TILE_VMAX_SYM)
     // shared-memory rows per warp of the JIT sweep: the largest tile limit in use
     uint32_t kernel_vmax() const { return has_sym ? std::max(vmax, vmax_sym) : vmax; }
+    std::vector<uint32_t> class_tile_begin;   // [n_jit_kclasses + 1]: class k's tiles are [begin[k], begin[k+1])
 };
 
 Plan make_plan(const Formula& f, const Built& b, bool enable_jit);
 // CUDA source of the specialised sweep kernel for the plan's JIT classes.
 // u_prefetch_default: how many constraints ahead the sweep loads U (FSMT_JIT_UPF overrides)
-// k1_min_ctas > 0: __launch_bounds__(32, k1_min_ctas) on the hot sweep kernel (register cap)
-std::string jit_source(const Formula& f, const Built& b, const Plan& p, int u_prefetch_default = 0, int k1_min_ctas = 0);
+// k1_min_ctas > 0: __launch_bounds__(32, k1_min_ctas) on the hot sweep kernel (register cap);
+// class_caps (optional, one per JIT class): the caps of the per-class hot kernels fsmt_k1_c<k>
+std::string jit_source(const Formula& f, const Built& b, const Plan& p, int u_prefetch_default = 0, int k1_min_ctas = 0,
+                       const std::vector<int>* class_caps = nullptr);
 // Exponent k with max_c w_c 2^-k in (1/2, 1] (0 for no constraints): the weight normalisation of
 // the sweep (DESIGN.md §7 item 14).
 int weight_exponent(const Built& b);

@@ -154,6 +154,28 @@ bool jit_compile(const std::string& src, JitKernel& out, std::string& err) {
     out.lib = lib;
     out.kernel = k;
     out.kernel_dbg = kd;
+    out.kclass.clear();
+    for (int c = 0;; ++c) {            // per-class hot kernels, as many as the module has
+        cudaKernel_t kc = nullptr;
+        const std::string name = "fsmt_k1_c" + std::to_string(c);
+        if (cudaLibraryGetKernel(&kc, lib, name.c_str()) != cudaSuccess) {
+            cudaGetLastError();
+            break;
+        }
+        out.kclass.push_back(kc);
+    }
+    // which classes gain from their own kernel: >= 8 fewer registers (more resident warps) or less
+    // local memory (fewer spills) than the all-class kernel, whose allocation is the classes' max
+    out.kclass_sep.assign(out.kclass.size(), 0);
+    cudaFuncAttributes fa{};
+    if (cudaFuncGetAttributes(&fa, (const void*)k) == cudaSuccess) {
+        for (size_t c = 0; c < out.kclass.size(); ++c) {
+            cudaFuncAttributes fc{};
+            if (cudaFuncGetAttributes(&fc, (const void*)out.kclass[c]) != cudaSuccess) continue;
+            out.kclass_sep[c] = fc.numRegs + 8 <= fa.numRegs || fc.localSizeBytes < fa.localSizeBytes;
+        }
+    }
+    cudaGetLastError();
     out.kernel5 = k5;
     out.kprob = kp;
     out.kchain = kc;
@@ -169,6 +191,8 @@ void jit_release(JitKernel& k) {
     k.kernel_dbg = nullptr;
     k.kernel5 = nullptr;
     k.kprob = k.kchain = k.ktruth = nullptr;
+    k.kclass.clear();
+    k.kclass_sep.clear();
 }
 
 }  // namespace fsmt

@@ -15,7 +15,9 @@ struct JitKernel {
     cudaKernel_t kchain = nullptr;     // fsmt_kc_jit (slot-table gradients -> grad_a / grad_b)
     cudaKernel_t ktruth = nullptr;     // fsmt_kt_jit (slot truth table for the exact check)
     size_t cubin_bytes = 0;
-    uint32_t rpl = 1;                  // restarts per lane of fsmt_k1_jit (2: f32x2 module of fsmt_prepare)
+    std::vector<cudaKernel_t> kclass;  // fsmt_k1_c<k>: the hot sweep of JIT class k alone (own registers)
+    std::vector<char> kclass_sep;      // 1: class k launches its own kernel (fewer registers or less local
+                                       // memory than the all-class kernel), 0: it runs in fsmt_k1_jit
     std::string log;
 };
 

@@ -147,6 +147,7 @@ struct DevTiles {
     uint32_t vmax;               // stream variables (shared-memory accumulator rows) per tile (Plan::vmax)
     uint32_t rmax;               // run variables per tile (Plan::rmax)
     const void* vrecs;           // K5 records (atom ids), tile.pad1 = offset in uint4
+    uint32_t first;              // global index of tiles[0] (constraint shards start mid-plan)
 };
 // Slot tables of the symmetric JIT classes (rows: Booleans [0, n_bool), table atom t at nv + t).
 struct DevSlots {

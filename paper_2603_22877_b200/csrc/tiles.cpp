@@ -607,6 +607,10 @@ Plan make_plan(const Formula& f, const Built& b, bool enable_jit) {
         T.pad0 = T.n_cons * K.stride4;
     }
     p.recs.swap(packed);
+    // each JIT class's tiles are contiguous (the internal order sorts by class first)
+    p.class_tile_begin.assign(p.n_jit_kclasses + 1, (uint32_t)p.tiles.size());
+    for (uint32_t t = (uint32_t)p.tiles.size(); t-- > 0;) p.class_tile_begin[p.tiles[t].kclass] = t;
+    for (uint32_t k = p.n_jit_kclasses; k-- > 0;) p.class_tile_begin[k] = std::min(p.class_tile_begin[k], p.class_tile_begin[k + 1]);
     return p;
 }
 
@@ -1338,7 +1342,8 @@ void emit_verify_class(std::ostringstream& o, uint32_t kid, const KClass& K, con
 
 }  // namespace
 
-std::string jit_source(const Formula& f, const Built& b, const Plan& p, int u_prefetch_default, int k1_min_ctas) {
+std::string jit_source(const Formula& f, const Built& b, const Plan& p, int u_prefetch_default, int k1_min_ctas,
+                       const std::vector<int>* class_caps) {
     g_upf = u_prefetch_default;
     std::ostringstream o;
     o << "// generated by fsmt tiles.cpp: specialised K1 sweep for " << p.n_jit_kclasses << " kernel classes\n"
@@ -1351,12 +1356,16 @@ std::string jit_source(const Formula& f, const Built& b, const Plan& p, int u_pr
     // fsmt_k1_jit: the hot kernel (U present, no E_c output); fsmt_k1_jit_dbg: U may be NULL and
     // the per-constraint E_c debug hook is live.  Separate kernels, so the hot one keeps its own
     // register allocation.  One warp per CTA (CTA-uniform control flow, DESIGN.md §7 item 5).
-    for (int dbgk = 0; dbgk < 2; ++dbgk) {
+    // fsmt_k1_c<k>: the hot kernel of class k alone, launched over that class's tiles, so each class
+    // gets its own register allocation and cap (DESIGN.md §7 item 17).
+    for (int kv = -2; kv < (int)p.n_jit_kclasses; ++kv) {
+    const int dbgk = kv == -1;
     // hot kernel: k1_min_ctas resident warps per SM as a register cap (fsmt_prepare picks
     // the largest of 32 / 28 that compiles without spills; 0 = none); FSMT_JIT_MINB overrides
-    const std::string mb = minb ? std::string(minb) : (dbgk || k1_min_ctas <= 0 ? std::string() : std::to_string(k1_min_ctas));
+    const int cap = kv >= 0 && class_caps ? (*class_caps)[(size_t)kv] : k1_min_ctas;
+    const std::string mb = minb ? std::string(minb) : (dbgk || cap <= 0 ? std::string() : std::to_string(cap));
     o << "extern \"C\" __global__ void __launch_bounds__(32" << (atoi(mb.c_str()) > 0 ? ", " + mb : std::string())
-      << ") fsmt_k1_jit" << (dbgk ? "_dbg" : "") << "(\n"
+      << ") " << (kv >= 0 ? "fsmt_k1_c" + std::to_string(kv) : std::string(dbgk ? "fsmt_k1_jit_dbg" : "fsmt_k1_jit")) << "(\n"
          "    const TileDesc* __restrict__ tiles, u32 n_tiles, const uint4* __restrict__ recs,\n"
          "    const u32* __restrict__ tile_vars, const float* __restrict__ a, const float* __restrict__ b,\n"
          "    double* __restrict__ ga, double* __restrict__ gb, const unsigned char* __restrict__ U,\n"
@@ -1398,6 +1407,7 @@ std::string jit_source(const Formula& f, const Built& b, const Plan& p, int u_pr
          "  bool symt = false;   // symmetric class: the tile's variables are slot-table rows\n"
          "  switch (T.kclass) {\n";
     for (uint32_t k = 0; k < p.n_jit_kclasses; ++k) {
+        if (kv >= 0 && (int)k != kv) continue;
         const std::string args = "(T, rp, vs, vr, acc + lane, ab, bb, ga, gb, U, R, R4, rr, r, live, n_bool, kq, dcoef, ebias, "
                                  "gif, objacc, terms, terms_r, orig, PTl, PFl, gu); ";
         o << "    case " << k << ": kc" << k << (dbgk ? "<true>" : "<false>") << args
