@@ -321,6 +321,118 @@ def placement(n_m=32, n_l=4, counts=(148, 592, 148, 296), seed=4, gap=1e-6) -> I
                      "sizes": sizes, "bins": binof})
 
 
+def placement_routed(n_m=64, n_l=8, seed=5) -> Instance:
+    """The paper's placement family itself, routing-aware constraints included.
+
+    Modules: n_m large PEs (0.4 x 0.4), n_m*n_l small PEs (0.2 x 0.2), n_m large
+    memories (0.1 x 0.1), n_m*n_l/2 small memories (0.1 x 0.05, axis alternating).
+    Reading R25 (the paper's counts: 10,880 routing constraints at n_m = 64, n_l = 8 = 1,088
+    associated pairs x (log2 n_m bit equalities + 4 adjacency atoms)): each large PE is paired with
+    one large memory, and each small PE with two small memories; small PE (m, l) of macro m goes with
+    small memories (m, 2 floor(l / 4)) and (m, 2 floor(l / 4) + 1), so every small memory serves four
+    PEs.  Routing constraints per associated (j, j'): m_{i,j} = m_{i,j'} for every macro bit, and the
+    adjacency unit atoms x_j - x_j' <= w_j', x_j' - x_j <= w_j, y_j - y_j' <= d_j', y_j' - y_j <= d_j
+    (multi-variable unit atoms: halfspaces of the R33 projection, or soft terms).  Non-overlap and
+    feasibility as `placement`.  Planted witness: per macro, small PEs of layers 0-3 at spot A and
+    of layers 4-7 at spot B, their memories at the same spot in layers the spot's PEs do not use,
+    large PE and memory stacked in layers 0 / 1 (>= 0.05 clearance wherever modules share a layer).
+    n_m = 64, n_l = 8: 896 modules, 9,856 variables, 415,424 constraints.
+    """
+    assert n_l == 8, "the planted layout uses 8 layers (4 per spot)"
+    rng = np.random.default_rng(seed)
+    bm = int(n_m).bit_length() - 1
+    bl = int(n_l).bit_length() - 1
+    K = bm + bl
+    mods = []              # (kind, macro, index-within-macro)
+    for m in range(n_m):
+        mods.append(("large_pe", m, 0))
+        mods.extend(("small_pe", m, l) for l in range(n_l))
+        mods.append(("large_mem", m, 0))
+        mods.extend(("small_mem", m, k) for k in range(n_l // 2))
+    perm = rng.permutation(len(mods))
+    mods = [mods[i] for i in perm]
+    M = len(mods)
+    sizes, pos, layer = [], np.zeros((M, 2)), np.zeros(M, dtype=np.int64)
+    at = {}
+    sm = 0
+    for j, (kind, m, i) in enumerate(mods):
+        at[(kind, m, i)] = j
+        if kind == "small_mem":
+            sz = _SIZES["small_mem_x" if sm % 2 == 0 else "small_mem_y"]
+            sm += 1
+        else:
+            sz = _SIZES[kind]
+        sizes.append(sz)
+        if kind == "small_pe":                     # spot A (layers 0-3) or spot B (layers 4-7)
+            pos[j] = (0.05, 0.05) if i < 4 else (0.5, 0.05)
+            layer[j] = i
+        elif kind == "small_mem":                  # mems 0,1 at spot A in layers 4,5; mems 2,3 at B in 0,1
+            pos[j] = (0.1, 0.1) if i < 2 else (0.55, 0.1)
+            layer[j] = 4 + i if i < 2 else i - 2
+        elif kind == "large_pe":
+            pos[j] = (0.05, 0.5)
+            layer[j] = 0
+        else:                                      # large memory, adjacent to (inside the window of) its PE
+            pos[j] = (0.2, 0.6)
+            layer[j] = 1
+    pairs = []
+    for m in range(n_m):
+        pairs.append((at[("large_pe", m, 0)], at[("large_mem", m, 0)]))
+        for l in range(n_l):
+            base = 2 * (l // 4)
+            for k in (base, base + 1):
+                pairs.append((at[("small_pe", m, l)], at[("small_mem", m, k)]))
+    macro = np.array([m for _, m, _ in mods])
+    x_star = np.ones(M * K, dtype=np.int8)
+    for j in range(M):
+        for i in range(bm):
+            if (macro[j] >> i) & 1:
+                x_star[j * K + i] = -1
+        for i in range(bl):
+            if (layer[j] >> i) & 1:
+                x_star[j * K + bm + i] = -1
+    y_star = np.empty(2 * M, dtype=np.float32)
+    y_star[0::2] = pos[:, 0]
+    y_star[1::2] = pos[:, 1]
+    out = [f"p hsmt {M * K} {2 * M}"]
+    atoms, cons = [], []
+    na = 0
+    for j in range(M):
+        xj, yj = 2 * j, 2 * j + 1
+        wj, dj = sizes[j]
+        for jp in range(j + 1, M):
+            xp, yp = 2 * jp, 2 * jp + 1
+            wp, dp = sizes[jp]
+            atoms.append(f"a {na} >= {wp} {xj}:1 {xp}:-1\n"
+                         f"a {na + 1} >= {wj} {xp}:1 {xj}:-1\n"
+                         f"a {na + 2} >= {dp} {yj}:1 {yp}:-1\n"
+                         f"a {na + 3} >= {dj} {yp}:1 {yj}:-1")
+            bits = " ".join(f"(xor b{j * K + i} b{jp * K + i})" for i in range(K))
+            cons.append(f"e 1 (or {bits} a{na} a{na + 1} a{na + 2} a{na + 3})")
+            na += 4
+    for j in range(M):
+        xj, yj = 2 * j, 2 * j + 1
+        wj, dj = sizes[j]
+        atoms.append(f"a {na} >= 0 {xj}:1\na {na + 1} <= {_ONE_MINUS[wj]} {xj}:1\n"
+                     f"a {na + 2} >= 0 {yj}:1\na {na + 3} <= {_ONE_MINUS[dj]} {yj}:1")
+        cons.append(f"c or 1 +a{na}\nc or 1 +a{na + 1}\nc or 1 +a{na + 2}\nc or 1 +a{na + 3}")
+        na += 4
+    for j, jp in pairs:                            # routing-aware (P:667-673, reading R25)
+        xj, yj, xp, yp = 2 * j, 2 * j + 1, 2 * jp, 2 * jp + 1
+        (wj, dj), (wp, dp) = sizes[j], sizes[jp]
+        for i in range(bm):
+            cons.append(f"e 1 (not (xor b{j * K + i} b{jp * K + i}))")
+        atoms.append(f"a {na} <= {wp} {xj}:1 {xp}:-1\na {na + 1} <= {wj} {xp}:1 {xj}:-1\n"
+                     f"a {na + 2} <= {dp} {yj}:1 {yp}:-1\na {na + 3} <= {dj} {yp}:1 {yj}:-1")
+        cons.append(f"c or 1 +a{na}\nc or 1 +a{na + 1}\nc or 1 +a{na + 2}\nc or 1 +a{na + 3}")
+        na += 4
+    text = "\n".join(out + atoms + cons) + "\n"
+    n_cons = M * (M - 1) // 2 + 4 * M + len(pairs) * (bm + 4)
+    return Instance("place9856", text, M * K, 2 * M, n_cons, x_star, y_star,
+                    {"seed": seed, "modules": M, "bits_per_module": K, "n_m": n_m, "n_l": n_l, "n_atoms": na,
+                     "pairs": len(pairs), "routing": len(pairs) * (bm + 4)})
+
+
 def config(name: str) -> Instance:
     return CONFIGS[name]()
 
@@ -338,5 +450,9 @@ CONFIGS = {
     "cfg2s": lambda: random_hybrid(n_bool=20, n_real=20, n_atoms=20, n_card=30, n_nae=30, n_xor=6,
                                    l_card=8, l_nae=8, l_xor=12, seed=12),
 }
+# the paper's placement family with routing (R25): 9,856 variables / 415,424 constraints,
+# and a small version (n_m = 4, n_l = 8: 56 modules) for oracle-sized parity
+CONFIGS["place9856"] = placement_routed
+CONFIGS["place9856s"] = lambda: placement_routed(n_m=4, n_l=8, seed=15)
 # the paper's random family at every n: "rand100" ... "rand1000"
 CONFIGS.update({f"rand{n}": (lambda n=n: paper_random(n)) for n in range(100, 1001, 100)})

@@ -473,13 +473,31 @@ def test_min_vertex_objective_iff_sat():
         assert (model is not None) == (best == -sw)
 
 
-@pytest.mark.parametrize("name", ["cfg1", "cfg2s", "cfg3s", "cfg4s", "cfg2"])
+@pytest.mark.parametrize("name", ["cfg1", "cfg2s", "cfg3s", "cfg4s", "cfg2", "cfg4m", "place9856s", "rand100", "rand300"])
 def test_generator_witnesses_exact(name):
     inst = fsmt_gen.config(name)
     f = hsmt.parse(inst.text)
     assert (f.n_bool, f.n_real, len(f.constraints)) == (inst.n_bool, inst.n_real, inst.n_cons)
     obj, sat = semantics.eval_formula(f, inst.x_star, inst.y_star)
     assert all(sat) and obj == -sum(c.weight for c in f.constraints)
+
+
+def test_paper_family_sizes():
+    """The generators reproduce the paper's instance sizes: the placement family at n_m = 64, n_l = 8
+    (896 modules, 9,856 variables; 400,960 non-overlap + 3,584 feasibility + 10,880 routing =
+    415,424 constraints) and the random family's counts per n
+    (n/5 card + n/5 nae + n/50 xor of lengths min(50, n/5) / 50)."""
+    p = fsmt_gen.config("place9856")
+    assert (p.n_bool + p.n_real, p.meta["modules"], p.n_cons, p.meta["routing"]) == (9856, 896, 415424, 10880)
+    assert p.text.count("\ne 1 (or ") == 400960 and p.text.count("\ne 1 (not (xor ") == 1088 * 6
+    for n in (100, 600, 1000):
+        r = fsmt_gen.config(f"rand{n}")
+        lines = r.text.splitlines()
+        l = min(50, n // 5)
+        assert (r.n_bool, r.n_real, r.n_cons) == (n, n, n // 5 * 2 + n // 50)
+        assert sum(ln.startswith(f"c card {l // 2} ") and len(ln.split()) == 4 + l for ln in lines) == n // 5
+        assert sum(ln.startswith("c nae ") and len(ln.split()) == 3 + l for ln in lines) == n // 5
+        assert sum(ln.startswith("c xor ") and len(ln.split()) == 3 + 50 for ln in lines) == n // 50
 
 
 # ----------------------------------------------------------------------------- Alg.2 / projection / rounding
