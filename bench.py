@@ -38,8 +38,9 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-SURVEY_BYTES_PER_EVAL = {"cfg4": 193.0, "cfg3": 97.9, "cfg2": 193.0}    # SURVEY §8(d), per (c, r)
-FMA_PER_EVAL = {"cfg4": 264.0, "cfg3": 142.0, "cfg2": 480.0}            # SURVEY §8(d) model
+SURVEY_BYTES_PER_EVAL = {"cfg4": 194.0, "cfg3": 98.9, "cfg2": 194.0}    # SURVEY §8(d) + 1 B (U is u16), per (c, r)
+FMA_PER_EVAL = {"cfg4": 264.0, "cfg3": 142.0, "cfg2": 480.0,            # SURVEY §8(d) model
+                "place9856": 296.0}   # the same model for 9 bit pairs + 4 atoms: 31 nodes x 6 + 22 slots + 4 x 22
 KAPPA = 1.0                                                              # fixed kappa, t = 1
 METRIC = "xBDD COP+grad evals/s (constraints x restarts)"
 TTS_KAPPAS = [300.0 ** (i / 19) for i in range(20)] + [300.0] * 200     # DESIGN.md §9 recipe
@@ -253,7 +254,8 @@ def time_to_sat(P, inst, device: int, R: int, seeds=range(8)) -> dict:
 
 def workload_config(args, n_vars: int, n_cons: int, world: int = 1) -> dict:
     """The workload both arms name in `config` (same keys, so the driver compares like with like)."""
-    names = {"cfg4": "placement-10k", "cfg3": "scheduling-2k", "cfg2": "random-200"}
+    names = {"cfg4": "placement-10k", "cfg3": "scheduling-2k", "cfg2": "random-200",
+             "place9856": "paper placement n_m=64 n_l=8 with routing"}
     g = args.restarts * world if args.mode == "restart" else args.restarts
     return {"workload": f"{args.config}: {names.get(args.config, args.config)}, {n_vars} vars / {n_cons} constraints",
             "restarts_per_gpu": args.restarts if args.mode == "restart" else None, "global_restarts": g,
@@ -416,7 +418,7 @@ def main():
     hbm, peak_src, sm_max = peaks()
     k1_avg_s = (k1_ms / max(k1_n, 1)) / 1e3
     evals_per_launch = dims["n_cons"] * R / (world if constraint_mode else 1)
-    bpe = SURVEY_BYTES_PER_EVAL.get(args.config, 193.0)
+    bpe = SURVEY_BYTES_PER_EVAL.get(args.config, 194.0)
     achieved = bpe * evals_per_launch / k1_avg_s / 1e9
     traffic = None
     prof = os.path.join(ROOT, "profiles", f"k1_traffic_{args.config}.json")

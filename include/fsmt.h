@@ -19,7 +19,7 @@
  *
  * Layouts: per-restart state is restart-minor, row = variable:
  *     a[n_bool][R] f32, b[n_real][R] f32, grad_a[n_bool][R] f64, grad_b[n_real][R] f64,
- *     U[n_cons][R] u8, x[n_bool][R] i8, obj[R] f64, unsat[R] u32, umax[R] u32.
+ *     U[n_cons][R] u16, x[n_bool][R] i8, obj[R] f64, unsat[R] u32, umax[R] u32.
  * Truth encoding: -1 = True, +1 = False.
  */
 #ifndef FSMT_H
@@ -44,8 +44,8 @@ typedef enum {
     FSMT_ERR_OOM = 6,          /* device or host allocation failed */
     FSMT_ERR_CUDA = 7,         /* CUDA runtime error (no device, launch failure, ...) */
     FSMT_ERR_TIMEOUT = 8,      /* time limit hit inside fsmt_solve (verdict is still set) */
-    FSMT_ERR_RANGE = 9         /* an ERWA counter U[c][r] (u8, R18) passed 255 violations, or the stage
-                                  exponent e_t = (t-2)/2 of Alg.2 verbatim passed 600 (weights beyond fp64) */
+    FSMT_ERR_RANGE = 9         /* ERWA weights 2^(U[c][r] + e_t) (R18) beyond the fp64 range of the
+                                  accumulation (U + e_t past ~900), or a u16 counter past 65535 */
 } fsmt_status;
 
 typedef enum { FSMT_UNKNOWN = 0, FSMT_SAT = 10 } fsmt_verdict;   /* S:514 exit codes */
@@ -168,9 +168,9 @@ fsmt_status fsmt_begin(fsmt_ctx* ctx, uint32_t restarts, uint64_t seed, uint32_t
 /* Overwrite / read the relaxed point (a[n_bool][R], b[n_real][R]). set_state does NOT project. */
 fsmt_status fsmt_set_state(fsmt_ctx* ctx, const float* a, const float* b, int where);
 fsmt_status fsmt_get_state(fsmt_ctx* ctx, float* a, float* b, int where);
-/* Overwrite / read the ERWA violation counters U[n_cons][R] (R18). */
-fsmt_status fsmt_set_counters(fsmt_ctx* ctx, const uint8_t* U, int where);
-fsmt_status fsmt_get_counters(fsmt_ctx* ctx, uint8_t* U, int where);
+/* Overwrite / read the ERWA violation counters U[n_cons][R] u16 (R18), original constraint order. */
+fsmt_status fsmt_set_counters(fsmt_ctx* ctx, const uint16_t* U, int where);
+fsmt_status fsmt_get_counters(fsmt_ctx* ctx, uint16_t* U, int where);
 
 /* K1: objective and gradient at the current point for all restarts (a1-a4 of SURVEY §8(a)):
  * obj[r] = sum_c w_cr E_c (Eq.10), grad = dC/d(a,b) (Alg.B with the sign of R1, chain rule
@@ -190,7 +190,7 @@ fsmt_status fsmt_get_sweep(fsmt_ctx* ctx, double* grad_a, double* grad_b, double
  * NULL = all 0), runs K1 (= fsmt_sweep(kappa, stage_t)) and writes obj[R], grad_a[n_bool][R],
  * grad_b[n_real][R] (f64; any output may be NULL).  All pointers are host (FSMT_HOST) or device
  * (FSMT_DEVICE) per `where`.  Replaces the context's current state. */
-fsmt_status fsmt_eval(fsmt_ctx* ctx, uint32_t R, const float* a, const float* b, float kappa, const uint8_t* U,
+fsmt_status fsmt_eval(fsmt_ctx* ctx, uint32_t R, const float* a, const float* b, float kappa, const uint16_t* U,
                       uint32_t stage_t, double* obj, double* grad_a, double* grad_b, int where);
 /* Per-constraint E_c for restart r from the last sweep's kernels (debug/parity hook, host E[n_cons]). */
 fsmt_status fsmt_constraint_terms(fsmt_ctx* ctx, float kappa, uint32_t restart, double* E);
@@ -208,8 +208,9 @@ fsmt_status fsmt_step_sizes(const fsmt_ctx* ctx, float kappa, float* eta_a, floa
 
 /* K4+K5 (a6-a9): round x = sgn(a) or R(a) (R17), y = b; exact check of every constraint
  * (R22); U[c][r] += u_c; umax[r] = max_c U[c][r]; unsat[r] = #violated; clears the per-stage
- * frozen flags.  unsat_out[R] (host, may be NULL).  FSMT_ERR_RANGE when a counter would pass
- * 255 (it is then held at 255; the u8 counter is never silently saturated). */
+ * frozen flags.  unsat_out[R] (host, may be NULL).  FSMT_ERR_RANGE when a stage's sweep took the
+ * ERWA weights 2^(U + e_t) beyond the fp64 range (U + e_t past ~900) or a counter passed 65535
+ * (never silently saturated). */
 fsmt_status fsmt_stage_end(fsmt_ctx* ctx, uint32_t stage_t, uint32_t* unsat_out);
 /* One whole annealing stage for all restarts, as fsmt_solve runs it (Alg.2 loop body,
  * P:513-528): `steps` x {K1 sweep at kappa, K3 update(fsmt_step_sizes(kappa), eps)} then K4+K5

@@ -201,15 +201,17 @@ float wfrac_of(uint32_t stage_t, uint32_t mode) {
     if (mode == FSMT_ERWA_RESET0 || stage_t <= 2 || (stage_t - 2) % 2 == 0) return 1.0f;
     return 1.41421356237309505f;
 }
-// stage exponents past this would take 2^(U + e_t) beyond the fp64 range of the flush scales
-constexpr uint32_t kMaxStageExp = 600;
+
 
 // after a stage end and a sync: the K5 overflow flag (an ERWA counter passed 255; R18 needs the
 // exact count, so the u8 counter is never silently saturated)
 fsmt_status check_flags(fsmt_ctx* ctx) {
     if (ctx->hflags && (*ctx->hflags & 1u))
-        return fail(ctx, FSMT_ERR_RANGE, "ERWA counter overflow: a constraint was violated more than 255 times in one restart "
-                                         "(u8 U[c][r], R18)");
+        return fail(ctx, FSMT_ERR_RANGE, "ERWA counter overflow: a constraint was violated more than 65535 times in one "
+                                         "restart (u16 U[c][r], R18)");
+    if (ctx->hflags && (*ctx->hflags & 2u))
+        return fail(ctx, FSMT_ERR_RANGE, "ERWA weights 2^(U + e_t) beyond the fp64 range of the accumulation (U + e_t > "
+                                         "~900, R18)");
     return FSMT_OK;
 }
 
@@ -671,7 +673,7 @@ fsmt_status fsmt_begin(fsmt_ctx* ctx, uint32_t R, uint64_t seed, uint32_t restar
     const size_t nb = (size_t)F.n_bool * R, nr = (size_t)F.n_real * R, nc = (size_t)F.n_cons * R;
     const size_t parts = (size_t)update_parts(F, R);
     if ((s = alloc((void**)&S.a, nb * 4)) || (s = alloc((void**)&S.b, nr * 4)) || (s = alloc((void**)&S.ga, nb * 8)) ||
-        (s = alloc((void**)&S.gb, nr * 8)) || (s = alloc((void**)&S.U, nc)) || (s = alloc((void**)&S.obj, (size_t)R * 8)) ||
+        (s = alloc((void**)&S.gb, nr * 8)) || (s = alloc((void**)&S.U, nc * 2)) || (s = alloc((void**)&S.obj, (size_t)R * 8)) ||
         (s = alloc((void**)&S.x, nb)) || (s = alloc((void**)&S.unsat, (size_t)R * 4)) ||
         (s = alloc((void**)&S.frozen, R)) || (s = alloc((void**)&S.gm2, (size_t)R * 8)) ||
         (s = alloc((void**)&S.gm2_part, std::max<size_t>(parts, 1) * R * 8))) {
@@ -703,7 +705,7 @@ fsmt_status fsmt_begin(fsmt_ctx* ctx, uint32_t R, uint64_t seed, uint32_t restar
             return s;
         }
     }
-    CK(cudaMemsetAsync(S.U, 0, nc, ctx->stream));
+    CK(cudaMemsetAsync(S.U, 0, nc * 2, ctx->stream));
     CK(cudaMemsetAsync(S.umax, 0, (size_t)R * 4, ctx->stream));
     CK(cudaMemsetAsync(S.flags, 0, 16, ctx->stream));
     CK(cudaMemsetAsync(S.frozen, 0, R, ctx->stream));
@@ -736,18 +738,18 @@ fsmt_status fsmt_get_state(fsmt_ctx* ctx, float* a, float* b, int where) {
 }
 
 // U is kept in the internal constraint order; the ABI speaks the original order.
-fsmt_status fsmt_set_counters(fsmt_ctx* ctx, const uint8_t* U, int where) {
+fsmt_status fsmt_set_counters(fsmt_ctx* ctx, const uint16_t* U, int where) {
     fsmt_status s = need(ctx, 3, "fsmt_set_counters");
     if (s) return s;
     const size_t n = (size_t)ctx->F.n_cons * ctx->S.R;
     if (n == 0) return FSMT_OK;
     if (!U) return fail(ctx, FSMT_ERR_ARG, "null input pointer");
-    uint8_t* tmp = nullptr;
-    CK(cudaMalloc((void**)&tmp, n));
-    cudaError_t e = cudaMemcpyAsync(tmp, U, n, where == FSMT_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+    uint16_t* tmp = nullptr;
+    CK(cudaMalloc((void**)&tmp, n * 2));
+    cudaError_t e = cudaMemcpyAsync(tmp, U, n * 2, where == FSMT_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
                                     ctx->stream);
     if (e == cudaSuccess) {
-        launch_gather_rows_u8(ctx->S.U, tmp, ctx->F.orig, ctx->F.n_cons, ctx->S.R, ctx->stream);
+        launch_gather_rows_u16(ctx->S.U, tmp, ctx->F.orig, ctx->F.n_cons, ctx->S.R, ctx->stream);
         launch_umax(ctx->F, ctx->S, ctx->stream);      // the weight shift follows the new counters
         ctx->launches += 2;
         e = cudaStreamSynchronize(ctx->stream);
@@ -757,16 +759,16 @@ fsmt_status fsmt_set_counters(fsmt_ctx* ctx, const uint8_t* U, int where) {
     return check_launch(ctx);
 }
 
-fsmt_status fsmt_get_counters(fsmt_ctx* ctx, uint8_t* U, int where) {
+fsmt_status fsmt_get_counters(fsmt_ctx* ctx, uint16_t* U, int where) {
     fsmt_status s = need(ctx, 3, "fsmt_get_counters");
     if (s) return s;
     const size_t n = (size_t)ctx->F.n_cons * ctx->S.R;
     if (n == 0 || !U) return FSMT_OK;
-    uint8_t* tmp = nullptr;
-    CK(cudaMalloc((void**)&tmp, n));
-    launch_gather_rows_u8(tmp, ctx->S.U, ctx->d_pos, ctx->F.n_cons, ctx->S.R, ctx->stream);
+    uint16_t* tmp = nullptr;
+    CK(cudaMalloc((void**)&tmp, n * 2));
+    launch_gather_rows_u16(tmp, ctx->S.U, ctx->d_pos, ctx->F.n_cons, ctx->S.R, ctx->stream);
     ctx->launches += 1;
-    cudaError_t e = cudaMemcpyAsync(U, tmp, n, where == FSMT_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+    cudaError_t e = cudaMemcpyAsync(U, tmp, n * 2, where == FSMT_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
                                     ctx->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
     cudaFree(tmp);
@@ -919,8 +921,6 @@ static fsmt_status sweep_impl(fsmt_ctx* ctx, float kappa, uint32_t stage_t, doub
     const DevFormula& F = ctx->F;
     const DevState& S = ctx->S;
     const int et = et_int_of(stage_t, ctx->erwa_mode);
-    if ((uint32_t)et > kMaxStageExp)
-        return fail(ctx, FSMT_ERR_RANGE, "stage exponent e_t = (t - 2)/2 beyond the fp64 range of the ERWA weights (R18)");
     {
         Timed tm(ctx, 0);
         const float ws = wfrac_of(stage_t, ctx->erwa_mode);
@@ -999,7 +999,7 @@ static fsmt_status update_impl(fsmt_ctx* ctx, float eta, float eps, float eta_b 
 }
 
 // K5 over this context's constraints for the rounded model in S2.x (unsat into S2.unsat)
-static void verify_rounded(fsmt_ctx* ctx, const DevState& S2, uint8_t* U_update) {
+static void verify_rounded(fsmt_ctx* ctx, const DevState& S2, uint16_t* U_update) {
     if (ctx->T.n_tiles && ctx->jit.kernel5) {    // specialised check of this context's tiles
         if (ctx->has_sym) {
             launch_slot_truth(jk(ctx, S2.R).ktruth, ctx->F, S2, ctx->slots, S2.x, S2.b, ctx->stream);
@@ -1100,10 +1100,12 @@ fsmt_status fsmt_get_sweep(fsmt_ctx* ctx, double* ga, double* gb, double* obj, i
     };
     if ((s = grad_out(ga, S.ga, ctx->F.n_bool))) return s;
     if ((s = grad_out(gb, S.gb, ctx->F.n_real))) return s;
-    return copy_out(ctx, obj, S.obj, (size_t)S.R, where);
+    if ((s = copy_out(ctx, obj, S.obj, (size_t)S.R, where))) return s;
+    CK(cudaMemcpy(ctx->hflags, S.flags, 4, cudaMemcpyDeviceToHost));    // a sweep past the fp64 weight range
+    return check_flags(ctx);
 }
 
-fsmt_status fsmt_eval(fsmt_ctx* ctx, uint32_t R, const float* a, const float* b, float kappa, const uint8_t* U,
+fsmt_status fsmt_eval(fsmt_ctx* ctx, uint32_t R, const float* a, const float* b, float kappa, const uint16_t* U,
                       uint32_t stage_t, double* obj, double* grad_a, double* grad_b, int where) {
     fsmt_status s = need(ctx, 2, "fsmt_eval");
     if (s) return s;
@@ -1111,7 +1113,7 @@ fsmt_status fsmt_eval(fsmt_ctx* ctx, uint32_t R, const float* a, const float* b,
     if (ctx->stage < 3 || ctx->S.R != R) {
         if ((s = fsmt_begin(ctx, R, 0, 0))) return s;
     } else if (!U) {
-        CK(cudaMemsetAsync(ctx->S.U, 0, (size_t)ctx->F.n_cons * R, ctx->stream));
+        CK(cudaMemsetAsync(ctx->S.U, 0, (size_t)ctx->F.n_cons * R * 2, ctx->stream));
         CK(cudaMemsetAsync(ctx->S.umax, 0, (size_t)R * 4, ctx->stream));
     }
     if ((s = fsmt_set_state(ctx, a, b, where))) return s;
@@ -1439,8 +1441,7 @@ static fsmt_status solve_graph(fsmt_ctx* ctx, uint32_t steps, std::chrono::stead
         d.t = t;
         d.et_int = et_int_of(t, ctx->erwa_mode);
         d.wfrac = wfrac_of(t, ctx->erwa_mode);
-        if ((uint32_t)d.et_int > kMaxStageExp)
-            return fail(ctx, FSMT_ERR_RANGE, "stage exponent e_t = (t - 2)/2 beyond the fp64 range of the ERWA weights (R18)");
+
     }
     const uint32_t chunk = ctx->time_limit > 0 ? 16u : T;
     DevStage* d_sched = nullptr;

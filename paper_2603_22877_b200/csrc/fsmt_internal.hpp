@@ -133,6 +133,10 @@ struct KClass {
     // count class (CARD only): the sweep evaluates the constraint by its count distribution
     // (O(L^2)) instead of the xBDD's messages, and K5 counts true literals
     bool count = false;
+    // product class (OR / NAE / XOR): the COP is a closed form in leave-one-out products of the literal
+    // probabilities (OR 1 - prod pf, NAE 1 - prod pt - prod pf, XOR (1 - prod (pf - pt)) / 2; Cor.1),
+    // evaluated in O(L) with prefix / suffix products (no division, R28b)
+    bool prod = false;
     // K5 record folding: every constraint of the class has the same coefficients and strictness
     // at each atom slot (kept here, emitted as exact fp64 literals); the K5 record then holds only
     // the atoms' fp64 right-hand sides

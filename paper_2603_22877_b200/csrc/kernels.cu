@@ -214,6 +214,8 @@ __global__ void k1_prologue(DevFormula F, DevState S, float kappa, int et_int, f
             const int G = min(120, max(-100, ceil_log2(ldexp(fmax(F.fx_fb, (double)kappa * F.fx_fa), wm)) - 48));
             const int O = ceil_log2(ldexp(F.fx_sw, wm)) - 48;
             const int tail = sh + F.wexp + et_int;
+            // the largest value a sum can reach is 2^(G or O + tail + 50): beyond fp64, report
+            if (max(G, O) + tail > 960) atomicOr(S.flags, 2u);
             FxScale fx;
             fx.gs = ldexp(1.0, G + tail);
             fx.ti = ldexp(1.0, -(G + tail));
@@ -235,7 +237,7 @@ __global__ void k_scale_rows(double* __restrict__ dst, const double* __restrict_
         dst[i] = src[i] * gsc[i % R];
 }
 
-__global__ void k_umax(const uint8_t* __restrict__ U, uint32_t C, uint32_t R, uint32_t* __restrict__ umax) {
+__global__ void k_umax(const uint16_t* __restrict__ U, uint32_t C, uint32_t R, uint32_t* __restrict__ umax) {
     const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= R) return;
     uint32_t m = 0;
@@ -404,7 +406,7 @@ __global__ void k4_round(DevFormula F, DevState S, uint32_t rounding, uint64_t s
 // ---------------------------------------------------------------------------------------- K5
 
 __global__ void __launch_bounds__(256) k5_verify(DevFormula F, DevState S, const int8_t* __restrict__ x,
-                                                 const float* __restrict__ y, uint8_t* __restrict__ Uupd,
+                                                 const float* __restrict__ y, uint16_t* __restrict__ Uupd,
                                                  uint8_t* __restrict__ per_con, uint32_t cb, uint32_t ce) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t R = S.R;
@@ -440,11 +442,11 @@ __global__ void __launch_bounds__(256) k5_verify(DevFormula F, DevState S, const
         const uint32_t u = (v == kFalseT) ? 1u : 0u;            // u_c = f_c/2 + 1/2 (Alg.2 line 7)
         cnt += u;
         if (Uupd && u) {                                      // U += u: only violated constraints touch memory
-            uint8_t& cell = Uupd[(size_t)c * R + r];
+            uint16_t& cell = Uupd[(size_t)c * R + r];
             const uint32_t nv = (uint32_t)cell + 1u;
-            ovf |= nv > 255u;                                 // reported (FSMT_ERR_RANGE), never silent
-            const uint32_t nc = min(255u, nv);
-            cell = (uint8_t)nc;
+            ovf |= nv > 65535u;                               // reported (FSMT_ERR_RANGE), never silent
+            const uint32_t nc = min(65535u, nv);
+            cell = (uint16_t)nc;
             umx = max(umx, nc);
         }
         if (per_con) per_con[(size_t)F.orig[c] * R + r] = (uint8_t)u;
@@ -476,8 +478,8 @@ void launch_init(const DevFormula& F, const DevState& S, uint64_t seed, uint32_t
     if (n) k0_init<<<(unsigned)std::max<uint64_t>(blocks, 1), threads, 0, st>>>(F, S, seed, off);
 }
 
-__global__ void k_gather_rows_u8(uint8_t* __restrict__ dst, const uint8_t* __restrict__ src,
-                                 const uint32_t* __restrict__ idx, uint32_t rows, uint32_t R, int scatter) {
+__global__ void k_gather_rows_u16(uint16_t* __restrict__ dst, const uint16_t* __restrict__ src,
+                                  const uint32_t* __restrict__ idx, uint32_t rows, uint32_t R, int scatter) {
     const uint64_t n = (uint64_t)rows * R;
     for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t i = (uint32_t)(t / R), r = (uint32_t)(t % R);
@@ -486,16 +488,10 @@ __global__ void k_gather_rows_u8(uint8_t* __restrict__ dst, const uint8_t* __res
     }
 }
 
-void launch_gather_rows_u8(uint8_t* dst, const uint8_t* src, const uint32_t* idx, uint32_t rows, uint32_t R,
-                           cudaStream_t st) {
-    if (!rows || !R) return;
-    k_gather_rows_u8<<<148 * 8, 256, 0, st>>>(dst, src, idx, rows, R, 0);
-}
-
-void launch_scatter_rows_u8(uint8_t* dst, const uint8_t* src, const uint32_t* idx, uint32_t rows, uint32_t R,
+void launch_gather_rows_u16(uint16_t* dst, const uint16_t* src, const uint32_t* idx, uint32_t rows, uint32_t R,
                             cudaStream_t st) {
     if (!rows || !R) return;
-    k_gather_rows_u8<<<148 * 8, 256, 0, st>>>(dst, src, idx, rows, R, 1);
+    k_gather_rows_u16<<<148 * 8, 256, 0, st>>>(dst, src, idx, rows, R, 0);
 }
 
 void launch_sweep_jit(cudaKernel_t k, const DevFormula& F, const DevState& S, const DevTiles& T, float kappa,
@@ -509,7 +505,7 @@ void launch_sweep_jit(cudaKernel_t k, const DevFormula& F, const DevState& S, co
     if (smem > 48 * 1024) cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     uint32_t n_tiles = T.n_tiles, R = S.R, n_bool = F.n_bool;
     const float* kdev = S.ds ? &S.ds->kappa : nullptr;
-    const uint8_t* U = S.U;
+    const uint16_t* U = S.U;
     const float* PT = D ? D->PT : nullptr;
     const float* PF = D ? D->PF : nullptr;
     double* GU = D ? D->GU : nullptr;
@@ -551,7 +547,7 @@ void launch_slot_truth(cudaKernel_t k, const DevFormula& F, const DevState& S, c
 }
 
 void launch_verify_jit(cudaKernel_t k, const DevFormula& F, const DevState& S, const DevTiles& T, const int8_t* x,
-                       const float* y, uint8_t* U_update, uint8_t* per_con, cudaStream_t st, const uint8_t* TT) {
+                       const float* y, uint16_t* U_update, uint8_t* per_con, cudaStream_t st, const uint8_t* TT) {
     if (T.n_tiles == 0 || S.R == 0) return;
     const int vtot = (int)(T.vmax + T.rmax);
     const unsigned blocks = (unsigned)((uint64_t)T.n_tiles * ((S.R + 31) / 32));   // one warp per (tile, 32 restarts)
@@ -732,7 +728,7 @@ void launch_round(const DevFormula& F, const DevState& S, uint32_t rounding, uin
     k4_round<<<(unsigned)blocks, 256, 0, st>>>(F, S, rounding, seed, off, stage);
 }
 
-void launch_verify(const DevFormula& F, const DevState& S, const int8_t* x, const float* y, uint8_t* U_update,
+void launch_verify(const DevFormula& F, const DevState& S, const int8_t* x, const float* y, uint16_t* U_update,
                    uint8_t* per_con, cudaStream_t st, uint32_t cb, uint32_t ce) {
     if (ce == UINT32_MAX) ce = F.n_cons;
     if (ce <= cb || S.R == 0) return;

@@ -103,7 +103,7 @@ struct DevState {
     float* b;          // [n_real][R]
     double* ga;        // [n_bool][R] gradient in grid units (times gsc[r]: FxScale)
     double* gb;        // [n_real][R] gradient in grid units
-    uint8_t* U;        // [C][R]
+    uint16_t* U;       // [C][R] ERWA violation counts (R18)
     double* obj;       // [R]
     int8_t* x;         // [n_bool][R]
     uint32_t* unsat;   // [R]
@@ -119,7 +119,8 @@ struct DevState {
     FxScale* fx;       // [R] per-restart scales of the current sweep (k1_prologue)
     const DevStage* ds = nullptr;   // device-side stage parameters (graph solve loop), or null
     double* gsc;       // [R] fx[r].gs (grid scale of the gradients, read by K3 / the output copy)
-    uint32_t* flags;   // [4] bit 0 of flags[0]: an ERWA counter passed 255
+    uint32_t* flags;   // [4] flags[0]: bit 0 an ERWA counter reached 65535, bit 1 ERWA weights 2^(U + e_t)
+                       //     beyond the fp64 range of the accumulation (FSMT_ERR_RANGE)
 };
 
 int sweep_smem_bytes(const DevFormula& F, int warps);
@@ -165,13 +166,11 @@ void launch_slot_truth(cudaKernel_t k, const DevFormula& F, const DevState& S, c
                        const float* y, cudaStream_t st);
 // K5 (JIT-specialised, tiles): exact check over the tiles of T (+ ERWA counters / per_con).
 void launch_verify_jit(cudaKernel_t k, const DevFormula& F, const DevState& S, const DevTiles& T, const int8_t* x,
-                       const float* y, uint8_t* U_update, uint8_t* per_con, cudaStream_t st, const uint8_t* TT = nullptr);
+                       const float* y, uint16_t* U_update, uint8_t* per_con, cudaStream_t st, const uint8_t* TT = nullptr);
 void launch_sweep_jit(cudaKernel_t k, const DevFormula& F, const DevState& S, const DevTiles& T, float kappa,
                       double* terms, uint32_t terms_r, cudaStream_t st, const DevSlots* D = nullptr);
-// row gather for u8 matrices: dst[i][:] = src[idx[i]][:]  (U between original and internal order)
-void launch_gather_rows_u8(uint8_t* dst, const uint8_t* src, const uint32_t* idx, uint32_t rows, uint32_t R,
-                           cudaStream_t st);
-void launch_scatter_rows_u8(uint8_t* dst, const uint8_t* src, const uint32_t* idx, uint32_t rows, uint32_t R,
+// row gather for u16 matrices: dst[i][:] = src[idx[i]][:]  (U between original and internal order)
+void launch_gather_rows_u16(uint16_t* dst, const uint16_t* src, const uint32_t* idx, uint32_t rows, uint32_t R,
                             cudaStream_t st);
 // K3: projected step (three launches: partial norms, finalize, apply).
 int update_parts(const DevFormula& F, uint32_t R);   // parts of the K3 norm (size of gm2_part / R)
@@ -195,7 +194,7 @@ void launch_round(const DevFormula& F, const DevState& S, uint32_t rounding, uin
                   uint32_t stage, cudaStream_t st);
 // K5: exact verification + ERWA counter update (R18, R22).
 // K5 over internal constraints [cb, ce) (ce = UINT32_MAX: to the end).
-void launch_verify(const DevFormula& F, const DevState& S, const int8_t* x, const float* y, uint8_t* U_update,
+void launch_verify(const DevFormula& F, const DevState& S, const int8_t* x, const float* y, uint16_t* U_update,
                    uint8_t* per_con, cudaStream_t st, uint32_t cb = 0, uint32_t ce = UINT32_MAX);
 
 }  // namespace fsmt

@@ -102,7 +102,9 @@ Plan make_plan(const Formula& f, const Built& b, bool enable_jit) {
                 const bool big = kc.stmpl.nodes.size() > kJitMaxNodesSym;
                 kc.count = kind == K_CARD && Ls <= kCountMaxL && kc.stmpl.root >= 0 && kk < Ls &&
                            (ce ? ce[0] == '1' : big);
-                kc.jit = enable_jit && (!big || kc.count) && Ls <= kJitMaxRefs && kc.stmpl.root >= 0;
+                const char* pe = getenv("FSMT_JIT_PROD");
+                kc.prod = kind != K_CARD && Ls <= kCountMaxL && kc.stmpl.root >= 0 && !(pe && pe[0] == '0');
+                kc.jit = enable_jit && (!big || kc.count || kc.prod) && Ls <= kJitMaxRefs && kc.stmpl.root >= 0;
                 kc.n_cons = 0;
                 p.kclasses.push_back(kc);
             } else {
@@ -735,7 +737,7 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
     o << "template <bool DBG> __device__ __forceinline__ void kc" << kid
       << "(const TileDesc& T, const uint4* __restrict__ rp, const u32* __restrict__ vs, const u32* __restrict__ vr,\n"
          "    " << TY << "* __restrict__ accs, const float* __restrict__ ab, const float* __restrict__ bb,\n"
-         "    double* __restrict__ ga, double* __restrict__ gb, const unsigned char* __restrict__ U,\n"
+         "    double* __restrict__ ga, double* __restrict__ gb, const unsigned short* __restrict__ U,\n"
          "    u32 R, u32 R4, u64 rr, u32 r, bool live, u32 n_bool, float kq, float dcoef, int ebias,\n"
          "    float gif, float& objacc,\n"
          "    double* __restrict__ terms, u32 terms_r, const u32* __restrict__ orig,\n"
@@ -793,7 +795,7 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
     const char* uld = "__ldg";
     const std::string ucast = "";
     if (upf > 0) {
-        o << "  const unsigned char* Up = hasU ? U + (u64)T.cons_begin * R + rr : nullptr;\n";
+        o << "  const unsigned short* Up = hasU ? U + (u64)T.cons_begin * R + rr : nullptr;\n";
         for (int k = 0; k < upf; ++k)
             o << "  u32 un" << k << " = (hasU && " << k << "u < T.n_cons) ? (u32)" << uld << "(" << ucast << "(Up + (u64)" << k << "u * R)) : 0u;\n";
     }
@@ -944,7 +946,7 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
     // which is Alg.F/Alg.B over n, h, l regrouped (P_X + P_Y = 1).  For two Boolean slots
     // P_X = (1 + v_s v_s')/2 and pt - pf = -v.
     // (A count class has no node passes: nn = 0 and the count DP below sets pT and G.)
-    const size_t nn = K.count ? 0 : t.nodes.size();
+    const size_t nn = (K.count || K.prod) ? 0 : t.nodes.size();
     std::vector<int> indeg(nn, 0);
     for (size_t v = 0; v < nn; ++v) {
         if (t.nodes[v].hi >= 0) ++indeg[t.nodes[v].hi];
@@ -1103,6 +1105,39 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
         else if (bh == "0.f") gfma(nd.level, mv, "(-" + bl + ")");
         else gfma(nd.level, mv, "(" + bh + " - " + bl + ")");
     }
+    if (K.prod) {
+        // OR / NAE / XOR over the L literals (pt_s = P(literal s true)): the COP in closed form and
+        // dCOP/dpt_s from leave-one-out products, prefix products in registers times a running suffix:
+        //   OR:  COP = 1 - prod pf,              G_s = prod_{j != s} pf_j
+        //   NAE: COP = 1 - prod pt - prod pf,    G_s = prod_{j != s} pf_j - prod_{j != s} pt_j
+        //   XOR: COP = (1 - prod d) / 2, d = pf - pt (E[(-1)^count]),  G_s = prod_{j != s} d_j
+        // (pf_s = 1 - pt_s in the derivative; Eq.8 / Cor.1 for symmetric constraints)
+        const uint32_t L = (uint32_t)ns, kind = K.sym_kind;
+        auto S = [](uint32_t s) { return std::to_string(s); };
+        if (kind == K_XOR)
+            for (uint32_t s2 = 0; s2 < L; ++s2) o << "    const float xd" << s2 << " = pf" << s2 << " - pt" << s2 << ";\n";
+        const std::string f1 = kind == K_XOR ? "xd" : "pf";          // the product every kind uses
+        o << "    float ua0 = 1.f;";
+        for (uint32_t s2 = 1; s2 <= L; ++s2) o << " const float ua" << s2 << " = ua" << s2 - 1 << (s2 == 1 ? "" : "") << " * " << f1 << S(s2 - 1) << ";";
+        o << "\n";
+        if (kind == K_NAE) {
+            o << "    float va0 = 1.f;";
+            for (uint32_t s2 = 1; s2 <= L; ++s2) o << " const float va" << s2 << " = va" << s2 - 1 << " * pt" << S(s2 - 1) << ";";
+            o << "\n    pT = 1.f - ua" << L << " - va" << L << ";\n";
+        } else if (kind == K_XOR) {
+            o << "    pT = 0.5f * (1.f - ua" << L << ");\n";
+        } else {
+            o << "    pT = 1.f - ua" << L << ";\n";
+        }
+        o << "    { float ub = 1.f" << (kind == K_NAE ? ", vb = 1.f" : "") << ";\n";
+        for (uint32_t s2 = L; s2-- > 0;) {
+            if (kind == K_NAE)
+                o << "      G" << s2 << " = fmaf(ua" << s2 << ", ub, -(va" << s2 << " * vb)); ub *= pf" << s2 << "; vb *= pt" << s2 << ";\n";
+            else
+                o << "      G" << s2 << " = ua" << s2 << " * ub; ub *= " << f1 << s2 << ";\n";
+        }
+        o << "    }\n";
+    }
     if (K.count) {
         // CARD(L, k) by its count distribution ("O((n+k)^2)" for symmetric literals): with
         // pt_s = P(literal s true), q_c = P(c of the literals true) by the DP q'_c = q_c pf + q_{c-1} pt
@@ -1199,7 +1234,7 @@ void emit_verify_class(std::ostringstream& o, uint32_t kid, const KClass& K, con
     const size_t ns = t.kinds.size();
     o << "__device__ __forceinline__ u32 kv" << kid
       << "(const TileDesc& T, const uint4* __restrict__ rp, const uint4* __restrict__ vp, const u32* __restrict__ vs,\n"
-         "    const u32* __restrict__ vr, const signed char* __restrict__ x, const float* __restrict__ y, unsigned char* __restrict__ U,\n"
+         "    const u32* __restrict__ vr, const signed char* __restrict__ x, const float* __restrict__ y, unsigned short* __restrict__ U,\n"
          "    unsigned char* __restrict__ per_con, const u32* __restrict__ orig, u32 R, u64 rr, u32 r, bool live,\n"
          "    u32 n_bool, const u32* __restrict__ arow, const double* __restrict__ aval,\n"
          "    const double* __restrict__ arhs, const unsigned char* __restrict__ astrict,\n"
@@ -1313,10 +1348,14 @@ void emit_verify_class(std::ostringstream& o, uint32_t kid, const KClass& K, con
         if (child >= 0) return "s" + std::to_string(child);
         return child == kTrue ? "true" : "false";
     };
-    if (K.count) {   // CARD(L, k): satisfied iff at most k literals are true
+    if (K.count || K.prod) {   // symmetric: satisfied by the number of true literals
         o << "    u32 nt = 0u;";
         for (size_t s = 0; s < ns; ++s) o << " nt += (u32)t" << s << ";";
-        o << "\n    const u32 u = nt <= " << K.sym_k << "u ? 0u : 1u;\n";
+        const std::string sat = K.sym_kind == K_CARD ? "nt <= " + std::to_string(K.sym_k) + "u"
+                              : K.sym_kind == K_OR   ? std::string("nt >= 1u")
+                              : K.sym_kind == K_NAE  ? "(nt >= 1u && nt < " + std::to_string(ns) + "u)"
+                                                     : std::string("(nt & 1u)");
+        o << "\n    const u32 u = " << sat << " ? 0u : 1u;\n";
     } else {
         for (size_t vv = t.nodes.size(); vv-- > 0;) {
             const TNode& nd = t.nodes[vv];
@@ -1327,12 +1366,12 @@ void emit_verify_class(std::ostringstream& o, uint32_t kid, const KClass& K, con
     }
     o << ""
          "    if (live) {\n"
-         "      if (U && u) {   // U += u (R18): only violated constraints touch memory; > 255 is reported\n"
-         "        unsigned char* cell = U + (u64)(T.cons_begin + c) * R + rr;\n"
+         "      if (U && u) {   // U += u (R18): only violated constraints touch memory; past 65535 is reported\n"
+         "        unsigned short* cell = U + (u64)(T.cons_begin + c) * R + rr;\n"
          "        const u32 nv = (u32)*cell + 1u;\n"
-         "        ovf |= nv > 255u;\n"
-         "        const u32 nc = nv > 255u ? 255u : nv;\n"
-         "        *cell = (unsigned char)nc;\n"
+         "        ovf |= nv > 65535u;\n"
+         "        const u32 nc = nv > 65535u ? 65535u : nv;\n"
+         "        *cell = (unsigned short)nc;\n"
          "        umx = umx > nc ? umx : nc;\n"
          "      }\n"
          "      if (per_con) per_con[(u64)orig[T.cons_begin + c] * R + rr] = (unsigned char)u;\n"
@@ -1368,7 +1407,7 @@ std::string jit_source(const Formula& f, const Built& b, const Plan& p, int u_pr
       << ") " << (kv >= 0 ? "fsmt_k1_c" + std::to_string(kv) : std::string(dbgk ? "fsmt_k1_jit_dbg" : "fsmt_k1_jit")) << "(\n"
          "    const TileDesc* __restrict__ tiles, u32 n_tiles, const uint4* __restrict__ recs,\n"
          "    const u32* __restrict__ tile_vars, const float* __restrict__ a, const float* __restrict__ b,\n"
-         "    double* __restrict__ ga, double* __restrict__ gb, const unsigned char* __restrict__ U,\n"
+         "    double* __restrict__ ga, double* __restrict__ gb, const unsigned short* __restrict__ U,\n"
          "    double* __restrict__ obj, u32 R, u32 n_bool, float kappa,\n"
          "    double* __restrict__ terms, u32 terms_r, const u32* __restrict__ orig,\n"
          "    const float* __restrict__ PT, const float* __restrict__ PF, double* __restrict__ gu,\n"
@@ -1430,7 +1469,7 @@ std::string jit_source(const Formula& f, const Built& b, const Plan& p, int u_pr
     o << "extern \"C\" __global__ void __launch_bounds__(32) fsmt_k5_jit(\n"
          "    const TileDesc* __restrict__ tiles, u32 n_tiles, const uint4* __restrict__ recs,\n"
          "    const uint4* __restrict__ vrecs, const u32* __restrict__ tile_vars, const signed char* __restrict__ x,\n"
-         "    const float* __restrict__ y, unsigned char* __restrict__ U, u32* __restrict__ unsat,\n"
+         "    const float* __restrict__ y, unsigned short* __restrict__ U, u32* __restrict__ unsat,\n"
          "    unsigned char* __restrict__ per_con, const u32* __restrict__ orig, u32 R, u32 n_bool,\n"
          "    const u32* __restrict__ arow, const double* __restrict__ aval, const double* __restrict__ arhs,\n"
          "    const unsigned char* __restrict__ astrict, const unsigned char* __restrict__ TT,\n"
@@ -1462,7 +1501,7 @@ std::string jit_source(const Formula& f, const Built& b, const Plan& p, int u_pr
     o << "    default: break;\n  }\n"
          "  if (live && cnt) atomicAdd(unsat + r, cnt);\n"
          "  if (live && umx) atomicMax(umax + r, umx);   // the restart's largest counter (k1_prologue's shift)\n"
-         "  if (ovf) atomicOr(flags, 1u);                 // a counter passed 255: fsmt_stage_end fails (FSMT_ERR_RANGE)\n"
+         "  if (ovf) atomicOr(flags, 1u);                 // a counter passed 65535: fsmt_stage_end fails (FSMT_ERR_RANGE)\n"
          "}\n";
     // slot tables for the symmetric classes: probabilities of every Boolean and
     // table atom once per sweep, the row gradients chained back to grad_a / grad_b, and the rows'

@@ -75,7 +75,7 @@ class Solver:
         a = np.ascontiguousarray(a, dtype=np.float32)
         b = np.ascontiguousarray(b, dtype=np.float32)
         R = a.shape[1] if a.ndim == 2 and a.shape[0] else b.shape[1]
-        u = None if U is None else np.ascontiguousarray(U, dtype=np.uint8)
+        u = None if U is None else np.ascontiguousarray(U, dtype=np.uint16)
         obj = np.empty(R, dtype=np.float64)
         ga = np.empty((self.dims.n_bool, R), dtype=np.float64)
         gb = np.empty((self.dims.n_real, R), dtype=np.float64)
@@ -150,11 +150,14 @@ class Solver:
         return a, b
 
     def set_counters(self, U):
-        p, w = N._ptr(U, np.uint8)
+        """U[n_cons][R] ERWA violation counts (u16; host arrays of any integer dtype are converted)."""
+        if isinstance(U, np.ndarray):
+            U = np.ascontiguousarray(U, dtype=np.uint16)
+        p, w = N._ptr(U, np.uint16)
         self._check(N.lib.fsmt_set_counters(self._h, p, w))
 
     def get_counters(self):
-        U = np.empty((self.dims.n_cons, self.R), dtype=np.uint8)
+        U = np.empty((self.dims.n_cons, self.R), dtype=np.uint16)
         self._check(N.lib.fsmt_get_counters(self._h, U.ctypes.data, N.HOST))
         return U
 

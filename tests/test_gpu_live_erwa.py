@@ -258,8 +258,9 @@ def test_erwa_300_stages_verbatim_at_the_witness():
 
 
 def test_erwa_counter_overflow_is_reported():
-    """U is a u8 count of violations (R18); the 256th violation of a constraint in a restart is
-    reported as FSMT_ERR_RANGE (the counter is held at 255), never silently saturated."""
+    """U is a u16 count of violations (R18); the 65536th violation of a constraint in a restart is
+    reported as FSMT_ERR_RANGE (the counter is held at 65535), never silently saturated.  A sweep whose
+    weights 2^(U + e_t) leave the fp64 range (U = 1000 here) is reported the same way."""
     import paper_2603_22877_b200 as P
     from paper_2603_22877_b200 import native as N
     inst = fsmt_gen.config("cfg4s")
@@ -269,18 +270,26 @@ def test_erwa_counter_overflow_is_reported():
     s.begin(Rr, 1)
     a, b = random_points(f.n_bool, f.n_real, Rr, seed=5, b_lo=0.0, b_hi=1.0)
     s.set_state(a, b)
-    U = np.full((len(f.constraints), Rr), 254, dtype=np.uint8)
+    U = np.full((len(f.constraints), Rr), 65534, dtype=np.uint16)
     s.set_counters(U)
-    u1 = s.stage_end(1)                               # 254 -> 255: fine
+    u1 = s.stage_end(1)                               # 65534 -> 65535: fine
     assert u1.sum() > 0
     with pytest.raises(P.FsmtError) as ei:
-        s.stage_end(2)                                # 255 -> 256: reported
+        s.stage_end(2)                                # 65535 -> 65536: reported
     assert ei.value.status == N.ERR_RANGE
-    assert s.get_counters().max() == 255
+    assert s.get_counters().max() == 65535
+    s2 = _solver(P, inst.text)
+    s2.begin(Rr, 1)
+    s2.set_state(a, b)
+    s2.set_counters(np.full((len(f.constraints), Rr), 1000, dtype=np.uint16))
+    s2.sweep(1.0, 1)
+    with pytest.raises(P.FsmtError) as ei:
+        s2.get_sweep()
+    assert ei.value.status == N.ERR_RANGE
 
 
 def test_cfg4_large_r_sampled():
-    """SURVEY §8(d) config 5 scale: cfg4 at R = 16,384 restarts (U 11.6 GB, state 0.7 GB: beyond the
+    """SURVEY §8(d) config 5 scale: cfg4 at R = 16,384 restarts (U 23 GB, state 0.7 GB: beyond the
     L2, so the stream values come from HBM) with the kernels fsmt_prepare(16384) builds; the K0 init
     point of sampled restarts in three different warps and restart blocks, sampled variables'
     gradients and E_c against the oracle."""
