@@ -100,3 +100,35 @@ def test_count_form_matches_xbdd_form_cfg2_and_rand100():
             check_objective(out[1][0][r], C, float(len(f.constraints)), what=f"{name} count")
             check_gradient(out[1][1][:, r], oga, what=f"{name} count grad_a")
             check_gradient(out[1][2][:, r], ogb, what=f"{name} count grad_b")
+
+
+def test_product_form_matches_xbdd_form_cfg2_and_rand100():
+    """OR / NAE / XOR over symmetric literals: the closed-form product classes (default, DESIGN.md
+    §7 item 15) and their xBDD classes (FSMT_JIT_PROD=0) agree (fp32 rounding) and both match the
+    oracle, with live ERWA counters at t = 4."""
+    import paper_2603_22877_b200 as P
+    for name in ("rand100", "cfg2"):
+        inst = fsmt_gen.config(name)
+        f = hsmt.parse(inst.text)
+        pr = _solver(P, inst.text)
+        xb = _solver(P, inst.text, {"FSMT_JIT_PROD": "0"})
+        R = 40
+        a, b = random_points(f.n_bool, f.n_real, R, seed=19)
+        U = random_counters(len(f.constraints), R, seed=20, max_u=3)
+        out = []
+        for s in (pr, xb):
+            s.begin(R, 1)
+            s.set_state(a, b)
+            s.set_counters(U)
+            s.sweep(0.8, 4)
+            out.append(s.get_sweep())
+        for A, B in zip(out[0], out[1]):
+            np.testing.assert_allclose(A, B, rtol=1e-5, atol=2e-6 * float(np.max(np.abs(B)) or 1.0))
+        for r in (0, R - 1):
+            w = np.array([c.weight for c in f.constraints]) * 2.0 ** (U[:, r].astype(np.float64) + 1.0)
+            C, oga, ogb = objective.objective_and_gradient_grouped(f, a[:, r], b[:, r], 0.8, w)
+            for k, (obj, ga, gb) in enumerate(out):
+                what = f"{name} {'product' if k == 0 else 'xbdd'} r={r}"
+                check_objective(obj[r], C, float(w.sum()), what=what)
+                check_gradient(np.concatenate([ga[:, r], gb[:, r]]), np.concatenate([oga, ogb]), scale_relative=True,
+                               what=what)
