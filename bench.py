@@ -55,6 +55,8 @@ def parse_args():
     p.add_argument("--restarts", type=int, default=1024)
     p.add_argument("--pgd-steps", type=int, default=8)
     p.add_argument("--mode", default="restart", choices=["restart", "constraint"])
+    p.add_argument("--nvls", action="store_true", help="constraint mode: C4 as the in-switch multicast all-reduce "
+                   "(fsmt_mc_allreduce_f64 on symmetric memory) instead of NCCL")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -340,7 +342,7 @@ def main():
     if constraint_mode:
         s.shard(rank, world, 1)
         s.begin(R, seed=12345, restart_offset=0)
-        bufs = D.ConstraintShardedBuffers(s, dims["n_bool"], dims["n_real"], R)
+        bufs = D.ConstraintShardedBuffers(s, dims["n_bool"], dims["n_real"], R, nvls=args.nvls)
         eta_a, eta_b = s.step_sizes(KAPPA)
 
         def step(t):
@@ -439,12 +441,12 @@ def main():
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {**workload_config(args, dims["n_bool"] + dims["n_real"], dims["n_cons"], world),
                        "kernels": "generic" if args.no_prepare else "specialised for R (fsmt_prepare)",
-                       "parallelism": (f"constraint-sharded x{world} (one flat all-reduce per PGD step)" if constraint_mode
+                       "parallelism": (f"constraint-sharded x{world} (one flat {'NVLS multicast' if args.nvls else 'NCCL'} all-reduce per PGD step)" if constraint_mode
                                        else f"restart-sharded x{world}"),
-                       "l2": "inputs exceed L2 (U counters %.0f MB + structure + state per step)" % (dims["n_cons"] * R / 1e6),
+                       "l2": "inputs exceed L2 (u16 U counters %.0f MB + structure + state per step)" % (dims["n_cons"] * R * 2 / 1e6),
                        "accumulation": "fp64, exact on-grid sums (deterministic)", "build_s": round(build_s, 2)},
             "roofline": {"bound": "alu", "achieved": alu_achieved, "peak": alu_peak, "unit": "TFLOP/s",
-                         "frac": alu_achieved / alu_peak, "traffic": traffic, "kernel": "fsmt_k1_jit",
+                         "frac": alu_achieved / alu_peak, "traffic": traffic, "kernel": "fsmt_k1_c0 (+ fsmt_k1_c1 concurrently; the JIT sweep of cfg4's two classes)" if args.config == "cfg4" else "fsmt_k1_jit / fsmt_k1_c<k>",
                          "basis": f"SURVEY 8(d) model {fma_pe:.0f} FMA-eq (x2 flop) per (constraint,restart) eval x "
                                   f"{evals_per_launch:.0f} evals per launch / live CUDA-event launch time; peak = 148 SMs x "
                                   f"128 FP32 lanes x 2 x {sm_max:.0f} MHz (DESIGN.md §7)",

@@ -246,6 +246,19 @@ fsmt_status fsmt_bind_slot_grads(fsmt_ctx* ctx, void* gu);
  * must keep them alive; the ctx's kernels run on its bound stream (fsmt_bind_stream). */
 fsmt_status fsmt_bind_buffers(fsmt_ctx* ctx, void* grad_a, void* grad_b, void* obj, void* unsat, void* umax);
 
+/* C4 through the NVSwitch (P:690-696 runs the method on 8 GPUs): an in-switch
+ * all-reduce SUM of n f64 elements of a MULTICAST buffer (NVLS) -- the flat [grad_a | grad_b | obj |
+ * slot rows] buffer of the constraint-sharded mode, allocated as symmetric memory on every rank
+ * (e.g. torch.distributed._symmetric_memory) with mc_ptr its multicast address.  Rank k reduces the
+ * elements [k n / world, (k+1) n / world) with multimem.ld_reduce.add.f64 (the switch adds the
+ * world ranks' copies) and multimem.st's the sum back to every rank's copy.  The values are on-grid
+ * integers (fsmt_sweep's exact sums), so the switch's fp64 adds are exact and the result is bit-for-
+ * bit the NCCL all-reduce's.  The caller brackets the call with a device barrier across the ranks
+ * (every rank's sweep finished before; every rank's stores landed after).  Runs on the ctx's bound
+ * stream; FSMT_ERR_ARG for a null mc_ptr, world == 0 or rank >= world.  Needs >= 2 GPUs behind
+ * NVSwitch with multicast support (not testable on one GPU). */
+fsmt_status fsmt_mc_allreduce_f64(fsmt_ctx* ctx, void* mc_ptr, uint64_t n, uint32_t rank, uint32_t world);
+
 /* Rounded model of one restart from the last stage_end: x[n_bool] (-1/+1), y[n_real] (host). */
 fsmt_status fsmt_get_model(fsmt_ctx* ctx, uint32_t restart, int8_t* x_out, float* y_out);
 /* Rounded Booleans of all restarts from the last stage_end: x[n_bool][R] int8 (where). */

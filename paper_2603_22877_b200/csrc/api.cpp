@@ -538,7 +538,11 @@ fsmt_status fsmt_build_xbdd(fsmt_ctx* ctx, uint64_t node_budget) {
             ctx->T.recs = rp;
             ctx->T.tile_vars = vp;
             ctx->T.vmax = P.kernel_vmax();
-            ctx->T.rmax = P.rmax;
+            // run-variable id slots the tiles actually use (<= Plan::rmax): the sweep's shared memory
+            // is sized by it, so more one-warp CTAs fit per SM
+            uint32_t rmax_used = 1;
+            for (const TileDesc& td : P.tiles) rmax_used = std::max(rmax_used, td.n_vars >> 16);
+            ctx->T.rmax = rmax_used;
             const uint32_t* vr = nullptr;
             s = upload(ctx, P.vrecs, vr, ctx->fallocs);
             if (s) return s;
@@ -672,14 +676,18 @@ fsmt_status fsmt_begin(fsmt_ctx* ctx, uint32_t R, uint64_t seed, uint32_t restar
     };
     const size_t nb = (size_t)F.n_bool * R, nr = (size_t)F.n_real * R, nc = (size_t)F.n_cons * R;
     const size_t parts = (size_t)update_parts(F, R);
-    if ((s = alloc((void**)&S.a, nb * 4)) || (s = alloc((void**)&S.b, nr * 4)) || (s = alloc((void**)&S.ga, nb * 8)) ||
-        (s = alloc((void**)&S.gb, nr * 8)) || (s = alloc((void**)&S.U, nc * 2)) || (s = alloc((void**)&S.obj, (size_t)R * 8)) ||
+    // grad_a and grad_b are one allocation ([var][R] over the unified variable id: gb = ga + nb), so
+    // a stream row flushes to ga + g*R whatever the variable's kind; U has kUPad spare constraint
+    // rows so the sweep's U prefetch may read past the last tile without a bounds test
+    if ((s = alloc((void**)&S.a, nb * 4)) || (s = alloc((void**)&S.b, nr * 4)) || (s = alloc((void**)&S.ga, (nb + nr) * 8)) ||
+        (s = alloc((void**)&S.U, (nc + (size_t)kUPad * R) * 2)) || (s = alloc((void**)&S.obj, (size_t)R * 8)) ||
         (s = alloc((void**)&S.x, nb)) || (s = alloc((void**)&S.unsat, (size_t)R * 4)) ||
         (s = alloc((void**)&S.frozen, R)) || (s = alloc((void**)&S.gm2, (size_t)R * 8)) ||
         (s = alloc((void**)&S.gm2_part, std::max<size_t>(parts, 1) * R * 8))) {
         drop_state(ctx);
         return s;
     }
+    S.gb = S.ga + nb;
     if (ctx->has_sym) {   // slot tables (rows: Booleans, reals (unused), table atoms)
         DevSlots& D = ctx->slots;
         const size_t rows = (size_t)D.nv + D.n_sa;
@@ -705,7 +713,7 @@ fsmt_status fsmt_begin(fsmt_ctx* ctx, uint32_t R, uint64_t seed, uint32_t restar
             return s;
         }
     }
-    CK(cudaMemsetAsync(S.U, 0, nc * 2, ctx->stream));
+    CK(cudaMemsetAsync(S.U, 0, (nc + (size_t)kUPad * R) * 2, ctx->stream));
     CK(cudaMemsetAsync(S.umax, 0, (size_t)R * 4, ctx->stream));
     CK(cudaMemsetAsync(S.flags, 0, 16, ctx->stream));
     CK(cudaMemsetAsync(S.frozen, 0, R, ctx->stream));
@@ -839,7 +847,7 @@ static long spill_stores(const std::string& log, const std::string& kernel) {
 // then 28 one-warp CTAs per SM: 64 / 72 registers) whose compile has no spills, else no cap
 // (cfg3 best at 64, cfg4 at 72, cfg2 uncapped)
 static std::string prepared_source_tuned(const fsmt_ctx* ctx, uint32_t R, int* cap) {
-    for (int mc : {32, 28}) {
+    for (int mc : {32, 28, 24}) {
         const std::string src = prepared_source(ctx, R, mc);
         std::vector<char> cubin;
         std::string log, err;
@@ -882,7 +890,7 @@ fsmt_status fsmt_prepare(fsmt_ctx* ctx, uint32_t R) {
         cudaFuncAttributes fa{};
         return cudaFuncGetAttributes(&fa, (const void*)k) != cudaSuccess || fa.localSizeBytes > 0;
     };
-    for (int mc : {32, 28}) {
+    for (int mc : {32, 28, 24}) {
         JitKernel cand;
         if (!jit_compile(prepared_source(ctx, R, mc), cand, err)) continue;
         if (!cap_found && !spills(cand.kernel)) {
@@ -1232,6 +1240,17 @@ fsmt_status fsmt_bind_buffers(fsmt_ctx* ctx, void* grad_a, void* grad_b, void* o
     if (umax) ctx->S.umax = (uint32_t*)umax;
     CK(cudaStreamSynchronize(ctx->stream));
     return FSMT_OK;
+}
+
+fsmt_status fsmt_mc_allreduce_f64(fsmt_ctx* ctx, void* mc_ptr, uint64_t n, uint32_t rank, uint32_t world) {
+    if (!ctx) return FSMT_ERR_ARG;
+    if (ctx->host_only) return fail(ctx, FSMT_ERR_CUDA, "fsmt_mc_allreduce_f64: host-only context has no device");
+    if (!mc_ptr || world == 0 || rank >= world) return fail(ctx, FSMT_ERR_ARG, "fsmt_mc_allreduce_f64: null multicast pointer or bad rank");
+    if (n == 0) return FSMT_OK;
+    cudaSetDevice(ctx->device);
+    launch_mc_allreduce_f64((double*)mc_ptr, n, rank, world, ctx->stream);
+    ctx->launches += 1;
+    return check_launch(ctx);
 }
 
 fsmt_status fsmt_run_stage(fsmt_ctx* ctx, uint32_t stage_t, float kappa, uint32_t steps, uint32_t* unsat_out,

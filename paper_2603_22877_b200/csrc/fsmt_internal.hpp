@@ -101,6 +101,7 @@ struct Built {
 constexpr uint32_t kTileVmaxDefault = 48;    // stream variables (shared-memory rows) per tile (FSMT_TILE_VMAX)
 constexpr uint32_t kTileRmaxDefault = 128;   // run variables per tile (FSMT_TILE_RMAX)
 constexpr uint32_t kTileCmax = 64;        // constraints per tile
+constexpr uint32_t kUPad = 16;            // spare constraint rows after U (the sweep's U prefetch, <= 12 ahead)
 constexpr uint32_t kGroupVarsDefault = 64;   // variables per footprint group (VMAX/2)
 
 struct KClass {

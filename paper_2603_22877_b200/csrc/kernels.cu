@@ -738,4 +738,25 @@ void launch_verify(const DevFormula& F, const DevState& S, const int8_t* x, cons
     k5_verify<<<(unsigned)blocks, 256, 0, st>>>(F, S, x, y, U_update, per_con, cb, ce);
 }
 
+// ------------------------------------------------------------------------- C4 through the NVSwitch
+// One-shot in-switch all-reduce of a multicast f64 buffer (fsmt_mc_allreduce_f64): each rank owns a
+// contiguous slice; multimem.ld_reduce returns the sum over the ranks' copies (computed in the
+// switch), multimem.st writes it to every rank's copy.  sm_90+ PTX; f64 has no vector form.
+namespace {
+__global__ void k_mc_allreduce_f64(double* __restrict__ mc, uint64_t lo, uint64_t hi) {
+    for (uint64_t i = lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < hi; i += (uint64_t)gridDim.x * blockDim.x) {
+        double v;
+        asm volatile("multimem.ld_reduce.relaxed.sys.global.add.f64 %0, [%1];" : "=d"(v) : "l"(mc + i) : "memory");
+        asm volatile("multimem.st.relaxed.sys.global.f64 [%0], %1;" ::"l"(mc + i), "d"(v) : "memory");
+    }
+}
+}  // namespace
+
+void launch_mc_allreduce_f64(double* mc, uint64_t n, uint32_t rank, uint32_t world, cudaStream_t st) {
+    const uint64_t lo = n * rank / world, hi = n * (rank + 1) / world;
+    if (hi <= lo) return;
+    const uint64_t blocks = std::min<uint64_t>((hi - lo + 255) / 256, 148ull * 8);
+    k_mc_allreduce_f64<<<(unsigned)blocks, 256, 0, st>>>(mc, lo, hi);
+}
+
 }  // namespace fsmt

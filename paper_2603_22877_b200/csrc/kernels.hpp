@@ -137,6 +137,8 @@ void launch_prologue(const DevFormula& F, const DevState& S, float kappa, int et
                      uint64_t gu_rows, cudaStream_t st);
 // umax[r] = max_c U[c][r] (after fsmt_set_counters).
 void launch_umax(const DevFormula& F, const DevState& S, cudaStream_t st);
+// C4 in the switch: multimem all-reduce SUM of this rank's slice of a multicast f64 buffer (NVLS)
+void launch_mc_allreduce_f64(double* mc, uint64_t n, uint32_t rank, uint32_t world, cudaStream_t st);
 // dst[i][r] = src[i][r] * gsc[r] (grid units -> gradient), rows x R doubles.
 void launch_scale_rows(double* dst, const double* src, const double* gsc, uint64_t rows, uint32_t R, cudaStream_t st);
 // K1 (JIT-specialised, tiles): see tiles.cpp / jit.cpp.

@@ -569,6 +569,20 @@ Plan make_plan(const Formula& f, const Built& b, bool enable_jit) {
         varies[k].assign(p.kclasses[k].words, fold ? 0 : 1);
         first[k].assign(p.kclasses[k].words, 0);
     }
+    // a reference word whose two references are both aliases or affine-group members is never read
+    // (K1 and K5 address those from their target / group head): dropped like a constant word
+    // (cfg4: 16 -> 8 words per record, half the record loads)
+    std::vector<std::vector<uint8_t>> unread(p.n_jit_kclasses);
+    for (uint32_t k = 0; k < p.n_jit_kclasses; ++k) {
+        const KClass& K = p.kclasses[k];
+        unread[k].assign(K.words, 0);
+        if (!fold) continue;
+        auto skipped = [&](uint32_t r) {
+            return r >= K.n_refs || (r < K.alias.size() && K.alias[r] >= 0) || (r < K.aff_head.size() && K.aff_head[r] >= 0);
+        };
+        for (uint32_t r = 0; r < K.n_refs; r += 2)
+            if (1 + r / 2 < K.words && skipped(r) && skipped(r + 1)) unread[k][1 + r / 2] = 1;
+    }
     std::vector<uint8_t> have(p.n_jit_kclasses, 0);
     for (const TileDesc& T : p.tiles) {
         const KClass& K = p.kclasses[T.kclass];
@@ -589,7 +603,7 @@ Plan make_plan(const Formula& f, const Built& b, bool enable_jit) {
         K.wconst = first[k];
         int32_t n = 0;
         for (uint32_t w = 0; w < K.words; ++w)
-            if (varies[k][w]) K.wpos[w] = n++;
+            if (varies[k][w] && !unread[k][w]) K.wpos[w] = n++;
         K.stride4 = std::max<uint32_t>(1, ((uint32_t)n + 3) / 4);
     }
     std::vector<uint32_t> packed;
@@ -609,6 +623,13 @@ Plan make_plan(const Formula& f, const Built& b, bool enable_jit) {
         T.pad0 = T.n_cons * K.stride4;
     }
     p.recs.swap(packed);
+    // one spare record (of the widest class) after the last: the sweep loads the NEXT constraint's
+    // record one iteration ahead without a bounds test (the value read past a tile is never used)
+    {
+        uint32_t ms = 1;
+        for (uint32_t k = 0; k < p.n_jit_kclasses; ++k) ms = std::max(ms, p.kclasses[k].stride4);
+        p.recs.insert(p.recs.end(), (size_t)ms * 4, 0u);
+    }
     // each JIT class's tiles are contiguous (the internal order sorts by class first)
     p.class_tile_begin.assign(p.n_jit_kclasses + 1, (uint32_t)p.tiles.size());
     for (uint32_t t = (uint32_t)p.tiles.size(); t-- > 0;) p.class_tile_begin[p.tiles[t].kclass] = t;
@@ -775,29 +796,36 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
     }
     // value of reference i at byte offset `off` of its column base: Booleans in a (ab), reals
     // by unified id in b (bb), table rows in PT / PF (PTl / PFl)
-    auto ld_at = [&](size_t i, const std::string& off) {
+    auto ld_at = [&](size_t i, const std::string& off, const std::string& px = "") {
         const std::string is = std::to_string(i);
-        if (ref_kind[i] == 2) return "val" + is + " = FSMT_AT(PTl, " + off + "); vaf" + is + " = FSMT_AT(PFl, " + off + ");";
-        return "val" + is + " = " + AT + "(" + (ref_kind[i] == 0 ? "ab" : "bb") + ", " + off + ");";
+        if (ref_kind[i] == 2) return px + "val" + is + " = FSMT_AT(PTl, " + off + "); " + px + "vaf" + is + " = FSMT_AT(PFl, " + off + ");";
+        return px + "val" + is + " = " + AT + "(" + (ref_kind[i] == 0 ? "ab" : "bb") + ", " + off + ");";
     };
     auto dgoff = [&](size_t m) { return "(u64)(" + std::to_string(K.aff_dg[m]) + " * (long long)R4)"; };
-    // a run accumulator goes straight to the fp64 gradient (one atomic per run); g = the variable
-    auto flush_run = [&](size_t i, const std::string& g) {
-        const std::string dst = ref_kind[i] == 0 ? "ga + (u64)(" + g + ") * R + r"
-                              : ref_kind[i] == 2 ? "gu + (u64)(" + g + ") * R + r"
-                                                 : "gb + (u64)(" + g + " - n_bool) * R + r";
-        return "if (live) atomicAdd(" + dst + ", fsmt_q(acc" + std::to_string(i) + ", gif));";
+    // a run group's flush: one address for the head, the members at constant row offsets from it
+    // (dg * R elements: an immediate in the R-specialised module)
+    auto flush_group = [&](size_t i) {
+        const std::string g = "gcur" + std::to_string(i);
+        const std::string base = ref_kind[i] == 0 ? "ga + (u64)" + g + " * R + r"
+                               : ref_kind[i] == 2 ? "gu + (u64)" + g + " * R + r"
+                                                  : "gb + (u64)(" + g + " - n_bool) * R + r";
+        std::string c = "if (live) { double* gp = " + base + "; atomicAdd(gp, fsmt_q(acc" + std::to_string(i) + ", gif));";
+        for (size_t m : members[i])
+            c += " atomicAdd(gp + (long long)(" + std::to_string(K.aff_dg[m]) + ") * R, fsmt_q(acc" + std::to_string(m) + ", gif));";
+        return c + " }";
     };
-    auto gm = [&](size_t h, size_t m) { return "gcur" + std::to_string(h) + " + (" + std::to_string(K.aff_dg[m]) + ")"; };
     // ERWA counters: a byte load per constraint, issued u_prefetch() constraints ahead so its
     // DRAM latency overlaps the passes of the current constraints
     const int upf = u_prefetch();
     const char* uld = "__ldg";
     const std::string ucast = "";
+    // (U has kUPad spare rows after the last constraint, so the look-ahead loads need no bounds
+    // test; the values read past the tile are never used; one running pointer, no index math)
     if (upf > 0) {
         o << "  const unsigned short* Up = hasU ? U + (u64)T.cons_begin * R + rr : nullptr;\n";
         for (int k = 0; k < upf; ++k)
-            o << "  u32 un" << k << " = (hasU && " << k << "u < T.n_cons) ? (u32)" << uld << "(" << ucast << "(Up + (u64)" << k << "u * R)) : 0u;\n";
+            o << "  u32 un" << k << " = hasU ? (u32)" << uld << "(" << ucast << "(Up + (u64)" << k << "u * R)) : 0u;\n";
+        o << "  const unsigned short* Upf = hasU ? Up + (u64)" << upf << "u * R : nullptr;\n";
     }
     // the constraint loop unrolled twice for small classes (FSMT_JIT_UNROLL overrides; DESIGN.md §9:
     // round 1 cfg3 0.884 -> 0.849 ms, cfg4 8.36 -> 8.33 ms; 4 is slower on cfg4)
@@ -807,13 +835,50 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
         const char* ur = getenv("FSMT_JIT_UNROLL");
         o << "#pragma unroll " << (ur ? std::max(1, atoi(ur)) : (K.n_refs <= 16 ? 2 : 1)) << "\n";
     }
+    // Software pipeline over the constraints (FSMT_JIT_VPF=0 disables; DESIGN.md §7 item 18): the
+    // record is loaded one constraint ahead, and from it the stream references' values of the NEXT
+    // constraint are loaded during this one, so their L2 latency hides behind a whole iteration
+    // (ncu v18: the record load and then the value loads were the top long-scoreboard stalls; the
+    // record look-ahead alone measured neutral).  The plan keeps a spare record after the last, so
+    // the look-ahead load needs no bounds test; past a tile's end the look-ahead row is the current one.
+    const char* vpf_env = getenv("FSMT_JIT_VPF");
+    const bool vpf = !(vpf_env && vpf_env[0] == '0');
+    const bool rpf = vpf;
+    auto nword = [&](uint32_t w) { const std::string x = word(w); return x[0] == 'q' ? "n" + x : x; };
+    // next-constraint stream values: psl (local index) and pval/pvaf per stream head and member
+    auto stream_prefetch = [&](const std::string& ind, bool decl, bool guarded) {
+        for (size_t i = 0; i < nr; ++i) {
+            if (!is_stream(i) || alias_of(i) >= 0 || head_of(i) >= 0) continue;
+            const std::string is = std::to_string(i);
+            const std::string ext = "(" + nword(1 + (uint32_t)i / 2) + " >> " + std::to_string(16 * (i % 2)) + ") & 0xffffu";
+            // past the tile's last constraint the look-ahead record is another tile's: the current row
+            // again (a row of this reference's kind, so the address stays inside its array)
+            o << ind << (decl ? "u32 " : "") << "psl" << is << " = " << (guarded ? "c + 1u < T.n_cons ? " : "") << "(" << ext << ")"
+              << (guarded ? " : psl" + is : std::string()) << ";\n";
+            o << ind << "{ const u64 pso = (u64)vs[psl" << is << "] * R4; " << ld_at(i, "pso", "p");
+            for (size_t m : members[i]) o << " " << ld_at(m, "pso + " + dgoff(m), "p");
+            o << " }\n";
+        }
+    };
+    if (rpf)
+        for (uint32_t q = 0; q < K.stride4; ++q) o << "  uint4 nq" << q << " = __ldg(rp + " << q << ");\n";
+    if (vpf) {
+        for (size_t i = 0; i < nr; ++i)
+            if (is_stream(i) && alias_of(i) < 0)
+                o << "  " << TY << " pval" << i << (ref_kind[i] == 2 ? ", pvaf" + std::to_string(i) : std::string()) << ";\n";
+        stream_prefetch("  ", true, false);
+    }
     o << "  for (u32 c = 0; c < T.n_cons; ++c, rp += " << K.stride4 << ") {\n";
-    for (uint32_t q = 0; q < K.stride4; ++q) o << "    const uint4 q" << q << " = __ldg(rp + " << q << ");\n";
+    for (uint32_t q = 0; q < K.stride4; ++q) {
+        if (rpf)
+            o << "    const uint4 q" << q << " = nq" << q << ";\n    nq" << q << " = __ldg(rp + " << K.stride4 + q << ");\n";
+        else
+            o << "    const uint4 q" << q << " = __ldg(rp + " << q << ");\n";
+    }
     if (upf > 0) {
         o << "    const u32 uc = un0;\n";
         for (int k = 0; k + 1 < upf; ++k) o << "    un" << k << " = un" << k + 1 << ";\n";
-        o << "    if (hasU) un" << upf - 1 << " = c + " << upf << "u < T.n_cons ? (u32)" << uld << "(" << ucast << "(Up + (u64)(c + " << upf
-          << "u) * R)) : 0u;\n";
+        o << "    if (hasU) { un" << upf - 1 << " = (u32)" << uld << "(" << ucast << "Upf); Upf += R; }\n";
     } else {
         o << "    const u32 uc = hasU ? (u32)U[(u64)(T.cons_begin + c) * R + rr] : 0u;\n";
     }
@@ -827,7 +892,13 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
             continue;
         }
         if (head_of(i) >= 0) continue;   // loaded with its group head
-        if (is_stream(i)) {
+        if (is_stream(i) && vpf) {   // loaded during the previous constraint
+            o << "    const u32 sl" << i << " = psl" << i << ";\n    const " << TY << " val" << i << " = pval" << i
+              << (ref_kind[i] == 2 ? ", vaf" + std::to_string(i) + " = pvaf" + std::to_string(i) : std::string()) << ";\n";
+            for (size_t m : members[i])
+                o << "    const " << TY << " val" << m << " = pval" << m
+                  << (ref_kind[m] == 2 ? ", vaf" + std::to_string(m) + " = pvaf" + std::to_string(m) : std::string()) << ";\n";
+        } else if (is_stream(i)) {
             // stream reference: new variable (almost) every constraint; no run register
             o << "    const u32 sl" << i << " = " << ext << ";\n"
               << "    const u64 so" << i << " = (u64)vs[sl" << i << "] * R4;\n";
@@ -837,14 +908,14 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
                   << ld_at(m, "so" + std::to_string(i) + " + " + dgoff(m)) << "   // affine\n";
         } else {
             o << "    { const u32 l = " << ext << "; if (l != cur" << i << ") { if (cur" << i << " != 0xffffffffu) { "
-              << flush_run(i, "gcur" + std::to_string(i));
-            for (size_t m : members[i]) o << " " << flush_run(m, gm(i, m));
+              << flush_group(i);
             o << " } cur" << i << " = l; gcur" << i << " = vr[l]; acc" << i << " = " << ZR << "; "
               << ld_at(i, "(u64)gcur" + std::to_string(i) + " * R4");
             for (size_t m : members[i]) o << " acc" << m << " = " << ZR << "; " << ld_at(m, "(u64)gcur" + std::to_string(i) + " * R4 + " + dgoff(m));
             o << " } }\n";
         }
     }
+    if (vpf) stream_prefetch("    ", false, true);
     // slot probabilities
     uint32_t aw = 1 + ((uint32_t)nr + 1) / 2;
     std::vector<uint32_t> coef_word(nr, 0);
@@ -990,16 +1061,40 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
             dpre[va] = dpre[vb] = 1;
         }
     }
-    // forward pass (Alg.F): m_td in registers
+    // forward pass (Alg.F): m_td in registers.  Mass conservation: every node's outgoing
+    // probabilities sum to 1 (pt + pf = 1, P_X + P_Y = 1), so the two terminals' masses sum to
+    // m_root = 1 and only the terminal with fewer incoming edges is accumulated; when that is
+    // FALSE, E = 1 - 2 P(TRUE) = 2 P(FALSE) - 1 (cfg4: 11 of 12 edges reach TRUE).  A message's
+    // first contribution is a plain product (no fmaf with a zero addend).
+    size_t f_true = 0, f_false = 0;
+    for (size_t v = 0; v < nn; ++v) {
+        if (dskip[v]) continue;
+        const TNode& nd = t.nodes[v];
+        const int c1 = dhead[v] ? t.nodes[nd.hi].hi : nd.hi, c2 = dhead[v] ? t.nodes[nd.hi].lo : nd.lo;
+        for (int ch : {c1, c2}) {
+            f_true += ch == kTrue;
+            f_false += ch == kFalse;
+        }
+    }
+    const bool massF = nn > 0 && f_false < f_true;
+    const std::string PTERM = massF ? "pF" : "pT";
+    const int ptgt = massF ? kFalse : kTrue;
     for (size_t v = 0; v < nn; ++v)
         if (!dskip[v]) o << "    " << TY << " m" << v << " = " << ((int)v == t.root ? "1.f" : ZR) << ";\n";
-    o << "    " << TY << " pT = " << ZR << ";\n";
+    o << "    " << TY << " pT = " << ZR << (massF ? ", pF = 0.f" : "") << ";\n";
+    std::vector<char> mset(nn + 1, 0);   // message (or, at index nn, the terminal sum) already assigned
+    if (t.root >= 0 && (size_t)t.root < nn) mset[(size_t)t.root] = 1;
     for (size_t v = 0; v < nn; ++v) {
         if (dskip[v]) continue;
         const TNode& nd = t.nodes[v];
         auto push = [&](int child, const std::string& pn) {
-            if (child >= 0) o << "    m" << child << " = fmaf(" << pn << ", m" << v << ", m" << child << ");\n";
-            else if (child == kTrue) o << "    pT = fmaf(" << pn << ", m" << v << ", pT);\n";
+            if (child < 0 && child != ptgt) return;
+            const size_t slot = child >= 0 ? (size_t)child : nn;
+            const std::string dst = child >= 0 ? "m" + std::to_string(child) : PTERM;
+            const std::string src = (int)v == t.root ? std::string() : " * m" + std::to_string(v);
+            if (!mset[slot]) o << "    " << dst << " = " << pn << src << ";\n";
+            else o << "    " << dst << " = fmaf(" << pn << ", m" << v << ", " << dst << ");\n";
+            mset[slot] = 1;
         };
         if (dhead[v]) {
             const TNode& h = t.nodes[nd.hi];
@@ -1038,23 +1133,21 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
     }
     const char* cmp_env = getenv("FSMT_JIT_CMP");
     const bool cmp = !(cmp_env && cmp_env[0] == '0') && e_true > e_false;
+    // Weight-seeded backward pass (xBDD classes): Alg.B is linear in the terminal values, so
+    // seeding the non-zero terminal with the constraint weight w instead of 1 yields w m_bu and
+    // w dCOP/dp directly; a Boolean slot's product terms then add straight into its accumulator
+    // (one FFMA each) instead of G = a b followed by acc += w G (DESIGN.md §7 item 18).
+    const bool wseed = nn > 0;
+    const std::string ONE = wseed ? "w" : "1.f";
     for (size_t s = 0; s < ns; ++s) o << "    " << TY << " G" << s << " = " << ZR << ";\n";
-    // G_s += a * b; the first contribution is a plain product (G starts at 0: only the sign
-    // of a zero can differ)
-    std::vector<char> gz(ns, 1);
-    auto gfma = [&](size_t s, const std::string& a, const std::string& b) {
-        if (gz[s]) o << "    G" << s << " = " << a << " * " << b << ";\n";
-        else o << "    G" << s << " = fmaf(" << a << ", " << b << ", G" << s << ");\n";
-        gz[s] = 0;
-    };
-    auto gadd = [&](size_t s, const std::string& a, bool neg) {
-        if (gz[s]) o << "    G" << s << " = " << (neg ? "-" : "") << a << ";\n";
-        else o << "    G" << s << (neg ? " -= " : " += ") << a << ";\n";
-        gz[s] = 0;
-    };
+    // G_s = sum of product terms a * b, collected here and emitted after the pass (first term a
+    // plain product, then fmaf in the pass's order) unless folded into the accumulation
+    std::vector<std::vector<std::pair<std::string, std::string>>> gt(ns);
+    auto gfma = [&](size_t s, const std::string& a, const std::string& b) { gt[s].emplace_back(a, b); };
+    auto gadd = [&](size_t s, const std::string& a, bool neg) { gt[s].emplace_back(neg ? "(-" + a + ")" : a, "1.f"); };
     auto bu = [&](int child) -> std::string {
         if (child >= 0) return "bu" + std::to_string(child);
-        return (child == kTrue) != cmp ? "1.f" : "0.f";
+        return (child == kTrue) != cmp ? ONE : "0.f";
     };
     for (size_t vv = nn; vv-- > 0;) {
         if (dskip[vv]) continue;
@@ -1083,10 +1176,11 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
         std::string lv = std::to_string(nd.level);
         // m_bu[v] = p m_bu[hi] + (1-p) m_bu[lo]
         std::string val;
-        if (bh == "1.f" && bl == "0.f") val = "pt" + lv;
-        else if (bh == "0.f" && bl == "1.f") val = "pf" + lv;
-        else if (bh == "1.f") val = "fmaf(pf" + lv + ", " + bl + ", pt" + lv + ")";
-        else if (bl == "1.f") val = "fmaf(pt" + lv + ", " + bh + ", pf" + lv + ")";
+        const std::string wpt = wseed ? "w * pt" + lv : "pt" + lv, wpf = wseed ? "w * pf" + lv : "pf" + lv;
+        if (bh == ONE && bl == "0.f") val = wpt;
+        else if (bh == "0.f" && bl == ONE) val = wpf;
+        else if (bh == ONE) val = "fmaf(pf" + lv + ", " + bl + ", " + wpt + ")";
+        else if (bl == ONE) val = "fmaf(pt" + lv + ", " + bh + ", " + wpf + ")";
         else if (bh == "0.f") val = "pf" + lv + " * " + bl;
         else if (bl == "0.f") val = "pt" + lv + " * " + bh;
         else {
@@ -1099,8 +1193,8 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
         }
         o << "    const " << TY << " bu" << vv << " = " << val << ";\n";
         const std::string mv = "m" + std::to_string(vv);
-        if (bh == "1.f" && bl == "0.f") gadd(nd.level, mv, false);
-        else if (bh == "0.f" && bl == "1.f") gadd(nd.level, mv, true);
+        if (bh == ONE && bl == "0.f") wseed ? gfma(nd.level, mv, "w") : gadd(nd.level, mv, false);
+        else if (bh == "0.f" && bl == ONE) wseed ? gfma(nd.level, mv, "(-w)") : gadd(nd.level, mv, true);
         else if (bl == "0.f") gfma(nd.level, mv, bh);
         else if (bh == "0.f") gfma(nd.level, mv, "(-" + bl + ")");
         else gfma(nd.level, mv, "(" + bh + " - " + bl + ")");
@@ -1169,8 +1263,32 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
             o << "\n      G" << ss << " = pt" << ss << " <= 0.5f ? -cf : -cb; }\n";
         }
     }
+    // a Boolean slot of a weight-seeded class whose G is only accumulated: its terms go straight
+    // into the accumulator (signs taken back for the complement form); every other G is emitted
+    auto is_ident = [](const std::string& x) {
+        if (x.empty()) return false;
+        for (char ch : x)
+            if (!(isalnum((unsigned char)ch) || ch == '_')) return false;
+        return true;
+    };
+    auto negate = [&](const std::string& a) -> std::string {
+        if (a.size() > 1 && a[0] == '-' && is_ident(a.substr(1))) return a.substr(1);
+        if (a.size() > 3 && a.compare(0, 2, "(-") == 0 && a.back() == ')' && is_ident(a.substr(2, a.size() - 3)))
+            return a.substr(2, a.size() - 3);
+        return "(-(" + a + "))";
+    };
+    auto folded = [&](size_t s) { return wseed && t.kinds[s] == 0 && !gt[s].empty(); };
+    for (size_t s = 0; s < ns; ++s) {
+        if (folded(s)) continue;
+        for (size_t k = 0; k < gt[s].size(); ++k) {
+            const auto& ab = gt[s][k];
+            if (k == 0) o << "    G" << s << " = " << ab.first << " * " << ab.second << ";\n";
+            else o << "    G" << s << " = fmaf(" << ab.first << ", " << ab.second << ", G" << s << ");\n";
+        }
+    }
     auto gref = [&](size_t s) { return cmp ? "(-G" + std::to_string(s) + ")" : "G" + std::to_string(s); };
-    o << "    const " << TY << " E = 1.f - 2.f * pT;\n";
+    if (massF) o << "    const " << TY << " E = fmaf(2.f, pF, -1.f);\n";
+    else o << "    const " << TY << " E = 1.f - 2.f * pT;\n";
     // the objective's first level in fp32 over the tile's <= 64 constraints, flushed once per tile into
     // the fp64 objective (two-level accumulation, R28: the per-tile fp32 sum of <= 64 terms adds
     // <= 64 x 2^-24 relative; across tiles the sum is exact on the objective's grid)
@@ -1182,20 +1300,24 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
         const int tgt = alias_of((size_t)ri) >= 0 ? alias_of((size_t)ri) : ri;
         terms_of[(size_t)tgt].emplace_back(a, b);
     };
+    const std::string WG = wseed ? "1.f" : "w";   // weight factor still to apply to a G
     for (size_t s = 0; s < ns; ++s) {
         if (t.kinds[s] == 0) {
-            accum(slot_ref0[s], "w", gref(s));
+            if (folded(s))
+                for (const auto& ab : gt[s]) accum(slot_ref0[s], cmp ? negate(ab.first) : ab.first, ab.second);
+            else
+                accum(slot_ref0[s], WG, gref(s));
         } else if (t.kinds[s] == 2) {
             // dCOP/dp_true of the row = -dCOP/dp_true of a negated literal
-            accum(slot_ref0[s], "w", "(sg" + std::to_string(s) + " ? -" + gref(s) + " : " + gref(s) + ")");
+            accum(slot_ref0[s], WG, "(sg" + std::to_string(s) + " ? -" + gref(s) + " : " + gref(s) + ")");
         } else {
             if (pair_with[s] >= 0) {
                 const std::string sa = std::to_string(s), sb = std::to_string(pair_with[s]);
-                o << "    const float2 gdp" << sa << " = __fmul2_rn(__fmul2_rn(FSMT_C2(w), make_float2(" << gref(s) << ", " << gref((size_t)pair_with[s])
-                  << ")), ddp" << sa << ");\n"
+                const std::string gg = "make_float2(" + gref(s) + ", " + gref((size_t)pair_with[s]) + ")";
+                o << "    const float2 gdp" << sa << " = __fmul2_rn(" << (wseed ? gg : "__fmul2_rn(FSMT_C2(w), " + gg + ")") << ", ddp" << sa << ");\n"
                   << "    const float gd" << sa << " = gdp" << sa << ".x, gd" << sb << " = gdp" << sa << ".y;\n";
             } else if (!pair_second[s]) {
-                o << "    const " << TY << " gd" << s << " = w * " << gref(s) << " * dd" << s << ";\n";
+                o << "    const " << TY << " gd" << s << " = " << (wseed ? std::string() : "w * ") << gref(s) << " * dd" << s << ";\n";
             }
             size_t ai = 0;
             for (size_t s2 = 0; s2 < s; ++s2) ai += t.kinds[s2] == 1;
@@ -1218,9 +1340,7 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
     o << "  }\n";
     for (size_t i = 0; i < nr; ++i)
         if (!is_stream(i) && alias_of(i) < 0 && head_of(i) < 0) {
-            o << "  if (cur" << i << " != 0xffffffffu) { " << flush_run(i, "gcur" + std::to_string(i));
-            for (size_t m : members[i]) o << " " << flush_run(m, gm(i, m));
-            o << " }\n";
+            o << "  if (cur" << i << " != 0xffffffffu) { " << flush_group(i) << " }\n";
         }
     o << "}\n\n";
 }

@@ -121,7 +121,7 @@ class ConstraintShardedBuffers:
     keeps device buffers and stages each collective through host memory (the library rejects host
     buffers); a CPU engine (tests) binds the communication tensors directly."""
 
-    def __init__(self, engine, n_bool: int, n_real: int, R: int, group=None):
+    def __init__(self, engine, n_bool: int, n_real: int, R: int, group=None, nvls: bool = False):
         self.group = group
         self.engine = engine
         comm = _comm_device()
@@ -129,7 +129,22 @@ class ConstraintShardedBuffers:
         bind = torch.device("cuda", torch.cuda.current_device()) if gpu else comm
         rows = engine.get_dims().get("n_slot_rows", 0) if gpu else 0
         n = (n_bool + n_real + 1 + rows) * R
-        self.flat = torch.zeros(n, dtype=torch.float64, device=bind)
+        self.n = n
+        # nvls: the flat buffer is symmetric memory with a multicast address and C4 is the library's
+        # in-switch all-reduce (fsmt_mc_allreduce_f64) between two device barriers instead of NCCL
+        self.symm = None
+        if nvls:
+            if not (gpu and dist.get_backend(group) == "nccl"):
+                raise RuntimeError("nvls needs a GPU engine under the NCCL backend")
+            import torch.distributed._symmetric_memory as symm_mem
+            self.flat = symm_mem.empty(n, dtype=torch.float64, device=bind)
+            self.flat.zero_()
+            gname = (group or dist.group.WORLD).group_name
+            self.symm = symm_mem.rendezvous(self.flat, gname)
+            if not self.symm.multicast_ptr:
+                raise RuntimeError("nvls: no multicast support on this group (needs >= 2 GPUs behind NVSwitch)")
+        else:
+            self.flat = torch.zeros(n, dtype=torch.float64, device=bind)
         self.unsat = torch.zeros(R, dtype=torch.int32, device=bind)
         self.umax = torch.zeros(R, dtype=torch.int32, device=bind)
         self.stage = bind != comm
@@ -154,7 +169,13 @@ class ConstraintShardedBuffers:
             dist.all_reduce(dev_t, op=op, group=self.group)
 
     def reduce_grads(self):                                                       # C4
-        self._reduce(self.flat, self.flat_c if self.stage else None, dist.ReduceOp.SUM)
+        if self.symm is not None:
+            self.symm.barrier(channel=0)           # every rank's sweep has written its copy
+            self.engine.mc_allreduce_f64(self.symm.multicast_ptr, self.n, dist.get_rank(self.group),
+                                         dist.get_world_size(self.group))
+            self.symm.barrier(channel=1)           # every rank's multicast stores have landed
+        else:
+            self._reduce(self.flat, self.flat_c if self.stage else None, dist.ReduceOp.SUM)
         if self.chain:
             self.engine.sweep_finish()
 
@@ -164,7 +185,7 @@ class ConstraintShardedBuffers:
 
 
 def solve_constraint_sharded(engine, n_bool: int, n_real: int, restarts: int, steps: int, seed: int, kappas,
-                             eps: float, group=None) -> DistResult:
+                             eps: float, group=None, nvls: bool = False) -> DistResult:
     """Constraint-sharded Alg.2 (BASELINE config 5); step sizes per stage from the
     engine's params (engine.step_sizes(kappa): eta and eta_mode, as fsmt_run_stage uses them)."""
     rank = dist.get_rank(group)
@@ -173,7 +194,7 @@ def solve_constraint_sharded(engine, n_bool: int, n_real: int, restarts: int, st
     _bind_torch_stream(engine)
     engine.shard(rank, world, 1)
     engine.begin(R, seed, 0)
-    bufs = ConstraintShardedBuffers(engine, n_bool, n_real, R, group)
+    bufs = ConstraintShardedBuffers(engine, n_bool, n_real, R, group, nvls=nvls)
     best = None
     stages = 0
     for t, kappa in enumerate(kappas, start=1):

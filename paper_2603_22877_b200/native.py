@@ -96,6 +96,7 @@ _SIGS = {
     "fsmt_get_timing": (_i32, [_vp, _vp, _vp, _i32]),
     "fsmt_jit_info": (_i32, [_vp, C.POINTER(_u32), C.POINTER(_u32), C.POINTER(_u32), C.c_char_p, C.c_size_t]),
     "fsmt_jit_source": (C.c_size_t, [_vp, C.c_char_p, C.c_size_t]),
+    "fsmt_mc_allreduce_f64": (_i32, [_vp, _vp, C.c_uint64, C.c_uint32, C.c_uint32]),
     "fsmt_prepare": (_i32, [_vp, _u32]),
     "fsmt_eval": (_i32, [_vp, _u32, _vp, _vp, _f32, _vp, _u32, _vp, _vp, _vp, _i32]),
     "fsmt_jit_check": (_i32, [_vp, C.POINTER(C.c_size_t), C.c_char_p, C.c_size_t]),

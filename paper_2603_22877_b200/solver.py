@@ -280,6 +280,11 @@ class Solver:
         ptr = lambda t: None if t is None else t.data_ptr()
         self._check(N.lib.fsmt_bind_buffers(self._h, ptr(grad_a), ptr(grad_b), ptr(obj), ptr(unsat), ptr(umax)))
 
+    def mc_allreduce_f64(self, mc_ptr: int, n: int, rank: int, world: int):
+        """C4 in the NVSwitch: all-reduce SUM of n f64 of a multicast buffer (fsmt_mc_allreduce_f64;
+        the caller barriers the ranks before and after)."""
+        self._check(N.lib.fsmt_mc_allreduce_f64(self._h, C.c_void_p(mc_ptr), n, rank, world))
+
     def jit_check(self):
         """NVRTC-compile the specialised sweep (no device needed): (cubin bytes, compiler log)."""
         n = C.c_size_t()

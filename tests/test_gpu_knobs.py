@@ -23,6 +23,8 @@ KNOBS = [
     {"FSMT_JIT_UPF": "3"},
     {"FSMT_JIT_CMP": "0"},
     {"FSMT_JIT_UNROLL": "1"},
+    {"FSMT_JIT_VPF": "0"},
+    {"FSMT_JIT_VPF": "0", "FSMT_JIT_UNROLL": "2", "FSMT_JIT_UPF": "2"},
     {"FSMT_TILE_VMAX": "16", "FSMT_TILE_RMAX": "16", "FSMT_TILE_CMAX": "3"},
 ]
 
