@@ -538,6 +538,8 @@ fsmt_status fsmt_build_xbdd(fsmt_ctx* ctx, uint64_t node_budget) {
             ctx->T.recs = rp;
             ctx->T.tile_vars = vp;
             ctx->T.vmax = P.kernel_vmax();
+            ctx->T.ring_uint4 = P.ring_uint4();
+            ctx->T.vid_bytes = P.vid_bytes();
             // run-variable id slots the tiles actually use (<= Plan::rmax): the sweep's shared memory
             // is sized by it, so more one-warp CTAs fit per SM
             uint32_t rmax_used = 1;

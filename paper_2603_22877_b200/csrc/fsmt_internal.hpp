@@ -176,6 +176,18 @@ struct Plan {
     uint32_t vmax_sym = 128;          // stream rows of symmetric-class tiles (FSMT_TILE_VMAX_SYM)
     // shared-memory rows per warp of the JIT sweep: the largest tile limit in use
     uint32_t kernel_vmax() const { return has_sym ? std::max(vmax, vmax_sym) : vmax; }
+    // bytes per variable id in the sweep's shared-memory id table: u16 when every tile variable id fits
+    uint32_t vid_bytes() const {
+        for (uint32_t v : tile_vars)
+            if (v > 0xFFFFu) return 4;
+        return 2;
+    }
+    // the sweep's per-warp shared-memory record ring (two records of the widest JIT class, 16 B units)
+    uint32_t ring_uint4() const {
+        uint32_t ms = 1;
+        for (uint32_t k = 0; k < n_jit_kclasses && k < kclasses.size(); ++k) ms = std::max(ms, kclasses[k].stride4);
+        return 2 * ms;
+    }
     std::vector<uint32_t> class_tile_begin;   // [n_jit_kclasses + 1]: class k's tiles are [begin[k], begin[k+1])
 };
 

@@ -501,7 +501,7 @@ void launch_sweep_jit(cudaKernel_t k, const DevFormula& F, const DevState& S, co
     // one one-warp CTA per (tile, 32 restarts)
     const uint64_t rtiles = (S.R + 31) / 32;
     const unsigned blocks = (unsigned)((uint64_t)T.n_tiles * rtiles);
-    const size_t smem = (size_t)kVmax * 32 * 4 + (size_t)kVtot * 4;
+    const size_t smem = (size_t)T.ring_uint4 * 16 + (size_t)kVmax * 32 * 4 + (size_t)kVtot * T.vid_bytes;   // ring | rows | ids
     if (smem > 48 * 1024) cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     uint32_t n_tiles = T.n_tiles, R = S.R, n_bool = F.n_bool;
     const float* kdev = S.ds ? &S.ds->kappa : nullptr;

@@ -149,6 +149,8 @@ struct DevTiles {
     const uint32_t* tile_vars;
     uint32_t vmax;               // stream variables (shared-memory accumulator rows) per tile (Plan::vmax)
     uint32_t rmax;               // run variables per tile (Plan::rmax)
+    uint32_t ring_uint4;         // K1's per-warp shared-memory record ring, in uint4 (Plan::ring_uint4)
+    uint32_t vid_bytes;          // K1's shared-memory variable-id width, 2 or 4 (Plan::vid_bytes)
     const void* vrecs;           // K5 records (atom ids), tile.pad1 = offset in uint4
     uint32_t first;              // global index of tiles[0] (constraint shards start mid-plan)
 };

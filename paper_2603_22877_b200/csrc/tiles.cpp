@@ -623,13 +623,9 @@ Plan make_plan(const Formula& f, const Built& b, bool enable_jit) {
         T.pad0 = T.n_cons * K.stride4;
     }
     p.recs.swap(packed);
-    // one spare record (of the widest class) after the last: the sweep loads the NEXT constraint's
-    // record one iteration ahead without a bounds test (the value read past a tile is never used)
-    {
-        uint32_t ms = 1;
-        for (uint32_t k = 0; k < p.n_jit_kclasses; ++k) ms = std::max(ms, p.kclasses[k].stride4);
-        p.recs.insert(p.recs.end(), (size_t)ms * 4, 0u);
-    }
+    // two spare records (of the widest class) after the last: the sweep copies the records two
+    // constraints ahead without a bounds test (the values read past a tile are never used)
+    p.recs.insert(p.recs.end(), (size_t)p.ring_uint4() * 4, 0u);
     // each JIT class's tiles are contiguous (the internal order sorts by class first)
     p.class_tile_begin.assign(p.n_jit_kclasses + 1, (uint32_t)p.tiles.size());
     for (uint32_t t = (uint32_t)p.tiles.size(); t-- > 0;) p.class_tile_begin[p.tiles[t].kclass] = t;
@@ -685,6 +681,12 @@ const char* kErfcPrelude =
     "#define FSMT_SPECIALISE_R\n"
     "#endif\n"
     "#define FSMT_AT(base, off) (*(const float*)((const char*)(base) + (off)))\n"
+    "// 16-byte asynchronous global -> shared copy (the sweep's record ring)\n"
+    "__device__ __forceinline__ void fsmt_cpa16(uint4* dst, const uint4* src) {\n"
+    "  asm volatile(\"cp.async.ca.shared.global [%0], [%1], 16;\" :: \"r\"((u32)__cvta_generic_to_shared(dst)), \"l\"(__cvta_generic_to_global(src)) : \"memory\");\n"
+    "}\n"
+    "__device__ __forceinline__ void fsmt_cpa_commit() { asm volatile(\"cp.async.commit_group;\" ::: \"memory\"); }\n"
+    "template <int N> __device__ __forceinline__ void fsmt_cpa_wait() { asm volatile(\"cp.async.wait_group %0;\" :: \"n\"(N) : \"memory\"); }\n"
     "__device__ __forceinline__ float fsmt_ex2(float x) { float r; asm(\"ex2.approx.ftz.f32 %0, %1;\" : \"=f\"(r) : \"f\"(x)); return r; }\n"
     "// 0.5*erfc(z) for z >= 0 and ez = exp(-z^2) (dd/db factor, P:1326-1327).  Coefficients from\n"
     "// scripts/fit_erfc.py: z < 0.75: 0.5 (1 - z P(z^2)), P ~ erf(z)/z (degree 5);\n"
@@ -756,13 +758,14 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
     // DBG = false (the hot instantiation): U present, no per-constraint E_c debug output, so
     // neither test is in the loop
     o << "template <bool DBG> __device__ __forceinline__ void kc" << kid
-      << "(const TileDesc& T, const uint4* __restrict__ rp, const u32* __restrict__ vs, const u32* __restrict__ vr,\n"
+      << "(const TileDesc& T, const uint4* __restrict__ rp, const VID* __restrict__ vs, const VID* __restrict__ vr,\n"
          "    " << TY << "* __restrict__ accs, const float* __restrict__ ab, const float* __restrict__ bb,\n"
          "    double* __restrict__ ga, double* __restrict__ gb, const unsigned short* __restrict__ U,\n"
          "    u32 R, u32 R4, u64 rr, u32 r, bool live, u32 n_bool, float kq, float dcoef, int ebias,\n"
          "    float gif, float& objacc,\n"
          "    double* __restrict__ terms, u32 terms_r, const u32* __restrict__ orig,\n"
-         "    const float* __restrict__ PTl, const float* __restrict__ PFl, double* __restrict__ gu) {\n"
+         "    const float* __restrict__ PTl, const float* __restrict__ PFl, double* __restrict__ gu,\n"
+         "    uint4* __restrict__ rring, u32 lane) {\n"
          "  const bool hasU = !DBG || U != nullptr, hasT = DBG && terms != nullptr;\n";
     // refs
     std::vector<int> ref_kind;      // 0 Boolean, 1 real, 2 slot-table row (symmetric classes)
@@ -860,8 +863,17 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
             o << " }\n";
         }
     };
-    if (rpf)
-        for (uint32_t q = 0; q < K.stride4; ++q) o << "  uint4 nq" << q << " = __ldg(rp + " << q << ");\n";
+    // The records travel through a two-slot shared-memory ring (cp.async by lanes < stride, record
+    // c + 2 issued in iteration c, waited for at the top of iteration c + 1): the wait is explicit, so
+    // the compiler cannot hoist the record's move into the uniform datapath right behind its load
+    // (ncu v19: with the look-ahead in registers, 27 % of the stall samples sat on that R2UR).
+    const uint32_t S4 = K.stride4;
+    if (rpf) {
+        o << "  if (lane < " << S4 << "u) fsmt_cpa16(rring + lane, rp + lane);\n  fsmt_cpa_commit();\n"
+          << "  if (lane < " << S4 << "u) fsmt_cpa16(rring + " << S4 << "u + lane, rp + " << S4 << "u + lane);\n  fsmt_cpa_commit();\n"
+          << "  fsmt_cpa_wait<1>();\n  __syncwarp();\n";
+        for (uint32_t q = 0; q < S4; ++q) o << "  uint4 nq" << q << " = rring[" << q << "];\n";
+    }
     if (vpf) {
         for (size_t i = 0; i < nr; ++i)
             if (is_stream(i) && alias_of(i) < 0)
@@ -869,11 +881,14 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
         stream_prefetch("  ", true, false);
     }
     o << "  for (u32 c = 0; c < T.n_cons; ++c, rp += " << K.stride4 << ") {\n";
-    for (uint32_t q = 0; q < K.stride4; ++q) {
-        if (rpf)
-            o << "    const uint4 q" << q << " = nq" << q << ";\n    nq" << q << " = __ldg(rp + " << K.stride4 + q << ");\n";
-        else
-            o << "    const uint4 q" << q << " = __ldg(rp + " << q << ");\n";
+    if (rpf) {
+        for (uint32_t q = 0; q < S4; ++q) o << "    const uint4 q" << q << " = nq" << q << ";\n";
+        o << "    fsmt_cpa_wait<0>();\n    __syncwarp();\n";   // record c + 1 has landed in slot (c + 1) & 1
+        for (uint32_t q = 0; q < S4; ++q) o << "    nq" << q << " = rring[((c + 1u) & 1u) * " << S4 << "u + " << q << "u];\n";
+        o << "    if (lane < " << S4 << "u) fsmt_cpa16(rring + (c & 1u) * " << S4 << "u + lane, rp + " << 2 * S4 << "u + lane);\n"
+          << "    fsmt_cpa_commit();\n";
+    } else {
+        for (uint32_t q = 0; q < S4; ++q) o << "    const uint4 q" << q << " = __ldg(rp + " << q << ");\n";
     }
     if (upf > 0) {
         o << "    const u32 uc = un0;\n";
@@ -909,8 +924,8 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
         } else {
             o << "    { const u32 l = " << ext << "; if (l != cur" << i << ") { if (cur" << i << " != 0xffffffffu) { "
               << flush_group(i);
-            o << " } cur" << i << " = l; gcur" << i << " = vr[l]; acc" << i << " = " << ZR << "; "
-              << ld_at(i, "(u64)gcur" + std::to_string(i) + " * R4");
+            o << " } cur" << i << " = l; gcur" << i << " = vr[l]; acc" << i << " = " << ZR << "; ";
+            o << ld_at(i, "(u64)gcur" + std::to_string(i) + " * R4");
             for (size_t m : members[i]) o << " acc" << m << " = " << ZR << "; " << ld_at(m, "(u64)gcur" + std::to_string(i) + " * R4 + " + dgoff(m));
             o << " } }\n";
         }
@@ -1508,7 +1523,8 @@ std::string jit_source(const Formula& f, const Built& b, const Plan& p, int u_pr
     o << "// generated by fsmt tiles.cpp: specialised K1 sweep for " << p.n_jit_kclasses << " kernel classes\n"
          "typedef unsigned int u32;\ntypedef unsigned long long u64;\n"
          "struct TileDesc { u32 kclass, cons_begin, n_cons, var_off, n_vars, rec_off, pad0, pad1; };\n"
-      << "#define VMAX " << p.kernel_vmax() << "\n#define VTOT " << p.kernel_vmax() + p.rmax << "\n\n" << kErfcPrelude;
+      << "#define VMAX " << p.kernel_vmax() << "\n#define VTOT " << p.kernel_vmax() + p.rmax << "\n#define RING " << p.ring_uint4() << "\ntypedef " << (p.vid_bytes() == 2 ? "unsigned short" : "u32") << " VID;   // sweep id-table entry"
+      << "\n\n" << kErfcPrelude;
     auto tmpl_of = [&](const KClass& K) -> const Template& { return K.sym ? K.stmpl : b.tmpls[K.tmpl]; };
     for (uint32_t k = 0; k < p.n_jit_kclasses; ++k) emit_class(o, k, p.kclasses[k], tmpl_of(p.kclasses[k]));
     const char* minb = getenv("FSMT_JIT_MINB");      // optional min CTAs/SM (register cap), A/B tuning
@@ -1536,8 +1552,9 @@ std::string jit_source(const Formula& f, const Built& b, const Plan& p, int u_pr
          "  if (kdev) kappa = *kdev;   // the device-side solve loop's stage kappa (DevStage)\n"
          "  extern __shared__ float smem[];\n"
          "  const int lane = threadIdx.x & 31;\n"
-         "  float* acc = smem;                                    // stream-variable rows\n"
-         "  u32* vs = (u32*)(smem + VMAX * 32);                   // stream then run variable ids\n"
+         "  uint4* ring = (uint4*)smem;                           // record ring (RING uint4)\n"
+         "  float* acc = smem + RING * 4;                         // stream-variable rows\n"
+         "  VID* vs = (VID*)(acc + VMAX * 32);                    // stream then run variable ids\n"
          "  const u32 rtiles = (R + 31) / 32;\n"
       << "  const u64 ti = blockIdx.x / rtiles;                  // tile-major: a tile's restart tiles together\n"
          "  const u32 rt = (u32)(blockIdx.x % rtiles);\n"
@@ -1550,7 +1567,7 @@ std::string jit_source(const Formula& f, const Built& b, const Plan& p, int u_pr
          "  for (u32 l = lane; l < n_v; l += 32) vs[l] = tile_vars[T.var_off + l];\n"
          "  for (u32 l = 0; l < n_s; ++l) acc[l * 32 + lane] = 0.f;\n"
          "  __syncwarp();\n"
-         "  const u32* vr = vs + n_s;\n"
+         "  const VID* vr = vs + n_s;\n"
          "  const float kq = kappa * 0.70710678118654752f;\n"
          "  const float dcoef = kappa * 0.79788456080286536f;\n"
          "  const float gif = fxs[rr].gif;\n"
@@ -1568,7 +1585,7 @@ std::string jit_source(const Formula& f, const Built& b, const Plan& p, int u_pr
     for (uint32_t k = 0; k < p.n_jit_kclasses; ++k) {
         if (kv >= 0 && (int)k != kv) continue;
         const std::string args = "(T, rp, vs, vr, acc + lane, ab, bb, ga, gb, U, R, R4, rr, r, live, n_bool, kq, dcoef, ebias, "
-                                 "gif, objacc, terms, terms_r, orig, PTl, PFl, gu); ";
+                                 "gif, objacc, terms, terms_r, orig, PTl, PFl, gu, ring, (u32)lane); ";
         o << "    case " << k << ": kc" << k << (dbgk ? "<true>" : "<false>") << args
           << (p.kclasses[k].sym ? "symt = true; " : "") << "break;\n";
     }
