@@ -158,7 +158,7 @@ void drop_state(fsmt_ctx* ctx) {
     if (ctx->gexec) { cudaGraphExecDestroy(ctx->gexec); ctx->gexec = nullptr; }
     free_list(ctx->sallocs);
     ctx->S = DevState{};
-    ctx->slots.PT = ctx->slots.PF = ctx->slots.DD = nullptr;
+    ctx->slots.PT = ctx->slots.DD = nullptr;
     ctx->slots.GU = nullptr;
     ctx->slots.TT = nullptr;
     ctx->scratch = nullptr;     // freed with the state allocations
@@ -693,7 +693,7 @@ fsmt_status fsmt_begin(fsmt_ctx* ctx, uint32_t R, uint64_t seed, uint32_t restar
     if (ctx->has_sym) {   // slot tables (rows: Booleans, reals (unused), table atoms)
         DevSlots& D = ctx->slots;
         const size_t rows = (size_t)D.nv + D.n_sa;
-        if ((s = alloc((void**)&D.PT, rows * R * 4)) || (s = alloc((void**)&D.PF, rows * R * 4)) ||
+        if ((s = alloc((void**)&D.PT, rows * R * 4)) ||
             (s = alloc((void**)&D.DD, (size_t)D.n_sa * R * 4)) || (s = alloc((void**)&D.GU, rows * R * 8)) ||
             (s = alloc((void**)&D.TT, rows * R))) {
             drop_state(ctx);

@@ -507,11 +507,10 @@ void launch_sweep_jit(cudaKernel_t k, const DevFormula& F, const DevState& S, co
     const float* kdev = S.ds ? &S.ds->kappa : nullptr;
     const uint16_t* U = S.U;
     const float* PT = D ? D->PT : nullptr;
-    const float* PF = D ? D->PF : nullptr;
     double* GU = D ? D->GU : nullptr;
     void* args[] = {(void*)&T.tiles, &n_tiles, (void*)&T.recs, (void*)&T.tile_vars, (void*)&S.a, (void*)&S.b,
                     (void*)&S.ga, (void*)&S.gb, (void*)&U, (void*)&S.obj, &R, &n_bool, &kappa,
-                    &terms, &terms_r, (void*)&F.orig, (void*)&PT, (void*)&PF, (void*)&GU, (void*)&S.fx, (void*)&kdev};
+                    &terms, &terms_r, (void*)&F.orig, (void*)&PT, (void*)&GU, (void*)&S.fx, (void*)&kdev};
     cudaLaunchKernel((const void*)k, dim3(blocks), dim3(32), args, smem, st);
 }
 
@@ -522,7 +521,7 @@ void launch_slot_prob(cudaKernel_t k, const DevFormula& F, const DevState& S, co
     const float* kdev = S.ds ? &S.ds->kappa : nullptr;
     void* args[] = {&n_bool, &nv, &n_sa, (void*)&D.atoms, (void*)&S.a, (void*)&S.b, (void*)&F.atom_rowptr,
                     (void*)&F.atom_col, (void*)&F.atom_val, (void*)&F.atom_rhs, (void*)&F.atom_invnorm, &R, &kappa,
-                    (void*)&D.PT, (void*)&D.PF, (void*)&D.DD, (void*)&kdev};
+                    (void*)&D.PT, (void*)&D.DD, (void*)&kdev};
     cudaLaunchKernel((const void*)k, dim3((unsigned)std::min<uint64_t>((n + 255) / 256, 148ull * 16)), dim3(256), args, 0, st);
 }
 

@@ -159,7 +159,6 @@ struct DevSlots {
     uint32_t n_sa = 0, nv = 0;          // table atoms; nv = n_bool + n_real
     const uint32_t* atoms = nullptr;    // [n_sa] atom ids
     float* PT = nullptr;                // [nv + n_sa][R] p_true of the row
-    float* PF = nullptr;                // [nv + n_sa][R] p_false
     float* DD = nullptr;                // [n_sa][R] dd/dz factor
     double* GU = nullptr;               // [nv + n_sa][R] dE/dp_true of the row (weighted)
     uint8_t* TT = nullptr;              // [nv + n_sa][R] exact truth of the row (K5)

@@ -764,7 +764,7 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
          "    u32 R, u32 R4, u64 rr, u32 r, bool live, u32 n_bool, float kq, float dcoef, int ebias,\n"
          "    float gif, float& objacc,\n"
          "    double* __restrict__ terms, u32 terms_r, const u32* __restrict__ orig,\n"
-         "    const float* __restrict__ PTl, const float* __restrict__ PFl, double* __restrict__ gu,\n"
+         "    const float* __restrict__ PTl, double* __restrict__ gu,\n"
          "    uint4* __restrict__ rring, u32 lane) {\n"
          "  const bool hasU = !DBG || U != nullptr, hasT = DBG && terms != nullptr;\n";
     // refs
@@ -795,13 +795,13 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
         if (is_stream(i) || alias_of(i) >= 0) continue;
         if (head_of(i) < 0) o << "  u32 cur" << i << " = 0xffffffffu, gcur" << i << " = 0u;";
         o << " " << TY << " val" << i << " = " << ZR << ", acc" << i << " = " << ZR
-          << (ref_kind[i] == 2 ? ", vaf" + std::to_string(i) + " = 0.f" : std::string()) << ";\n";
+          << ";\n";
     }
     // value of reference i at byte offset `off` of its column base: Booleans in a (ab), reals
     // by unified id in b (bb), table rows in PT / PF (PTl / PFl)
     auto ld_at = [&](size_t i, const std::string& off, const std::string& px = "") {
         const std::string is = std::to_string(i);
-        if (ref_kind[i] == 2) return px + "val" + is + " = FSMT_AT(PTl, " + off + "); " + px + "vaf" + is + " = FSMT_AT(PFl, " + off + ");";
+        if (ref_kind[i] == 2) return px + "val" + is + " = FSMT_AT(PTl, " + off + ");";   // p_true of the row; p_false = 1 - p_true
         return px + "val" + is + " = " + AT + "(" + (ref_kind[i] == 0 ? "ab" : "bb") + ", " + off + ");";
     };
     auto dgoff = [&](size_t m) { return "(u64)(" + std::to_string(K.aff_dg[m]) + " * (long long)R4)"; };
@@ -848,7 +848,7 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
     const bool vpf = !(vpf_env && vpf_env[0] == '0');
     const bool rpf = vpf;
     auto nword = [&](uint32_t w) { const std::string x = word(w); return x[0] == 'q' ? "n" + x : x; };
-    // next-constraint stream values: psl (local index) and pval/pvaf per stream head and member
+    // next-constraint stream values: psl (local index) and pval per stream head and member
     auto stream_prefetch = [&](const std::string& ind, bool decl, bool guarded) {
         for (size_t i = 0; i < nr; ++i) {
             if (!is_stream(i) || alias_of(i) >= 0 || head_of(i) >= 0) continue;
@@ -877,7 +877,7 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
     if (vpf) {
         for (size_t i = 0; i < nr; ++i)
             if (is_stream(i) && alias_of(i) < 0)
-                o << "  " << TY << " pval" << i << (ref_kind[i] == 2 ? ", pvaf" + std::to_string(i) : std::string()) << ";\n";
+                o << "  " << TY << " pval" << i << ";\n";
         stream_prefetch("  ", true, false);
     }
     o << "  for (u32 c = 0; c < T.n_cons; ++c, rp += " << K.stride4 << ") {\n";
@@ -909,17 +909,17 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
         if (head_of(i) >= 0) continue;   // loaded with its group head
         if (is_stream(i) && vpf) {   // loaded during the previous constraint
             o << "    const u32 sl" << i << " = psl" << i << ";\n    const " << TY << " val" << i << " = pval" << i
-              << (ref_kind[i] == 2 ? ", vaf" + std::to_string(i) + " = pvaf" + std::to_string(i) : std::string()) << ";\n";
+              << ";\n";
             for (size_t m : members[i])
                 o << "    const " << TY << " val" << m << " = pval" << m
-                  << (ref_kind[m] == 2 ? ", vaf" + std::to_string(m) + " = pvaf" + std::to_string(m) : std::string()) << ";\n";
+                  << ";\n";
         } else if (is_stream(i)) {
             // stream reference: new variable (almost) every constraint; no run register
             o << "    const u32 sl" << i << " = " << ext << ";\n"
               << "    const u64 so" << i << " = (u64)vs[sl" << i << "] * R4;\n";
-            o << "    " << TY << " val" << i << (ref_kind[i] == 2 ? ", vaf" + std::to_string(i) : std::string()) << "; " << ld_at(i, "so" + std::to_string(i)) << "\n";
+            o << "    " << TY << " val" << i << "; " << ld_at(i, "so" + std::to_string(i)) << "\n";
             for (size_t m : members[i])
-                o << "    " << TY << " val" << m << (ref_kind[m] == 2 ? ", vaf" + std::to_string(m) : std::string()) << "; "
+                o << "    " << TY << " val" << m << "; "
                   << ld_at(m, "so" + std::to_string(i) + " + " + dgoff(m)) << "   // affine\n";
         } else {
             o << "    { const u32 l = " << ext << "; if (l != cur" << i << ") { if (cur" << i << " != 0xffffffffu) { "
@@ -996,11 +996,13 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
             o << "    const " << TY << " pt" << s << " = 0.5f * (1.f - val" << slot_ref0[s] << "), pf" << s << " = 0.5f * (1.f + val"
               << slot_ref0[s] << ");\n";
         } else if (t.kinds[s] == 2) {
-            // negated literal: p_true and p_false of its row swap (Eq.4 / Eq.7 of the literal)
+            // negated literal: p_true and p_false of its row swap (Eq.4 / Eq.7 of the literal); the
+            // tables hold p_true only, p_false = 1 - p_true (one load and one register per literal)
             const int ri = slot_ref0[s];
             o << "    const bool sg" << s << " = (" << word(sign_word + (uint32_t)s / 32) << " >> " << s % 32 << ") & 1u;\n"
-              << "    const float pt" << s << " = sg" << s << " ? vaf" << ri << " : val" << ri << ", pf" << s << " = sg" << s
-              << " ? val" << ri << " : vaf" << ri << ";\n";
+              << "    const float qf" << s << " = 1.f - val" << ri << ";\n"
+              << "    const float pt" << s << " = sg" << s << " ? qf" << s << " : val" << ri << ", pf" << s << " = sg" << s
+              << " ? val" << ri << " : qf" << s << ";\n";
         } else {
             const uint32_t nnz = K.nnz[ai++];
             o << "    float z" << s << " = -__uint_as_float(" << word(aw) << ");\n";
@@ -1546,7 +1548,7 @@ std::string jit_source(const Formula& f, const Built& b, const Plan& p, int u_pr
          "    double* __restrict__ ga, double* __restrict__ gb, const unsigned short* __restrict__ U,\n"
          "    double* __restrict__ obj, u32 R, u32 n_bool, float kappa,\n"
          "    double* __restrict__ terms, u32 terms_r, const u32* __restrict__ orig,\n"
-         "    const float* __restrict__ PT, const float* __restrict__ PF, double* __restrict__ gu,\n"
+         "    const float* __restrict__ PT, double* __restrict__ gu,\n"
          "    const FxScale* __restrict__ fxs, const float* __restrict__ kdev) {\n"
          "  FSMT_SPECIALISE_R\n"
          "  if (kdev) kappa = *kdev;   // the device-side solve loop's stage kappa (DevStage)\n"
@@ -1579,13 +1581,13 @@ std::string jit_source(const Formula& f, const Built& b, const Plan& p, int u_pr
          "  const float* ab = a + rr;\n"
          "  const float* bb = b + (rr - (u64)n_bool * R);   // reals are addressed by their unified id\n"
          "  const float* PTl = PT ? PT + rr : nullptr;\n"
-         "  const float* PFl = PF ? PF + rr : nullptr;\n"
+
          "  bool symt = false;   // symmetric class: the tile's variables are slot-table rows\n"
          "  switch (T.kclass) {\n";
     for (uint32_t k = 0; k < p.n_jit_kclasses; ++k) {
         if (kv >= 0 && (int)k != kv) continue;
         const std::string args = "(T, rp, vs, vr, acc + lane, ab, bb, ga, gb, U, R, R4, rr, r, live, n_bool, kq, dcoef, ebias, "
-                                 "gif, objacc, terms, terms_r, orig, PTl, PFl, gu, ring, (u32)lane); ";
+                                 "gif, objacc, terms, terms_r, orig, PTl, gu, ring, (u32)lane); ";
         o << "    case " << k << ": kc" << k << (dbgk ? "<true>" : "<false>") << args
           << (p.kclasses[k].sym ? "symt = true; " : "") << "break;\n";
     }
@@ -1646,7 +1648,7 @@ std::string jit_source(const Formula& f, const Built& b, const Plan& p, int u_pr
     o << "extern \"C\" __global__ void fsmt_kp_jit(u32 n_bool, u32 nv, u32 n_sa, const u32* __restrict__ satoms,\n"
          "    const float* __restrict__ a, const float* __restrict__ b, const u32* __restrict__ arow,\n"
          "    const u32* __restrict__ acol, const float* __restrict__ aval, const float* __restrict__ arhs,\n"
-         "    const float* __restrict__ ainv, u32 R, float kappa, float* __restrict__ PT, float* __restrict__ PF,\n"
+         "    const float* __restrict__ ainv, u32 R, float kappa, float* __restrict__ PT,\n"
          "    float* __restrict__ DD, const float* __restrict__ kdev) {\n"
          "  if (kdev) kappa = *kdev;\n"
          "  const u64 n = (u64)(n_bool + n_sa) * R;\n"
@@ -1655,7 +1657,7 @@ std::string jit_source(const Formula& f, const Built& b, const Plan& p, int u_pr
          "    const u32 row = (u32)(idx / R), r = (u32)(idx % R);\n"
          "    if (row < n_bool) {                       // Eq.4: p_true = (1 - a)/2\n"
          "      const float v = a[idx];\n"
-         "      PT[idx] = 0.5f * (1.f - v); PF[idx] = 0.5f * (1.f + v);\n"
+         "      PT[idx] = 0.5f * (1.f - v);\n"
          "    } else {                                  // Eq.7 with the erfc form (R28b)\n"
          "      const u32 t = row - n_bool, at = satoms[t];\n"
          "      float z = -arhs[at];\n"
@@ -1664,7 +1666,7 @@ std::string jit_source(const Formula& f, const Built& b, const Plan& p, int u_pr
          "      float ez;\n"
          "      const float e = fsmt_half_erfc(fabsf(u), ez);\n"
          "      const u64 o = (u64)(nv + t) * R + r;\n"
-         "      PT[o] = u >= 0.f ? e : 1.f - e; PF[o] = u >= 0.f ? 1.f - e : e;\n"
+         "      PT[o] = u >= 0.f ? e : 1.f - e;\n"
          "      DD[(u64)t * R + r] = dcoef * inv * ez;\n"
          "    }\n"
          "  }\n"
