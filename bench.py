@@ -333,6 +333,7 @@ def main():
     if not args.no_prepare:
         s.prepare(R)                  # kernels specialised for R restarts (part of the build)
     build_s = time.perf_counter() - t0
+    jit_status = s.jit_info()["status"]    # e.g. "active; prepared R=1024 k1 cap=28" (register cap chosen)
     dims = s.get_dims()
     S = args.pgd_steps
     s.set_params(eta=0.01, eps=1e-2)
@@ -444,7 +445,8 @@ def main():
                        "parallelism": (f"constraint-sharded x{world} (one flat {'NVLS multicast' if args.nvls else 'NCCL'} all-reduce per PGD step)" if constraint_mode
                                        else f"restart-sharded x{world}"),
                        "l2": "inputs exceed L2 (u16 U counters %.0f MB + structure + state per step)" % (dims["n_cons"] * R * 2 / 1e6),
-                       "accumulation": "fp64, exact on-grid sums (deterministic)", "build_s": round(build_s, 2)},
+                       "accumulation": "fp64, exact on-grid sums (deterministic)", "build_s": round(build_s, 2),
+                       "jit": jit_status},
             "roofline": {"bound": "alu", "achieved": alu_achieved, "peak": alu_peak, "unit": "TFLOP/s",
                          "frac": alu_achieved / alu_peak, "traffic": traffic, "kernel": "fsmt_k1_c0 (+ fsmt_k1_c1 concurrently; the JIT sweep of cfg4's two classes)" if args.config == "cfg4" else "fsmt_k1_jit / fsmt_k1_c<k>",
                          "basis": f"SURVEY 8(d) model {fma_pe:.0f} FMA-eq (x2 flop) per (constraint,restart) eval x "

@@ -40,6 +40,7 @@ struct fsmt_ctx {
     JitKernel jit_r;            // fsmt_prepare(R): the same module with R a compile-time constant
     uint32_t jit_r_R = 0;
     int jit_r_cap = 0;          // the prepared hot sweep's register cap (min CTAs/SM; 0 = none)
+    std::vector<int> jit_r_caps;   // the per-class sweep kernels' caps (fsmt_k1_c<k>)
     DevTiles T{};
     DevSlots slots{};                  // slot tables of the symmetric JIT classes (has_sym)
     cudaGraphExec_t gexec = nullptr;   // fsmt_run_stage's PGD steps as one CUDA graph (re-used, updated)
@@ -797,7 +798,10 @@ fsmt_status fsmt_jit_info(const fsmt_ctx* ctx, uint32_t* n_jit_classes, uint32_t
     if (msg && msg_len) {
         std::string m = ctx->host_only ? "host-only" : (active ? "active" : (ctx->plan.tiles.empty() ? "no JIT classes" : ctx->jit_error));
         if (active && ctx->jit_r.kernel)
-            m += "; prepared R=" + std::to_string(ctx->jit_r_R) + " k1 cap=" + std::to_string(ctx->jit_r_cap);
+        {
+            m += "; prepared R=" + std::to_string(ctx->jit_r_R) + " k1 cap=" + std::to_string(ctx->jit_r_cap) + " class caps=";
+            for (size_t k = 0; k < ctx->jit_r_caps.size(); ++k) m += (k ? "," : "") + std::to_string(ctx->jit_r_caps[k]);
+        }
         snprintf(msg, msg_len, "%s", m.c_str());
     }
     return FSMT_OK;
@@ -908,6 +912,7 @@ fsmt_status fsmt_prepare(fsmt_ctx* ctx, uint32_t R) {
     }
     if (!jit_compile(prepared_source(ctx, R, cap, &caps), ctx->jit_r, err)) return fail(ctx, FSMT_ERR_CUDA, "fsmt_prepare: " + err);
     ctx->jit_r_cap = cap;
+    ctx->jit_r_caps = caps;
     ctx->jit_r_R = R;
     return FSMT_OK;
 }

@@ -29,7 +29,7 @@ def main():
         d = json.loads(line)
         print(json.dumps({"variant": v or "default", "k1_ms": round(d["roofline"]["k1_ms_per_launch"], 3),
                           "value": d["value"], "frac": round(d["roofline"]["frac"], 4),
-                          "sm_mhz": d["clocks"].get("sm_mhz")}), flush=True)
+                          "sm_mhz": d["clocks"].get("sm_mhz"), "jit": d["config"].get("jit")}), flush=True)
 
 
 if __name__ == "__main__":
