@@ -687,6 +687,7 @@ const char* kErfcPrelude =
     "}\n"
     "__device__ __forceinline__ void fsmt_cpa_commit() { asm volatile(\"cp.async.commit_group;\" ::: \"memory\"); }\n"
     "template <int N> __device__ __forceinline__ void fsmt_cpa_wait() { asm volatile(\"cp.async.wait_group %0;\" :: \"n\"(N) : \"memory\"); }\n"
+    "__device__ __forceinline__ float fsmt_rcp(float x) { float r; asm(\"rcp.approx.ftz.f32 %0, %1;\" : \"=f\"(r) : \"f\"(x)); return r; }\n"
     "__device__ __forceinline__ float fsmt_ex2(float x) { float r; asm(\"ex2.approx.ftz.f32 %0, %1;\" : \"=f\"(r) : \"f\"(x)); return r; }\n"
     "// 0.5*erfc(z) for z >= 0 and ez = exp(-z^2) (dd/db factor, P:1326-1327).  Coefficients from\n"
     "// scripts/fit_erfc.py: z < 0.75: 0.5 (1 - z P(z^2)), P ~ erf(z)/z (degree 5);\n"
@@ -845,7 +846,13 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
     // record look-ahead alone measured neutral).  The plan keeps a spare record after the last, so
     // the look-ahead load needs no bounds test; past a tile's end the look-ahead row is the current one.
     const char* vpf_env = getenv("FSMT_JIT_VPF");
-    const bool vpf = !(vpf_env && vpf_env[0] == '0');
+    size_t n_stream_vals = 0;   // registers the value look-ahead holds (stream heads + members)
+    for (size_t i = 0; i < nr; ++i) n_stream_vals += is_stream(i) && alias_of(i) < 0;
+    const char* vmx_env = getenv("FSMT_JIT_VPF_MAX");
+    // (classes with more look-ahead values than this keep the in-iteration loads: their registers are
+    // scarcer than the latency; random family n = 500 1.52 -> 1.43 ms, cfg2 0.138 -> 0.134)
+    const size_t vpf_max = vmx_env ? (size_t)std::max(0, atoi(vmx_env)) : 32;
+    const bool vpf = !(vpf_env && vpf_env[0] == '0') && n_stream_vals <= vpf_max;
     const bool rpf = vpf;
     auto nword = [&](uint32_t w) { const std::string x = word(w); return x[0] == 'q' ? "n" + x : x; };
     // next-constraint stream values: psl (local index) and pval per stream head and member
@@ -1216,6 +1223,22 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
         else if (bh == "0.f") gfma(nd.level, mv, "(-" + bl + ")");
         else gfma(nd.level, mv, "(" + bh + " - " + bl + ")");
     }
+    // symmetric (count / product) classes add each slot's gradient into its accumulator as soon as
+    // it is formed, so the L gradients are never live together (registers: DESIGN.md §7 item 15)
+    auto acc_dst = [&](size_t ri) -> std::string {
+        if (!is_stream(ri)) return "acc" + std::to_string(ri);
+        return head_of(ri) >= 0 ? "accs[(sl" + std::to_string(head_of(ri)) + " + " + std::to_string(K.aff_dl[ri]) + ") * 32]"
+                                : "accs[sl" + std::to_string(ri) + " * 32]";
+    };
+    std::vector<char> g_inline(ns, 0);
+    auto emit_inline_acc = [&](size_t s2, const std::string& ind) {
+        const int ri0 = slot_ref0[s2];
+        const size_t ri = (size_t)(alias_of((size_t)ri0) >= 0 ? alias_of((size_t)ri0) : ri0);
+        const std::string d = acc_dst(ri), gs = "G" + std::to_string(s2), sg = "sg" + std::to_string(s2);
+        o << ind << d << " = fmaf(w, " << sg << " ? -" << gs << " : " << gs << ", " << d << ");\n";
+        g_inline[s2] = 1;
+    };
+    const bool sym_inline = (K.count || K.prod) && std::all_of(t.kinds.begin(), t.kinds.end(), [](int k) { return k == 2; });
     if (K.prod) {
         // OR / NAE / XOR over the L literals (pt_s = P(literal s true)): the COP in closed form and
         // dCOP/dpt_s from leave-one-out products, prefix products in registers times a running suffix:
@@ -1246,6 +1269,7 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
                 o << "      G" << s2 << " = fmaf(ua" << s2 << ", ub, -(va" << s2 << " * vb)); ub *= pf" << s2 << "; vb *= pt" << s2 << ";\n";
             else
                 o << "      G" << s2 << " = ua" << s2 << " * ub; ub *= " << f1 << s2 << ";\n";
+            if (sym_inline) emit_inline_acc(s2, "      ");
         }
         o << "    }\n";
     }
@@ -1257,27 +1281,44 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
         // recursion q_c = r_c pf_s + r_{c-1} pt_s: upward (r_c = (q_c - pt_s r_{c-1}) / pf_s) when
         // pt_s <= 1/2, downward from r_{L-1} = q_L / pt_s when pt_s > 1/2 -- the direction whose
         // ratio pt/pf (pf/pt) is <= 1, so rounding errors do not grow.
+        // Both passes on the packed f32x2 pipe (each component rounds like the scalar code, so the
+        // values are those of the scalar DP): the forward update treats q_{-1} = q_{i+1} = 0, which
+        // makes every literal update the fixed pairs (q_{2m+1}, q_{2m}); the backward runs the two
+        // directions (cf, cb) as one pair for min(k, L-1-k) steps.
         const uint32_t L = (uint32_t)ns, kk = K.sym_k;
         auto cq = [](uint32_t c) { return "cq" + std::to_string(c); };
-        o << "    float cq0 = pf0, cq1 = pt0;\n";
+        o << "    float cq0 = pf0, cq1 = pt0";
+        for (uint32_t c = 2; c <= L + 1; ++c) o << ", " << cq(c) << " = 0.f";
+        o << ";\n";
         for (uint32_t i = 1; i < L; ++i) {
             const std::string is = std::to_string(i);
-            o << "    float " << cq(i + 1) << " = " << cq(i) << " * pt" << is << ";\n";
-            for (uint32_t c = i; c >= 1; --c)
-                o << "    " << cq(c) << " = fmaf(" << cq(c - 1) << ", pt" << is << ", " << cq(c) << " * pf" << is << ");\n";
-            o << "    cq0 = cq0 * pf" << is << ";\n";
+            o << "    { const float2 P2 = FSMT_C2(pt" << is << "), F2 = FSMT_C2(pf" << is << ");\n";
+            for (int m = (int)(i + 1) / 2; m >= 0; --m) {
+                const uint32_t hi = 2 * (uint32_t)m + 1, lo = 2 * (uint32_t)m;
+                if (lo > i + 1) continue;
+                const std::string lm1 = m == 0 ? std::string("0.f") : cq(lo - 1);
+                o << "      { const float2 nw = __ffma2_rn(make_float2(" << cq(lo) << ", " << lm1 << "), P2, __fmul2_rn(make_float2("
+                  << cq(hi) << ", " << cq(lo) << "), F2)); " << cq(hi) << " = nw.x; " << cq(lo) << " = nw.y; }\n";
+            }
+            o << "    }\n";
         }
         o << "    pT = cq0;";
         for (uint32_t c = 1; c <= kk; ++c) o << " pT += " << cq(c) << ";";
         o << "\n";
+        const uint32_t nf = kk, nb = L - 1 - kk, np = std::min(nf, nb);
         for (uint32_t s2 = 0; s2 < L; ++s2) {
             const std::string ss = std::to_string(s2);
-            o << "    { const float rf = __frcp_rn(pf" << ss << "), rb = __frcp_rn(pt" << ss << ");\n"
-              << "      float cf = cq0 * rf;";
-            for (uint32_t c = 1; c <= kk; ++c) o << " cf = fmaf(-pt" << ss << ", cf, " << cq(c) << ") * rf;";
-            o << "\n      float cb = " << cq(L) << " * rb;";
-            for (uint32_t c = L - 1; c >= kk + 1; --c) o << " cb = fmaf(-pf" << ss << ", cb, " << cq(c) << ") * rb;";
-            o << "\n      G" << ss << " = pt" << ss << " <= 0.5f ? -cf : -cb; }\n";
+            // (rcp.approx: the divisor of the direction kept is >= 1/2, where MUFU.RCP is within 1 ulp;
+            // the discarded direction may divide by ~0, its inf / NaN never reaches G)
+            o << "    { const float rf = fsmt_rcp(pf" << ss << "), rb = fsmt_rcp(pt" << ss << ");\n"
+              << "      const float2 NP = make_float2(-pt" << ss << ", -pf" << ss << "), RR = make_float2(rf, rb);\n"
+              << "      float2 cc = __fmul2_rn(make_float2(cq0, " << cq(L) << "), RR);";
+            for (uint32_t j = 1; j <= np; ++j) o << " cc = __fmul2_rn(__ffma2_rn(NP, cc, make_float2(" << cq(j) << ", " << cq(L - j) << ")), RR);";
+            for (uint32_t j = np + 1; j <= nf; ++j) o << " cc.x = fmaf(-pt" << ss << ", cc.x, " << cq(j) << ") * rf;";
+            for (uint32_t j = np + 1; j <= nb; ++j) o << " cc.y = fmaf(-pf" << ss << ", cc.y, " << cq(L - j) << ") * rb;";
+            o << "\n      G" << ss << " = pt" << ss << " <= 0.5f ? -cc.x : -cc.y;\n";
+            if (sym_inline) emit_inline_acc(s2, "      ");
+            o << "    }\n";
         }
     }
     // a Boolean slot of a weight-seeded class whose G is only accumulated: its terms go straight
@@ -1326,7 +1367,7 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
                 accum(slot_ref0[s], WG, gref(s));
         } else if (t.kinds[s] == 2) {
             // dCOP/dp_true of the row = -dCOP/dp_true of a negated literal
-            accum(slot_ref0[s], WG, "(sg" + std::to_string(s) + " ? -" + gref(s) + " : " + gref(s) + ")");
+            if (!g_inline[s]) accum(slot_ref0[s], WG, "(sg" + std::to_string(s) + " ? -" + gref(s) + " : " + gref(s) + ")");
         } else {
             if (pair_with[s] >= 0) {
                 const std::string sa = std::to_string(s), sb = std::to_string(pair_with[s]);
