@@ -832,12 +832,14 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
         o << "  const unsigned short* Upf = hasU ? Up + (u64)" << upf << "u * R : nullptr;\n";
     }
     // the constraint loop unrolled twice for small classes (FSMT_JIT_UNROLL overrides; DESIGN.md §9:
-    // round 1 cfg3 0.884 -> 0.849 ms, cfg4 8.36 -> 8.33 ms; 4 is slower on cfg4)
+    // round 1 cfg3 0.884 -> 0.849 ms, cfg4 8.36 -> 8.33 ms; 4 is slower on cfg4); emitted right
+    // before the loop (after the look-ahead prologue)
+    std::string unroll_pragma;
     {
         // round 2: with the exact flush, the 22-reference placement class is faster not unrolled (cfg4
         // 8.08 vs 8.42 ms) while the 12-reference scheduling class keeps unroll 2 (cfg3 0.774 vs 0.864 ms)
         const char* ur = getenv("FSMT_JIT_UNROLL");
-        o << "#pragma unroll " << (ur ? std::max(1, atoi(ur)) : (K.n_refs <= 16 ? 2 : 1)) << "\n";
+        unroll_pragma = "#pragma unroll " + std::to_string(ur ? std::max(1, atoi(ur)) : (K.n_refs <= 16 ? 2 : 1)) + "\n";
     }
     // Software pipeline over the constraints (FSMT_JIT_VPF=0 disables; DESIGN.md §7 item 18): the
     // record is loaded one constraint ahead, and from it the stream references' values of the NEXT
@@ -887,7 +889,7 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
                 o << "  " << TY << " pval" << i << ";\n";
         stream_prefetch("  ", true, false);
     }
-    o << "  for (u32 c = 0; c < T.n_cons; ++c, rp += " << K.stride4 << ") {\n";
+    o << unroll_pragma << "  for (u32 c = 0; c < T.n_cons; ++c, rp += " << K.stride4 << ") {\n";
     if (rpf) {
         for (uint32_t q = 0; q < S4; ++q) o << "    const uint4 q" << q << " = nq" << q << ";\n";
         o << "    fsmt_cpa_wait<0>();\n    __syncwarp();\n";   // record c + 1 has landed in slot (c + 1) & 1
