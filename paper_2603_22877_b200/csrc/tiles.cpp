@@ -229,7 +229,8 @@ Plan make_plan(const Formula& f, const Built& b, bool enable_jit) {
     // stream-row budget from the typical constraint: 3x its distinct variables, in [40, 56]
     // (cfg4, 18 variables, best at 54; cfg3, 10 variables, best at 40), unless
     // FSMT_TILE_VMAX / FSMT_TILE_GROUP set it
-    if (!getenv("FSMT_TILE_VMAX")) {
+    size_t typical_vars = 0;   // distinct variables of the most common (non-symmetric JIT) constraint
+    if (!getenv("FSMT_TILE_VMAX") || !getenv("FSMT_TILE_MERGE")) {
         std::map<size_t, uint32_t> nvars;
         for (uint32_t c = 0; c < C; ++c) {
             const KClass& K = p.kclasses[kcl[c]];
@@ -242,7 +243,8 @@ Plan make_plan(const Formula& f, const Built& b, bool enable_jit) {
         uint32_t best = 0;
         for (const auto& kv : nvars)
             if (kv.second > best) { best = kv.second; mode = kv.first; }
-        if (best) {
+        typical_vars = mode;
+        if (best && !getenv("FSMT_TILE_VMAX")) {
             p.vmax = (uint32_t)std::max<size_t>(40, std::min<size_t>(56, 3 * mode));
             if (!getenv("FSMT_TILE_GROUP")) p.group = p.vmax;
         }
@@ -260,6 +262,14 @@ Plan make_plan(const Formula& f, const Built& b, bool enable_jit) {
         for (uint32_t u : batch) group[u] = cur_group;
         cur_size += (uint32_t)batch.size();
     }
+    // Tile merging (FSMT_TILE_MERGE=0/1 overrides): the stream side's group leads the sort key, and a
+    // tile may span several keys that share it, within the row / run / constraint budgets (up to 128
+    // constraints), so the per-tile start and stream-row flush are amortised over more constraints.
+    // Default for formulas whose typical constraint has >= 16 variables (cfg4 7.08 ->
+    // 6.66 ms; cfg3, 10 variables, 0.711 -> 0.735 ms merged).
+    const char* tm_env = getenv("FSMT_TILE_MERGE");
+    const bool tile_merge = tm_env ? tm_env[0] == '1' : typical_vars >= 16;
+    if (tile_merge && !getenv("FSMT_TILE_CMAX")) p.cmax = 128;
     // 3. sort keys
     struct Key {
         uint32_t kc;
@@ -276,6 +286,9 @@ Plan make_plan(const Formula& f, const Built& b, bool enable_jit) {
         Key k{kcl[c], {UINT32_MAX, UINT32_MAX, UINT32_MAX, UINT32_MAX}};
         if (gs.size() <= 4) {
             for (size_t i = 0; i < gs.size(); ++i) k.g[i] = gs[i];
+            // merge mode: the newest group (whose variables change fastest in first-appearance order:
+            // the stream side) leads the key, so the blocks sharing a stream group are adjacent
+            if (tile_merge && gs.size() > 1) std::rotate(k.g, k.g + gs.size() - 1, k.g + gs.size());
         } else {
             k.g[0] = UINT32_MAX - 1;          // wide footprint: keep original order
         }
@@ -393,7 +406,7 @@ Plan make_plan(const Formula& f, const Built& b, bool enable_jit) {
         const Key& k0 = keys[p.order[i]];
         while (i < C && p.cons_kclass[i] == kc && T.n_cons < p.cmax) {
             const Key& ki = keys[p.order[i]];
-            if (T.n_cons > 0 && (memcmp(ki.g, k0.g, sizeof(k0.g)) != 0)) break;
+            if (T.n_cons > 0 && !tile_merge && (memcmp(ki.g, k0.g, sizeof(k0.g)) != 0)) break;
             cons_vars(p.order[i], vars);
             adds.clear();
             addr.clear();
@@ -831,16 +844,6 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
             o << "  u32 un" << k << " = hasU ? (u32)" << uld << "(" << ucast << "(Up + (u64)" << k << "u * R)) : 0u;\n";
         o << "  const unsigned short* Upf = hasU ? Up + (u64)" << upf << "u * R : nullptr;\n";
     }
-    // the constraint loop unrolled twice for small classes (FSMT_JIT_UNROLL overrides; DESIGN.md §9:
-    // round 1 cfg3 0.884 -> 0.849 ms, cfg4 8.36 -> 8.33 ms; 4 is slower on cfg4); emitted right
-    // before the loop (after the look-ahead prologue)
-    std::string unroll_pragma;
-    {
-        // round 2: with the exact flush, the 22-reference placement class is faster not unrolled (cfg4
-        // 8.08 vs 8.42 ms) while the 12-reference scheduling class keeps unroll 2 (cfg3 0.774 vs 0.864 ms)
-        const char* ur = getenv("FSMT_JIT_UNROLL");
-        unroll_pragma = "#pragma unroll " + std::to_string(ur ? std::max(1, atoi(ur)) : (K.n_refs <= 16 ? 2 : 1)) + "\n";
-    }
     // Software pipeline over the constraints (FSMT_JIT_VPF=0 disables; DESIGN.md §7 item 18): the
     // record is loaded one constraint ahead, and from it the stream references' values of the NEXT
     // constraint are loaded during this one, so their L2 latency hides behind a whole iteration
@@ -877,10 +880,21 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
     // the compiler cannot hoist the record's move into the uniform datapath right behind its load
     // (ncu v19: with the look-ahead in registers, 27 % of the stall samples sat on that R2UR).
     const uint32_t S4 = K.stride4;
+    // FSMT_JIT_RALL=1: every lane copies every chunk (identical bytes to the same address), so its own
+    // wait suffices and no __syncwarp is needed (A/B)
+    const char* rall_env = getenv("FSMT_JIT_RALL");
+    const bool rall = rall_env && rall_env[0] == '1';
+    auto cpy = [&](const std::string& ind, const std::string& dst, const std::string& src) {
+        if (rall)
+            for (uint32_t q = 0; q < S4; ++q) o << ind << "fsmt_cpa16(" << dst << " + " << q << "u, " << src << " + " << q << "u);\n";
+        else
+            o << ind << "if (lane < " << S4 << "u) fsmt_cpa16(" << dst << " + lane, " << src << " + lane);\n";
+    };
     if (rpf) {
-        o << "  if (lane < " << S4 << "u) fsmt_cpa16(rring + lane, rp + lane);\n  fsmt_cpa_commit();\n"
-          << "  if (lane < " << S4 << "u) fsmt_cpa16(rring + " << S4 << "u + lane, rp + " << S4 << "u + lane);\n  fsmt_cpa_commit();\n"
-          << "  fsmt_cpa_wait<1>();\n  __syncwarp();\n";
+        cpy("  ", "rring", "rp");
+        o << "  fsmt_cpa_commit();\n";
+        cpy("  ", "rring + " + std::to_string(S4) + "u", "rp + " + std::to_string(S4) + "u");
+        o << "  fsmt_cpa_commit();\n  fsmt_cpa_wait<1>();\n" << (rall ? "" : "  __syncwarp();\n");
         for (uint32_t q = 0; q < S4; ++q) o << "  uint4 nq" << q << " = rring[" << q << "];\n";
     }
     if (vpf) {
@@ -889,13 +903,27 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
                 o << "  " << TY << " pval" << i << ";\n";
         stream_prefetch("  ", true, false);
     }
+    // the constraint loop unrolled twice for small classes (FSMT_JIT_UNROLL overrides; DESIGN.md §9:
+    // round 1 cfg3 0.884 -> 0.849 ms, cfg4 8.36 -> 8.33 ms; 4 is slower on cfg4); emitted right
+    // before the loop (after the look-ahead prologue)
+    std::string unroll_pragma;
+    {
+        // round 2: with the exact flush, the 22-reference placement class is faster not unrolled (cfg4
+        // 8.08 vs 8.42 ms) while the 12-reference scheduling class keeps unroll 2 (cfg3 0.774 vs 0.864 ms)
+        const char* ur = getenv("FSMT_JIT_UNROLL");
+        // v21: with the value look-ahead, unroll 2 also for the placement class (no register-rotation
+        // moves: cfg4 7.41 -> 7.12 ms at 80 registers); symmetric classes and classes without it keep
+        // the round-2 rule (cfg2 0.133 vs 0.157 ms, random family n = 100 0.121 vs 0.131 ms unrolled)
+        unroll_pragma = "#pragma unroll " +
+                        std::to_string(ur ? std::max(1, atoi(ur)) : (K.n_refs <= 16 || (vpf && !K.sym) ? 2 : 1)) + "\n";
+    }
     o << unroll_pragma << "  for (u32 c = 0; c < T.n_cons; ++c, rp += " << K.stride4 << ") {\n";
     if (rpf) {
         for (uint32_t q = 0; q < S4; ++q) o << "    const uint4 q" << q << " = nq" << q << ";\n";
-        o << "    fsmt_cpa_wait<0>();\n    __syncwarp();\n";   // record c + 1 has landed in slot (c + 1) & 1
+        o << "    fsmt_cpa_wait<0>();\n" << (rall ? "" : "    __syncwarp();\n");   // record c + 1 has landed in slot (c + 1) & 1
         for (uint32_t q = 0; q < S4; ++q) o << "    nq" << q << " = rring[((c + 1u) & 1u) * " << S4 << "u + " << q << "u];\n";
-        o << "    if (lane < " << S4 << "u) fsmt_cpa16(rring + (c & 1u) * " << S4 << "u + lane, rp + " << 2 * S4 << "u + lane);\n"
-          << "    fsmt_cpa_commit();\n";
+        cpy("    ", "rring + (c & 1u) * " + std::to_string(S4) + "u", "rp + " + std::to_string(2 * S4) + "u");
+        o << "    fsmt_cpa_commit();\n";
     } else {
         for (uint32_t q = 0; q < S4; ++q) o << "    const uint4 q" << q << " = __ldg(rp + " << q << ");\n";
     }
@@ -1349,9 +1377,9 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
     auto gref = [&](size_t s) { return cmp ? "(-G" + std::to_string(s) + ")" : "G" + std::to_string(s); };
     if (massF) o << "    const " << TY << " E = fmaf(2.f, pF, -1.f);\n";
     else o << "    const " << TY << " E = 1.f - 2.f * pT;\n";
-    // the objective's first level in fp32 over the tile's <= 64 constraints, flushed once per tile into
-    // the fp64 objective (two-level accumulation, R28: the per-tile fp32 sum of <= 64 terms adds
-    // <= 64 x 2^-24 relative; across tiles the sum is exact on the objective's grid)
+    // the objective's first level in fp32 over the tile's <= 128 constraints, flushed once per tile into
+    // the fp64 objective (two-level accumulation, R28: the per-tile fp32 sum of <= 128 terms adds
+    // <= 128 x 2^-24 relative; across tiles the sum is exact on the objective's grid)
     o << "    objacc = fmaf(w, E, objacc);\n"
          "    if (hasT && live && r == terms_r) terms[orig[T.cons_begin + c]] = (double)E;\n";
     // gradient terms per target reference (aliases fold into their target: one read-modify-write)
@@ -1610,7 +1638,7 @@ std::string jit_source(const Formula& f, const Built& b, const Plan& p, int u_pr
          "  const bool live = r < R;\n"
          "  const u64 rr = live ? r : 0;\n"
          "  for (u32 l = lane; l < n_v; l += 32) vs[l] = tile_vars[T.var_off + l];\n"
-         "  for (u32 l = 0; l < n_s; ++l) acc[l * 32 + lane] = 0.f;\n"
+         "  for (u32 l = lane; l < n_s * 8u; l += 32u) ((float4*)acc)[l] = make_float4(0.f, 0.f, 0.f, 0.f);   // rows, 16 B stores\n"
          "  __syncwarp();\n"
          "  const VID* vr = vs + n_s;\n"
          "  const float kq = kappa * 0.70710678118654752f;\n"
