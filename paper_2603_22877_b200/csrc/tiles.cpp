@@ -263,13 +263,15 @@ Plan make_plan(const Formula& f, const Built& b, bool enable_jit) {
         cur_size += (uint32_t)batch.size();
     }
     // Tile merging (FSMT_TILE_MERGE=0/1 overrides): the stream side's group leads the sort key, and a
-    // tile may span several keys that share it, within the row / run / constraint budgets (up to 128
-    // constraints), so the per-tile start and stream-row flush are amortised over more constraints.
-    // Default for formulas whose typical constraint has >= 16 variables (cfg4 7.08 ->
-    // 6.66 ms; cfg3, 10 variables, 0.711 -> 0.735 ms merged).
+    // tile may span several keys that share it, within the row / run / constraint budgets (up to 256
+    // run variables and 256 constraints), so the per-tile start and stream-row flush are amortised
+    // over more constraints.  Default for formulas whose typical constraint has >= 16 variables
+    // (cfg4 7.08 -> 6.58 ms, place9856 6.03 -> 4.98 ms; cfg3, 10 variables, 0.711 ->
+    // 0.735 ms merged).
     const char* tm_env = getenv("FSMT_TILE_MERGE");
     const bool tile_merge = tm_env ? tm_env[0] == '1' : typical_vars >= 16;
-    if (tile_merge && !getenv("FSMT_TILE_CMAX")) p.cmax = 128;
+    if (tile_merge && !getenv("FSMT_TILE_CMAX")) p.cmax = 256;
+    if (tile_merge && !getenv("FSMT_TILE_RMAX")) p.rmax = 256;   // run ids are 2 B of shared memory each
     // 3. sort keys
     struct Key {
         uint32_t kc;
@@ -1377,9 +1379,9 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
     auto gref = [&](size_t s) { return cmp ? "(-G" + std::to_string(s) + ")" : "G" + std::to_string(s); };
     if (massF) o << "    const " << TY << " E = fmaf(2.f, pF, -1.f);\n";
     else o << "    const " << TY << " E = 1.f - 2.f * pT;\n";
-    // the objective's first level in fp32 over the tile's <= 128 constraints, flushed once per tile into
-    // the fp64 objective (two-level accumulation, R28: the per-tile fp32 sum of <= 128 terms adds
-    // <= 128 x 2^-24 relative; across tiles the sum is exact on the objective's grid)
+    // the objective's first level in fp32 over the tile's <= 256 constraints, flushed once per tile into
+    // the fp64 objective (two-level accumulation, R28: the per-tile fp32 sum of <= 256 terms adds
+    // <= 256 x 2^-24 relative; across tiles the sum is exact on the objective's grid)
     o << "    objacc = fmaf(w, E, objacc);\n"
          "    if (hasT && live && r == terms_r) terms[orig[T.cons_begin + c]] = (double)E;\n";
     // gradient terms per target reference (aliases fold into their target: one read-modify-write)
