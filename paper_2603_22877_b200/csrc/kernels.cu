@@ -494,13 +494,23 @@ void launch_gather_rows_u16(uint16_t* dst, const uint16_t* src, const uint32_t* 
     k_gather_rows_u16<<<148 * 8, 256, 0, st>>>(dst, src, idx, rows, R, 0);
 }
 
+// Tiles are split into constraint ranges at launch when (tiles x restart tiles) would leave the
+// GPU short of one-warp CTAs (few restarts, e.g. R = 32): ~16 K CTAs fill 148 SMs x 28 slots four
+// times over; at most 8 ranges per tile.
+static uint32_t tile_split(uint64_t ctas) {
+    const uint64_t target = 148ull * 28 * 4;
+    if (ctas == 0 || ctas >= target) return 1;
+    return (uint32_t)std::min<uint64_t>(8, (target + ctas - 1) / ctas);
+}
+
 void launch_sweep_jit(cudaKernel_t k, const DevFormula& F, const DevState& S, const DevTiles& T, float kappa,
                       double* terms, uint32_t terms_r, cudaStream_t st, const DevSlots* D) {
     if (T.n_tiles == 0 || S.R == 0) return;
     const int kVmax = (int)T.vmax, kVtot = (int)(T.vmax + T.rmax);    // Plan::vmax, Plan::rmax
     // one one-warp CTA per (tile, 32 restarts)
     const uint64_t rtiles = (S.R + 31) / 32;
-    const unsigned blocks = (unsigned)((uint64_t)T.n_tiles * rtiles);
+    uint32_t nsplit = tile_split((uint64_t)T.n_tiles * rtiles);
+    const unsigned blocks = (unsigned)((uint64_t)T.n_tiles * rtiles * nsplit);
     const size_t smem = (size_t)T.ring_uint4 * 16 + (size_t)kVmax * 32 * 4 + (size_t)kVtot * T.vid_bytes;   // ring | rows | ids
     if (smem > 48 * 1024) cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     uint32_t n_tiles = T.n_tiles, R = S.R, n_bool = F.n_bool;
@@ -510,7 +520,7 @@ void launch_sweep_jit(cudaKernel_t k, const DevFormula& F, const DevState& S, co
     double* GU = D ? D->GU : nullptr;
     void* args[] = {(void*)&T.tiles, &n_tiles, (void*)&T.recs, (void*)&T.tile_vars, (void*)&S.a, (void*)&S.b,
                     (void*)&S.ga, (void*)&S.gb, (void*)&U, (void*)&S.obj, &R, &n_bool, &kappa,
-                    &terms, &terms_r, (void*)&F.orig, (void*)&PT, (void*)&GU, (void*)&S.fx, (void*)&kdev};
+                    &terms, &terms_r, (void*)&F.orig, (void*)&PT, (void*)&GU, (void*)&S.fx, (void*)&kdev, &nsplit};
     cudaLaunchKernel((const void*)k, dim3(blocks), dim3(32), args, smem, st);
 }
 
@@ -549,14 +559,15 @@ void launch_verify_jit(cudaKernel_t k, const DevFormula& F, const DevState& S, c
                        const float* y, uint16_t* U_update, uint8_t* per_con, cudaStream_t st, const uint8_t* TT) {
     if (T.n_tiles == 0 || S.R == 0) return;
     const int vtot = (int)(T.vmax + T.rmax);
-    const unsigned blocks = (unsigned)((uint64_t)T.n_tiles * ((S.R + 31) / 32));   // one warp per (tile, 32 restarts)
+    uint32_t nsplit = tile_split((uint64_t)T.n_tiles * ((S.R + 31) / 32));
+    const unsigned blocks = (unsigned)((uint64_t)T.n_tiles * ((S.R + 31) / 32) * nsplit);   // one warp per (tile range, 32 restarts)
     const size_t smem = (size_t)vtot * 4;
     uint32_t n_tiles = T.n_tiles, R = S.R, n_bool = F.n_bool;
     uint32_t* unsat = S.unsat;
     void* args[] = {(void*)&T.tiles, &n_tiles, (void*)&T.recs, (void*)&T.vrecs, (void*)&T.tile_vars, (void*)&x,
                     (void*)&y, (void*)&U_update, (void*)&unsat, (void*)&per_con, (void*)&F.orig, &R, &n_bool,
                     (void*)&F.atom_rowptr, (void*)&F.atom_val64, (void*)&F.atom_rhs64, (void*)&F.atom_strict, (void*)&TT,
-                    (void*)&S.umax, (void*)&S.flags};
+                    (void*)&S.umax, (void*)&S.flags, &nsplit};
     cudaLaunchKernel((const void*)k, dim3(blocks), dim3(32), args, smem, st);
 }
 

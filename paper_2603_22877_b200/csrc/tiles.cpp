@@ -1532,11 +1532,19 @@ void emit_verify_class(std::ostringstream& o, uint32_t kid, const KClass& K, con
             const uint32_t nnz = K.nnz[ai];
             if (K.vfold) {   // class-constant coefficients / strictness as exact literals, rhs from the record
                 auto vw = [&](uint32_t w) { return "v" + std::to_string(w / 4) + "." + comp(w); };
+                // s = 0; s += q_j y_j in stored order (R22).  A class-constant q_j = +-1 makes q_j y_j = +-y_j
+                // exactly, and 0 + x = x (up to the sign of a zero, which no comparison sees): the same
+                // values without the multiplications and the leading add
                 o << "    bool t" << s << ";\n    { double sacc = 0.0;\n";
                 for (uint32_t k = 0; k < nnz; ++k) {
+                    const double q = K.vcoef[ai][k];
                     uint64_t bits;
-                    memcpy(&bits, &K.vcoef[ai][k], 8);
-                    o << "      sacc = __dadd_rn(sacc, __dmul_rn(__longlong_as_double(" << (long long)bits << "LL), kv" << ref << "));\n";
+                    memcpy(&bits, &q, 8);
+                    const std::string kv = "kv" + std::to_string(ref);
+                    const std::string term = q == 1.0 ? kv : q == -1.0 ? "(-" + kv + ")"
+                                                     : "__dmul_rn(__longlong_as_double(" + std::to_string((long long)bits) + "LL), " + kv + ")";
+                    if (k == 0) o << "      sacc = " << term << ";\n";
+                    else o << "      sacc = __dadd_rn(sacc, " << term << ");\n";
                     ++ref;
                 }
                 o << "      const double rhs = __hiloint2double((int)" << vw(2 * ai + 1) << ", (int)" << vw(2 * ai) << ");\n"
@@ -1622,7 +1630,7 @@ std::string jit_source(const Formula& f, const Built& b, const Plan& p, int u_pr
          "    double* __restrict__ obj, u32 R, u32 n_bool, float kappa,\n"
          "    double* __restrict__ terms, u32 terms_r, const u32* __restrict__ orig,\n"
          "    const float* __restrict__ PT, double* __restrict__ gu,\n"
-         "    const FxScale* __restrict__ fxs, const float* __restrict__ kdev) {\n"
+         "    const FxScale* __restrict__ fxs, const float* __restrict__ kdev, u32 nsplit) {\n"
          "  FSMT_SPECIALISE_R\n"
          "  if (kdev) kappa = *kdev;   // the device-side solve loop's stage kappa (DevStage)\n"
          "  extern __shared__ float smem[];\n"
@@ -1631,10 +1639,22 @@ std::string jit_source(const Formula& f, const Built& b, const Plan& p, int u_pr
          "  float* acc = smem + RING * 4;                         // stream-variable rows\n"
          "  VID* vs = (VID*)(acc + VMAX * 32);                    // stream then run variable ids\n"
          "  const u32 rtiles = (R + 31) / 32;\n"
-      << "  const u64 ti = blockIdx.x / rtiles;                  // tile-major: a tile's restart tiles together\n"
+      << "  const u64 tsub = blockIdx.x / rtiles;                // tile-major: a tile's restart tiles together\n"
+         "  const u64 ti = tsub / nsplit;\n"
          "  const u32 rt = (u32)(blockIdx.x % rtiles);\n"
          "  if (ti >= n_tiles) return;\n"
-         "  const TileDesc T = tiles[ti];\n"
+         "  TileDesc T = tiles[ti];\n"
+         "  // launch-time split of a tile into nsplit constraint ranges (few restarts: enough CTAs to fill\n"
+         "  // the GPU); each range flushes its own stream rows (exact on-grid adds, any order)\n"
+         "  u32 cb = 0u;\n"
+         "  if (nsplit > 1u) {\n"
+         "    const u32 sub = (u32)(tsub % nsplit);\n"
+         "    cb = (u32)((u64)T.n_cons * sub / nsplit);\n"
+         "    const u32 ce = (u32)((u64)T.n_cons * (sub + 1u) / nsplit);\n"
+         "    if (ce <= cb) return;\n"
+         "    T.cons_begin += cb;\n"
+         "    T.n_cons = ce - cb;\n"
+         "  }\n"
          "  const u32 n_s = T.n_vars & 0xffffu, n_v = n_s + (T.n_vars >> 16);\n"
          "  const u32 r = rt * 32 + lane;\n"
          "  const bool live = r < R;\n"
@@ -1659,7 +1679,8 @@ std::string jit_source(const Formula& f, const Built& b, const Plan& p, int u_pr
          "  switch (T.kclass) {\n";
     for (uint32_t k = 0; k < p.n_jit_kclasses; ++k) {
         if (kv >= 0 && (int)k != kv) continue;
-        const std::string args = "(T, rp, vs, vr, acc + lane, ab, bb, ga, gb, U, R, R4, rr, r, live, n_bool, kq, dcoef, ebias, "
+        const std::string args = "(T, rp + (u64)cb * " + std::to_string(p.kclasses[k].stride4) +
+                                 "u, vs, vr, acc + lane, ab, bb, ga, gb, U, R, R4, rr, r, live, n_bool, kq, dcoef, ebias, "
                                  "gif, objacc, terms, terms_r, orig, PTl, gu, ring, (u32)lane); ";
         o << "    case " << k << ": kc" << k << (dbgk ? "<true>" : "<false>") << args
           << (p.kclasses[k].sym ? "symt = true; " : "") << "break;\n";
@@ -1685,7 +1706,7 @@ std::string jit_source(const Formula& f, const Built& b, const Plan& p, int u_pr
          "    unsigned char* __restrict__ per_con, const u32* __restrict__ orig, u32 R, u32 n_bool,\n"
          "    const u32* __restrict__ arow, const double* __restrict__ aval, const double* __restrict__ arhs,\n"
          "    const unsigned char* __restrict__ astrict, const unsigned char* __restrict__ TT,\n"
-         "    u32* __restrict__ umax, u32* __restrict__ flags) {\n"
+         "    u32* __restrict__ umax, u32* __restrict__ flags, u32 nsplit) {\n"
          "  FSMT_SPECIALISE_R\n"
          "  extern __shared__ float smem[];\n"
          "  const int lane = threadIdx.x & 31;\n"
@@ -1693,9 +1714,19 @@ std::string jit_source(const Formula& f, const Built& b, const Plan& p, int u_pr
          "  const u32 rtiles = (R + 31) / 32;\n"
          "  const u64 gw = (u64)blockIdx.x;\n"
          "  const u32 rt = (u32)(gw % rtiles);\n"
-         "  const u64 ti = gw / rtiles;\n"
+         "  const u64 tsub = gw / rtiles;\n"
+         "  const u64 ti = tsub / nsplit;\n"
          "  if (ti >= n_tiles) return;\n"
-         "  const TileDesc T = tiles[ti];\n"
+         "  TileDesc T = tiles[ti];\n"
+         "  u32 cb = 0u;   // launch-time split (as the sweep)\n"
+         "  if (nsplit > 1u) {\n"
+         "    const u32 sub = (u32)(tsub % nsplit);\n"
+         "    cb = (u32)((u64)T.n_cons * sub / nsplit);\n"
+         "    const u32 ce = (u32)((u64)T.n_cons * (sub + 1u) / nsplit);\n"
+         "    if (ce <= cb) return;\n"
+         "    T.cons_begin += cb;\n"
+         "    T.n_cons = ce - cb;\n"
+         "  }\n"
          "  const u32 r = rt * 32 + lane;\n"
          "  const bool live = r < R;\n"
          "  const u64 rr = live ? r : 0;\n"
@@ -1708,8 +1739,8 @@ std::string jit_source(const Formula& f, const Built& b, const Plan& p, int u_pr
          "  u32 cnt = 0u, umx = 0u, ovf = 0u;\n"
          "  switch (T.kclass) {\n";
     for (uint32_t k = 0; k < p.n_jit_kclasses; ++k)
-        o << "    case " << k << ": cnt = kv" << k
-          << "(T, rp, vp, vs, vr, x, y, U, per_con, orig, R, rr, r, live, n_bool, arow, aval, arhs, astrict, TT, umx, ovf); break;\n";
+        o << "    case " << k << ": cnt = kv" << k << "(T, rp + (u64)cb * " << p.kclasses[k].stride4 << "u, vp + (u64)cb * "
+          << p.kclasses[k].vstride4 << "u, vs, vr, x, y, U, per_con, orig, R, rr, r, live, n_bool, arow, aval, arhs, astrict, TT, umx, ovf); break;\n";
     o << "    default: break;\n  }\n"
          "  if (live && cnt) atomicAdd(unsat + r, cnt);\n"
          "  if (live && umx) atomicMax(umax + r, umx);   // the restart's largest counter (k1_prologue's shift)\n"
