@@ -541,6 +541,7 @@ fsmt_status fsmt_build_xbdd(fsmt_ctx* ctx, uint64_t node_budget) {
             ctx->T.vmax = P.kernel_vmax();
             ctx->T.ring_uint4 = P.ring_uint4();
             ctx->T.vid_bytes = P.vid_bytes();
+            ctx->T.cons_per_tile = P.tiles.empty() ? 0u : (uint32_t)(P.jit_cons_end / P.tiles.size());
             // run-variable id slots the tiles actually use (<= Plan::rmax): the sweep's shared memory
             // is sized by it, so more one-warp CTAs fit per SM
             uint32_t rmax_used = 1;

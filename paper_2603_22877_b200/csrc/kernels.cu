@@ -497,10 +497,15 @@ void launch_gather_rows_u16(uint16_t* dst, const uint16_t* src, const uint32_t* 
 // Tiles are split into constraint ranges at launch when (tiles x restart tiles) would leave the
 // GPU short of one-warp CTAs (few restarts, e.g. R = 32): ~16 K CTAs fill 148 SMs x 28 slots four
 // times over; at most 8 ranges per tile.
-static uint32_t tile_split(uint64_t ctas) {
+// Each range re-runs the tile's start and flushes all its stream rows, so a range keeps >= 32
+// constraints (cfg2's 8-constraint symmetric tiles: 0.13 -> 0.30 ms split 3 ways).
+static uint32_t tile_split(uint64_t ctas, uint64_t cons_per_tile) {
+    static const int forced = [] { const char* e = getenv("FSMT_TILE_SPLIT"); return e ? atoi(e) : 0; }();   // A/B
+    if (forced > 0) return (uint32_t)std::min(forced, 64);
     const uint64_t target = 148ull * 28 * 4;
     if (ctas == 0 || ctas >= target) return 1;
-    return (uint32_t)std::min<uint64_t>(8, (target + ctas - 1) / ctas);
+    const uint64_t by_size = std::max<uint64_t>(1, cons_per_tile / 32);
+    return (uint32_t)std::min<uint64_t>(std::min<uint64_t>(8, by_size), (target + ctas - 1) / ctas);
 }
 
 void launch_sweep_jit(cudaKernel_t k, const DevFormula& F, const DevState& S, const DevTiles& T, float kappa,
@@ -509,7 +514,7 @@ void launch_sweep_jit(cudaKernel_t k, const DevFormula& F, const DevState& S, co
     const int kVmax = (int)T.vmax, kVtot = (int)(T.vmax + T.rmax);    // Plan::vmax, Plan::rmax
     // one one-warp CTA per (tile, 32 restarts)
     const uint64_t rtiles = (S.R + 31) / 32;
-    uint32_t nsplit = tile_split((uint64_t)T.n_tiles * rtiles);
+    uint32_t nsplit = tile_split((uint64_t)T.n_tiles * rtiles, T.cons_per_tile);
     const unsigned blocks = (unsigned)((uint64_t)T.n_tiles * rtiles * nsplit);
     const size_t smem = (size_t)T.ring_uint4 * 16 + (size_t)kVmax * 32 * 4 + (size_t)kVtot * T.vid_bytes;   // ring | rows | ids
     if (smem > 48 * 1024) cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -559,7 +564,7 @@ void launch_verify_jit(cudaKernel_t k, const DevFormula& F, const DevState& S, c
                        const float* y, uint16_t* U_update, uint8_t* per_con, cudaStream_t st, const uint8_t* TT) {
     if (T.n_tiles == 0 || S.R == 0) return;
     const int vtot = (int)(T.vmax + T.rmax);
-    uint32_t nsplit = tile_split((uint64_t)T.n_tiles * ((S.R + 31) / 32));
+    uint32_t nsplit = tile_split((uint64_t)T.n_tiles * ((S.R + 31) / 32), T.cons_per_tile);
     const unsigned blocks = (unsigned)((uint64_t)T.n_tiles * ((S.R + 31) / 32) * nsplit);   // one warp per (tile range, 32 restarts)
     const size_t smem = (size_t)vtot * 4;
     uint32_t n_tiles = T.n_tiles, R = S.R, n_bool = F.n_bool;

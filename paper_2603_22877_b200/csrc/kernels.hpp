@@ -151,6 +151,7 @@ struct DevTiles {
     uint32_t rmax;               // run variables per tile (Plan::rmax)
     uint32_t ring_uint4;         // K1's per-warp shared-memory record ring, in uint4 (Plan::ring_uint4)
     uint32_t vid_bytes;          // K1's shared-memory variable-id width, 2 or 4 (Plan::vid_bytes)
+    uint32_t cons_per_tile;      // mean constraints per tile (launch-time split rule)
     const void* vrecs;           // K5 records (atom ids), tile.pad1 = offset in uint4
     uint32_t first;              // global index of tiles[0] (constraint shards start mid-plan)
 };
