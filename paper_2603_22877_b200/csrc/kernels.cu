@@ -500,7 +500,8 @@ void launch_gather_rows_u16(uint16_t* dst, const uint16_t* src, const uint32_t* 
 // Each range re-runs the tile's start and flushes all its stream rows, so a range keeps >= 32
 // constraints (cfg2's 8-constraint symmetric tiles: 0.13 -> 0.30 ms split 3 ways).
 static uint32_t tile_split(uint64_t ctas, uint64_t cons_per_tile) {
-    static const int forced = [] { const char* e = getenv("FSMT_TILE_SPLIT"); return e ? atoi(e) : 0; }();   // A/B
+    const char* fe = getenv("FSMT_TILE_SPLIT");   // A/B and the parity matrix (read per launch)
+    const int forced = fe ? atoi(fe) : 0;
     if (forced > 0) return (uint32_t)std::min(forced, 64);
     const uint64_t target = 148ull * 28 * 4;
     if (ctas == 0 || ctas >= target) return 1;

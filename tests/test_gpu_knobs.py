@@ -26,6 +26,8 @@ KNOBS = [
     {"FSMT_JIT_VPF": "0"},
     {"FSMT_JIT_VPF": "0", "FSMT_JIT_UNROLL": "2", "FSMT_JIT_UPF": "2"},
     {"FSMT_TILE_VMAX": "16", "FSMT_TILE_RMAX": "16", "FSMT_TILE_CMAX": "3"},
+    {"FSMT_TILE_MERGE": "1"},
+    {"FSMT_TILE_MERGE": "0"},
 ]
 
 
@@ -123,4 +125,44 @@ def test_prepared_r_bit_identical(name):
         check_objective(p1[0][r], C, float(sum(w)), what=f"{name} prepared")
         check_gradient(p1[1][:, r], oga, what=f"{name} prepared grad_a")
         check_gradient(p1[2][:, r], ogb, what=f"{name} prepared grad_b")
+        assert np.array_equal(ppc[:, r].astype(int), want)
+
+
+@pytest.mark.parametrize("split", ["2", "5"])
+@pytest.mark.parametrize("name", ["cfg3s", "cfg4s", "cfg2"])
+def test_tile_split_parity(name, split):
+    """The launch-time split of tiles into constraint ranges (FSMT_TILE_SPLIT, read per launch; the
+    default splits only tiles of >= 64 constraints when the restarts are few): the exact check (stage
+    end, ERWA counters, per-constraint verdicts) is bit-identical to the unsplit launch, and the
+    sweep -- whose fp32 partial sums the split regroups -- matches the oracle."""
+    import paper_2603_22877_b200 as P
+    inst, f, a, b, x, w, vals = oracle_case(name)
+    R = 45
+    out = []
+    for sp in ("1", split):
+        old = os.environ.get("FSMT_TILE_SPLIT")
+        os.environ["FSMT_TILE_SPLIT"] = sp
+        try:
+            s = P.Solver(0)
+            s.load_formula(inst.text)
+            s.build_xbdd()
+            s.begin(R, 3)
+            s.set_state(a, b)
+            s.sweep(1.3, 1)
+            r1 = s.get_sweep()
+            unsat = s.stage_end(1)
+            _, pc = s.verify_batch(x, b, per_con=True)
+            out.append((r1, np.array(unsat), pc, s.get_counters()))
+        finally:
+            if old is None:
+                os.environ.pop("FSMT_TILE_SPLIT", None)
+            else:
+                os.environ["FSMT_TILE_SPLIT"] = old
+    (g1, gu, gpc, gU), (p1, pu, ppc, pU) = out
+    assert np.array_equal(gu, pu) and np.array_equal(gpc, ppc) and np.array_equal(gU, pU)
+    for r in (0, 44):
+        C, oga, ogb, want = vals[r]
+        check_objective(p1[0][r], C, float(sum(w)), what=f"{name} split {split}")
+        check_gradient(p1[1][:, r], oga, what=f"{name} split grad_a")
+        check_gradient(p1[2][:, r], ogb, what=f"{name} split grad_b")
         assert np.array_equal(ppc[:, r].astype(int), want)
