@@ -668,6 +668,7 @@ bool jit_pair() {
 // FSMT_JIT_UPF=d: the sweep loads U[c][r] d constraints ahead (0: in the iteration, plain load).
 // Without the variable: g_upf (jit_source's argument; fsmt_prepare picks it from the size of U).
 thread_local int g_upf = 0;   // per thread: contexts may build concurrently
+thread_local bool g_all_small = false;   // every JIT class non-symmetric with <= 16 references (loop unroll)
 int u_prefetch() {
     const char* e = getenv("FSMT_JIT_UPF");
     return e ? std::max(0, std::min(12, atoi(e))) : g_upf;
@@ -916,8 +917,11 @@ void emit_class(std::ostringstream& o, uint32_t kid, const KClass& K, const Temp
         // v21: with the value look-ahead, unroll 2 also for the placement class (no register-rotation
         // moves: cfg4 7.41 -> 7.12 ms at 80 registers); symmetric classes and classes without it keep
         // the round-2 rule (cfg2 0.133 vs 0.157 ms, random family n = 100 0.121 vs 0.131 ms unrolled)
-        unroll_pragma = "#pragma unroll " +
-                        std::to_string(ur ? std::max(1, atoi(ur)) : (K.n_refs <= 16 || (vpf && !K.sym) ? 2 : 1)) + "\n";
+        // v24: when every class is small and non-symmetric (<= 16 references: they share the all-class
+        // kernel's registers), unroll 4 (cfg3 0.733 -> 0.694 ms; a heavy class beside an unrolled small
+        // one lost its register cap on cfg4, 6.54 -> 6.72 ms)
+        const int def_unroll = K.n_refs <= 16 ? (g_all_small ? 4 : 2) : (vpf && !K.sym ? 2 : 1);
+        unroll_pragma = "#pragma unroll " + std::to_string(ur ? std::max(1, atoi(ur)) : def_unroll) + "\n";
     }
     o << unroll_pragma << "  for (u32 c = 0; c < T.n_cons; ++c, rp += " << K.stride4 << ") {\n";
     if (rpf) {
@@ -1609,6 +1613,8 @@ void emit_verify_class(std::ostringstream& o, uint32_t kid, const KClass& K, con
 std::string jit_source(const Formula& f, const Built& b, const Plan& p, int u_prefetch_default, int k1_min_ctas,
                        const std::vector<int>* class_caps) {
     g_upf = u_prefetch_default;
+    g_all_small = p.n_jit_kclasses > 0;
+    for (uint32_t k = 0; k < p.n_jit_kclasses; ++k) g_all_small = g_all_small && !p.kclasses[k].sym && p.kclasses[k].n_refs <= 16;
     std::ostringstream o;
     o << "// generated by fsmt tiles.cpp: specialised K1 sweep for " << p.n_jit_kclasses << " kernel classes\n"
          "typedef unsigned int u32;\ntypedef unsigned long long u64;\n"
