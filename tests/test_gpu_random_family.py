@@ -132,3 +132,22 @@ def test_product_form_matches_xbdd_form_cfg2_and_rand100():
                 check_objective(obj[r], C, float(w.sum()), what=what)
                 check_gradient(np.concatenate([ga[:, r], gb[:, r]]), np.concatenate([oga, ogb]), scale_relative=True,
                                what=what)
+
+
+@pytest.mark.parametrize("n", [100, 300])
+def test_random_family_solves(n):
+    """Alg.2 end to end on the paper's random family: the time-to-SAT recipe of the
+    bench (eta 0.4, eta_mode 3, reset-to-0 ERWA, kappa 1 -> 300 geometric then held) reaches SAT
+    within its schedule, and the returned model satisfies every constraint under the oracle's
+    exact semantics (Thm.1: a rounded model with no violated constraint is a witness)."""
+    import paper_2603_22877_b200 as P
+    inst = fsmt_gen.config(f"rand{n}")
+    f = hsmt.parse(inst.text)
+    s = P.Solver(0)
+    s.load_formula(inst.text)
+    s.build_xbdd()
+    kappas = [300.0 ** (i / 19) for i in range(20)] + [300.0] * 200
+    s.set_params(kappas=kappas, eta=0.4, eta_mode=3, erwa_mode=1)
+    res = s.solve(1024, 2, 0)
+    assert res.verdict == P.SAT
+    assert all(semantics.eval_formula(f, res.x, res.y)[1])
