@@ -177,7 +177,9 @@ struct Plan {
     // shared-memory rows per warp of the JIT sweep: the largest tile limit in use
     uint32_t kernel_vmax() const { return has_sym ? std::max(vmax, vmax_sym) : vmax; }
     // bytes per variable id in the sweep's shared-memory id table: u16 when every tile variable id fits
+    bool vid32 = false;   // FSMT_JIT_VID32=1: 4-byte ids even when they fit 2 (parity matrix)
     uint32_t vid_bytes() const {
+        if (vid32) return 4;
         for (uint32_t v : tile_vars)
             if (v > 0xFFFFu) return 4;
         return 2;

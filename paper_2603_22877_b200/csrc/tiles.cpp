@@ -48,6 +48,7 @@ int weight_exponent(const Built& b) {
 Plan make_plan(const Formula& f, const Built& b, bool enable_jit) {
     Plan p;
     p.wexp = weight_exponent(b);
+    if (const char* v = getenv("FSMT_JIT_VID32")) p.vid32 = v[0] == '1';
     if (const char* v = getenv("FSMT_TILE_VMAX")) p.vmax = (uint32_t)std::max(16, std::min(256, atoi(v)));
     if (const char* v = getenv("FSMT_TILE_CMAX")) p.cmax = (uint32_t)std::max(1, std::min(1024, atoi(v)));
     if (const char* v = getenv("FSMT_TILE_RMAX")) p.rmax = (uint32_t)std::max(16, std::min(1024, atoi(v)));

@@ -26,6 +26,7 @@ KNOBS = [
     {"FSMT_JIT_VPF": "0"},
     {"FSMT_JIT_VPF": "0", "FSMT_JIT_UNROLL": "2", "FSMT_JIT_UPF": "2"},
     {"FSMT_TILE_VMAX": "16", "FSMT_TILE_RMAX": "16", "FSMT_TILE_CMAX": "3"},
+    {"FSMT_JIT_VID32": "1"},
     {"FSMT_TILE_MERGE": "1"},
     {"FSMT_TILE_MERGE": "0"},
 ]
