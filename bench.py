@@ -448,7 +448,8 @@ def main():
                        "accumulation": "fp64, exact on-grid sums (deterministic)", "build_s": round(build_s, 2),
                        "jit": jit_status},
             "roofline": {"bound": "alu", "achieved": alu_achieved, "peak": alu_peak, "unit": "TFLOP/s",
-                         "frac": alu_achieved / alu_peak, "traffic": traffic, "kernel": "fsmt_k1_c0 (+ fsmt_k1_c1 concurrently; the JIT sweep of cfg4's two classes)" if args.config == "cfg4" else "fsmt_k1_jit / fsmt_k1_c<k>",
+                         "frac": alu_achieved / alu_peak, "traffic": traffic, "kernel": ("fsmt_k1_jit (the JIT sweep; cfg4's 1-slot bound class runs as fsmt_k1_c1 on an auxiliary stream)"
+                                    if args.config == "cfg4" else "fsmt_k1_jit / fsmt_k1_c<k> (JIT sweep kernels)"),
                          "basis": f"SURVEY 8(d) model {fma_pe:.0f} FMA-eq (x2 flop) per (constraint,restart) eval x "
                                   f"{evals_per_launch:.0f} evals per launch / live CUDA-event launch time; peak = 148 SMs x "
                                   f"128 FP32 lanes x 2 x {sm_max:.0f} MHz (DESIGN.md §7)",
