@@ -827,11 +827,12 @@ fsmt_status fsmt_jit_check(fsmt_ctx* ctx, size_t* cubin_bytes, char* log, size_t
 }
 
 // The source fsmt_prepare(R) compiles: the restart count as a constant (FSMT_RC); U loaded 3
-// constraints ahead when U[c][r] (1 B per constraint and restart) exceeds ~1.5x the 126 MB L2
-// and so comes from HBM every sweep (cfg4 9.78 -> 8.85 ms; cfg3, whose 117 MB
-// of U stays in L2, is faster without).
+// constraints ahead when U[c][r] exceeds ~1.5x the 126 MB L2 and so comes from HBM every sweep
+// (cfg4 9.78 -> 8.85 ms), else 2 ahead.
 static std::string prepared_source(const fsmt_ctx* ctx, uint32_t R, int min_ctas, const std::vector<int>* caps = nullptr) {
-    const int upf = (double)ctx->plan.jit_cons_end * R > 192e6 ? 3 : 0;
+    // (v25: also for an L2-resident U -- its ~600-cycle L2 latency was cfg3's top stall: cfg3 K1
+    // 0.694 -> 0.637 ms with 2 ahead)
+    const int upf = (double)ctx->plan.jit_cons_end * R > 192e6 ? 3 : 2;
     std::vector<int> all(ctx->plan.n_jit_kclasses, min_ctas);
     const std::string src = (upf || min_ctas || caps) ? jit_source(ctx->f, ctx->b, ctx->plan, upf, min_ctas, caps ? caps : &all)
                                                        : ctx->jit_src;
