@@ -855,7 +855,7 @@ static long spill_stores(const std::string& log, const std::string& kernel) {
 // then 28 one-warp CTAs per SM: 64 / 72 registers) whose compile has no spills, else no cap
 // (cfg3 best at 64, cfg4 at 72, cfg2 uncapped)
 static std::string prepared_source_tuned(const fsmt_ctx* ctx, uint32_t R, int* cap) {
-    for (int mc : {32, 28, 24}) {
+    for (int mc : {32, 28, 24, 20}) {
         const std::string src = prepared_source(ctx, R, mc);
         std::vector<char> cubin;
         std::string log, err;
@@ -898,7 +898,7 @@ fsmt_status fsmt_prepare(fsmt_ctx* ctx, uint32_t R) {
         cudaFuncAttributes fa{};
         return cudaFuncGetAttributes(&fa, (const void*)k) != cudaSuccess || fa.localSizeBytes > 0;
     };
-    for (int mc : {32, 28, 24}) {
+    for (int mc : {32, 28, 24, 20}) {
         JitKernel cand;
         if (!jit_compile(prepared_source(ctx, R, mc), cand, err)) continue;
         if (!cap_found && !spills(cand.kernel)) {
