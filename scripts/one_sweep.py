@@ -16,13 +16,15 @@ def main():
     s = P.Solver(0)
     s.load_formula(fsmt_gen.config(name).text)
     s.build_xbdd()
+    if len(sys.argv) > 3 and sys.argv[3] == "prepare":
+        s.prepare(R)                       # the R-specialised module with its register caps
     d = s.get_dims()
     a, b = random_points(d["n_bool"], d["n_real"], R, seed=5)
     s.begin(R, 1)
     s.set_state(a, b)
     s.sweep(0.5, 1)
     ms = s.time_sweep(0.5, 1, 20)
-    print(json.dumps({"config": name, "R": R, "sweep_ms": ms, "evals_per_s": d["n_cons"] * R / (ms / 1e3),
+    print(json.dumps({"config": name, "R": R, "sweep_ms": ms, "evals_per_s": d["n_cons"] * R / (ms / 1e3), "jit": s.jit_info()["status"],
                       "env": {k: v for k, v in os.environ.items() if k.startswith("FSMT_")}}), flush=True)
 
 
