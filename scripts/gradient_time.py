@@ -74,9 +74,9 @@ def main():
                 s.sweep(g / 100.0, 1)
             ms, cnt = s.get_timing(reset=True)["k1_sweep"]
             s.set_timing(False)
-            # the same 10,000 points as one sweep (one kappa)
-            s.prepare(0)
+            # the same 10,000 points as one sweep (one kappa), with the module prepared for it
             RB = G * R
+            s.prepare(RB)
             a = np.concatenate([p[0] for p in pts], axis=1)
             b = np.concatenate([p[1] for p in pts], axis=1)
             s.begin(RB, 1)
