@@ -40,6 +40,7 @@ struct fsmt_ctx {
     JitKernel jit_r;            // fsmt_prepare(R): the same module with R a compile-time constant
     uint32_t jit_r_R = 0;
     int jit_r_cap = 0;          // the prepared hot sweep's register cap (min CTAs/SM; 0 = none)
+    bool ext_bound = false;     // fsmt_bind_buffers / fsmt_bind_slot_grads replaced state buffers
     std::vector<int> jit_r_caps;   // the per-class sweep kernels' caps (fsmt_k1_c<k>)
     DevTiles T{};
     DevSlots slots{};                  // slot tables of the symmetric JIT classes (has_sym)
@@ -164,6 +165,7 @@ void drop_state(fsmt_ctx* ctx) {
     ctx->slots.TT = nullptr;
     ctx->scratch = nullptr;     // freed with the state allocations
     ctx->rounded = false;
+    ctx->ext_bound = false;
     if (ctx->terms) { cudaFree(ctx->terms); ctx->terms = nullptr; }
 }
 
@@ -668,7 +670,16 @@ fsmt_status fsmt_begin(fsmt_ctx* ctx, uint32_t R, uint64_t seed, uint32_t restar
     if (ctx->F.proj_iters && ctx->F.n_half && project_smem_bytes(ctx->F, ctx->F.h_nnz) > 227 * 1024)
         return fail(ctx, FSMT_ERR_ARG, "too many multi-variable unit atoms for the on-chip Dykstra projection (R33)");
     cudaSetDevice(ctx->device);
-    drop_state(ctx);
+    // the state of a previous begin with the same restart count is reused (no cudaFree / cudaMalloc:
+    // they cost 40-50 ms at R = 32, i.e. most of a time-to-SAT run) unless buffers were bound
+    const bool reuse = ctx->S.a && ctx->S.R == R && !ctx->ext_bound;
+    if (reuse) {
+        if (ctx->gexec) { cudaGraphExecDestroy(ctx->gexec); ctx->gexec = nullptr; }
+        ctx->rounded = false;
+        if (ctx->terms) { cudaFree(ctx->terms); ctx->terms = nullptr; }
+    } else {
+        drop_state(ctx);
+    }
     const DevFormula& F = ctx->F;
     DevState& S = ctx->S;
     S.R = R;
@@ -679,42 +690,44 @@ fsmt_status fsmt_begin(fsmt_ctx* ctx, uint32_t R, uint64_t seed, uint32_t restar
         return FSMT_OK;
     };
     const size_t nb = (size_t)F.n_bool * R, nr = (size_t)F.n_real * R, nc = (size_t)F.n_cons * R;
-    const size_t parts = (size_t)update_parts(F, R);
-    // grad_a and grad_b are one allocation ([var][R] over the unified variable id: gb = ga + nb), so
-    // a stream row flushes to ga + g*R whatever the variable's kind; U has kUPad spare constraint
-    // rows so the sweep's U prefetch may read past the last tile without a bounds test
-    if ((s = alloc((void**)&S.a, nb * 4)) || (s = alloc((void**)&S.b, nr * 4)) || (s = alloc((void**)&S.ga, (nb + nr) * 8)) ||
-        (s = alloc((void**)&S.U, (nc + (size_t)kUPad * R) * 2)) || (s = alloc((void**)&S.obj, (size_t)R * 8)) ||
-        (s = alloc((void**)&S.x, nb)) || (s = alloc((void**)&S.unsat, (size_t)R * 4)) ||
-        (s = alloc((void**)&S.frozen, R)) || (s = alloc((void**)&S.gm2, (size_t)R * 8)) ||
-        (s = alloc((void**)&S.gm2_part, std::max<size_t>(parts, 1) * R * 8))) {
-        drop_state(ctx);
-        return s;
-    }
-    S.gb = S.ga + nb;
-    if (ctx->has_sym) {   // slot tables (rows: Booleans, reals (unused), table atoms)
-        DevSlots& D = ctx->slots;
-        const size_t rows = (size_t)D.nv + D.n_sa;
-        if ((s = alloc((void**)&D.PT, rows * R * 4)) ||
-            (s = alloc((void**)&D.DD, (size_t)D.n_sa * R * 4)) || (s = alloc((void**)&D.GU, rows * R * 8)) ||
-            (s = alloc((void**)&D.TT, rows * R))) {
+    if (!reuse) {
+        const size_t parts = (size_t)update_parts(F, R);
+        // grad_a and grad_b are one allocation ([var][R] over the unified variable id: gb = ga + nb), so
+        // a stream row flushes to ga + g*R whatever the variable's kind; U has kUPad spare constraint
+        // rows so the sweep's U prefetch may read past the last tile without a bounds test
+        if ((s = alloc((void**)&S.a, nb * 4)) || (s = alloc((void**)&S.b, nr * 4)) || (s = alloc((void**)&S.ga, (nb + nr) * 8)) ||
+            (s = alloc((void**)&S.U, (nc + (size_t)kUPad * R) * 2)) || (s = alloc((void**)&S.obj, (size_t)R * 8)) ||
+            (s = alloc((void**)&S.x, nb)) || (s = alloc((void**)&S.unsat, (size_t)R * 4)) ||
+            (s = alloc((void**)&S.frozen, R)) || (s = alloc((void**)&S.gm2, (size_t)R * 8)) ||
+            (s = alloc((void**)&S.gm2_part, std::max<size_t>(parts, 1) * R * 8))) {
             drop_state(ctx);
             return s;
         }
-    }
-    if ((s = alloc((void**)&S.x_best, nb)) || (s = alloc((void**)&S.unsat_m, (size_t)R * 4)) ||
-        (s = alloc((void**)&S.unsat_best, (size_t)R * 4)) || (s = alloc((void**)&S.better, R)) ||
-        (s = alloc((void**)&S.umax, (size_t)R * 4)) || (s = alloc((void**)&S.fx, (size_t)R * sizeof(FxScale))) ||
-        (s = alloc((void**)&S.gsc, (size_t)R * 8)) || (s = alloc((void**)&S.flags, 16)) ||
-        (s = alloc((void**)&ctx->scratch, (size_t)std::max(F.n_bool, F.n_real) * R * 8))) {
-        drop_state(ctx);
-        return s;
-    }
-    S.bn = nullptr;
-    if (F.n_half) {   // R33: the candidate b of the projected step
-        if ((s = alloc((void**)&S.bn, nr * 4))) {
+        S.gb = S.ga + nb;
+        if (ctx->has_sym) {   // slot tables (rows: Booleans, reals (unused), table atoms)
+            DevSlots& D = ctx->slots;
+            const size_t rows = (size_t)D.nv + D.n_sa;
+            if ((s = alloc((void**)&D.PT, rows * R * 4)) ||
+                (s = alloc((void**)&D.DD, (size_t)D.n_sa * R * 4)) || (s = alloc((void**)&D.GU, rows * R * 8)) ||
+                (s = alloc((void**)&D.TT, rows * R))) {
+                drop_state(ctx);
+                return s;
+            }
+        }
+        if ((s = alloc((void**)&S.x_best, nb)) || (s = alloc((void**)&S.unsat_m, (size_t)R * 4)) ||
+            (s = alloc((void**)&S.unsat_best, (size_t)R * 4)) || (s = alloc((void**)&S.better, R)) ||
+            (s = alloc((void**)&S.umax, (size_t)R * 4)) || (s = alloc((void**)&S.fx, (size_t)R * sizeof(FxScale))) ||
+            (s = alloc((void**)&S.gsc, (size_t)R * 8)) || (s = alloc((void**)&S.flags, 16)) ||
+            (s = alloc((void**)&ctx->scratch, (size_t)std::max(F.n_bool, F.n_real) * R * 8))) {
             drop_state(ctx);
             return s;
+        }
+        S.bn = nullptr;
+        if (F.n_half) {   // R33: the candidate b of the projected step
+            if ((s = alloc((void**)&S.bn, nr * 4))) {
+                drop_state(ctx);
+                return s;
+            }
         }
     }
     CK(cudaMemsetAsync(S.U, 0, (nc + (size_t)kUPad * R) * 2, ctx->stream));
@@ -1114,7 +1127,10 @@ fsmt_status fsmt_bind_slot_grads(fsmt_ctx* ctx, void* gu) {
         cudaGetLastError();
         return fail(ctx, FSMT_ERR_ARG, "fsmt_bind_slot_grads: device memory only");
     }
-    if (gu) ctx->slots.GU = (double*)gu;
+    if (gu) {
+        ctx->slots.GU = (double*)gu;
+        ctx->ext_bound = true;
+    }
     return FSMT_OK;
 }
 
@@ -1262,6 +1278,7 @@ fsmt_status fsmt_bind_buffers(fsmt_ctx* ctx, void* grad_a, void* grad_b, void* o
         }
     }
     if (umax && ctx->S.umax) CK(cudaMemcpyAsync(umax, ctx->S.umax, (size_t)ctx->S.R * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+    if (grad_a || grad_b || obj || unsat || umax) ctx->ext_bound = true;
     if (grad_a) ctx->S.ga = (double*)grad_a;
     if (grad_b) ctx->S.gb = (double*)grad_b;
     if (obj) ctx->S.obj = (double*)obj;
